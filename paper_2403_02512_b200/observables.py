@@ -1,0 +1,94 @@
+"""Observable records of the drop-in boundary.
+
+Variants: ``PauliWord`` (list of (wire, P) with P in I/X/Y/Z), ``Hamiltonian``
+(coefficients + Pauli words, H = sum_t c_t P_t) and
+``DenseHermitian`` (wires + 2^w x 2^w matrix). Sparse CSR observables are the
+"next" row of SURVEY.md §8(f) and raise UnsupportedOperationError.
+These classes only validate and pack; every number is computed on the GPU.
+"""
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import ValidationError
+
+PAULIS = "IXYZ"
+
+
+@dataclass
+class PauliWord:
+    """Tensor product of single-qubit Paulis, e.g. ``PauliWord([(0, "Z"), (3, "X")])``."""
+
+    factors: tuple
+
+    def __post_init__(self):
+        facs = []
+        for w, p in self.factors:
+            p = str(p).upper()
+            if p not in PAULIS:
+                raise ValidationError(f"unknown Pauli {p!r}")
+            facs.append((int(w), p))
+        wires = [w for w, _ in facs]
+        if len(set(wires)) != len(wires):
+            raise ValidationError(f"duplicate wire within Pauli word: {wires}")
+        self.factors = tuple(facs)
+
+    @classmethod
+    def from_string(cls, s, wires=None):
+        """``"XZ"`` on wires (0,1) by default, or explicit ``wires``."""
+        wires = range(len(s)) if wires is None else wires
+        return cls(tuple(zip(wires, s)))
+
+    @property
+    def wires(self):
+        return tuple(w for w, _ in self.factors)
+
+    def max_wire(self):
+        return max(self.wires, default=-1)
+
+
+@dataclass
+class Hamiltonian:
+    """Weighted sum of Pauli words."""
+
+    coeffs: tuple
+    terms: tuple
+
+    def __post_init__(self):
+        self.coeffs = tuple(float(c) for c in self.coeffs)
+        self.terms = tuple(t if isinstance(t, PauliWord) else PauliWord(t) for t in self.terms)
+        if len(self.coeffs) != len(self.terms):
+            raise ValidationError(
+                f"Hamiltonian has {len(self.coeffs)} coefficients but {len(self.terms)} terms")
+
+    def max_wire(self):
+        return max((t.max_wire() for t in self.terms), default=-1)
+
+
+@dataclass
+class DenseHermitian:
+    """Dense observable on ``wires`` (wires[0] = MSB of the matrix index, state.py:281)."""
+
+    wires: tuple
+    matrix: np.ndarray = field(repr=False)
+
+    def __post_init__(self):
+        self.wires = tuple(int(w) for w in self.wires)
+        self.matrix = np.ascontiguousarray(self.matrix, dtype=np.complex128)
+        dim = 1 << len(self.wires)
+        if self.matrix.shape != (dim, dim):
+            raise ValidationError(
+                f"matrix shape {self.matrix.shape} does not match {len(self.wires)} wires")
+        if len(set(self.wires)) != len(self.wires):
+            raise ValidationError(f"duplicate wires: {self.wires}")
+
+    def max_wire(self):
+        return max(self.wires, default=-1)
+
+
+def as_observable(obs):
+    """Accept a PauliWord/Hamiltonian/DenseHermitian or a ``[(wire, P), ...]`` list."""
+    if isinstance(obs, (PauliWord, Hamiltonian, DenseHermitian)):
+        return obs
+    return PauliWord(tuple(obs))
