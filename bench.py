@@ -1,0 +1,317 @@
+#!/usr/bin/env python
+"""Headline benchmark: BASELINE.json config 2 -- random RX/RY/RZ/CNOT circuit, depth 50,
+complex128 gate application on B200 (30 qubits at N=1; weak scaling 30 + log2 N qubits,
+sharded over N GPUs with global-qubit swaps over NCCL, at N > 1).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one pass of the whole circuit over the HBM-resident state.
+metric = gate-apply GB/s, "effective": the circuit's UNFUSED algorithmic bytes (32 B per
+amplitude read+written per gate) / device time; with fusion this exceeds the
+HBM peak by design -- `roofline` reports the dominant kernel against the measured peak.
+"""
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "gate-apply GB/s (effective; random RX/RY/RZ/CNOT circuit depth 50, complex128)"
+UNIT = "GB/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n-qubits", type=int, default=0, help="default 30 + log2(N)")
+    ap.add_argument("--depth", type=int, default=50)
+    ap.add_argument("--no-fuse", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    return rank, world, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic(kernel_class):
+    """dram bytes per launch from the committed ncu capture summary, if any."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(kernel_class)
+    except Exception:
+        return None
+
+
+def circuit(n, depth, seed):
+    from paper_2403_02512_b200 import workloads
+    ops = workloads.random_circuit(n, depth, seed=seed)
+    return ops, workloads.algorithmic_bytes(ops, n)
+
+
+def cpu_port_baseline(n, ops, budget_s):
+    """Time the C port of the reference's Alg. 1/Alg. 2 (oracle/c/svport.c, OpenMP) on the host,
+    on the first gates of the same circuit, until ~budget_s of work. Returns (GB/s, sample, cores, n_used)."""
+    from oracle import cport
+    from paper_2403_02512_b200 import workloads
+    import psutil
+    n_used = n
+    while n_used > 20 and psutil.virtual_memory().available < 2.5 * 16 * (1 << n_used):
+        n_used -= 1
+    if n_used != n:
+        ops = workloads.random_circuit(n_used, 50, seed=0)
+    amps = np.zeros(1 << n_used, dtype=np.complex128)
+    amps[0] = 1
+    threads = cport.max_threads()
+    cport.apply_op(amps, n_used, ops[0], threads)      # warm-up (page-in)
+    t0 = time.perf_counter()
+    done, nbytes = 0, 0
+    for op in ops[1:]:
+        cport.apply_op(amps, n_used, op, threads)
+        done += 1
+        nbytes += workloads.algorithmic_bytes([op], n_used)
+        if time.perf_counter() - t0 > budget_s and done >= 2:
+            break
+    dt = time.perf_counter() - t0
+    sample = f"gates 2..{done + 1} of the depth-50 circuit at n={n_used} ({done} gates, {dt:.1f} s)"
+    return nbytes / dt / 1e9, sample, threads, n_used
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm's CPU port on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    n = args.n_qubits or (30 + (world.bit_length() - 1))
+    ops, _ = circuit(n, args.depth, args.seed)
+    per_step = max(2.0, args.cpu_seconds / max(1, args.steps))
+    vals = []
+    for i in range(args.warmup + args.steps):
+        v, sample, cores, n_used = cpu_port_baseline(n, ops, per_step if i >= args.warmup else 1.0)
+        if i >= args.warmup:
+            vals.append(v)
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "higher_is_better": True, "dtype": "c128",
+        "data": "synthetic", "scaling": "weak",
+        "config": {"workload": f"random RX/RY/RZ/CNOT circuit depth {args.depth} (BASELINE config 2), n={n}",
+                   "n_qubits_sampled": n_used},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": "per step: " + sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "vs_baseline": None,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if world != args.gpus and "RANK" in os.environ:
+        args.gpus = world
+    pg = None
+    if world > 1:
+        import torch.distributed as tdist
+        tdist.init_process_group("gloo", init_method="env://")
+        pg = tdist
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        if pg:
+            pg.barrier()
+        return
+
+    import torch
+    from paper_2403_02512_b200 import _lib
+    from paper_2403_02512_b200.device import Device
+    from paper_2403_02512_b200.observables import PauliWord
+
+    g = world.bit_length() - 1
+    n = args.n_qubits or (30 + g)
+    fuse = not args.no_fuse
+    torch.cuda.set_device(local)
+    if world > 1:
+        nid = [Device.nccl_unique_id() if rank == 0 else None]
+        pg.broadcast_object_list(nid, src=0)
+        dev = Device.sharded(n, rank, world, nid[0], device=local, fuse=fuse)
+    else:
+        dev = Device(n, device=local, fuse=fuse)
+    ops, alg_bytes = circuit(n, args.depth, args.seed)
+    stream = torch.cuda.ExternalStream(dev.stream, device=f"cuda:{local}")
+
+    def barrier():
+        dev.synchronize()
+        if pg:
+            pg.barrier()
+
+    for _ in range(args.warmup):
+        dev.apply(ops)
+    barrier()
+    dev.reset_stats()
+    dev.set_profiling(True)
+    launches0 = dev.launch_count
+    clk = ClockSampler(local)
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for _ in range(args.steps):
+        dev.apply(ops)
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    clocks = clk.stop()
+    launches = dev.launch_count - launches0
+    stats = dev.kernel_stats()
+    dev.set_profiling(False)
+    if pg:
+        t = torch.tensor([ms], dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        ms = float(t[0])
+    ms_per_step = ms / args.steps
+    value = alg_bytes * args.steps / (ms / 1e3) / 1e9
+
+    # roofline of the dominant kernel class (device time inside the timed region)
+    dom = max(stats, key=lambda k: stats[k]["ms"])
+    st = stats[dom]
+    peak, peak_src = measured_peak()
+    achieved = st["bytes"] / (st["ms"] / 1e3) / 1e9 if st["ms"] > 0 else 0.0
+    per_launch = st["bytes"] / max(st["launches"], 1)
+    traffic = ncu_traffic(dom)
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": traffic, "kernel": dom, "algorithmic_bytes_per_launch": per_launch,
+                "launches": st["launches"], "share_of_step": st["ms"] / ms if ms else None, "peak_source": peak_src,
+                "frac_of_8000": achieved / 8000.0}
+
+    # e2e through the public API: host op list in, <Z_0> out, every step
+    obs = PauliWord(((0, "Z"),))
+    packed = _lib.PackedOps(ops)
+    h2d = ctypes.sizeof(_lib.SvOp) * len(ops) + sum(a.nbytes for a in packed._keep if hasattr(a, "nbytes"))
+    for _ in range(1):
+        dev.reset()
+        dev.apply(ops)
+        dev.expval(obs)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        dev.reset()
+        dev.apply(ops)
+        ev = dev.expval(obs)
+    e2e_s = time.perf_counter() - t0
+    if pg:
+        t = torch.tensor([e2e_s], dtype=torch.float64)
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        e2e_s = float(t[0])
+    e2e = {"value": alg_bytes * args.steps / e2e_s / 1e9, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": 8, "s_per_step": e2e_s / args.steps,
+           "call": "Device.reset + Device.apply(op list) + Device.expval(Z0) -> host float"}
+
+    cpu = None
+    if rank == 0 and world == 1:
+        try:
+            v, sample, cores, n_used = cpu_port_baseline(n, ops, args.cpu_seconds)
+            cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "port", "sample": sample}
+        except Exception as exc:  # the CPU leg is a reported baseline, never fatal
+            cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "s_per_circuit": ms_per_step / 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+            "data": "synthetic",
+            "config": {"workload": f"random RX/RY/RZ/CNOT circuit depth {args.depth} (BASELINE config 2)",
+                       "n_qubits": n, "gates": len(ops), "seed": args.seed, "fused": fuse,
+                       "unfused_algorithmic_bytes_per_step": alg_bytes,
+                       "parallelism": f"sharded over {world} GPU(s), {g} global qubit(s)" if world > 1 else "1 GPU",
+                       "l2": f"state {16 * (1 << (n - g)) / 2**30:.0f} GiB per GPU >> 126 MB L2 (no flush needed)"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clocks, "expval_check": ev,
+        }
+        print(json.dumps(line), flush=True)
+    dev.release()
+    if pg:
+        pg.barrier()
+        pg.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

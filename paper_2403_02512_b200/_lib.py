@@ -1,0 +1,197 @@
+"""ctypes binding of libsvb200.so (include/svb200.h).
+
+The library is the product: if it is missing this module raises at load time -- there is
+no CPU fallback. Build it with ``python -m paper_2403_02512_b200.build``.
+"""
+
+import ctypes
+import os
+from ctypes import POINTER, c_char, c_char_p, c_double, c_int, c_int32, c_int64, c_uint64, c_void_p
+
+import numpy as np
+
+from .errors import raise_for_status
+from .observables import DenseHermitian, Hamiltonian, PauliWord, as_observable
+from .ops import KIND_CODE, Op
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsvb200.so")
+
+# Every symbol include/svb200.h declares (checked by tests/test_boundary.py).
+EXPORTS = (
+    "sv_device_count", "sv_create", "sv_nccl_unique_id", "sv_create_sharded", "sv_destroy", "sv_info",
+    "sv_reset", "sv_set_basis_state", "sv_set_state", "sv_get_state", "sv_norm",
+    "sv_apply_single_qubit", "sv_apply_controlled_single_qubit", "sv_apply_matrix", "sv_apply_ops",
+    "sv_expval", "sv_probs", "sv_adjoint_jacobian", "sv_last_error", "sv_synchronize", "sv_stream",
+    "sv_launch_count", "sv_set_profiling", "sv_kernel_stats", "sv_reset_stats", "sv_plan_summary",
+)
+
+
+class SvOp(ctypes.Structure):
+    _fields_ = [
+        ("kind", c_int32), ("n_wires", c_int32), ("wires", POINTER(c_int32)),
+        ("n_ctrls", c_int32), ("ctrls", POINTER(c_int32)), ("ctrl_values", POINTER(c_int32)),
+        ("params", c_double * 3), ("inverse", c_int32), ("trainable_mask", c_int32),
+        ("matrix", POINTER(c_double)),
+    ]
+
+
+class SvObs(ctypes.Structure):
+    _fields_ = [
+        ("type", c_int32), ("n_terms", c_int32), ("coeffs", POINTER(c_double)),
+        ("term_len", POINTER(c_int32)), ("term_wires", POINTER(c_int32)), ("term_paulis", c_char_p),
+        ("n_wires", c_int32), ("wires", POINTER(c_int32)), ("matrix", POINTER(c_double)),
+    ]
+
+
+_lib = None
+
+
+def lib():
+    """Load libsvb200.so once; raise loudly if it has not been built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2403_02512_b200.build` "
+                              "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        H = c_void_p
+        sig = {
+            "sv_device_count": [POINTER(c_int)],
+            "sv_create": [c_int, c_int, POINTER(H)],
+            "sv_nccl_unique_id": [c_void_p],
+            "sv_create_sharded": [c_int, c_int, c_int, c_int, c_void_p, POINTER(H)],
+            "sv_destroy": [H],
+            "sv_info": [H, POINTER(c_int64)],
+            "sv_reset": [H],
+            "sv_set_basis_state": [H, c_uint64],
+            "sv_set_state": [H, POINTER(c_double), c_uint64],
+            "sv_get_state": [H, POINTER(c_double), c_uint64],
+            "sv_norm": [H, POINTER(c_double)],
+            "sv_apply_single_qubit": [H, c_int, POINTER(c_double)],
+            "sv_apply_controlled_single_qubit": [H, POINTER(c_int32), c_int, c_int, POINTER(c_double), POINTER(c_int32)],
+            "sv_apply_matrix": [H, POINTER(c_int32), c_int, POINTER(c_double)],
+            "sv_apply_ops": [H, POINTER(SvOp), c_int, c_int],
+            "sv_expval": [H, POINTER(SvObs), POINTER(c_double)],
+            "sv_probs": [H, POINTER(c_int32), c_int, POINTER(c_double)],
+            "sv_adjoint_jacobian": [H, POINTER(SvOp), c_int, POINTER(SvObs), c_int, c_int, POINTER(c_double),
+                                    POINTER(c_double)],
+            "sv_synchronize": [H],
+            "sv_set_profiling": [H, c_int],
+            "sv_kernel_stats": [H, POINTER(c_double), c_int, POINTER(c_int), POINTER(c_char), c_int],
+            "sv_reset_stats": [H],
+            "sv_plan_summary": [c_int, POINTER(SvOp), c_int, POINTER(c_int64)],
+        }
+        for name, args in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = c_int
+        L.sv_last_error.argtypes = []
+        L.sv_last_error.restype = c_char_p
+        L.sv_stream.argtypes = [H]
+        L.sv_stream.restype = c_void_p
+        L.sv_launch_count.argtypes = [H]
+        L.sv_launch_count.restype = c_int64
+        _lib = L
+    return _lib
+
+
+def check(status):
+    if status != 0:
+        raise_for_status(status, lib().sv_last_error().decode(errors="replace"))
+
+
+def device_count():
+    n = c_int(0)
+    check(lib().sv_device_count(ctypes.byref(n)))
+    return n.value
+
+
+def _iptr(a):
+    return a.ctypes.data_as(POINTER(c_int32))
+
+
+def _dptr(a):
+    return a.ctypes.data_as(POINTER(c_double))
+
+
+class PackedOps:
+    """Op records marshalled into C structs; owns every buffer the structs point to."""
+
+    def __init__(self, ops):
+        ops = list(ops)
+        self.n = len(ops)
+        self.arr = (SvOp * max(self.n, 1))()
+        self._keep = []
+        for i, op in enumerate(ops):
+            if not isinstance(op, Op):
+                raise TypeError(f"expected Op, got {type(op).__name__}")
+            rec = self.arr[i]
+            rec.kind = KIND_CODE[op.name]
+            w = np.ascontiguousarray(op.wires, dtype=np.int32)
+            rec.n_wires = len(w)
+            rec.wires = _iptr(w)
+            self._keep.append(w)
+            if op.ctrls:
+                c = np.ascontiguousarray(op.ctrls, dtype=np.int32)
+                v = np.ascontiguousarray(op.ctrl_values, dtype=np.int32)
+                rec.n_ctrls = len(c)
+                rec.ctrls = _iptr(c)
+                rec.ctrl_values = _iptr(v)
+                self._keep += [c, v]
+            for j, p in enumerate(op.params[:3]):
+                rec.params[j] = p
+            rec.inverse = int(bool(op.inverse))
+            rec.trainable_mask = sum(1 << j for j, t in enumerate(op.trainable) if t)
+            if op.matrix is not None:
+                m = np.ascontiguousarray(op.matrix, dtype=np.complex128).view(np.float64)
+                rec.matrix = _dptr(m)
+                self._keep.append(m)
+
+    @property
+    def ptr(self):
+        return self.arr
+
+
+class PackedObs:
+    """Observable records marshalled into C structs."""
+
+    def __init__(self, observables):
+        obs = [as_observable(o) for o in observables]
+        self.n = len(obs)
+        self.arr = (SvObs * max(self.n, 1))()
+        self._keep = []
+        for i, o in enumerate(obs):
+            rec = self.arr[i]
+            if isinstance(o, DenseHermitian):
+                rec.type = 2
+                w = np.ascontiguousarray(o.wires, dtype=np.int32)
+                m = np.ascontiguousarray(o.matrix, dtype=np.complex128).view(np.float64)
+                rec.n_wires = len(w)
+                rec.wires = _iptr(w)
+                rec.matrix = _dptr(m)
+                self._keep += [w, m]
+                continue
+            if isinstance(o, PauliWord):
+                rec.type = 0
+                terms, coeffs = [o], None
+            elif isinstance(o, Hamiltonian):
+                rec.type = 1
+                terms = list(o.terms)
+                coeffs = np.ascontiguousarray(o.coeffs, dtype=np.float64)
+            else:
+                raise TypeError(f"unsupported observable {type(o).__name__}")
+            lens = np.array([len(t.factors) for t in terms], dtype=np.int32)
+            wires = np.array([w for t in terms for w, _ in t.factors], dtype=np.int32)
+            paulis = "".join(p for t in terms for _, p in t.factors).encode() + b"\0"
+            rec.n_terms = len(terms)
+            rec.term_len = _iptr(lens)
+            rec.term_wires = _iptr(wires)
+            rec.term_paulis = paulis
+            self._keep += [lens, wires, paulis]
+            if coeffs is not None:
+                rec.coeffs = _dptr(coeffs)
+                self._keep.append(coeffs)
+
+    @property
+    def ptr(self):
+        return self.arr

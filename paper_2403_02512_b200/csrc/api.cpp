@@ -1,0 +1,791 @@
+// C-ABI of libsvb200 (include/svb200.h): handle lifecycle, validation with the reference's
+// error taxonomy, op-list execution, measurements and the adjoint-Jacobian driver.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <new>
+
+#include "dist.h"
+#include "sv_internal.h"
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+[[noreturn]] void sv_fail(int status, const std::string& msg) { throw SvError{status, msg}; }
+
+void sv_cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    sv_fail(SV_ERR_CAPACITY, std::string("device allocation failed: ") + what);
+  }
+  sv_fail(SV_ERR_DEVICE, std::string(cudaGetErrorString(e)) + " in " + what);
+}
+
+void sv_nccl_check(ncclResult_t r, const char* what) {
+  if (r == ncclSuccess) return;
+  sv_fail(SV_ERR_DEVICE, std::string("NCCL: ") + ncclGetErrorString(r) + " in " + what);
+}
+
+#define API_BEGIN try {
+#define API_END                                  \
+  return SV_OK;                                  \
+  }                                              \
+  catch (const SvError& e) {                     \
+    g_last_error = e.msg;                        \
+    return e.status;                             \
+  }                                              \
+  catch (const std::bad_alloc&) {                \
+    g_last_error = "host allocation failed";     \
+    return SV_ERR_CAPACITY;                      \
+  }                                              \
+  catch (const std::exception& e) {              \
+    g_last_error = e.what();                     \
+    return SV_ERR_DEVICE;                        \
+  }
+
+// ---------------------------------------------------------------------------
+// scratch / stats helpers
+// ---------------------------------------------------------------------------
+void ensure_partials(sv_handle* h, size_t doubles) {
+  if (h->partials_cap >= doubles) return;
+  if (h->d_partials) {
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    CUDA_CHECK(cudaFree(h->d_partials));
+  }
+  size_t cap = std::max<size_t>(doubles, 4096);
+  CUDA_CHECK(cudaMalloc(&h->d_partials, cap * sizeof(double)));
+  h->partials_cap = cap;
+}
+
+void ensure_results(sv_handle* h, size_t doubles) {
+  if (h->results_cap >= doubles) return;
+  if (h->d_results) {
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    CUDA_CHECK(cudaFree(h->d_results));
+  }
+  size_t cap = std::max<size_t>(doubles, 1024);
+  CUDA_CHECK(cudaMalloc(&h->d_results, cap * sizeof(double)));
+  h->results_cap = cap;
+}
+
+static double* ensure_pinned(sv_handle* h, size_t doubles) {
+  if (h->h_pinned_cap < doubles) {
+    if (h->h_pinned) cudaFreeHost(h->h_pinned);
+    size_t cap = std::max<size_t>(doubles, 1024);
+    CUDA_CHECK(cudaMallocHost(&h->h_pinned, cap * sizeof(double)));
+    h->h_pinned_cap = cap;
+  }
+  return h->h_pinned;
+}
+
+static cudaEvent_t pool_event(sv_handle* h) {
+  if (!h->event_pool.empty()) {
+    cudaEvent_t e = h->event_pool.back();
+    h->event_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  CUDA_CHECK(cudaEventCreate(&e));
+  return e;
+}
+
+void stat_begin(sv_handle* h, int cls, double bytes, cudaEvent_t* ev) {
+  (void)cls;
+  (void)bytes;
+  if (!h->profiling) return;
+  ev[0] = pool_event(h);
+  ev[1] = pool_event(h);
+  CUDA_CHECK(cudaEventRecord(ev[0], h->stream));
+}
+
+void stat_end(sv_handle* h, int cls, double bytes, cudaEvent_t* ev) {
+  h->launches++;
+  h->kc_launches[cls] += 1;
+  h->kc_bytes[cls] += bytes;
+  if (!h->profiling) return;
+  CUDA_CHECK(cudaEventRecord(ev[1], h->stream));
+  h->pending.push_back({cls, bytes, ev[0], ev[1]});
+}
+
+static void drain_timings(sv_handle* h) {
+  if (h->pending.empty()) return;
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  for (auto& p : h->pending) {
+    float ms = 0;
+    CUDA_CHECK(cudaEventElapsedTime(&ms, p.start, p.stop));
+    h->kc_ms[p.cls] += ms;
+    h->event_pool.push_back(p.start);
+    h->event_pool.push_back(p.stop);
+  }
+  h->pending.clear();
+}
+
+// ---------------------------------------------------------------------------
+// op execution
+// ---------------------------------------------------------------------------
+static void check_handle(const sv_handle* h) {
+  if (!h) sv_fail(SV_ERR_VALIDATION, "null device handle (released?)");
+}
+
+static void exec_prims(sv_handle* h, const std::vector<double2*>& states, std::vector<Prim>& prims, int fuse) {
+  if (prims.empty()) return;
+  for (double2* st : states) {
+    if (fuse)
+      apply_prims_fused(h, st, prims);
+    else
+      for (const Prim& p : prims) launch_prim(h, st, p);
+  }
+  prims.clear();
+}
+
+// Lower and run an op list on `states` (psi, plus lambdas during the adjoint sweep all share
+// the layout).  Global-qubit targets trigger a layout swap first (dist.cpp).
+static void run_ops(sv_handle* h, const std::vector<double2*>& states, const sv_op* ops, int n_ops, int fuse) {
+  std::vector<Prim> pending;
+  for (int i = 0; i < n_ops; ++i) {
+    const sv_op& op = ops[i];
+    int dummy = 0;
+    auto pieces = lower_op(op, h->n, dummy, false, h->phys.data());
+    if (h->world > 1) {
+      bool need = false;
+      for (auto& pc : pieces) need |= prim_needs_swap(pc.fwd, h->nl);
+      if (need) {
+        exec_prims(h, states, pending, fuse);
+        dist_make_local(h, states, std::vector<int>(op.wires, op.wires + op.n_wires));
+        dummy = 0;
+        pieces = lower_op(op, h->n, dummy, false, h->phys.data());
+      }
+    }
+    for (auto& pc : pieces) {
+      resolve_global(pc.fwd, h->nl, h->rank);
+      if (!pc.fwd.skip) pending.push_back(pc.fwd);
+    }
+  }
+  exec_prims(h, states, pending, fuse);
+}
+
+static void validate_ops(const sv_handle* h, const sv_op* ops, int n_ops) {
+  if (n_ops < 0 || (n_ops > 0 && !ops)) sv_fail(SV_ERR_VALIDATION, "bad op list");
+  for (int i = 0; i < n_ops; ++i) validate_op(ops[i], h->n);
+}
+
+// ---------------------------------------------------------------------------
+// observables
+// ---------------------------------------------------------------------------
+struct PauliGroup {
+  u64 x;
+  std::vector<PauliTerm> terms;
+};
+
+// Terms of a PAULI / HAMILTONIAN observable in physical bits, grouped by x-mask (one read per group).
+static std::vector<PauliGroup> pauli_groups(sv_handle* h, const sv_obs& o, const std::vector<double2*>& states) {
+  if (o.type != SV_OBS_PAULI && o.type != SV_OBS_HAMILTONIAN) sv_fail(SV_ERR_VALIDATION, "not a Pauli observable");
+  if (o.n_terms < 0 || (o.n_terms && (!o.term_len))) sv_fail(SV_ERR_VALIDATION, "malformed observable");
+  if (o.type == SV_OBS_HAMILTONIAN && o.n_terms && !o.coeffs) sv_fail(SV_ERR_VALIDATION, "Hamiltonian without coefficients");
+  struct Raw {
+    std::vector<int> xw;
+    u64 xl = 0, zl = 0;   // logical offsets
+    int ny = 0;
+    double c = 1.0;
+  };
+  std::vector<Raw> raw(o.n_terms);
+  int at = 0;
+  for (int t = 0; t < o.n_terms; ++t) {
+    Raw& r = raw[t];
+    r.c = (o.type == SV_OBS_HAMILTONIAN) ? o.coeffs[t] : 1.0;
+    for (int f = 0; f < o.term_len[t]; ++f, ++at) {
+      int w = o.term_wires[at];
+      char p = o.term_paulis[at];
+      if (w < 0 || w >= h->n)
+        sv_fail(SV_ERR_VALIDATION, "wire " + std::to_string(w) + " out of range for " + std::to_string(h->n) + "-qubit register");
+      u64 bit = 1ull << (h->n - 1 - w);
+      if ((r.xl | r.zl) & bit) sv_fail(SV_ERR_VALIDATION, "duplicate wire within Pauli word");
+      if (p == 'X') {
+        r.xl |= bit;
+        r.xw.push_back(w);
+      } else if (p == 'Y') {
+        r.xl |= bit;
+        r.zl |= bit;
+        r.ny++;
+        r.xw.push_back(w);
+      } else if (p == 'Z') {
+        r.zl |= bit;
+      } else if (p == 'I') {
+        r.zl |= 0;   // identity factor still reserves the wire for the duplicate check
+        r.xl |= 0;
+      } else {
+        sv_fail(SV_ERR_VALIDATION, std::string("unknown Pauli '") + p + "'");
+      }
+    }
+  }
+  // bring X/Y wires onto local bits (swaps permute every state sharing the layout)
+  if (h->world > 1) {
+    std::vector<int> xw;
+    for (auto& r : raw)
+      for (int w : r.xw) xw.push_back(w);
+    std::sort(xw.begin(), xw.end());
+    xw.erase(std::unique(xw.begin(), xw.end()), xw.end());
+    dist_make_local_set(h, states, xw);
+  }
+  std::map<u64, PauliGroup> groups;
+  const cplx ipow[4] = {cplx(1, 0), cplx(0, 1), cplx(-1, 0), cplx(0, -1)};
+  for (auto& r : raw) {
+    u64 xp = 0, zp = 0;
+    for (int o2 = 0; o2 < h->n; ++o2) {
+      int p = h->phys[o2];
+      if ((r.xl >> o2) & 1) xp |= 1ull << p;
+      if ((r.zl >> o2) & 1) zp |= 1ull << p;
+    }
+    cplx cc = r.c * ipow[r.ny & 3];
+    u64 local = (h->nl >= 64) ? ~0ull : ((1ull << h->nl) - 1);
+    if (zp & ~local) {
+      u64 zg = (zp & ~local) >> h->nl;
+      if (popcount64(zg & u64(h->rank)) & 1) cc = -cc;
+      zp &= local;
+    }
+    auto& g = groups[xp];
+    g.x = xp;
+    g.terms.push_back({zp, cc});
+  }
+  std::vector<PauliGroup> out;
+  for (auto& kv : groups) out.push_back(kv.second);
+  return out;
+}
+
+// <psi|O|psi> summed on the host in fixed group order (device partials are deterministic)
+static double expval_impl(sv_handle* h, const sv_obs& o) {
+  if (o.type == SV_OBS_DENSE) {
+    if (o.n_wires < 1 || !o.wires || !o.matrix) sv_fail(SV_ERR_VALIDATION, "malformed dense observable");
+    sv_op op{};
+    op.kind = SV_GATE_MATRIX;
+    op.n_wires = o.n_wires;
+    op.wires = o.wires;
+    op.matrix = o.matrix;
+    validate_op(op, h->n);
+    std::vector<int> tw(o.wires, o.wires + o.n_wires);
+    dist_make_local_set(h, {h->state}, tw);
+    std::vector<cplx> m(size_t(1) << (2 * o.n_wires));
+    for (size_t i = 0; i < m.size(); ++i) m[i] = cplx(o.matrix[2 * i], o.matrix[2 * i + 1]);
+    Prim g = make_dense_prim(tw, m, h->n, {}, {}, h->phys.data());
+    ensure_results(h, 2);
+    double z[2];
+    if (g.nb <= 4) {
+      braket_prim_async(h, h->state, h->state, g, h->d_results);
+      CUDA_CHECK(cudaMemcpyAsync(z, h->d_results, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+      CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    } else {
+      sv_fail(SV_ERR_UNSUPPORTED, "dense observables on more than 4 wires are not supported yet");
+    }
+    double v = z[0];
+    dist_allreduce_sum(h, &v, 1);
+    return v;
+  }
+  auto groups = pauli_groups(h, o, {h->state});
+  ensure_results(h, groups.size() + 1);
+  for (size_t gi = 0; gi < groups.size(); ++gi)
+    pauli_group_expval_async(h, h->state, groups[gi].x, groups[gi].terms, h->d_results + gi);
+  std::vector<double> vals(groups.size());
+  if (!groups.empty()) {
+    CUDA_CHECK(cudaMemcpyAsync(vals.data(), h->d_results, groups.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  }
+  dist_allreduce_sum(h, vals.data(), vals.size());
+  double s = 0.0;
+  for (double v : vals) s += v;
+  return s;
+}
+
+// lam = O psi (out of place), the lambda initialisation of the adjoint sweep
+static void apply_observable(sv_handle* h, const sv_obs& o, const double2* psi, double2* lam,
+                             const std::vector<double2*>& all_states) {
+  if (o.type == SV_OBS_DENSE) {
+    std::vector<int> tw(o.wires, o.wires + o.n_wires);
+    dist_make_local_set(h, all_states, tw);
+    std::vector<cplx> m(size_t(1) << (2 * o.n_wires));
+    for (size_t i = 0; i < m.size(); ++i) m[i] = cplx(o.matrix[2 * i], o.matrix[2 * i + 1]);
+    Prim g = make_dense_prim(tw, m, h->n, {}, {}, h->phys.data());
+    launch_copy(h, lam, psi, h->n_local);
+    launch_prim(h, lam, g);
+    return;
+  }
+  auto groups = pauli_groups(h, o, all_states);
+  if (groups.empty()) {
+    CUDA_CHECK(cudaMemsetAsync(lam, 0, h->n_local * sizeof(double2), h->stream));
+    return;
+  }
+  for (size_t gi = 0; gi < groups.size(); ++gi)
+    pauli_group_apply(h, psi, lam, groups[gi].x, groups[gi].terms, gi > 0);
+}
+
+static void free_aux(sv_handle* h) {
+  for (auto* p : h->aux) cudaFree(p);
+  h->aux.clear();
+}
+
+// ---------------------------------------------------------------------------
+// C-ABI
+// ---------------------------------------------------------------------------
+extern "C" {
+
+const char* sv_last_error(void) { return g_last_error.c_str(); }
+
+int sv_device_count(int* out) {
+  API_BEGIN
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    c = 0;
+  }
+  *out = c;
+  API_END
+}
+
+static void create_common(sv_handle* h, int n_qubits, int device) {
+  if (n_qubits < 1) sv_fail(SV_ERR_VALIDATION, "n_qubits must be a positive integer, got " + std::to_string(n_qubits));
+  if (n_qubits > 62) sv_fail(SV_ERR_CAPACITY, "n_qubits=" + std::to_string(n_qubits) + " exceeds the 62-qubit addressing limit");
+  h->n = n_qubits;
+  h->nl = n_qubits - h->g;
+  if (h->nl < 1) sv_fail(SV_ERR_VALIDATION, "too many shards for " + std::to_string(n_qubits) + " qubits");
+  h->n_local = 1ull << h->nl;
+  h->device = device;
+  h->phys.resize(n_qubits);
+  for (int o = 0; o < n_qubits; ++o) h->phys[o] = o;
+  CUDA_CHECK(cudaSetDevice(device));
+  size_t free_b = 0, total_b = 0;
+  CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+  const double need = double(h->n_local) * sizeof(double2);
+  if (h->nl >= 40 || need > double(free_b))
+    sv_fail(SV_ERR_CAPACITY, "cannot allocate 2**" + std::to_string(h->nl) + " amplitudes (" + std::to_string(need / 1e9) +
+                                 " GB) on device " + std::to_string(device) + " with " + std::to_string(free_b / 1e9) +
+                                 " GB free");
+  CUDA_CHECK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+  CUDA_CHECK(cudaMalloc(&h->state, h->n_local * sizeof(double2)));
+  launch_init_zero(h, h->state, 0, h->rank == 0);
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+}
+
+static void destroy_handle(sv_handle* h) {
+  if (!h) return;
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  free_aux(h);
+  release_scratch(h);
+  dist_destroy(h);
+  if (h->state) cudaFree(h->state);
+  if (h->d_partials) cudaFree(h->d_partials);
+  if (h->d_results) cudaFree(h->d_results);
+  if (h->h_pinned) cudaFreeHost(h->h_pinned);
+  for (auto& p : h->pending) {
+    cudaEventDestroy(p.start);
+    cudaEventDestroy(p.stop);
+  }
+  for (auto e : h->event_pool) cudaEventDestroy(e);
+  if (h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+int sv_create(int n_qubits, int device, sv_handle** out) {
+  sv_handle* h = nullptr;
+  API_BEGIN
+  if (!out) sv_fail(SV_ERR_VALIDATION, "null output handle");
+  *out = nullptr;
+  h = new sv_handle();
+  create_common(h, n_qubits, device);
+  *out = h;
+  h = nullptr;
+  API_END
+}
+
+int sv_nccl_unique_id(void* out128) {
+  API_BEGIN
+  ncclUniqueId id;
+  NCCL_CHECK(ncclGetUniqueId(&id));
+  std::memcpy(out128, &id, sizeof(id));
+  API_END
+}
+
+int sv_create_sharded(int n_qubits, int rank, int world, int device, const void* nccl_id, sv_handle** out) {
+  sv_handle* h = nullptr;
+  try {
+    if (!out) sv_fail(SV_ERR_VALIDATION, "null output handle");
+    *out = nullptr;
+    if (world < 1 || (world & (world - 1))) sv_fail(SV_ERR_VALIDATION, "n_shards must be a power of two");
+    if (rank < 0 || rank >= world) sv_fail(SV_ERR_VALIDATION, "rank out of range");
+    h = new sv_handle();
+    h->rank = rank;
+    h->world = world;
+    h->g = __builtin_ctz(unsigned(world));
+    create_common(h, n_qubits, device);
+    if (world > 1) dist_init(h, nccl_id);
+    *out = h;
+    return SV_OK;
+  } catch (const SvError& e) {
+    g_last_error = e.msg;
+    destroy_handle(h);
+    return e.status;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    destroy_handle(h);
+    return SV_ERR_DEVICE;
+  }
+}
+
+int sv_destroy(sv_handle* h) {
+  API_BEGIN
+  destroy_handle(h);
+  API_END
+}
+
+int sv_info(const sv_handle* h, int64_t* out6) {
+  API_BEGIN
+  check_handle(h);
+  out6[0] = h->n;
+  out6[1] = h->nl;
+  out6[2] = h->rank;
+  out6[3] = h->world;
+  out6[4] = h->device;
+  out6[5] = 0;
+  API_END
+}
+
+int sv_reset(sv_handle* h) {
+  API_BEGIN
+  check_handle(h);
+  std::lock_guard<std::mutex> lk(h->mu);
+  dist_reset_layout(h);
+  launch_init_zero(h, h->state, 0, h->rank == 0);
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+int sv_set_basis_state(sv_handle* h, uint64_t index) {
+  API_BEGIN
+  check_handle(h);
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->n < 64 && index >= (1ull << h->n)) sv_fail(SV_ERR_VALIDATION, "basis index out of range");
+  dist_reset_layout(h);
+  const u64 owner = index >> h->nl;
+  launch_init_zero(h, h->state, index & (h->n_local - 1), owner == u64(h->rank));
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+int sv_set_state(sv_handle* h, const double* amps, uint64_t n_amps) {
+  API_BEGIN
+  check_handle(h);
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (!amps) sv_fail(SV_ERR_VALIDATION, "null amplitude buffer");
+  if (n_amps != (1ull << h->n))
+    sv_fail(SV_ERR_VALIDATION, "amplitude array length " + std::to_string(n_amps) + " does not match 2**" + std::to_string(h->n));
+  dist_reset_layout(h);
+  const double* src = amps + 2 * (u64(h->rank) << h->nl);
+  CUDA_CHECK(cudaMemcpyAsync(h->state, src, h->n_local * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+int sv_get_state(sv_handle* h, double* out, uint64_t n_amps) {
+  API_BEGIN
+  check_handle(h);
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (!out) sv_fail(SV_ERR_VALIDATION, "null output buffer");
+  if (n_amps != (1ull << h->n))
+    sv_fail(SV_ERR_VALIDATION, "output length " + std::to_string(n_amps) + " does not match 2**" + std::to_string(h->n));
+  dist_canonicalize(h, {h->state});
+  if (h->world == 1) {
+    CUDA_CHECK(cudaMemcpyAsync(out, h->state, h->n_local * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  } else {
+    dist_gather_state(h, out);
+  }
+  API_END
+}
+
+int sv_norm(sv_handle* h, double* out) {
+  API_BEGIN
+  check_handle(h);
+  std::lock_guard<std::mutex> lk(h->mu);
+  double s = reduce_norm2(h, h->state);
+  dist_allreduce_sum(h, &s, 1);
+  *out = std::sqrt(s);
+  API_END
+}
+
+int sv_apply_ops(sv_handle* h, const sv_op* ops, int n_ops, int fuse) {
+  API_BEGIN
+  check_handle(h);
+  std::lock_guard<std::mutex> lk(h->mu);
+  validate_ops(h, ops, n_ops);
+  for (int i = 0; i < n_ops; ++i)
+    if (ops[i].trainable_mask) {
+      // trainable flags are irrelevant for plain application; validation already checked arity
+    }
+  run_ops(h, {h->state}, ops, n_ops, fuse);
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+int sv_apply_single_qubit(sv_handle* h, int q, const double* m2x2) {
+  API_BEGIN
+  check_handle(h);
+  if (q < 0 || q >= h->n)
+    sv_fail(SV_ERR_VALIDATION, "qubit " + std::to_string(q) + " out of range for " + std::to_string(h->n) + "-qubit register");
+  if (!m2x2) sv_fail(SV_ERR_VALIDATION, "null matrix");
+  sv_op op{};
+  op.kind = SV_GATE_MATRIX;
+  op.n_wires = 1;
+  op.wires = &q;
+  op.matrix = m2x2;
+  std::lock_guard<std::mutex> lk(h->mu);
+  run_ops(h, {h->state}, &op, 1, 0);
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+int sv_apply_controlled_single_qubit(sv_handle* h, const int32_t* ctrls, int n_ctrls, int q, const double* m2x2,
+                                     const int32_t* ctrl_values) {
+  API_BEGIN
+  check_handle(h);
+  if (q < 0 || q >= h->n)
+    sv_fail(SV_ERR_VALIDATION, "qubit " + std::to_string(q) + " out of range for " + std::to_string(h->n) + "-qubit register");
+  if (!m2x2) sv_fail(SV_ERR_VALIDATION, "null matrix");
+  sv_op op{};
+  op.kind = SV_GATE_CONTROLLED_MATRIX;
+  op.n_wires = 1;
+  op.wires = &q;
+  op.n_ctrls = n_ctrls;
+  op.ctrls = ctrls;
+  op.ctrl_values = ctrl_values;
+  op.matrix = m2x2;
+  validate_op(op, h->n);
+  std::lock_guard<std::mutex> lk(h->mu);
+  run_ops(h, {h->state}, &op, 1, 0);
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+int sv_apply_matrix(sv_handle* h, const int32_t* wires, int n_wires, const double* matrix) {
+  API_BEGIN
+  check_handle(h);
+  if (!matrix) sv_fail(SV_ERR_VALIDATION, "null matrix");
+  sv_op op{};
+  op.kind = SV_GATE_MATRIX;
+  op.n_wires = n_wires;
+  op.wires = wires;
+  op.matrix = matrix;
+  validate_op(op, h->n);
+  std::lock_guard<std::mutex> lk(h->mu);
+  run_ops(h, {h->state}, &op, 1, 0);
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+int sv_expval(sv_handle* h, const sv_obs* obs, double* out) {
+  API_BEGIN
+  check_handle(h);
+  if (!obs || !out) sv_fail(SV_ERR_VALIDATION, "null observable");
+  std::lock_guard<std::mutex> lk(h->mu);
+  *out = expval_impl(h, *obs);
+  API_END
+}
+
+int sv_probs(sv_handle* h, const int32_t* wires, int n_wires, double* out) {
+  API_BEGIN
+  check_handle(h);
+  std::lock_guard<std::mutex> lk(h->mu);
+  std::vector<int> w;
+  if (n_wires <= 0) {
+    for (int q = 0; q < h->n; ++q) w.push_back(q);
+  } else {
+    for (int i = 0; i < n_wires; ++i) {
+      if (wires[i] < 0 || wires[i] >= h->n)
+        sv_fail(SV_ERR_VALIDATION, "wire " + std::to_string(wires[i]) + " out of range for " + std::to_string(h->n) +
+                                       "-qubit register");
+      for (int j = 0; j < i; ++j)
+        if (wires[j] == wires[i]) sv_fail(SV_ERR_VALIDATION, "duplicate wires in probabilities");
+      w.push_back(wires[i]);
+    }
+  }
+  if (w.size() > 40) sv_fail(SV_ERR_CAPACITY, "probability vector too large");
+  dist_probs(h, w, out);
+  API_END
+}
+
+int sv_adjoint_jacobian(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs* obs, int n_obs, int fuse, double* jac,
+                        double* expvals) {
+  API_BEGIN
+  check_handle(h);
+  std::lock_guard<std::mutex> lk(h->mu);
+  validate_ops(h, ops, n_ops);
+  if (n_obs < 0 || (n_obs > 0 && !obs)) sv_fail(SV_ERR_VALIDATION, "bad observable list");
+  // lower once (logical layout) to learn columns and validate differentiability
+  int ncols = 0;
+  for (int i = 0; i < n_ops; ++i) lower_op(ops[i], h->n, ncols, true, nullptr);
+  // capacity: one lambda per observable
+  size_t free_b = 0, total_b = 0;
+  CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+  const double need = double(n_obs) * double(h->n_local) * sizeof(double2);
+  if (need > double(free_b))
+    sv_fail(SV_ERR_CAPACITY, "adjoint sweep needs " + std::to_string(n_obs) + " extra state copies (" +
+                                 std::to_string(need / 1e9) + " GB) but only " + std::to_string(free_b / 1e9) + " GB are free");
+  free_aux(h);
+  for (int k = 0; k < n_obs; ++k) {
+    double2* p = nullptr;
+    CUDA_CHECK(cudaMalloc(&p, h->n_local * sizeof(double2)));
+    h->aux.push_back(p);
+  }
+  std::vector<double2*> lam_states = h->aux;
+  std::vector<double2*> all = {h->state};
+  all.insert(all.end(), lam_states.begin(), lam_states.end());
+
+  // forward pass
+  run_ops(h, {h->state}, ops, n_ops, fuse);
+  // lambda_k = O_k psi ; expvals from Re<psi|lambda_k> via the expval kernels
+  std::vector<double> ev(n_obs, 0.0);
+  for (int k = 0; k < n_obs; ++k) ev[k] = expval_impl(h, obs[k]);
+  for (int k = 0; k < n_obs; ++k) apply_observable(h, obs[k], h->state, lam_states[k], all);
+
+  // reverse sweep
+  adjoint_sweep(h, ops, n_ops, lam_states, ncols, fuse, jac);
+  if (expvals)
+    for (int k = 0; k < n_obs; ++k) expvals[k] = ev[k];
+  free_aux(h);
+  API_END
+}
+
+int sv_synchronize(sv_handle* h) {
+  API_BEGIN
+  check_handle(h);
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+void* sv_stream(sv_handle* h) { return h ? (void*)h->stream : nullptr; }
+
+int64_t sv_launch_count(const sv_handle* h) { return h ? h->launches : -1; }
+
+int sv_set_profiling(sv_handle* h, int enabled) {
+  API_BEGIN
+  check_handle(h);
+  drain_timings(h);
+  h->profiling = enabled != 0;
+  API_END
+}
+
+int sv_kernel_stats(sv_handle* h, double* out, int max_classes, int* n_classes, char* names, int names_len) {
+  API_BEGIN
+  check_handle(h);
+  drain_timings(h);
+  int n = std::min<int>(max_classes, KC_COUNT);
+  for (int k = 0; k < n; ++k) {
+    out[3 * k + 0] = h->kc_launches[k];
+    out[3 * k + 1] = h->kc_ms[k];
+    out[3 * k + 2] = h->kc_bytes[k];
+  }
+  if (n_classes) *n_classes = n;
+  if (names && names_len > 0) {
+    std::string s;
+    for (int k = 0; k < KC_COUNT; ++k) s += std::string(kKernelClassNames[k]) + (k + 1 < KC_COUNT ? "," : "");
+    std::strncpy(names, s.c_str(), names_len - 1);
+    names[names_len - 1] = 0;
+  }
+  API_END
+}
+
+int sv_reset_stats(sv_handle* h) {
+  API_BEGIN
+  check_handle(h);
+  drain_timings(h);
+  for (int k = 0; k < KC_COUNT; ++k) h->kc_launches[k] = h->kc_ms[k] = h->kc_bytes[k] = 0;
+  API_END
+}
+
+int sv_plan_summary(int n_qubits, const sv_op* ops, int n_ops, int64_t* out4) {
+  API_BEGIN
+  if (n_qubits < 1 || n_qubits > 62) sv_fail(SV_ERR_VALIDATION, "bad qubit count");
+  std::vector<Prim> prims;
+  int col = 0;
+  for (int i = 0; i < n_ops; ++i) {
+    validate_op(ops[i], n_qubits);
+    for (auto& pc : lower_op(ops[i], n_qubits, col, false, nullptr))
+      if (!pc.fwd.skip) prims.push_back(pc.fwd);
+  }
+  PlanStats s = plan_stats(n_qubits, prims);
+  out4[0] = s.passes;
+  out4[1] = s.ops;
+  out4[2] = s.tile_bits;
+  out4[3] = s.phases;
+  API_END
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// adjoint reverse sweep (unfused reference schedule; the fused tile sweep lives in fused.cu)
+// ---------------------------------------------------------------------------
+void adjoint_sweep(sv_handle* h, const sv_op* ops, int n_ops, const std::vector<double2*>& lams, int ncols, int fuse,
+                   double* jac) {
+  const int n_obs = int(lams.size());
+  std::vector<double2*> all = {h->state};
+  all.insert(all.end(), lams.begin(), lams.end());
+  // complex <lambda_k|G|psi> per (column, obs) accumulated into d_results
+  ensure_results(h, size_t(ncols) * n_obs * 2 + 2);
+  std::vector<double> prefactor(ncols, 0.0);
+  // lower in forward order to know columns; then walk backwards
+  struct Rec {
+    int op;
+    Piece pc;
+  };
+  int col = 0;
+  std::vector<std::vector<Piece>> lowered(n_ops);
+  std::vector<int> col_start(n_ops);
+  for (int i = 0; i < n_ops; ++i) {
+    col_start[i] = col;
+    lowered[i] = lower_op(ops[i], h->n, col, true, nullptr);   // columns only; re-lowered with layout below
+  }
+  (void)fuse;
+  for (int i = n_ops - 1; i >= 0; --i) {
+    const sv_op& op = ops[i];
+    int c0 = col_start[i];
+    auto pieces = lower_op(op, h->n, c0, true, h->phys.data());
+    if (h->world > 1) {
+      bool need = false;
+      for (auto& pc : pieces) need |= prim_needs_swap(pc.inv, h->nl) || (pc.has_gen && prim_needs_swap(pc.gen.g, h->nl));
+      if (need) {
+        dist_make_local(h, all, std::vector<int>(op.wires, op.wires + op.n_wires));
+        c0 = col_start[i];
+        pieces = lower_op(op, h->n, c0, true, h->phys.data());
+      }
+    }
+    for (int pi = int(pieces.size()) - 1; pi >= 0; --pi) {
+      Piece& pc = pieces[pi];
+      if (pc.has_gen) {
+        Prim g = pc.gen.g;
+        resolve_global(g, h->nl, h->rank);
+        prefactor[pc.gen.column] = pc.gen.prefactor;
+        for (int k = 0; k < n_obs; ++k) {
+          double* dst = h->d_results + 2 * (size_t(pc.gen.column) * n_obs + k);
+          if (g.skip)
+            CUDA_CHECK(cudaMemsetAsync(dst, 0, 2 * sizeof(double), h->stream));
+          else
+            braket_prim_async(h, lams[k], h->state, g, dst);
+        }
+      }
+      Prim inv = pc.inv;
+      resolve_global(inv, h->nl, h->rank);
+      if (!inv.skip)
+        for (double2* st : all) launch_prim(h, st, inv);
+    }
+  }
+  std::vector<double> z(size_t(ncols) * n_obs * 2, 0.0);
+  if (!z.empty()) {
+    CUDA_CHECK(cudaMemcpyAsync(z.data(), h->d_results, z.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  }
+  dist_allreduce_sum(h, z.data(), z.size());
+  for (int k = 0; k < n_obs; ++k)
+    for (int c = 0; c < ncols; ++c) jac[size_t(k) * ncols + c] = -2.0 * prefactor[c] * z[2 * (size_t(c) * n_obs + k) + 1];
+}

@@ -1,0 +1,164 @@
+// Internal types shared by the host runtime and the sm_100a kernels of libsvb200.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <complex>
+#include <cstdint>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/svb200.h"
+
+typedef unsigned long long u64;
+using cplx = std::complex<double>;
+
+// ---------------------------------------------------------------------------
+// errors: thrown inside the library, converted to status codes at the C-ABI
+// ---------------------------------------------------------------------------
+struct SvError {
+  int status;
+  std::string msg;
+};
+[[noreturn]] void sv_fail(int status, const std::string& msg);
+void sv_cuda_check(cudaError_t e, const char* what);
+void sv_nccl_check(ncclResult_t r, const char* what);
+#define CUDA_CHECK(x) sv_cuda_check((x), #x)
+#define NCCL_CHECK(x) sv_nccl_check((x), #x)
+
+// ---------------------------------------------------------------------------
+// Primitive ops: what every gate lowers to, in PHYSICAL local bit positions.
+//   PAIR : 2x2 update of (a[i0], a[i0 ^ xmask]) for every i0 with (i0 & fmask) == fval.
+//          fmask contains the controls and the xmask bits (i0's pattern on them).
+//          Covers Alg. 1 / Alg. 2 (state.py:154-226), SWAP, IsingXY, Single/DoubleExcitation.
+//   DIAG : a[i] *= table[bits of i at pos[0..nb)] for every i with (i & fmask) == fval.
+//   DENSE: 2^k x 2^k matvec on target bits pos[0..k) (ascending; matrix index bit j <-> pos[j])
+//          for every group base with (base & fmask) == fval (fmask includes the targets).
+// ---------------------------------------------------------------------------
+enum PrimType { PRIM_PAIR = 0, PRIM_DIAG = 1, PRIM_DENSE = 2 };
+
+struct Prim {
+  int type = PRIM_PAIR;
+  u64 fmask = 0, fval = 0;
+  u64 xmask = 0;          // PAIR
+  int nb = 0;             // DIAG / DENSE: number of bits in pos
+  int pos[16] = {0};      // ascending physical positions
+  std::vector<cplx> m;    // PAIR: 4 (row-major), DIAG: 2^nb, DENSE: 4^nb (row-major)
+  bool skip = false;      // resolved to identity on this shard
+};
+
+// Generator record of a single-parameter piece for the adjoint sweep:
+// <lambda| G |psi> with G a DENSE-style small matrix on pos[] restricted by fmask/fval.
+struct GenPrim {
+  Prim g;                 // type PRIM_DENSE (k = nb) with m = generator matrix
+  double prefactor = 0;   // gate(theta) = exp(i prefactor theta G)
+  int column = -1;        // Jacobian column
+};
+
+// A lowered op: one or more prims (Rot -> 3 pieces) plus adjoint bookkeeping.
+struct Piece {
+  Prim fwd;               // the unitary U as a prim
+  Prim inv;               // U^dagger
+  bool has_gen = false;
+  GenPrim gen;
+};
+
+// ---------------------------------------------------------------------------
+// handle
+// ---------------------------------------------------------------------------
+enum KernelClass {
+  KC_PAIR = 0, KC_DIAG, KC_DENSE, KC_FUSED, KC_REDUCE, KC_APPLY_OBS, KC_BRAKET,
+  KC_PROBS, KC_INIT, KC_SWAP, KC_COUNT
+};
+extern const char* kKernelClassNames[KC_COUNT];
+
+struct PendingTiming {
+  int cls;
+  double bytes;
+  cudaEvent_t start, stop;
+};
+
+struct sv_handle {
+  int n = 0;          // total qubits
+  int nl = 0;         // local qubits
+  int rank = 0, world = 1, g = 0;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  double2* state = nullptr;     // 2^nl amplitudes
+  u64 n_local = 0;
+  // logical bit offset o = n-1-q  ->  physical position (>= nl: global/rank bit)
+  std::vector<int> phys;
+  ncclComm_t comm = nullptr;
+  double2* staging = nullptr;
+  u64 staging_amps = 0;
+  // reduction scratch
+  double* d_partials = nullptr;
+  size_t partials_cap = 0;      // doubles
+  double* d_results = nullptr;  // small result vector
+  size_t results_cap = 0;
+  double* h_pinned = nullptr;
+  size_t h_pinned_cap = 0;
+  std::vector<double2*> aux;    // lambda states for the adjoint sweep
+  std::mutex mu;
+  // stats
+  int64_t launches = 0;
+  bool profiling = false;
+  std::vector<PendingTiming> pending;
+  std::vector<cudaEvent_t> event_pool;
+  double kc_launches[KC_COUNT] = {0};
+  double kc_ms[KC_COUNT] = {0};
+  double kc_bytes[KC_COUNT] = {0};
+};
+
+// ---------------------------------------------------------------------------
+// host-side modules
+// ---------------------------------------------------------------------------
+// gates.cpp
+void validate_op(const sv_op& op, int n);
+// phys: logical offset (n-1-q) -> physical position (>= nl: shard-index bit); nullptr = identity
+std::vector<Piece> lower_op(const sv_op& op, int n, int& next_column, bool need_gen, const int* phys);
+Prim make_dense_prim(const std::vector<int>& wires, const std::vector<cplx>& m, int n,
+                     const std::vector<int>& ctrls, const std::vector<int>& cvals, const int* phys);
+void resolve_global(Prim& p, int nl, int rank);
+std::vector<cplx> gate_matrix(int kind, const double* params, int n_wires, const double* matrix);
+void classify_prim(Prim& p);   // DENSE -> DIAG / PAIR specialisations when exact
+Prim adjoint_prim(const Prim& p);
+
+
+// kernels.cu
+double prim_bytes(const sv_handle* h, const Prim& p);
+void release_scratch(sv_handle* h);
+void launch_prim(sv_handle* h, double2* state, const Prim& p);
+void launch_init_zero(sv_handle* h, double2* state, u64 basis_local, bool set_one);
+void launch_copy(sv_handle* h, double2* dst, const double2* src, u64 n);
+double reduce_norm2(sv_handle* h, const double2* state);
+// per-term Pauli expectation: terms sharing an x-mask; returns sum_t Re(cc_t * <P_t>) (local part)
+struct PauliTerm {
+  u64 zmask;
+  cplx cc;   // coefficient * i^{nY} * global-sign
+};
+void pauli_group_expval_async(sv_handle* h, const double2* state, u64 xmask, const std::vector<PauliTerm>& terms,
+                              double* d_out);
+void pauli_group_apply(sv_handle* h, const double2* psi, double2* lam, u64 xmask,
+                       const std::vector<PauliTerm>& terms, bool accumulate);
+// <bra| P_f (G) |ket> complex, written to d_out[0..1]
+void braket_prim_async(sv_handle* h, const double2* bra, const double2* ket, const Prim& g, double* d_out);
+void probs_async(sv_handle* h, const double2* state, const std::vector<int>& pos_msb_first, double* d_out);
+void sum_partials(sv_handle* h, const double* partials, int nblocks, int ncomp, double* d_out);
+
+// stats
+void stat_begin(sv_handle* h, int cls, double bytes, cudaEvent_t* ev_pair);
+void stat_end(sv_handle* h, int cls, double bytes, cudaEvent_t* ev_pair);
+void ensure_partials(sv_handle* h, size_t doubles);
+void ensure_results(sv_handle* h, size_t doubles);
+
+// fused tile engine (fused.cu / planner.cpp)
+void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& prims);
+struct PlanStats {
+  int64_t passes = 0, ops = 0, tile_bits = 0, phases = 0;
+};
+PlanStats plan_stats(int nl, const std::vector<Prim>& prims);
+
+inline int popcount64(u64 x) { return __builtin_popcountll(x); }

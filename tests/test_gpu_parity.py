@@ -1,0 +1,321 @@
+"""GPU parity: libsvb200 (through the C-ABI) vs the reference's golden vectors and the oracle.
+
+Tolerances (SURVEY.md §8(d) / SPEC.md:681-686): states |d| < 1e-12 elementwise; expvals and
+Jacobian entries |d| <= 1e-10 * max(|ref|, ||O||_1) with ||O||_1 = sum |c_t|.
+"""
+
+import ast
+
+import numpy as np
+import pytest
+
+from oracle import svoracle as O
+from paper_2403_02512_b200 import errors, workloads
+from paper_2403_02512_b200.device import Device
+from paper_2403_02512_b200.observables import DenseHermitian, Hamiltonian, PauliWord
+from paper_2403_02512_b200.ops import ARITY, Op
+from tests.golden_io import ADJ_JOBS, load, unpack_obs, unpack_ops
+
+pytestmark = pytest.mark.gpu
+
+STATE_TOL = 1e-12
+
+
+def obs_norm1(o):
+    if isinstance(o, Hamiltonian):
+        return sum(abs(c) for c in o.coeffs)
+    if isinstance(o, DenseHermitian):
+        return float(np.abs(np.linalg.eigvalsh(o.matrix)).max())
+    return 1.0
+
+
+def assert_grad_close(got, ref, obs):
+    for k, o in enumerate(obs):
+        scale = max(obs_norm1(o), float(np.abs(ref[k]).max()) if ref[k].size else 1.0)
+        assert np.abs(got[k] - ref[k]).max() <= 1e-10 * scale, (k, np.abs(got[k] - ref[k]).max())
+
+
+def rand_state(rng, n):
+    v = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    return v / np.linalg.norm(v)
+
+
+@pytest.fixture(scope="module")
+def sg():
+    return load("state_golden.npz")
+
+
+@pytest.fixture(scope="module")
+def cg():
+    return load("circuit_golden.npz")
+
+
+# ---- reference golden vectors through the reference-shaped API (state.py mirror) -----------
+
+def test_alg1_golden_via_state_api(sg):
+    from paper_2403_02512_b200 import state as S
+    for n, q, psi, m, out in zip(sg["alg1_n"], sg["alg1_q"], sg["alg1_in"], sg["alg1_m"], sg["alg1_out"]):
+        sv = S.StateVector.from_amplitudes(psi[: 1 << n])
+        S.apply_single_qubit(sv, int(q), S.CoefficientInteraction(m))
+        assert np.abs(sv.amplitudes - out[: 1 << n]).max() < STATE_TOL
+
+
+def test_alg2_golden_via_state_api(sg):
+    from paper_2403_02512_b200 import state as S
+    for i in range(len(sg["alg2_n"])):
+        n, q = int(sg["alg2_n"][i]), int(sg["alg2_q"][i])
+        ctrls = [int(c) for c in sg["alg2_ctrls"][i] if c >= 0]
+        vals = [int(v) for v in sg["alg2_vals"][i] if v >= 0]
+        sv = S.StateVector.from_amplitudes(sg["alg2_in"][i][: 1 << n])
+        S.apply_controlled_single_qubit(sv, ctrls, q, S.CoefficientInteraction(sg["alg2_m"][i]), vals)
+        assert np.abs(sv.amplitudes - sg["alg2_out"][i][: 1 << n]).max() < STATE_TOL
+
+
+def test_apply_matrix_golden_via_state_api(sg):
+    from paper_2403_02512_b200 import state as S
+    off = sg["mat_m_off"]
+    for i in range(len(sg["mat_n"])):
+        n = int(sg["mat_n"][i])
+        wires = [int(w) for w in sg["mat_wires"][i] if w >= 0]
+        d = 1 << len(wires)
+        m = sg["mat_m_flat"][off[i]:off[i + 1]].reshape(d, d)
+        sv = S.StateVector.from_amplitudes(sg["mat_in"][i][: 1 << n])
+        S.apply_matrix(sv, wires, m)
+        ref = sg["mat_out"][i][: 1 << n]
+        assert np.abs(sv.amplitudes - ref).max() < 1e-12 * max(1.0, np.abs(ref).max())
+
+
+def test_state_api_errors():
+    from paper_2403_02512_b200 import state as S
+    sv = S.zero_state(3)
+    with pytest.raises(errors.ValidationError):
+        S.apply_single_qubit(sv, 3, S.CoefficientInteraction(np.eye(2)))
+    with pytest.raises(errors.ValidationError):
+        S.apply_controlled_single_qubit(sv, [1, 1], 0, S.CoefficientInteraction(np.eye(2)))
+    with pytest.raises(errors.ValidationError):
+        S.apply_controlled_single_qubit(sv, [1], 1, S.CoefficientInteraction(np.eye(2)))
+    with pytest.raises(errors.ValidationError):
+        S.apply_matrix(sv, [0, 1], np.eye(2))
+    with pytest.raises(errors.UnsupportedOperationError):
+        S.apply_single_qubit(sv, 0, lambda a, i, j: None)
+    with pytest.raises(errors.ValidationError):
+        S.StateVector(0)
+    with pytest.raises(errors.CapacityError):
+        S.StateVector(63)
+    with pytest.raises(errors.CapacityError):
+        Device(45)
+
+
+@pytest.mark.parametrize("fuse", [False, True])
+@pytest.mark.parametrize("i", range(4))
+def test_named_gate_circuits_golden(cg, i, fuse):
+    n = int(cg[f"circ{i}_n"])
+    ops = unpack_ops(cg, f"circ{i}")
+    with Device(n) as d:
+        d.set_state(cg[f"circ{i}_in"])
+        d.apply(ops, fuse=fuse)
+        assert np.abs(d.get_state() - cg[f"circ{i}_out"]).max() < STATE_TOL
+
+
+@pytest.mark.parametrize("fuse", [False, True])
+@pytest.mark.parametrize("job", ADJ_JOBS)
+def test_adjoint_golden(cg, job, fuse):
+    n = int(cg[f"adj_{job}_n"])
+    ops = unpack_ops(cg, f"adj_{job}")
+    obs = unpack_obs(cg, f"adj_{job}")
+    with Device(n) as d:
+        jac, ev = d.adjoint_jacobian(ops, obs, return_expvals=True, fuse=fuse)
+    ref = cg[f"adj_{job}_jac"]
+    assert jac.shape == ref.shape
+    assert_grad_close(jac, ref, obs)
+    ref_ev = cg[f"adj_{job}_expvals"]
+    for k, o in enumerate(obs):
+        assert abs(ev[k] - ref_ev[k]) <= 1e-10 * max(obs_norm1(o), abs(ref_ev[k]))
+
+
+@pytest.mark.parametrize("job", ADJ_JOBS)
+def test_probs_golden(cg, job):
+    n = int(cg[f"adj_{job}_n"])
+    if f"adj_{job}_probs_all" not in cg.files:
+        pytest.skip("no probs recorded")
+    ops = unpack_ops(cg, f"adj_{job}")
+    with Device(n) as d:
+        d.apply(ops)
+        assert np.abs(d.probs() - cg[f"adj_{job}_probs_all"]).max() < 1e-13
+        assert np.abs(d.probs([n - 1, 0]) - cg[f"adj_{job}_probs_w"]).max() < 1e-13
+
+
+def test_sel20_config1_golden():
+    try:
+        g = load("sel20_golden.npz")
+    except FileNotFoundError:
+        pytest.skip("sel20 golden not generated")
+    ops, obs = workloads.sel_config(20, 4, seed=0)
+    with Device(20) as d:
+        jac, ev = d.adjoint_jacobian(ops, obs, return_expvals=True)
+    assert_grad_close(jac, g["jac"], obs)
+    assert np.abs(ev - g["expvals"]).max() < 1e-10
+
+
+# ---- SPEC known-answer tests through the device ------------------------------------------
+
+def test_kats_device():
+    with Device(1) as d:
+        assert np.allclose(d.get_state(), [1, 0])
+        d.apply([Op("X", (0,))])
+        assert np.allclose(d.get_state(), [0, 1])
+    with Device(2) as d:
+        d.apply([Op("H", (1,))])
+        assert np.allclose(d.get_state(), [2 ** -0.5, 2 ** -0.5, 0, 0])
+    with Device(2) as d:
+        d.set_basis_state(2)
+        d.apply([Op("CNOT", (0, 1))])
+        assert np.allclose(d.get_state(), [0, 0, 0, 1])
+    with Device(2) as d:
+        d.apply([Op("IsingXX", (0, 1), (np.pi,))])
+        assert np.allclose(d.get_state(), [0, 0, 0, -1j])
+    with Device(1) as d:
+        d.apply([Op("H", (0,))])
+        assert abs(d.expval(PauliWord(((0, "X"),))) - 1) < 1e-12
+        assert np.allclose(d.probs(), [0.5, 0.5])
+    with Device(2) as d:
+        d.set_basis_state(1)
+        h = Hamiltonian([0.5, 0.5], [PauliWord(((0, "Z"),)), PauliWord(((1, "Z"),))])
+        assert abs(d.expval(h)) < 1e-12
+    with Device(1) as d:
+        jac = d.adjoint_jacobian([Op("RX", (0,), (np.pi / 2,), trainable=(True,))], [PauliWord(((0, "Z"),))])
+        assert abs(jac[0, 0] + 1) < 1e-12
+
+
+# ---- oracle sweeps: every kind, every target, random controls -------------------------------
+
+KINDS = [k for k in ARITY if k not in ("Matrix", "ControlledMatrix")]
+
+
+def random_op(rng, n, kind=None):
+    kind = kind or KINDS[int(rng.integers(len(KINDS)))]
+    nw, npar = ARITY[kind]
+    if kind in ("Matrix", "ControlledMatrix"):
+        nw = int(rng.integers(1, 4))
+    nc = int(rng.integers(0, min(2, n - nw) + 1)) if rng.random() < 0.3 else 0
+    qs = rng.choice(n, size=nw + nc, replace=False)
+    m = None
+    if kind in ("Matrix", "ControlledMatrix"):
+        z = rng.normal(size=(1 << nw, 1 << nw)) + 1j * rng.normal(size=(1 << nw, 1 << nw))
+        m = np.linalg.qr(z)[0]
+    return Op(kind, tuple(int(q) for q in qs[:nw]), tuple(rng.uniform(-np.pi, np.pi, size=npar)),
+              ctrls=tuple(int(q) for q in qs[nw:]), ctrl_values=tuple(int(v) for v in rng.integers(0, 2, size=nc)),
+              inverse=bool(rng.random() < 0.2), matrix=m)
+
+
+@pytest.mark.parametrize("kind", KINDS + ["Matrix", "ControlledMatrix"])
+def test_every_kind_every_target(kind):
+    rng = np.random.default_rng(sum(map(ord, kind)))
+    n = 9
+    psi = rand_state(rng, n)
+    nw = ARITY[kind][0] or 2
+    for t in range(n - nw + 1 if nw > 1 else n):
+        op = random_op(rng, n, kind)
+        if nw == 1:
+            op.wires = (t,)
+            op.ctrls = tuple(c for c in op.ctrls if c != t)
+            op.ctrl_values = op.ctrl_values[: len(op.ctrls)]
+        ref = psi.copy()
+        O.apply_op(ref, n, op)
+        for fuse in (False, True):
+            with Device(n) as d:
+                d.set_state(psi)
+                d.apply([op], fuse=fuse)
+                assert np.abs(d.get_state() - ref).max() < STATE_TOL, (op, fuse)
+
+
+@pytest.mark.parametrize("n", [6, 11, 16, 20])
+def test_random_circuits_vs_oracle(n):
+    rng = np.random.default_rng(n)
+    ops = [random_op(rng, n) for _ in range(120)]
+    psi = rand_state(rng, n)
+    ref = O.run_circuit(n, ops, psi)
+    for fuse in (False, True):
+        with Device(n) as d:
+            d.set_state(psi)
+            d.apply(ops, fuse=fuse)
+            assert np.abs(d.get_state() - ref).max() < 1e-11
+
+
+def test_every_ordered_pair_cnot():
+    n = 7
+    rng = np.random.default_rng(5)
+    psi = rand_state(rng, n)
+    for c in range(n):
+        for t in range(n):
+            if c == t:
+                continue
+            ref = psi.copy()
+            O.apply_op(ref, n, Op("CNOT", (c, t)))
+            with Device(n) as d:
+                d.set_state(psi)
+                d.apply([Op("CNOT", (c, t))])
+                assert np.abs(d.get_state() - ref).max() < STATE_TOL
+
+
+def test_measurements_vs_oracle():
+    rng = np.random.default_rng(11)
+    n = 10
+    psi = rand_state(rng, n)
+    ham = workloads.random_pauli_hamiltonian(n, 40, seed=3)
+    dense = rng.normal(size=(8, 8)) + 1j * rng.normal(size=(8, 8))
+    dense = DenseHermitian((7, 2, 4), dense + dense.conj().T)
+    with Device(n) as d:
+        d.set_state(psi)
+        assert abs(d.expval(ham) - O.expval(psi, n, ham)) < 1e-12 * max(1, obs_norm1(ham))
+        assert abs(d.expval(dense) - O.expval(psi, n, dense)) < 1e-11
+        for t in ham.terms[:10]:
+            assert abs(d.expval(t) - O.expval(psi, n, t)) < 1e-12
+        assert abs(d.norm() - 1) < 1e-13
+        for wires in ([0], [9], [3, 1], [9, 0, 4], list(range(n)), [5, 6, 7, 8, 9, 0, 1]):
+            assert np.abs(d.probs(wires) - O.probabilities(psi, n, wires)).max() < 1e-14
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_adjoint_vs_oracle_random(seed):
+    rng = np.random.default_rng(100 + seed)
+    n = 6
+    kinds = ["RX", "RY", "RZ", "Phase", "Rot", "IsingXX", "IsingXY", "IsingYY", "IsingZZ",
+             "SingleExcitation", "DoubleExcitation", "CNOT", "H", "CZ", "SWAP", "T"]
+    ops = []
+    for _ in range(30):
+        op = random_op(rng, n, kinds[int(rng.integers(len(kinds)))])
+        if ARITY[op.name][1]:
+            op.trainable = tuple(bool(x) for x in rng.integers(0, 2, size=ARITY[op.name][1]))
+        ops.append(op)
+    obs = [PauliWord(((0, "Z"), (3, "X"))), workloads.random_pauli_hamiltonian(n, 12, seed=seed),
+           DenseHermitian((4, 1), np.diag([1.0, -2.0, 0.5, 3.0]).astype(complex))]
+    ref, ref_ev = O.adjoint_jacobian(n, ops, obs)
+    for fuse in (False, True):
+        with Device(n) as d:
+            jac, ev = d.adjoint_jacobian(ops, obs, return_expvals=True, fuse=fuse)
+        assert_grad_close(jac, ref, obs)
+
+
+# ---- large-n size-independent properties --------------------------------------------------
+
+def test_large_n_inverse_roundtrip_and_norm():
+    n = 26
+    ops = workloads.random_circuit(n, 4, seed=1)
+    inv = [Op(o.name, o.wires, o.params, o.ctrls, o.ctrl_values, (), not o.inverse) for o in reversed(ops)]
+    with Device(n) as d:
+        d.apply(ops)
+        assert abs(d.norm() - 1) < 1e-12
+        d.apply(inv)
+        st = d.get_state()
+    assert abs(st[0] - 1) < 1e-12
+    assert np.abs(st[1:]).max() < 1e-12
+
+
+def test_fused_equals_unfused_mid_size():
+    n = 22
+    ops = workloads.random_circuit(n, 8, seed=4)
+    with Device(n) as a, Device(n) as b:
+        a.apply(ops, fuse=False)
+        b.apply(ops, fuse=True)
+        assert np.abs(a.get_state() - b.get_state()).max() < 1e-12
