@@ -373,6 +373,7 @@ static void destroy_handle(sv_handle* h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_aux(h);
   release_scratch(h);
+  release_fused(h);
   dist_destroy(h);
   if (h->state) cudaFree(h->state);
   if (h->d_partials) cudaFree(h->d_partials);

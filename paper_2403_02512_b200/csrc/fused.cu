@@ -1,15 +1,649 @@
-// Gate fusion engine (K7).  First slice: every primitive is its own HBM pass; the
-// shared-memory / register tile engine replaces this file's body.
+// K7: gate-fusion tile engine.
+//
+// One "pass" streams the whole shard through shared memory once: each CTA stages a tile of
+// 2^b amplitudes (b <= 12, 64 KiB) whose index bits are the pass's tile bits B (always the
+// three lowest physical bits -> 128-byte contiguous runs, plus any high bits the pass's gates
+// need), applies a whole list of gates to the tile, and writes it back: a run of G gates costs
+// one HBM read + write of the state instead of G (north_star: "a gate-fusion kernel stages
+// 2^k-amplitude blocks in shared memory so runs of low-qubit gates take one HBM pass").
+//
+// Inside a tile, work proceeds in "phases": every thread holds 16 amplitudes in registers,
+// indexed by 4 register bits R (tile positions); dense targets of the phase's gates must be in
+// R, while controls and diagonal gates may sit on ANY bit (register, thread or tile-outer bit:
+// they are predicates / per-thread constants).  Switching R costs one shared-memory round trip.
+// Shared memory is XOR-swizzled so every phase's 16-byte accesses are bank-conflict free.
+//
+// The host planner (bottom of this file) greedily builds passes over the dependency order of
+// the primitive list (prims only move past prims they commute with: disjoint support, or both
+// diagonal) and splits each pass into phases.
+#include <algorithm>
+#include <cstring>
+
 #include "sv_internal.h"
 
+namespace {
+
+constexpr int kMaxB = 12;        // tile bits (2^12 amps = 64 KiB)
+constexpr int kRB = 4;           // register bits per thread (16 amplitudes)
+constexpr int kRegs = 1 << kRB;
+
+enum FKind : uint8_t { FK_PAIR = 0, FK_DIAG = 1, FK_DENSE2 = 2 };
+enum MType : uint8_t { MT_GENERAL = 0, MT_REAL = 1, MT_RXLIKE = 2, MT_X = 3 };
+
+struct FOp {
+  u64 pm, pv;            // fixed pattern on non-register bits (tested on the thread's physical base)
+  uint8_t kind, mtype;
+  uint8_t xr;            // PAIR: register-space xmask; DENSE2: k0 | (k1 << 4), k0 < k1
+  uint8_t cm, cv;        // fixed pattern in register space (PAIR: includes i0's pattern on xr)
+  uint8_t nt;            // DIAG: table bits
+  uint8_t treg[6];       // DIAG: register bit of table bit j, or 0xFF
+  uint8_t tphys[6];      // DIAG: physical position of table bit j when not a register bit
+  int tab;               // offset into the coefficient array
+};
+
+struct FPhase {
+  uint8_t reg[kRB];      // tile positions held in registers
+  uint8_t thr[kMaxB];    // tile positions of thread-index bits (b - 4 of them; lanes 0..2 first)
+  int op_begin, op_end;
+};
+
+struct FPassArgs {
+  int b;                 // tile bits
+  int nthr;              // b - kRB
+  unsigned char tpos[kMaxB];   // physical positions of tile bits (ascending)
+  int n_outer_ins;       // == b; positions to insert when enumerating tiles
+  u64 n_tiles;
+  int phase_begin, n_phases;
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+
+__device__ __forceinline__ int swz(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
+
+// ---- 2x2 pair update on registers (i0 = r, i1 = r ^ XR) ------------------------------------
+template <int XR>
+__device__ __forceinline__ void pair_op(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef) {
+  const int cm = op.cm, cv = op.cv;
+  if (op.mtype == MT_X) {
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r) {
+      if ((r & cm) == cv) {
+        const double2 t = a[r];
+        a[r] = a[r ^ XR];
+        a[r ^ XR] = t;
+      }
+    }
+    return;
+  }
+  const double2 m0 = coef[op.tab], m1 = coef[op.tab + 1], m2 = coef[op.tab + 2], m3 = coef[op.tab + 3];
+  if (op.mtype == MT_REAL) {
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r)
+      if ((r & cm) == cv) {
+        const double2 x = a[r], y = a[r ^ XR];
+        a[r] = make_double2(fma(m0.x, x.x, m1.x * y.x), fma(m0.x, x.y, m1.x * y.y));
+        a[r ^ XR] = make_double2(fma(m2.x, x.x, m3.x * y.x), fma(m2.x, x.y, m3.x * y.y));
+      }
+  } else if (op.mtype == MT_RXLIKE) {
+    // m0, m3 real; m1, m2 imaginary:  (i b) * (x + i y) = -b y + i b x
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r)
+      if ((r & cm) == cv) {
+        const double2 x = a[r], y = a[r ^ XR];
+        a[r] = make_double2(fma(m0.x, x.x, -m1.y * y.y), fma(m0.x, x.y, m1.y * y.x));
+        a[r ^ XR] = make_double2(fma(m3.x, y.x, -m2.y * x.y), fma(m3.x, y.y, m2.y * x.x));
+      }
+  } else {
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r)
+      if ((r & cm) == cv) {
+        const double2 x = a[r], y = a[r ^ XR];
+        a[r] = cfma(m0, x, cmul(m1, y));
+        a[r ^ XR] = cfma(m2, x, cmul(m3, y));
+      }
+  }
+}
+
+template <int K0, int K1>
+__device__ __forceinline__ void dense2_op(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef) {
+  const int cm = op.cm, cv = op.cv;
+  constexpr int B0 = 1 << K0, B1 = 1 << K1;
+  const double2* __restrict__ M = coef + op.tab;   // uniform L1-cached reads; keeps registers for a[]
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if ((r & (B0 | B1)) != 0) continue;
+    if ((r & cm) != cv) continue;
+    const int idx[4] = {r, r | B0, r | B1, r | B0 | B1};   // matrix index bit 0 <-> K0, bit 1 <-> K1
+    double2 v[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) v[c] = a[idx[c]];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc = cfma(M[q * 4 + c], v[c], acc);
+      a[idx[q]] = acc;
+    }
+  }
+}
+
+__device__ __forceinline__ void diag_op(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef,
+                                        u64 phys_base) {
+  // table index = tconst | sum_k bit_k(r) * w[k]
+  int tconst = 0;
+  int w[kRB] = {0, 0, 0, 0};
+  for (int j = 0; j < op.nt; ++j) {
+    const int rg = op.treg[j];
+    if (rg == 0xFF)
+      tconst |= int((phys_base >> op.tphys[j]) & 1ull) << j;
+    else
+      w[rg] |= 1 << j;
+  }
+  const int cm = op.cm, cv = op.cv;
+  if (op.nt == 0) {
+    const double2 d = coef[op.tab];
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r)
+      if ((r & cm) == cv) a[r] = cmul(d, a[r]);
+    return;
+  }
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if ((r & cm) != cv) continue;
+    int t = tconst;
+#pragma unroll
+    for (int k = 0; k < kRB; ++k)
+      if ((r >> k) & 1) t |= w[k];
+    a[r] = cmul(coef[op.tab + t], a[r]);
+  }
+}
+
+__device__ __forceinline__ void apply_pair_dispatch(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef) {
+  switch (op.xr) {
+    case 1: pair_op<1>(a, op, coef); break;
+    case 2: pair_op<2>(a, op, coef); break;
+    case 3: pair_op<3>(a, op, coef); break;
+    case 4: pair_op<4>(a, op, coef); break;
+    case 5: pair_op<5>(a, op, coef); break;
+    case 6: pair_op<6>(a, op, coef); break;
+    case 7: pair_op<7>(a, op, coef); break;
+    case 8: pair_op<8>(a, op, coef); break;
+    case 9: pair_op<9>(a, op, coef); break;
+    case 10: pair_op<10>(a, op, coef); break;
+    case 11: pair_op<11>(a, op, coef); break;
+    case 12: pair_op<12>(a, op, coef); break;
+    case 13: pair_op<13>(a, op, coef); break;
+    case 14: pair_op<14>(a, op, coef); break;
+    case 15: pair_op<15>(a, op, coef); break;
+    default: break;
+  }
+}
+
+__device__ __forceinline__ void apply_dense2_dispatch(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef) {
+  switch (op.xr) {
+    case 0x10: dense2_op<0, 1>(a, op, coef); break;
+    case 0x20: dense2_op<0, 2>(a, op, coef); break;
+    case 0x30: dense2_op<0, 3>(a, op, coef); break;
+    case 0x21: dense2_op<1, 2>(a, op, coef); break;
+    case 0x31: dense2_op<1, 3>(a, op, coef); break;
+    case 0x32: dense2_op<2, 3>(a, op, coef); break;
+    default: break;
+  }
+}
+
+__global__ void __launch_bounds__(256, 2) k_fused(double2* __restrict__ state, const FPassArgs P,
+                                                   const FPhase* __restrict__ phases, const FOp* __restrict__ ops,
+                                                   const double2* __restrict__ coef) {
+  extern __shared__ double2 tile[];
+  const int tid = threadIdx.x;
+  const int nthreads = blockDim.x;            // 2^(b-4)
+  const int T = 1 << P.b;
+  // physical offset of this thread's load slots: s = tid + nthreads * i
+  u64 spread_tid = 0;
+  for (int j = 0; j < P.nthr; ++j)
+    if ((tid >> j) & 1) spread_tid |= 1ull << P.tpos[j];
+  // load slot i of a thread covers tile bits nthr..nthr+3 -> physical bits hb[0..3]
+  u64 hb[kRB];
+#pragma unroll
+  for (int j = 0; j < kRB; ++j) hb[j] = 1ull << P.tpos[P.nthr + j];
+#define SPREAD_HI(i) ((((i) & 1) ? hb[0] : 0ull) | (((i) & 2) ? hb[1] : 0ull) | (((i) & 4) ? hb[2] : 0ull) | \
+                      (((i) & 8) ? hb[3] : 0ull))
+  for (u64 t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+    // tile base: insert zero bits at the tile positions
+    u64 base = t;
+    for (int j = 0; j < P.b; ++j) {
+      const int p = P.tpos[j];
+      const u64 lo = base & ((1ull << p) - 1ull);
+      base = ((base ^ lo) << 1) | lo;
+    }
+    // global -> shared (cp.async, 16 B per amplitude, conflict-free through the swizzle)
+#pragma unroll
+    for (int i = 0; i < kRegs; ++i) {
+      const int s = tid + nthreads * i;
+      const double2* src = state + (base | spread_tid | SPREAD_HI(i));
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(&tile[swz(s)]);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+    for (int ph = 0; ph < P.n_phases; ++ph) {
+      const FPhase& F = phases[P.phase_begin + ph];
+      int sthr = 0;
+      u64 phys_base = base;
+      for (int j = 0; j < P.nthr; ++j)
+        if ((tid >> j) & 1) {
+          sthr |= 1 << F.thr[j];
+          phys_base |= 1ull << P.tpos[F.thr[j]];
+        }
+      int w[kRB];
+#pragma unroll
+      for (int k = 0; k < kRB; ++k) w[k] = 1 << F.reg[k];
+      double2 a[kRegs];
+#pragma unroll
+      for (int r = 0; r < kRegs; ++r) {
+        int s = sthr;
+#pragma unroll
+        for (int k = 0; k < kRB; ++k)
+          if ((r >> k) & 1) s |= w[k];
+        a[r] = tile[swz(s)];
+      }
+      for (int oi = F.op_begin; oi < F.op_end; ++oi) {
+        const FOp op = ops[oi];
+        if ((phys_base & op.pm) != op.pv) continue;
+        if (op.kind == FK_PAIR)
+          apply_pair_dispatch(a, op, coef);
+        else if (op.kind == FK_DIAG)
+          diag_op(a, op, coef, phys_base);
+        else
+          apply_dense2_dispatch(a, op, coef);
+      }
+#pragma unroll
+      for (int r = 0; r < kRegs; ++r) {
+        int s = sthr;
+#pragma unroll
+        for (int k = 0; k < kRB; ++k)
+          if ((r >> k) & 1) s |= w[k];
+        tile[swz(s)] = a[r];
+      }
+      __syncthreads();
+    }
+    // shared -> global
+#pragma unroll
+    for (int i = 0; i < kRegs; ++i) {
+      const int s = tid + nthreads * i;
+      state[base | spread_tid | SPREAD_HI(i)] = tile[swz(s)];
+    }
+    __syncthreads();
+  }
+  (void)T;
+}
+
+// ===========================================================================
+// host planner
+// ===========================================================================
+struct Req {
+  u64 dense = 0;     // bits that must be register bits
+  u64 support = 0;   // every bit the prim reads
+  bool diag = false;
+  bool fusable = true;
+};
+
+Req requirements(const Prim& p) {
+  Req r;
+  if (p.type == PRIM_PAIR) {
+    r.dense = p.xmask;
+    r.support = p.fmask | p.xmask;
+    r.fusable = popcount64(p.xmask) <= kRB;
+  } else if (p.type == PRIM_DIAG) {
+    r.diag = true;
+    r.support = p.fmask;
+    for (int j = 0; j < p.nb; ++j) r.support |= 1ull << p.pos[j];
+    r.fusable = p.nb <= 6;
+  } else {
+    for (int j = 0; j < p.nb; ++j) r.dense |= 1ull << p.pos[j];
+    r.support = p.fmask | r.dense;
+    r.fusable = p.nb <= 2;
+  }
+  return r;
+}
+
+struct PassPlan {
+  bool fused = false;
+  int single = -1;            // prim index when not fused
+  u64 tile_bits = 0;
+  std::vector<int> prims;     // in application order
+};
+
+std::vector<PassPlan> plan_passes(int nl, const std::vector<Prim>& prims, int b) {
+  std::vector<Req> req(prims.size());
+  for (size_t i = 0; i < prims.size(); ++i) req[i] = requirements(prims[i]);
+  std::vector<int> remaining(prims.size());
+  for (size_t i = 0; i < prims.size(); ++i) remaining[i] = int(i);
+  std::vector<PassPlan> out;
+  const u64 low = (1ull << std::min(3, nl)) - 1;
+  const size_t window = 4096;
+  while (!remaining.empty()) {
+    const int p0 = remaining[0];
+    if (!req[p0].fusable || nl < 5) {
+      PassPlan s;
+      s.single = p0;
+      out.push_back(s);
+      remaining.erase(remaining.begin());
+      continue;
+    }
+    PassPlan pp;
+    pp.fused = true;
+    u64 B = low;
+    u64 def_nd = 0, def_d = 0;
+    std::vector<int> rest;
+    for (size_t k = 0; k < remaining.size(); ++k) {
+      const int i = remaining[k];
+      const Req& r = req[i];
+      bool ok = k < window && r.fusable;
+      if (ok) {
+        const u64 blocked = r.diag ? (r.support & def_nd) : (r.support & (def_nd | def_d));
+        ok = blocked == 0 && popcount64(B | r.dense) <= b;
+      }
+      if (ok) {
+        B |= r.dense;
+        pp.prims.push_back(i);
+      } else {
+        if (r.diag)
+          def_d |= r.support;
+        else
+          def_nd |= r.support;
+        rest.push_back(i);
+      }
+    }
+    // fill the tile up to b bits with the lowest unused positions (longer contiguous runs)
+    for (int p = 0; p < nl && popcount64(B) < b; ++p) B |= 1ull << p;
+    pp.tile_bits = B;
+    out.push_back(pp);
+    remaining.swap(rest);
+  }
+  return out;
+}
+
+int mtype_of(const std::vector<cplx>& m) {
+  auto re = [](cplx c) { return c.imag() == 0.0; };
+  auto im = [](cplx c) { return c.real() == 0.0; };
+  if (m[0] == 0.0 && m[3] == 0.0 && m[1] == 1.0 && m[2] == 1.0) return MT_X;
+  if (re(m[0]) && re(m[1]) && re(m[2]) && re(m[3])) return MT_REAL;
+  if (re(m[0]) && re(m[3]) && im(m[1]) && im(m[2])) return MT_RXLIKE;
+  return MT_GENERAL;
+}
+
+struct Program {
+  std::vector<FPassArgs> passes;
+  std::vector<int> pass_of;        // for singles: -1
+  std::vector<FPhase> phases;
+  std::vector<FOp> ops;
+  std::vector<double2> coef;
+};
+
+// choose extra register positions so each bank class {p mod 3} keeps a free thread position
+void fill_regs(std::vector<int>& reg, int b) {
+  auto cls_free = [&](int c, const std::vector<int>& R) {
+    for (int p = c; p < b; p += 3)
+      if (std::find(R.begin(), R.end(), p) == R.end()) return true;
+    return false;
+  };
+  for (int p = b - 1; p >= 0 && int(reg.size()) < kRB; --p) {
+    if (std::find(reg.begin(), reg.end(), p) != reg.end()) continue;
+    std::vector<int> trial = reg;
+    trial.push_back(p);
+    if (cls_free(0, trial) && cls_free(1, trial) && cls_free(2, trial)) reg = trial;
+  }
+  for (int p = b - 1; p >= 0 && int(reg.size()) < kRB; --p)
+    if (std::find(reg.begin(), reg.end(), p) == reg.end()) reg.push_back(p);
+}
+
+void make_phase_thr(FPhase& F, const std::vector<int>& reg, int b) {
+  for (int k = 0; k < kRB; ++k) F.reg[k] = (uint8_t)reg[k];
+  std::vector<int> thr;
+  for (int c = 0; c < 3; ++c)
+    for (int p = c; p < b; p += 3)
+      if (std::find(reg.begin(), reg.end(), p) == reg.end()) {
+        thr.push_back(p);
+        break;
+      }
+  for (int p = 0; p < b; ++p)
+    if (std::find(reg.begin(), reg.end(), p) == reg.end() && std::find(thr.begin(), thr.end(), p) == thr.end())
+      thr.push_back(p);
+  for (int j = 0; j < b - kRB; ++j) F.thr[j] = (uint8_t)thr[j];
+}
+
+// emit the device ops of one phase
+void emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<int>& list, const int* tile_pos_of,
+              const std::vector<int>& reg) {
+  // phys bit -> register index (or -1)
+  auto reg_of_phys = [&](int phys) -> int {
+    int tp = tile_pos_of[phys];
+    if (tp < 0) return -1;
+    for (int k = 0; k < kRB; ++k)
+      if (reg[k] == tp) return k;
+    return -1;
+  };
+  for (int i : list) {
+    const Prim& p = prims[i];
+    FOp op;
+    std::memset(&op, 0, sizeof(op));
+    // split the fixed pattern into register / non-register parts
+    u64 fm = p.fmask;
+    for (int bpos = 0; bpos < 64 && fm; ++bpos) {
+      if (!((fm >> bpos) & 1)) continue;
+      fm &= ~(1ull << bpos);
+      const int k = reg_of_phys(bpos);
+      const int v = int((p.fval >> bpos) & 1);
+      if (k >= 0) {
+        op.cm |= uint8_t(1 << k);
+        if (v) op.cv |= uint8_t(1 << k);
+      } else {
+        op.pm |= 1ull << bpos;
+        if (v) op.pv |= 1ull << bpos;
+      }
+    }
+    op.tab = int(prog.coef.size());
+    if (p.type == PRIM_PAIR) {
+      op.kind = FK_PAIR;
+      for (int bpos = 0; bpos < 64; ++bpos)
+        if ((p.xmask >> bpos) & 1) op.xr |= uint8_t(1 << reg_of_phys(bpos));
+      op.mtype = uint8_t(mtype_of(p.m));
+      for (int j = 0; j < 4; ++j) prog.coef.push_back(make_double2(p.m[j].real(), p.m[j].imag()));
+    } else if (p.type == PRIM_DIAG) {
+      op.kind = FK_DIAG;
+      op.nt = uint8_t(p.nb);
+      for (int j = 0; j < p.nb; ++j) {
+        const int k = reg_of_phys(p.pos[j]);
+        op.treg[j] = k >= 0 ? uint8_t(k) : uint8_t(0xFF);
+        op.tphys[j] = uint8_t(p.pos[j]);
+      }
+      for (auto& c : p.m) prog.coef.push_back(make_double2(c.real(), c.imag()));
+    } else {
+      op.kind = FK_DENSE2;
+      int k0 = reg_of_phys(p.pos[0]), k1 = reg_of_phys(p.pos[1]);
+      // matrix index bit 0 <-> pos[0] (ascending physical); kernel wants bit 0 <-> lower register index
+      std::vector<cplx> m = p.m;
+      if (k0 > k1) {
+        std::swap(k0, k1);
+        const int sw[4] = {0, 2, 1, 3};
+        for (int r = 0; r < 4; ++r)
+          for (int c = 0; c < 4; ++c) m[r * 4 + c] = p.m[sw[r] * 4 + sw[c]];
+      }
+      op.xr = uint8_t(k0 | (k1 << 4));
+      for (auto& c : m) prog.coef.push_back(make_double2(c.real(), c.imag()));
+    }
+    prog.ops.push_back(op);
+  }
+}
+
+Program build_program(int nl, const std::vector<Prim>& prims, std::vector<PassPlan>& plan) {
+  Program prog;
+  const int b = std::min(kMaxB, nl);
+  plan = plan_passes(nl, prims, b);
+  for (auto& pp : plan) {
+    if (!pp.fused) continue;
+    FPassArgs A;
+    std::memset(&A, 0, sizeof(A));
+    A.b = b;
+    A.nthr = b - kRB;
+    int tile_pos_of[64];
+    for (int i = 0; i < 64; ++i) tile_pos_of[i] = -1;
+    int j = 0;
+    for (int p = 0; p < nl; ++p)
+      if ((pp.tile_bits >> p) & 1) {
+        A.tpos[j] = (unsigned char)p;
+        tile_pos_of[p] = j++;
+      }
+    A.n_tiles = 1ull << (nl - b);
+    A.phase_begin = int(prog.phases.size());
+    // phase split: sequential, registers hold <= 4 tile positions
+    std::vector<int> reg;
+    std::vector<int> cur;
+    auto flush = [&]() {
+      if (cur.empty()) return;
+      std::vector<int> R = reg;
+      fill_regs(R, b);
+      FPhase F;
+      std::memset(&F, 0, sizeof(F));
+      make_phase_thr(F, R, b);
+      F.op_begin = int(prog.ops.size());
+      emit_ops(prog, prims, cur, tile_pos_of, R);
+      F.op_end = int(prog.ops.size());
+      prog.phases.push_back(F);
+      cur.clear();
+      reg.clear();
+    };
+    for (int i : pp.prims) {
+      const Req r = requirements(prims[i]);
+      std::vector<int> need;
+      for (int p = 0; p < 64; ++p)
+        if ((r.dense >> p) & 1) need.push_back(tile_pos_of[p]);
+      std::vector<int> merged = reg;
+      for (int t : need)
+        if (std::find(merged.begin(), merged.end(), t) == merged.end()) merged.push_back(t);
+      if (int(merged.size()) > kRB) {
+        flush();
+        merged = need;
+      }
+      reg = merged;
+      cur.push_back(i);
+    }
+    flush();
+    A.n_phases = int(prog.phases.size()) - A.phase_begin;
+    prog.passes.push_back(A);
+  }
+  return prog;
+}
+
+struct DevProgram {
+  void* buf = nullptr;
+  size_t cap = 0;
+};
+std::mutex g_prog_mu;
+std::vector<std::pair<sv_handle*, DevProgram>> g_progs;
+
+void* program_buffer(sv_handle* h, size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_prog_mu);
+  for (auto& e : g_progs)
+    if (e.first == h) {
+      if (e.second.cap < bytes) {
+        CUDA_CHECK(cudaStreamSynchronize(h->stream));
+        CUDA_CHECK(cudaFree(e.second.buf));
+        e.second.cap = std::max(bytes, size_t(1) << 20);
+        CUDA_CHECK(cudaMalloc(&e.second.buf, e.second.cap));
+      }
+      return e.second.buf;
+    }
+  DevProgram d;
+  d.cap = std::max(bytes, size_t(1) << 20);
+  CUDA_CHECK(cudaMalloc(&d.buf, d.cap));
+  g_progs.push_back({h, d});
+  return d.buf;
+}
+
+}  // namespace
+
+void release_fused(sv_handle* h) {
+  std::lock_guard<std::mutex> lk(g_prog_mu);
+  for (size_t i = 0; i < g_progs.size(); ++i)
+    if (g_progs[i].first == h) {
+      cudaFree(g_progs[i].second.buf);
+      g_progs.erase(g_progs.begin() + i);
+      return;
+    }
+}
+
 void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& prims) {
-  for (const Prim& p : prims) launch_prim(h, state, p);
+  if (h->nl < 5) {
+    for (const Prim& p : prims) launch_prim(h, state, p);
+    return;
+  }
+  std::vector<PassPlan> plan;
+  Program prog = build_program(h->nl, prims, plan);
+  if (prog.passes.empty()) {
+    for (const Prim& p : prims) launch_prim(h, state, p);
+    return;
+  }
+  // upload phases | ops | coef in one copy (the buffer is only reused after a stream sync)
+  const size_t b_ph = prog.phases.size() * sizeof(FPhase);
+  const size_t b_op = prog.ops.size() * sizeof(FOp);
+  const size_t b_cf = prog.coef.size() * sizeof(double2);
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t total = align(b_ph) + align(b_op) + align(b_cf);
+  std::vector<char> host(total);
+  std::memcpy(host.data(), prog.phases.data(), b_ph);
+  std::memcpy(host.data() + align(b_ph), prog.ops.data(), b_op);
+  std::memcpy(host.data() + align(b_ph) + align(b_op), prog.coef.data(), b_cf);
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));   // previous program may still be in use
+  char* dbuf = (char*)program_buffer(h, total);
+  CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), total, cudaMemcpyHostToDevice, h->stream));
+  const FPhase* d_ph = (const FPhase*)dbuf;
+  const FOp* d_op = (const FOp*)(dbuf + align(b_ph));
+  const double2* d_cf = (const double2*)(dbuf + align(b_ph) + align(b_op));
+
+  static bool attr_set = false;
+  const int b = prog.passes[0].b;
+  const size_t smem = (size_t(1) << b) * sizeof(double2);
+  if (!attr_set) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(size_t(1) << kMaxB) * 16));
+    attr_set = true;
+  }
+  int dev_sms = 148;
+  size_t pi = 0;
+  for (auto& pp : plan) {
+    if (!pp.fused) {
+      launch_prim(h, state, prims[pp.single]);
+      continue;
+    }
+    const FPassArgs& A = prog.passes[pi++];
+    const int threads = 1 << (A.b - kRB);
+    const u64 grid = std::min<u64>(A.n_tiles, u64(dev_sms) * 2 * 8);
+    const double bytes = 32.0 * double(h->n_local);
+    cudaEvent_t ev[2];
+    stat_begin(h, KC_FUSED, bytes, ev);
+    k_fused<<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+    stat_end(h, KC_FUSED, bytes, ev);
+    CUDA_CHECK(cudaGetLastError());
+  }
 }
 
 PlanStats plan_stats(int nl, const std::vector<Prim>& prims) {
   PlanStats s;
-  (void)nl;
-  s.passes = int64_t(prims.size());
   s.ops = int64_t(prims.size());
+  if (nl < 5) {
+    s.passes = s.ops;
+    return s;
+  }
+  std::vector<PassPlan> plan;
+  Program prog = build_program(nl, prims, plan);
+  s.passes = int64_t(plan.size());
+  s.tile_bits = std::min(kMaxB, nl);
+  s.phases = int64_t(prog.phases.size());
   return s;
 }

@@ -156,6 +156,7 @@ void ensure_results(sv_handle* h, size_t doubles);
 
 // fused tile engine (fused.cu / planner.cpp)
 void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& prims);
+void release_fused(sv_handle* h);
 struct PlanStats {
   int64_t passes = 0, ops = 0, tile_bits = 0, phases = 0;
 };
