@@ -482,6 +482,58 @@ void emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<i
   }
 }
 
+// List-schedule a pass's prims into register phases.  Prims may be reordered only past prims
+// they commute with (disjoint support, or both diagonal); each phase picks up to 4 register
+// bits and runs every ready prim whose dense bits fit, to a fixpoint.
+// Returns (register-bit mask in physical positions, prims in execution order) per phase.
+std::vector<std::pair<u64, std::vector<int>>> schedule_phases(const std::vector<Prim>& prims,
+                                                              const std::vector<int>& list) {
+  const int L = int(list.size());
+  std::vector<Req> rq(L);
+  for (int i = 0; i < L; ++i) rq[i] = requirements(prims[list[i]]);
+  // remaining-predecessor counts and successor lists of the conflict DAG
+  std::vector<int> npred(L, 0);
+  std::vector<std::vector<int>> succ(L);
+  for (int i = 0; i < L; ++i)
+    for (int j = 0; j < i; ++j) {
+      const bool commute = (rq[i].diag && rq[j].diag) || (rq[i].support & rq[j].support) == 0;
+      if (!commute) {
+        succ[j].push_back(i);
+        npred[i]++;
+      }
+    }
+  std::vector<char> done(L, 0);
+  int ndone = 0;
+  std::vector<std::pair<u64, std::vector<int>>> phases;
+  while (ndone < L) {
+    u64 R = 0;
+    std::vector<int> order;
+    for (;;) {
+      bool progress = false;
+      for (int i = 0; i < L; ++i) {
+        if (done[i] || npred[i] != 0) continue;
+        if ((rq[i].dense & ~R) != 0) continue;
+        done[i] = 1;
+        ++ndone;
+        order.push_back(list[i]);
+        for (int s : succ[i]) npred[s]--;
+        progress = true;
+      }
+      if (progress) continue;
+      int pick = -1;
+      for (int i = 0; i < L; ++i)
+        if (!done[i] && npred[i] == 0 && popcount64(R | rq[i].dense) <= kRB) {
+          pick = i;
+          break;
+        }
+      if (pick < 0) break;
+      R |= rq[pick].dense;
+    }
+    phases.push_back({R, order});
+  }
+  return phases;
+}
+
 Program build_program(int nl, const std::vector<Prim>& prims, std::vector<PassPlan>& plan) {
   Program prog;
   const int b = std::min(kMaxB, nl);
@@ -502,39 +554,19 @@ Program build_program(int nl, const std::vector<Prim>& prims, std::vector<PassPl
       }
     A.n_tiles = 1ull << (nl - b);
     A.phase_begin = int(prog.phases.size());
-    // phase split: sequential, registers hold <= 4 tile positions
-    std::vector<int> reg;
-    std::vector<int> cur;
-    auto flush = [&]() {
-      if (cur.empty()) return;
-      std::vector<int> R = reg;
+    for (auto& ph : schedule_phases(prims, pp.prims)) {
+      std::vector<int> R;
+      for (int p = 0; p < 64; ++p)
+        if ((ph.first >> p) & 1) R.push_back(tile_pos_of[p]);
       fill_regs(R, b);
       FPhase F;
       std::memset(&F, 0, sizeof(F));
       make_phase_thr(F, R, b);
       F.op_begin = int(prog.ops.size());
-      emit_ops(prog, prims, cur, tile_pos_of, R);
+      emit_ops(prog, prims, ph.second, tile_pos_of, R);
       F.op_end = int(prog.ops.size());
       prog.phases.push_back(F);
-      cur.clear();
-      reg.clear();
-    };
-    for (int i : pp.prims) {
-      const Req r = requirements(prims[i]);
-      std::vector<int> need;
-      for (int p = 0; p < 64; ++p)
-        if ((r.dense >> p) & 1) need.push_back(tile_pos_of[p]);
-      std::vector<int> merged = reg;
-      for (int t : need)
-        if (std::find(merged.begin(), merged.end(), t) == merged.end()) merged.push_back(t);
-      if (int(merged.size()) > kRB) {
-        flush();
-        merged = need;
-      }
-      reg = merged;
-      cur.push_back(i);
     }
-    flush();
     A.n_phases = int(prog.phases.size()) - A.phase_begin;
     prog.passes.push_back(A);
   }
