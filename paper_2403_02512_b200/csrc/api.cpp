@@ -132,6 +132,7 @@ static void check_handle(const sv_handle* h) {
 
 static void exec_prims(sv_handle* h, const std::vector<double2*>& states, std::vector<Prim>& prims, int fuse) {
   if (prims.empty()) return;
+  fold_diag_phases(prims);
   for (double2* st : states) {
     if (fuse)
       apply_prims_fused(h, st, prims);

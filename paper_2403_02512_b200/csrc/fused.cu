@@ -27,19 +27,30 @@ constexpr int kMaxB = 12;        // tile bits (2^12 amps = 64 KiB)
 constexpr int kRB = 4;           // register bits per thread (16 amplitudes)
 constexpr int kRegs = 1 << kRB;
 
-enum FKind : uint8_t { FK_PAIR = 0, FK_DIAG = 1, FK_DENSE2 = 2 };
+// op kinds; the *1 kinds are fast paths whose register predicate is compile-time
+enum FKind : uint8_t {
+  FK_PAIR1 = 0,   // 2x2 on register bit k, no register-side control
+  FK_PAIRG = 1,   // 2x2 on register xmask xr with register pattern (cm, cv)
+  FK_PHASE1 = 2,  // a *= d where register bit k == v (no other register-side pattern)
+  FK_SCALAR = 3,  // a *= d on all 16 amplitudes (pattern only on thread / outer bits)
+  FK_DIAGG = 4,   // table lookup diagonal, general
+  FK_DENSE2 = 5,  // 4x4 on register bits (k0 < k1) = xr & 15, xr >> 4
+};
 enum MType : uint8_t { MT_GENERAL = 0, MT_REAL = 1, MT_RXLIKE = 2, MT_X = 3 };
 
-struct FOp {
+struct __align__(16) FOp {
   u64 pm, pv;            // fixed pattern on non-register bits (tested on the thread's physical base)
   uint8_t kind, mtype;
-  uint8_t xr;            // PAIR: register-space xmask; DENSE2: k0 | (k1 << 4), k0 < k1
-  uint8_t cm, cv;        // fixed pattern in register space (PAIR: includes i0's pattern on xr)
-  uint8_t nt;            // DIAG: table bits
-  uint8_t treg[6];       // DIAG: register bit of table bit j, or 0xFF
-  uint8_t tphys[6];      // DIAG: physical position of table bit j when not a register bit
+  uint8_t xr;            // PAIRG: register-space xmask; DENSE2: k0 | (k1 << 4)
+  uint8_t cm, cv;        // register-space pattern (PAIRG includes i0's pattern on xr)
+  uint8_t nt;            // DIAGG: table bits
+  uint8_t k, v;          // PAIR1 / PHASE1: register bit and value
+  uint8_t treg[6];       // DIAGG: register bit of table bit j, or 0xFF
+  uint8_t tphys[6];      // DIAGG: physical position of table bit j when not a register bit
   int tab;               // offset into the coefficient array
+  int pad[2];
 };
+static_assert(sizeof(FOp) == 48, "FOp layout");
 
 struct FPhase {
   uint8_t reg[kRB];      // tile positions held in registers
@@ -51,7 +62,7 @@ struct FPassArgs {
   int b;                 // tile bits
   int nthr;              // b - kRB
   unsigned char tpos[kMaxB];   // physical positions of tile bits (ascending)
-  int n_outer_ins;       // == b; positions to insert when enumerating tiles
+  int n_outer_ins;
   u64 n_tiles;
   int phase_begin, n_phases;
 };
@@ -63,57 +74,62 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
   return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
 }
 
+// XOR swizzle of a tile index: linear over GF(2), so swz(a ^ b) == swz(a) ^ swz(b)
 __device__ __forceinline__ int swz(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
 
-// ---- 2x2 pair update on registers (i0 = r, i1 = r ^ XR) ------------------------------------
-template <int XR>
-__device__ __forceinline__ void pair_op(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef) {
-  const int cm = op.cm, cv = op.cv;
-  if (op.mtype == MT_X) {
-#pragma unroll
-    for (int r = 0; r < kRegs; ++r) {
-      if ((r & cm) == cv) {
-        const double2 t = a[r];
-        a[r] = a[r ^ XR];
-        a[r ^ XR] = t;
-      }
-    }
-    return;
-  }
-  const double2 m0 = coef[op.tab], m1 = coef[op.tab + 1], m2 = coef[op.tab + 2], m3 = coef[op.tab + 3];
-  if (op.mtype == MT_REAL) {
-#pragma unroll
-    for (int r = 0; r < kRegs; ++r)
-      if ((r & cm) == cv) {
-        const double2 x = a[r], y = a[r ^ XR];
-        a[r] = make_double2(fma(m0.x, x.x, m1.x * y.x), fma(m0.x, x.y, m1.x * y.y));
-        a[r ^ XR] = make_double2(fma(m2.x, x.x, m3.x * y.x), fma(m2.x, x.y, m3.x * y.y));
-      }
-  } else if (op.mtype == MT_RXLIKE) {
-    // m0, m3 real; m1, m2 imaginary:  (i b) * (x + i y) = -b y + i b x
-#pragma unroll
-    for (int r = 0; r < kRegs; ++r)
-      if ((r & cm) == cv) {
-        const double2 x = a[r], y = a[r ^ XR];
-        a[r] = make_double2(fma(m0.x, x.x, -m1.y * y.y), fma(m0.x, x.y, m1.y * y.x));
-        a[r ^ XR] = make_double2(fma(m3.x, y.x, -m2.y * x.y), fma(m3.x, y.y, m2.y * x.x));
-      }
+template <int MT>
+__device__ __forceinline__ void pair_upd(double2& x0, double2& x1, const double2 m0, const double2 m1, const double2 m2,
+                                         const double2 m3) {
+  const double2 x = x0, y = x1;
+  if (MT == MT_X) {
+    x0 = y;
+    x1 = x;
+  } else if (MT == MT_REAL) {
+    x0 = make_double2(fma(m0.x, x.x, m1.x * y.x), fma(m0.x, x.y, m1.x * y.y));
+    x1 = make_double2(fma(m2.x, x.x, m3.x * y.x), fma(m2.x, x.y, m3.x * y.y));
+  } else if (MT == MT_RXLIKE) {   // m0, m3 real; m1, m2 imaginary: (i b)(x + i y) = -b y + i b x
+    x0 = make_double2(fma(m0.x, x.x, -m1.y * y.y), fma(m0.x, x.y, m1.y * y.x));
+    x1 = make_double2(fma(m3.x, y.x, -m2.y * x.y), fma(m3.x, y.y, m2.y * x.x));
   } else {
-#pragma unroll
-    for (int r = 0; r < kRegs; ++r)
-      if ((r & cm) == cv) {
-        const double2 x = a[r], y = a[r ^ XR];
-        a[r] = cfma(m0, x, cmul(m1, y));
-        a[r ^ XR] = cfma(m2, x, cmul(m3, y));
-      }
+    x0 = cfma(m0, x, cmul(m1, y));
+    x1 = cfma(m2, x, cmul(m3, y));
   }
 }
 
+// fast path: every (r, r | 1<<K) pair, no register-side predicate
+template <int K, int MT>
+__device__ __forceinline__ void pair1(double2 (&a)[kRegs], const double2* __restrict__ c) {
+  double2 m0, m1, m2, m3;
+  if (MT != MT_X) {
+    m0 = c[0]; m1 = c[1]; m2 = c[2]; m3 = c[3];
+  }
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r)
+    if (!((r >> K) & 1)) pair_upd<MT>(a[r], a[r | (1 << K)], m0, m1, m2, m3);
+}
+
+// general pair: xmask XR in register space, runtime register pattern (cm, cv)
+template <int XR, int MT>
+__device__ __forceinline__ void pairg(double2 (&a)[kRegs], const double2* __restrict__ c, int cm, int cv) {
+  double2 m0, m1, m2, m3;
+  if (MT != MT_X) {
+    m0 = c[0]; m1 = c[1]; m2 = c[2]; m3 = c[3];
+  }
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r)
+    if ((r & cm) == cv) pair_upd<MT>(a[r], a[r ^ XR], m0, m1, m2, m3);
+}
+
+template <int K, int V>
+__device__ __forceinline__ void phase1(double2 (&a)[kRegs], const double2 d) {
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r)
+    if (((r >> K) & 1) == V) a[r] = cmul(d, a[r]);
+}
+
 template <int K0, int K1>
-__device__ __forceinline__ void dense2_op(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef) {
-  const int cm = op.cm, cv = op.cv;
+__device__ __forceinline__ void dense2(double2 (&a)[kRegs], const double2* __restrict__ M, int cm, int cv) {
   constexpr int B0 = 1 << K0, B1 = 1 << K1;
-  const double2* __restrict__ M = coef + op.tab;   // uniform L1-cached reads; keeps registers for a[]
 #pragma unroll
   for (int r = 0; r < kRegs; ++r) {
     if ((r & (B0 | B1)) != 0) continue;
@@ -121,98 +137,132 @@ __device__ __forceinline__ void dense2_op(double2 (&a)[kRegs], const FOp& op, co
     const int idx[4] = {r, r | B0, r | B1, r | B0 | B1};   // matrix index bit 0 <-> K0, bit 1 <-> K1
     double2 v[4];
 #pragma unroll
-    for (int c = 0; c < 4; ++c) v[c] = a[idx[c]];
+    for (int q = 0; q < 4; ++q) v[q] = a[idx[q]];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int c = 0; c < 4; ++c) acc = cfma(M[q * 4 + c], v[c], acc);
+      for (int cc = 0; cc < 4; ++cc) acc = cfma(M[q * 4 + cc], v[cc], acc);
       a[idx[q]] = acc;
     }
   }
 }
 
-__device__ __forceinline__ void diag_op(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef,
-                                        u64 phys_base) {
-  // table index = tconst | sum_k bit_k(r) * w[k]
-  int tconst = 0;
-  int w[kRB] = {0, 0, 0, 0};
+__device__ __forceinline__ void diagg(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef,
+                                      u64 phys_base) {
+  // table index = tconst | sum_k bit_k(r) * w_k   (w_k built without dynamic register indexing)
+  int tconst = 0, w0 = 0, w1 = 0, w2 = 0, w3 = 0;
   for (int j = 0; j < op.nt; ++j) {
     const int rg = op.treg[j];
-    if (rg == 0xFF)
-      tconst |= int((phys_base >> op.tphys[j]) & 1ull) << j;
-    else
-      w[rg] |= 1 << j;
+    const int bit = 1 << j;
+    if (rg == 0xFF) tconst |= int((phys_base >> op.tphys[j]) & 1ull) << j;
+    w0 |= (rg == 0) ? bit : 0;
+    w1 |= (rg == 1) ? bit : 0;
+    w2 |= (rg == 2) ? bit : 0;
+    w3 |= (rg == 3) ? bit : 0;
   }
   const int cm = op.cm, cv = op.cv;
-  if (op.nt == 0) {
-    const double2 d = coef[op.tab];
-#pragma unroll
-    for (int r = 0; r < kRegs; ++r)
-      if ((r & cm) == cv) a[r] = cmul(d, a[r]);
-    return;
-  }
 #pragma unroll
   for (int r = 0; r < kRegs; ++r) {
     if ((r & cm) != cv) continue;
-    int t = tconst;
-#pragma unroll
-    for (int k = 0; k < kRB; ++k)
-      if ((r >> k) & 1) t |= w[k];
+    const int t = tconst | ((r & 1) ? w0 : 0) | ((r & 2) ? w1 : 0) | ((r & 4) ? w2 : 0) | ((r & 8) ? w3 : 0);
     a[r] = cmul(coef[op.tab + t], a[r]);
   }
 }
 
-__device__ __forceinline__ void apply_pair_dispatch(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef) {
-  switch (op.xr) {
-    case 1: pair_op<1>(a, op, coef); break;
-    case 2: pair_op<2>(a, op, coef); break;
-    case 3: pair_op<3>(a, op, coef); break;
-    case 4: pair_op<4>(a, op, coef); break;
-    case 5: pair_op<5>(a, op, coef); break;
-    case 6: pair_op<6>(a, op, coef); break;
-    case 7: pair_op<7>(a, op, coef); break;
-    case 8: pair_op<8>(a, op, coef); break;
-    case 9: pair_op<9>(a, op, coef); break;
-    case 10: pair_op<10>(a, op, coef); break;
-    case 11: pair_op<11>(a, op, coef); break;
-    case 12: pair_op<12>(a, op, coef); break;
-    case 13: pair_op<13>(a, op, coef); break;
-    case 14: pair_op<14>(a, op, coef); break;
-    case 15: pair_op<15>(a, op, coef); break;
-    default: break;
+#define PAIR1_CASE(K)                                            \
+  case K * 4 + MT_GENERAL: pair1<K, MT_GENERAL>(a, c); break;   \
+  case K * 4 + MT_REAL: pair1<K, MT_REAL>(a, c); break;         \
+  case K * 4 + MT_RXLIKE: pair1<K, MT_RXLIKE>(a, c); break;     \
+  case K * 4 + MT_X: pair1<K, MT_X>(a, c); break;
+
+#define PAIRG_CASE(XR)                                                              \
+  case XR: if (!FULL || op.mtype == MT_X) pairg<XR, MT_X>(a, c, op.cm, op.cv);       \
+           else pairg<XR, MT_GENERAL>(a, c, op.cm, op.cv); break;
+
+// FULL = false compiles only the common kinds (PAIR1, PHASE1, SCALAR, X-type PAIRG): fewer live
+// registers, no spills; passes that need DIAGG / DENSE2 / general PAIRG use the FULL kernel.
+template <bool FULL>
+__device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef,
+                                         u64 phys_base) {
+  const double2* c = coef + op.tab;
+  switch (op.kind) {
+    case FK_PAIR1:
+      switch (op.k * 4 + op.mtype) {
+        PAIR1_CASE(0) PAIR1_CASE(1) PAIR1_CASE(2) PAIR1_CASE(3)
+        default: break;
+      }
+      break;
+    case FK_PHASE1: {
+      const double2 d = c[0];
+      switch (op.k * 2 + op.v) {
+        case 0: phase1<0, 0>(a, d); break;
+        case 1: phase1<0, 1>(a, d); break;
+        case 2: phase1<1, 0>(a, d); break;
+        case 3: phase1<1, 1>(a, d); break;
+        case 4: phase1<2, 0>(a, d); break;
+        case 5: phase1<2, 1>(a, d); break;
+        case 6: phase1<3, 0>(a, d); break;
+        case 7: phase1<3, 1>(a, d); break;
+        default: break;
+      }
+      break;
+    }
+    case FK_SCALAR: {
+      const double2 d = c[0];
+#pragma unroll
+      for (int r = 0; r < kRegs; ++r) a[r] = cmul(d, a[r]);
+      break;
+    }
+    case FK_PAIRG:
+      switch (op.xr) {
+        PAIRG_CASE(1) PAIRG_CASE(2) PAIRG_CASE(3) PAIRG_CASE(4) PAIRG_CASE(5) PAIRG_CASE(6) PAIRG_CASE(7)
+        PAIRG_CASE(8) PAIRG_CASE(9) PAIRG_CASE(10) PAIRG_CASE(11) PAIRG_CASE(12) PAIRG_CASE(13)
+        PAIRG_CASE(14) PAIRG_CASE(15)
+        default: break;
+      }
+      break;
+    case FK_DIAGG:
+      if (FULL) diagg(a, op, coef, phys_base);
+      break;
+    case FK_DENSE2:
+      if (FULL) switch (op.xr) {
+        case 0x10: dense2<0, 1>(a, c, op.cm, op.cv); break;
+        case 0x20: dense2<0, 2>(a, c, op.cm, op.cv); break;
+        case 0x30: dense2<0, 3>(a, c, op.cm, op.cv); break;
+        case 0x21: dense2<1, 2>(a, c, op.cm, op.cv); break;
+        case 0x31: dense2<1, 3>(a, c, op.cm, op.cv); break;
+        case 0x32: dense2<2, 3>(a, c, op.cm, op.cv); break;
+        default: break;
+      }
+      break;
+    default:
+      break;
   }
 }
 
-__device__ __forceinline__ void apply_dense2_dispatch(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef) {
-  switch (op.xr) {
-    case 0x10: dense2_op<0, 1>(a, op, coef); break;
-    case 0x20: dense2_op<0, 2>(a, op, coef); break;
-    case 0x30: dense2_op<0, 3>(a, op, coef); break;
-    case 0x21: dense2_op<1, 2>(a, op, coef); break;
-    case 0x31: dense2_op<1, 3>(a, op, coef); break;
-    case 0x32: dense2_op<2, 3>(a, op, coef); break;
-    default: break;
-  }
-}
-
+template <bool FULL>
 __global__ void __launch_bounds__(256, 2) k_fused(double2* __restrict__ state, const FPassArgs P,
                                                    const FPhase* __restrict__ phases, const FOp* __restrict__ ops,
                                                    const double2* __restrict__ coef) {
   extern __shared__ double2 tile[];
   const int tid = threadIdx.x;
   const int nthreads = blockDim.x;            // 2^(b-4)
-  const int T = 1 << P.b;
-  // physical offset of this thread's load slots: s = tid + nthreads * i
+  // load slot i of this thread is tile index s = tid + nthreads * i
   u64 spread_tid = 0;
   for (int j = 0; j < P.nthr; ++j)
     if ((tid >> j) & 1) spread_tid |= 1ull << P.tpos[j];
-  // load slot i of a thread covers tile bits nthr..nthr+3 -> physical bits hb[0..3]
   u64 hb[kRB];
 #pragma unroll
   for (int j = 0; j < kRB; ++j) hb[j] = 1ull << P.tpos[P.nthr + j];
+  const int swz_tid = swz(tid);
+  int swz_hi[kRB];
+#pragma unroll
+  for (int j = 0; j < kRB; ++j) swz_hi[j] = swz(nthreads << j);
 #define SPREAD_HI(i) ((((i) & 1) ? hb[0] : 0ull) | (((i) & 2) ? hb[1] : 0ull) | (((i) & 4) ? hb[2] : 0ull) | \
                       (((i) & 8) ? hb[3] : 0ull))
+#define SWZ_HI(i) ((((i) & 1) ? swz_hi[0] : 0) ^ (((i) & 2) ? swz_hi[1] : 0) ^ (((i) & 4) ? swz_hi[2] : 0) ^ \
+                   (((i) & 8) ? swz_hi[3] : 0))
   for (u64 t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
     // tile base: insert zero bits at the tile positions
     u64 base = t;
@@ -221,12 +271,12 @@ __global__ void __launch_bounds__(256, 2) k_fused(double2* __restrict__ state, c
       const u64 lo = base & ((1ull << p) - 1ull);
       base = ((base ^ lo) << 1) | lo;
     }
+    const u64 gbase = base | spread_tid;
     // global -> shared (cp.async, 16 B per amplitude, conflict-free through the swizzle)
 #pragma unroll
     for (int i = 0; i < kRegs; ++i) {
-      const int s = tid + nthreads * i;
-      const double2* src = state + (base | spread_tid | SPREAD_HI(i));
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(&tile[swz(s)]);
+      const double2* src = state + (gbase | SPREAD_HI(i));
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(&tile[swz_tid ^ SWZ_HI(i)]);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
     }
     asm volatile("cp.async.wait_all;\n" ::);
@@ -240,47 +290,29 @@ __global__ void __launch_bounds__(256, 2) k_fused(double2* __restrict__ state, c
           sthr |= 1 << F.thr[j];
           phys_base |= 1ull << P.tpos[F.thr[j]];
         }
-      int w[kRB];
-#pragma unroll
-      for (int k = 0; k < kRB; ++k) w[k] = 1 << F.reg[k];
+      const int s0 = swz(sthr);
+      const int W0 = swz(1 << F.reg[0]), W1 = swz(1 << F.reg[1]), W2 = swz(1 << F.reg[2]), W3 = swz(1 << F.reg[3]);
+#define REG_OFF(r) (s0 ^ (((r) & 1) ? W0 : 0) ^ (((r) & 2) ? W1 : 0) ^ (((r) & 4) ? W2 : 0) ^ (((r) & 8) ? W3 : 0))
       double2 a[kRegs];
 #pragma unroll
-      for (int r = 0; r < kRegs; ++r) {
-        int s = sthr;
-#pragma unroll
-        for (int k = 0; k < kRB; ++k)
-          if ((r >> k) & 1) s |= w[k];
-        a[r] = tile[swz(s)];
-      }
+      for (int r = 0; r < kRegs; ++r) a[r] = tile[REG_OFF(r)];
       for (int oi = F.op_begin; oi < F.op_end; ++oi) {
         const FOp op = ops[oi];
         if ((phys_base & op.pm) != op.pv) continue;
-        if (op.kind == FK_PAIR)
-          apply_pair_dispatch(a, op, coef);
-        else if (op.kind == FK_DIAG)
-          diag_op(a, op, coef, phys_base);
-        else
-          apply_dense2_dispatch(a, op, coef);
+        apply_op<FULL>(a, op, coef, phys_base);
       }
 #pragma unroll
-      for (int r = 0; r < kRegs; ++r) {
-        int s = sthr;
-#pragma unroll
-        for (int k = 0; k < kRB; ++k)
-          if ((r >> k) & 1) s |= w[k];
-        tile[swz(s)] = a[r];
-      }
+      for (int r = 0; r < kRegs; ++r) tile[REG_OFF(r)] = a[r];
       __syncthreads();
+#undef REG_OFF
     }
     // shared -> global
 #pragma unroll
-    for (int i = 0; i < kRegs; ++i) {
-      const int s = tid + nthreads * i;
-      state[base | spread_tid | SPREAD_HI(i)] = tile[swz(s)];
-    }
+    for (int i = 0; i < kRegs; ++i) state[gbase | SPREAD_HI(i)] = tile[swz_tid ^ SWZ_HI(i)];
     __syncthreads();
   }
-  (void)T;
+#undef SPREAD_HI
+#undef SWZ_HI
 }
 
 // ===========================================================================
@@ -380,6 +412,7 @@ int mtype_of(const std::vector<cplx>& m) {
 
 struct Program {
   std::vector<FPassArgs> passes;
+  std::vector<char> full;          // pass needs the FULL kernel variant
   std::vector<int> pass_of;        // for singles: -1
   std::vector<FPhase> phases;
   std::vector<FOp> ops;
@@ -450,13 +483,29 @@ void emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<i
     }
     op.tab = int(prog.coef.size());
     if (p.type == PRIM_PAIR) {
-      op.kind = FK_PAIR;
       for (int bpos = 0; bpos < 64; ++bpos)
         if ((p.xmask >> bpos) & 1) op.xr |= uint8_t(1 << reg_of_phys(bpos));
-      op.mtype = uint8_t(mtype_of(p.m));
+      const int mt = mtype_of(p.m);
+      if (popcount64(op.xr) == 1 && op.cm == op.xr && op.cv == 0) {
+        op.kind = FK_PAIR1;
+        op.k = uint8_t(__builtin_ctz(op.xr));
+        op.mtype = uint8_t(mt);
+      } else {
+        op.kind = FK_PAIRG;
+        op.mtype = uint8_t(mt == MT_X ? MT_X : MT_GENERAL);
+      }
       for (int j = 0; j < 4; ++j) prog.coef.push_back(make_double2(p.m[j].real(), p.m[j].imag()));
+    } else if (p.type == PRIM_DIAG && p.nb == 0 && popcount64(op.cm) <= 1) {
+      if (op.cm == 0) {
+        op.kind = FK_SCALAR;
+      } else {
+        op.kind = FK_PHASE1;
+        op.k = uint8_t(__builtin_ctz(op.cm));
+        op.v = uint8_t(op.cv ? 1 : 0);
+      }
+      prog.coef.push_back(make_double2(p.m[0].real(), p.m[0].imag()));
     } else if (p.type == PRIM_DIAG) {
-      op.kind = FK_DIAG;
+      op.kind = FK_DIAGG;
       op.nt = uint8_t(p.nb);
       for (int j = 0; j < p.nb; ++j) {
         const int k = reg_of_phys(p.pos[j]);
@@ -568,6 +617,13 @@ Program build_program(int nl, const std::vector<Prim>& prims, std::vector<PassPl
       prog.phases.push_back(F);
     }
     A.n_phases = int(prog.phases.size()) - A.phase_begin;
+    bool full = false;
+    for (int ph = A.phase_begin; ph < A.phase_begin + A.n_phases; ++ph)
+      for (int oi = prog.phases[ph].op_begin; oi < prog.phases[ph].op_end; ++oi) {
+        const FOp& o = prog.ops[oi];
+        full |= o.kind == FK_DIAGG || o.kind == FK_DENSE2 || (o.kind == FK_PAIRG && o.mtype != MT_X);
+      }
+    prog.full.push_back(full ? 1 : 0);
     prog.passes.push_back(A);
   }
   return prog;
@@ -643,7 +699,8 @@ void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& pr
   const int b = prog.passes[0].b;
   const size_t smem = (size_t(1) << b) * sizeof(double2);
   if (!attr_set) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, int(size_t(1) << kMaxB) * 16));
+    CUDA_CHECK(cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(size_t(1) << kMaxB) * 16));
+    CUDA_CHECK(cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(size_t(1) << kMaxB) * 16));
     attr_set = true;
   }
   int dev_sms = 148;
@@ -659,7 +716,10 @@ void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& pr
     const double bytes = 32.0 * double(h->n_local);
     cudaEvent_t ev[2];
     stat_begin(h, KC_FUSED, bytes, ev);
-    k_fused<<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+    if (prog.full[pi - 1])
+      k_fused<true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+    else
+      k_fused<false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
     stat_end(h, KC_FUSED, bytes, ev);
     CUDA_CHECK(cudaGetLastError());
   }

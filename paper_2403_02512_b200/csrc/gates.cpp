@@ -410,6 +410,44 @@ std::vector<Piece> lower_op(const sv_op& op, int n, int& next_column, bool need_
   return out;
 }
 
+// Factor the first table entry out of every unrestricted DIAG prim (RZ = e^{-i t/2} diag(1, e^{i t}),
+// IsingZZ, ...) and fold the product of those scalars into the matrix of one uncontrolled
+// 1-qubit PAIR / DENSE prim (each amplitude passes through it exactly once).  The remaining
+// table then has a unit entry, so single-bit diagonals touch half of the amplitudes.  Exact up
+// to fp64 rounding of the divisions (|d| ~ 1e-16).
+void fold_diag_phases(std::vector<Prim>& prims) {
+  cplx phase(1.0, 0.0);
+  for (auto& p : prims) {
+    if (p.skip || p.type != PRIM_DIAG || p.fmask != 0 || p.nb == 0) continue;
+    const cplx f = p.m[0];
+    if (f == cplx(1.0, 0.0)) continue;
+    phase *= f;
+    for (size_t i = 1; i < p.m.size(); ++i) p.m[i] /= f;
+    p.m[0] = 1.0;
+    if (p.nb == 1) {   // [1, t] -> single entry on bit = 1
+      p.fmask = p.fval = 1ull << p.pos[0];
+      p.m = {p.m[1]};
+      p.nb = 0;
+    }
+  }
+  if (phase == cplx(1.0, 0.0)) return;
+  for (auto& p : prims) {
+    if (p.skip) continue;
+    const bool whole_pair = p.type == PRIM_PAIR && popcount64(p.xmask) == 1 && p.fmask == p.xmask;
+    u64 tm = 0;
+    for (int j = 0; j < p.nb; ++j) tm |= 1ull << p.pos[j];
+    const bool whole_dense = p.type == PRIM_DENSE && p.fmask == tm;
+    if (whole_pair || whole_dense) {
+      for (auto& v : p.m) v *= phase;
+      return;
+    }
+  }
+  Prim s;
+  s.type = PRIM_DIAG;
+  s.m = {phase};
+  prims.push_back(s);
+}
+
 // Resolve bits that live on the shard index (physical position >= nl) for this rank:
 // controls / fixed bits become a predicate (skip when unmet), DIAG table bits become a
 // per-rank constant -- no communication (SURVEY.md §8(e) "no-comm cases").

@@ -122,6 +122,7 @@ std::vector<Piece> lower_op(const sv_op& op, int n, int& next_column, bool need_
 Prim make_dense_prim(const std::vector<int>& wires, const std::vector<cplx>& m, int n,
                      const std::vector<int>& ctrls, const std::vector<int>& cvals, const int* phys);
 void resolve_global(Prim& p, int nl, int rank);
+void fold_diag_phases(std::vector<Prim>& prims);
 std::vector<cplx> gate_matrix(int kind, const double* params, int n_wires, const double* matrix);
 void classify_prim(Prim& p);   // DENSE -> DIAG / PAIR specialisations when exact
 Prim adjoint_prim(const Prim& p);
