@@ -242,10 +242,10 @@ __device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const FOp& op, con
 }
 
 template <bool FULL>
-__global__ void __launch_bounds__(256, 2) k_fused(double2* __restrict__ state, const FPassArgs P,
+__global__ void __launch_bounds__(256, 1) k_fused(double2* __restrict__ state, const FPassArgs P,
                                                    const FPhase* __restrict__ phases, const FOp* __restrict__ ops,
                                                    const double2* __restrict__ coef) {
-  extern __shared__ double2 tile[];
+  extern __shared__ double2 tile_mem[];   // two tiles of 2^b amplitudes (double buffer)
   const int tid = threadIdx.x;
   const int nthreads = blockDim.x;            // 2^(b-4)
   // load slot i of this thread is tile index s = tid + nthreads * i
@@ -263,24 +263,38 @@ __global__ void __launch_bounds__(256, 2) k_fused(double2* __restrict__ state, c
                       (((i) & 8) ? hb[3] : 0ull))
 #define SWZ_HI(i) ((((i) & 1) ? swz_hi[0] : 0) ^ (((i) & 2) ? swz_hi[1] : 0) ^ (((i) & 4) ? swz_hi[2] : 0) ^ \
                    (((i) & 8) ? swz_hi[3] : 0))
-  for (u64 t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
-    // tile base: insert zero bits at the tile positions
+  const int T = 1 << P.b;
+  // tile index -> global base (insert zero bits at the tile positions)
+  auto tile_base = [&](u64 t) {
     u64 base = t;
     for (int j = 0; j < P.b; ++j) {
       const int p = P.tpos[j];
       const u64 lo = base & ((1ull << p) - 1ull);
       base = ((base ^ lo) << 1) | lo;
     }
-    const u64 gbase = base | spread_tid;
-    // global -> shared (cp.async, 16 B per amplitude, conflict-free through the swizzle)
+    return base;
+  };
+  // global -> shared (cp.async 16 B per amplitude, conflict-free through the swizzle), one group
+  auto issue_load = [&](u64 t, double2* dst_buf) {
+    const u64 gb = tile_base(t) | spread_tid;
 #pragma unroll
     for (int i = 0; i < kRegs; ++i) {
-      const double2* src = state + (gbase | SPREAD_HI(i));
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(&tile[swz_tid ^ SWZ_HI(i)]);
+      const double2* src = state + (gb | SPREAD_HI(i));
+      const unsigned dst = (unsigned)__cvta_generic_to_shared(&dst_buf[swz_tid ^ SWZ_HI(i)]);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
     }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  // double buffer: tile t+grid streams in while tile t is being computed
+  int cur = 0;
+  if (blockIdx.x < P.n_tiles) issue_load(blockIdx.x, tile_mem);
+  for (u64 t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+    double2* tile = tile_mem + cur * T;
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
+    if (t + gridDim.x < P.n_tiles) issue_load(t + gridDim.x, tile_mem + (cur ^ 1) * T);
+    const u64 base = tile_base(t);
+    const u64 gbase = base | spread_tid;
     for (int ph = 0; ph < P.n_phases; ++ph) {
       const FPhase& F = phases[P.phase_begin + ph];
       int sthr = 0;
@@ -306,10 +320,10 @@ __global__ void __launch_bounds__(256, 2) k_fused(double2* __restrict__ state, c
       __syncthreads();
 #undef REG_OFF
     }
-    // shared -> global
+    // shared -> global (this buffer is refilled only after the next iteration's barrier)
 #pragma unroll
     for (int i = 0; i < kRegs; ++i) state[gbase | SPREAD_HI(i)] = tile[swz_tid ^ SWZ_HI(i)];
-    __syncthreads();
+    cur ^= 1;
   }
 #undef SPREAD_HI
 #undef SWZ_HI
@@ -696,14 +710,16 @@ void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& pr
   const double2* d_cf = (const double2*)(dbuf + align(b_ph) + align(b_op));
 
   static bool attr_set = false;
+  static int dev_sms = 148;
   const int b = prog.passes[0].b;
-  const size_t smem = (size_t(1) << b) * sizeof(double2);
+  const size_t smem = 2 * (size_t(1) << b) * sizeof(double2);   // double buffer
   if (!attr_set) {
-    CUDA_CHECK(cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(size_t(1) << kMaxB) * 16));
-    CUDA_CHECK(cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(size_t(1) << kMaxB) * 16));
+    const int maxs = int(2 * (size_t(1) << kMaxB) * sizeof(double2));
+    CUDA_CHECK(cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs));
+    CUDA_CHECK(cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs));
+    CUDA_CHECK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
     attr_set = true;
   }
-  int dev_sms = 148;
   size_t pi = 0;
   for (auto& pp : plan) {
     if (!pp.fused) {
@@ -712,7 +728,7 @@ void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& pr
     }
     const FPassArgs& A = prog.passes[pi++];
     const int threads = 1 << (A.b - kRB);
-    const u64 grid = std::min<u64>(A.n_tiles, u64(dev_sms) * 2 * 8);
+    const u64 grid = std::min<u64>(A.n_tiles, u64(dev_sms));   // persistent: one CTA per SM
     const double bytes = 32.0 * double(h->n_local);
     cudaEvent_t ev[2];
     stat_begin(h, KC_FUSED, bytes, ev);
