@@ -54,6 +54,7 @@ static_assert(sizeof(FOp) == 48, "FOp layout");
 
 struct FPhase {
   uint8_t reg[kRB];      // tile positions held in registers
+  uint8_t flip;          // absorbed X gates: logical register index j is stored in register j ^ flip
   uint8_t thr[kMaxB];    // tile positions of thread-index bits (b - 4 of them; lanes 0..2 first)
   int op_begin, op_end;
 };
@@ -77,23 +78,40 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
 // XOR swizzle of a tile index: linear over GF(2), so swz(a ^ b) == swz(a) ^ swz(b)
 __device__ __forceinline__ int swz(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
 
+// In-place friendly forms: every product that needs an OLD value is formed first, then the
+// final FMAs overwrite x0 / x1.  This lets ptxas keep a[] in fixed registers across the op
+// dispatch (the naive form costs ~4 register moves per amplitude per op at the switch merge).
 template <int MT>
 __device__ __forceinline__ void pair_upd(double2& x0, double2& x1, const double2 m0, const double2 m1, const double2 m2,
                                          const double2 m3) {
-  const double2 x = x0, y = x1;
   if (MT == MT_X) {
-    x0 = y;
-    x1 = x;
+    const double2 t = x0;
+    x0 = x1;
+    x1 = t;
   } else if (MT == MT_REAL) {
-    x0 = make_double2(fma(m0.x, x.x, m1.x * y.x), fma(m0.x, x.y, m1.x * y.y));
-    x1 = make_double2(fma(m2.x, x.x, m3.x * y.x), fma(m2.x, x.y, m3.x * y.y));
+    const double px = m1.x * x1.x, py = m1.x * x1.y, qx = m2.x * x0.x, qy = m2.x * x0.y;
+    x0.x = fma(m0.x, x0.x, px);
+    x0.y = fma(m0.x, x0.y, py);
+    x1.x = fma(m3.x, x1.x, qx);
+    x1.y = fma(m3.x, x1.y, qy);
   } else if (MT == MT_RXLIKE) {   // m0, m3 real; m1, m2 imaginary: (i b)(x + i y) = -b y + i b x
-    x0 = make_double2(fma(m0.x, x.x, -m1.y * y.y), fma(m0.x, x.y, m1.y * y.x));
-    x1 = make_double2(fma(m3.x, y.x, -m2.y * x.y), fma(m3.x, y.y, m2.y * x.x));
+    const double px = -m1.y * x1.y, py = m1.y * x1.x, qx = -m2.y * x0.y, qy = m2.y * x0.x;
+    x0.x = fma(m0.x, x0.x, px);
+    x0.y = fma(m0.x, x0.y, py);
+    x1.x = fma(m3.x, x1.x, qx);
+    x1.y = fma(m3.x, x1.y, qy);
   } else {
-    x0 = cfma(m0, x, cmul(m1, y));
-    x1 = cfma(m2, x, cmul(m3, y));
+    const double2 p = cmul(m1, x1), q = cmul(m2, x0);
+    x0 = cfma(m0, x0, p);
+    x1 = cfma(m3, x1, q);
   }
+}
+
+// a *= d in place (cross products first)
+__device__ __forceinline__ void cmul_ip(double2& a, const double2 d) {
+  const double t1 = a.y * d.y, t2 = a.x * d.y;
+  a.x = fma(a.x, d.x, -t1);
+  a.y = fma(a.y, d.x, t2);
 }
 
 // fast path: every (r, r | 1<<K) pair, no register-side predicate
@@ -124,7 +142,7 @@ template <int K, int V>
 __device__ __forceinline__ void phase1(double2 (&a)[kRegs], const double2 d) {
 #pragma unroll
   for (int r = 0; r < kRegs; ++r)
-    if (((r >> K) & 1) == V) a[r] = cmul(d, a[r]);
+    if (((r >> K) & 1) == V) cmul_ip(a[r], d);
 }
 
 template <int K0, int K1>
@@ -166,7 +184,7 @@ __device__ __forceinline__ void diagg(double2 (&a)[kRegs], const FOp& op, const 
   for (int r = 0; r < kRegs; ++r) {
     if ((r & cm) != cv) continue;
     const int t = tconst | ((r & 1) ? w0 : 0) | ((r & 2) ? w1 : 0) | ((r & 4) ? w2 : 0) | ((r & 8) ? w3 : 0);
-    a[r] = cmul(coef[op.tab + t], a[r]);
+    cmul_ip(a[r], coef[op.tab + t]);
   }
 }
 
@@ -211,7 +229,7 @@ __device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const FOp& op, con
     case FK_SCALAR: {
       const double2 d = c[0];
 #pragma unroll
-      for (int r = 0; r < kRegs; ++r) a[r] = cmul(d, a[r]);
+      for (int r = 0; r < kRegs; ++r) cmul_ip(a[r], d);
       break;
     }
     case FK_PAIRG:
@@ -241,11 +259,14 @@ __device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const FOp& op, con
   }
 }
 
-template <bool FULL>
-__global__ void __launch_bounds__(256, 1) k_fused(double2* __restrict__ state, const FPassArgs P,
-                                                   const FPhase* __restrict__ phases, const FOp* __restrict__ ops,
-                                                   const double2* __restrict__ coef) {
-  extern __shared__ double2 tile_mem[];   // two tiles of 2^b amplitudes (double buffer)
+// DB = true : one persistent CTA per SM, two tile buffers, tile t+grid prefetched during tile t.
+// DB = false: two CTAs per SM (128 registers), one buffer each; CTAs overlap each other instead.
+template <bool FULL, bool DB>
+__global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__ state, const FPassArgs P,
+                                                            const FPhase* __restrict__ phases,
+                                                            const FOp* __restrict__ ops,
+                                                            const double2* __restrict__ coef) {
+  extern __shared__ double2 tile_mem[];   // DB: two tiles of 2^b amplitudes; else one
   const int tid = threadIdx.x;
   const int nthreads = blockDim.x;            // 2^(b-4)
   // load slot i of this thread is tile index s = tid + nthreads * i
@@ -287,12 +308,16 @@ __global__ void __launch_bounds__(256, 1) k_fused(double2* __restrict__ state, c
   };
   // double buffer: tile t+grid streams in while tile t is being computed
   int cur = 0;
-  if (blockIdx.x < P.n_tiles) issue_load(blockIdx.x, tile_mem);
+  if (DB && blockIdx.x < P.n_tiles) issue_load(blockIdx.x, tile_mem);
   for (u64 t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
-    double2* tile = tile_mem + cur * T;
+    double2* tile = tile_mem + (DB ? cur * T : 0);
+    if (!DB) {
+      __syncthreads();   // previous tile fully stored before the buffer is refilled
+      issue_load(t, tile_mem);
+    }
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
-    if (t + gridDim.x < P.n_tiles) issue_load(t + gridDim.x, tile_mem + (cur ^ 1) * T);
+    if (DB && t + gridDim.x < P.n_tiles) issue_load(t + gridDim.x, tile_mem + (cur ^ 1) * T);
     const u64 base = tile_base(t);
     const u64 gbase = base | spread_tid;
     for (int ph = 0; ph < P.n_phases; ++ph) {
@@ -315,8 +340,14 @@ __global__ void __launch_bounds__(256, 1) k_fused(double2* __restrict__ state, c
         if ((phys_base & op.pm) != op.pv) continue;
         apply_op<FULL>(a, op, coef, phys_base);
       }
+      {
+        // register r holds logical index r ^ flip: store offset = swz(sthr) ^ W(r ^ flip) (W linear)
+        const int fl = F.flip;
+        const int sf = s0 ^ ((fl & 1) ? W0 : 0) ^ ((fl & 2) ? W1 : 0) ^ ((fl & 4) ? W2 : 0) ^ ((fl & 8) ? W3 : 0);
 #pragma unroll
-      for (int r = 0; r < kRegs; ++r) tile[REG_OFF(r)] = a[r];
+        for (int r = 0; r < kRegs; ++r)
+          tile[sf ^ ((r & 1) ? W0 : 0) ^ ((r & 2) ? W1 : 0) ^ ((r & 4) ? W2 : 0) ^ ((r & 8) ? W3 : 0)] = a[r];
+      }
       __syncthreads();
 #undef REG_OFF
     }
@@ -465,9 +496,11 @@ void make_phase_thr(FPhase& F, const std::vector<int>& reg, int b) {
   for (int j = 0; j < b - kRB; ++j) F.thr[j] = (uint8_t)thr[j];
 }
 
-// emit the device ops of one phase
-void emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<int>& list, const int* tile_pos_of,
-              const std::vector<int>& reg) {
+// Emit the device ops of one phase.  Unconditional X on a register bit is not executed: it is
+// absorbed into a flip mask F (logical register index j lives in register j ^ F); later ops of
+// the phase are rewritten for F and the phase's store offsets apply it.  Returns F.
+int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<int>& list, const int* tile_pos_of,
+             const std::vector<int>& reg) {
   // phys bit -> register index (or -1)
   auto reg_of_phys = [&](int phys) -> int {
     int tp = tile_pos_of[phys];
@@ -476,6 +509,7 @@ void emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<i
       if (reg[k] == tp) return k;
     return -1;
   };
+  int F = 0;
   for (int i : list) {
     const Prim& p = prims[i];
     FOp op;
@@ -495,20 +529,31 @@ void emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<i
         if (v) op.pv |= 1ull << bpos;
       }
     }
+    op.cv ^= uint8_t(F & op.cm);   // physical register = logical ^ F
     op.tab = int(prog.coef.size());
     if (p.type == PRIM_PAIR) {
       for (int bpos = 0; bpos < 64; ++bpos)
         if ((p.xmask >> bpos) & 1) op.xr |= uint8_t(1 << reg_of_phys(bpos));
       const int mt = mtype_of(p.m);
-      if (popcount64(op.xr) == 1 && op.cm == op.xr && op.cv == 0) {
+      const bool single = popcount64(op.xr) == 1 && op.cm == op.xr;
+      if (single && mt == MT_X && op.pm == 0) {   // unconditional X: relabel, no data movement
+        F ^= op.xr;
+        continue;
+      }
+      std::vector<cplx> m = p.m;
+      if (single && (op.cv & op.xr)) {            // i0 sits on the bit-1 register: swap roles
+        m = {p.m[3], p.m[2], p.m[1], p.m[0]};
+        op.cv = 0;
+      }
+      if (single && op.cv == 0) {
         op.kind = FK_PAIR1;
         op.k = uint8_t(__builtin_ctz(op.xr));
-        op.mtype = uint8_t(mt);
+        op.mtype = uint8_t(mtype_of(m));
       } else {
         op.kind = FK_PAIRG;
         op.mtype = uint8_t(mt == MT_X ? MT_X : MT_GENERAL);
       }
-      for (int j = 0; j < 4; ++j) prog.coef.push_back(make_double2(p.m[j].real(), p.m[j].imag()));
+      for (int j = 0; j < 4; ++j) prog.coef.push_back(make_double2(m[j].real(), m[j].imag()));
     } else if (p.type == PRIM_DIAG && p.nb == 0 && popcount64(op.cm) <= 1) {
       if (op.cm == 0) {
         op.kind = FK_SCALAR;
@@ -521,12 +566,17 @@ void emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<i
     } else if (p.type == PRIM_DIAG) {
       op.kind = FK_DIAGG;
       op.nt = uint8_t(p.nb);
+      int tflip = 0;
       for (int j = 0; j < p.nb; ++j) {
         const int k = reg_of_phys(p.pos[j]);
         op.treg[j] = k >= 0 ? uint8_t(k) : uint8_t(0xFF);
         op.tphys[j] = uint8_t(p.pos[j]);
+        if (k >= 0 && ((F >> k) & 1)) tflip |= 1 << j;
       }
-      for (auto& c : p.m) prog.coef.push_back(make_double2(c.real(), c.imag()));
+      for (size_t t = 0; t < p.m.size(); ++t) {
+        const cplx c = p.m[t ^ size_t(tflip)];
+        prog.coef.push_back(make_double2(c.real(), c.imag()));
+      }
     } else {
       op.kind = FK_DENSE2;
       int k0 = reg_of_phys(p.pos[0]), k1 = reg_of_phys(p.pos[1]);
@@ -538,11 +588,19 @@ void emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<i
         for (int r = 0; r < 4; ++r)
           for (int c = 0; c < 4; ++c) m[r * 4 + c] = p.m[sw[r] * 4 + sw[c]];
       }
+      const int f = ((F >> k0) & 1) | (((F >> k1) & 1) << 1);
+      std::vector<cplx> mf(16);
+      for (int r = 0; r < 4; ++r)
+        for (int c = 0; c < 4; ++c) mf[r * 4 + c] = m[(r ^ f) * 4 + (c ^ f)];
       op.xr = uint8_t(k0 | (k1 << 4));
-      for (auto& c : m) prog.coef.push_back(make_double2(c.real(), c.imag()));
+      const uint8_t tb = uint8_t((1 << k0) | (1 << k1));   // targets are enumerated by the kernel
+      op.cm &= uint8_t(~tb);
+      op.cv &= uint8_t(~tb);
+      for (auto& c : mf) prog.coef.push_back(make_double2(c.real(), c.imag()));
     }
     prog.ops.push_back(op);
   }
+  return F;
 }
 
 // List-schedule a pass's prims into register phases.  Prims may be reordered only past prims
@@ -626,7 +684,7 @@ Program build_program(int nl, const std::vector<Prim>& prims, std::vector<PassPl
       std::memset(&F, 0, sizeof(F));
       make_phase_thr(F, R, b);
       F.op_begin = int(prog.ops.size());
-      emit_ops(prog, prims, ph.second, tile_pos_of, R);
+      F.flip = uint8_t(emit_ops(prog, prims, ph.second, tile_pos_of, R));
       F.op_end = int(prog.ops.size());
       prog.phases.push_back(F);
     }
@@ -711,15 +769,20 @@ void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& pr
 
   static bool attr_set = false;
   static int dev_sms = 148;
+  static bool db = true;
   const int b = prog.passes[0].b;
-  const size_t smem = 2 * (size_t(1) << b) * sizeof(double2);   // double buffer
   if (!attr_set) {
     const int maxs = int(2 * (size_t(1) << kMaxB) * sizeof(double2));
-    CUDA_CHECK(cudaFuncSetAttribute(k_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs));
-    CUDA_CHECK(cudaFuncSetAttribute(k_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs));
+    CUDA_CHECK(cudaFuncSetAttribute(k_fused<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs));
+    CUDA_CHECK(cudaFuncSetAttribute(k_fused<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs));
+    CUDA_CHECK(cudaFuncSetAttribute(k_fused<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs / 2));
+    CUDA_CHECK(cudaFuncSetAttribute(k_fused<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxs / 2));
     CUDA_CHECK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
+    const char* mode = getenv("SVB200_FUSED_MODE");   // "sb": single-buffer 2 CTAs/SM (experiments)
+    db = !(mode && std::string(mode) == "sb");
     attr_set = true;
   }
+  const size_t smem = (db ? 2 : 1) * (size_t(1) << b) * sizeof(double2);
   size_t pi = 0;
   for (auto& pp : plan) {
     if (!pp.fused) {
@@ -728,14 +791,20 @@ void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& pr
     }
     const FPassArgs& A = prog.passes[pi++];
     const int threads = 1 << (A.b - kRB);
-    const u64 grid = std::min<u64>(A.n_tiles, u64(dev_sms));   // persistent: one CTA per SM
+    // persistent grid: one (DB) or two CTAs per SM
+    const u64 grid = std::min<u64>(A.n_tiles, u64(dev_sms) * (db ? 1 : 2));
     const double bytes = 32.0 * double(h->n_local);
     cudaEvent_t ev[2];
     stat_begin(h, KC_FUSED, bytes, ev);
-    if (prog.full[pi - 1])
-      k_fused<true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+    const bool full = prog.full[pi - 1];
+    if (db && full)
+      k_fused<true, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+    else if (db)
+      k_fused<false, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+    else if (full)
+      k_fused<true, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
     else
-      k_fused<false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+      k_fused<false, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
     stat_end(h, KC_FUSED, bytes, ev);
     CUDA_CHECK(cudaGetLastError());
   }
