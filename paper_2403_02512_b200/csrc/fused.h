@@ -1,0 +1,76 @@
+// K7 fusion engine: program format shared by the host planner (fused_plan.cpp) and the
+// sm_100a tile kernel (fused.cu).
+#pragma once
+
+#include <vector>
+
+#include "sv_internal.h"
+
+namespace fused {
+
+constexpr int kMaxB = 12;        // tile bits (2^12 amplitudes = 64 KiB)
+constexpr int kRB = 4;           // register bits per thread (16 amplitudes)
+constexpr int kRegs = 1 << kRB;
+constexpr int kMaxSmemOps = 320; // op records staged in shared memory per pass
+
+// op kinds; the *1 kinds are fast paths whose register predicate is compile-time
+enum FKind : uint8_t {
+  FK_PAIR1 = 0,   // 2x2 on register bit k, no register-side control
+  FK_PAIRG = 1,   // 2x2 on register xmask xr with register pattern (cm, cv)
+  FK_PHASE1 = 2,  // a *= d where register bit k == v (no other register-side pattern)
+  FK_SCALAR = 3,  // a *= d on all 16 amplitudes (pattern only on thread / outer bits)
+  FK_DIAGG = 4,   // table lookup diagonal, general
+  FK_DENSE2 = 5,  // 4x4 on register bits (k0 < k1) = xr & 15, xr >> 4
+};
+enum MType : uint8_t { MT_GENERAL = 0, MT_REAL = 1, MT_RXLIKE = 2, MT_X = 3 };
+
+struct __align__(16) FOp {
+  u64 pm, pv;            // fixed pattern on non-register bits (tested on the thread's physical base)
+  uint8_t kind, mtype;
+  uint8_t xr;            // PAIRG: register-space xmask; DENSE2: k0 | (k1 << 4)
+  uint8_t cm, cv;        // register-space pattern (PAIRG includes i0's pattern on xr)
+  uint8_t nt;            // DIAGG: table bits
+  uint8_t k, v;          // PAIR1 / PHASE1: register bit and value
+  uint8_t treg[6];       // DIAGG: register bit of table bit j, or 0xFF
+  uint8_t tphys[6];      // DIAGG: physical position of table bit j when not a register bit
+  int tab;               // offset into the coefficient array (DIAGG / DENSE2)
+  int pad[2];
+  double2 c[4];          // inline coefficients (PAIR1 / PAIRG: m00 m01 m10 m11; PHASE1 / SCALAR: d)
+};
+static_assert(sizeof(FOp) == 112, "FOp layout");
+
+struct FPhase {
+  uint8_t reg[kRB];      // tile positions held in registers
+  uint8_t flip;          // absorbed X gates: logical register index j is stored in register j ^ flip
+  uint8_t thr[kMaxB];    // tile positions of thread-index bits (b - 4 of them; lanes 0..2 first)
+  int op_begin, op_end;
+};
+
+struct FPassArgs {
+  int b;                 // tile bits
+  int nthr;              // b - kRB
+  unsigned char tpos[kMaxB];   // physical positions of tile bits (ascending)
+  int n_outer_ins;
+  u64 n_tiles;
+  int phase_begin, n_phases;
+  int op_begin, op_end;  // op records of the whole pass (contiguous)
+};
+
+struct PassPlan {
+  bool fused = false;
+  int single = -1;            // prim index when not fused
+  u64 tile_bits = 0;
+  std::vector<int> prims;     // in application order
+};
+
+struct Program {
+  std::vector<FPassArgs> passes;
+  std::vector<char> full;          // pass needs the FULL kernel variant
+  std::vector<FPhase> phases;
+  std::vector<FOp> ops;
+  std::vector<double2> coef;
+};
+
+Program build_program(int nl, const std::vector<Prim>& prims, std::vector<PassPlan>& plan);
+
+}  // namespace fused
