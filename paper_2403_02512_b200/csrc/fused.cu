@@ -152,69 +152,75 @@ __device__ __forceinline__ void diagg(double2 (&a)[kRegs], const FOp& op, const 
   case K * 4 + MT_RXLIKE: pair1<K, MT_RXLIKE>(a, c); break;     \
   case K * 4 + MT_X: pair1<K, MT_X>(a, c); break;
 
-#define PAIRG_CASE(XR)                                                              \
-  case XR: if (!FULL || op.mtype == MT_X) pairg<XR, MT_X>(a, c, op.cm, op.cv);       \
-           else pairg<XR, MT_GENERAL>(a, c, op.cm, op.cv); break;
+// Hot fields of an op record, prefetched one op ahead into registers (the op loop would
+// otherwise expose two dependent shared-memory latencies per op: record -> case -> coefficients).
+struct Hot {
+  u64 pm, pv;
+  int cs, cm, cv;
+  double2 c0, c1, c2, c3;
+};
 
-// FULL = false compiles only the common kinds (PAIR1, PHASE1, SCALAR, X-type PAIRG): fewer live
-// registers; passes that need DIAGG / DENSE2 / general PAIRG use the FULL kernel.
-// `op` lives in shared memory; the hot kinds carry their coefficients inline (op.c).
+__device__ __forceinline__ Hot fetch(const FOp& o) {
+  Hot h;
+  h.pm = o.pm;
+  h.pv = o.pv;
+  h.cs = o.cs;
+  h.cm = o.cm;
+  h.cv = o.cv;
+  h.c0 = o.c[0];
+  h.c1 = o.c[1];
+  h.c2 = o.c[2];
+  h.c3 = o.c[3];
+  return h;
+}
+
+#undef PAIR1_CASE
+#define PAIR1_CASE(K)                                                              \
+  case CS_PAIR1 + K * 4 + MT_GENERAL: pair1<K, MT_GENERAL>(a, c); break;          \
+  case CS_PAIR1 + K * 4 + MT_REAL: pair1<K, MT_REAL>(a, c); break;                \
+  case CS_PAIR1 + K * 4 + MT_RXLIKE: pair1<K, MT_RXLIKE>(a, c); break;            \
+  case CS_PAIR1 + K * 4 + MT_X: pair1<K, MT_X>(a, c); break;
+#define PAIRGX_CASE(XR) \
+  case CS_PAIRGX + XR - 1: pairg<XR, MT_X>(a, c, h.cm, h.cv); break;
+#define PAIRG_CASE(XR) \
+  case CS_PAIRG + XR - 1: if (FULL) pairg<XR, MT_GENERAL>(a, c, h.cm, h.cv); break;
+
+// One flat switch on the dense case index (a single indirect branch).  FULL = false compiles
+// only the common kinds (fewer live registers); passes that need DIAGG / DENSE2 / general
+// PAIRG use the FULL kernel.  `op` (shared memory) is only read by the rare kinds.
 template <bool FULL>
-__device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef,
-                                         u64 phys_base) {
-  const double2* c = op.c;
-  switch (op.kind) {
-    case FK_PAIR1:
-      switch (op.k * 4 + op.mtype) {
-        PAIR1_CASE(0) PAIR1_CASE(1) PAIR1_CASE(2) PAIR1_CASE(3)
-        default: break;
-      }
-      break;
-    case FK_PHASE1: {
-      const double2 d = c[0];
-      switch (op.k * 2 + op.v) {
-        case 0: phase1<0, 0>(a, d); break;
-        case 1: phase1<0, 1>(a, d); break;
-        case 2: phase1<1, 0>(a, d); break;
-        case 3: phase1<1, 1>(a, d); break;
-        case 4: phase1<2, 0>(a, d); break;
-        case 5: phase1<2, 1>(a, d); break;
-        case 6: phase1<3, 0>(a, d); break;
-        case 7: phase1<3, 1>(a, d); break;
-        default: break;
-      }
-      break;
-    }
-    case FK_SCALAR: {
-      const double2 d = c[0];
+__device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const Hot& h, const FOp& op,
+                                         const double2* __restrict__ coef, u64 phys_base) {
+  const double2 c[4] = {h.c0, h.c1, h.c2, h.c3};
+  switch (h.cs) {
+    PAIR1_CASE(0) PAIR1_CASE(1) PAIR1_CASE(2) PAIR1_CASE(3)
+    case CS_PHASE1 + 0: phase1<0, 0>(a, h.c0); break;
+    case CS_PHASE1 + 1: phase1<0, 1>(a, h.c0); break;
+    case CS_PHASE1 + 2: phase1<1, 0>(a, h.c0); break;
+    case CS_PHASE1 + 3: phase1<1, 1>(a, h.c0); break;
+    case CS_PHASE1 + 4: phase1<2, 0>(a, h.c0); break;
+    case CS_PHASE1 + 5: phase1<2, 1>(a, h.c0); break;
+    case CS_PHASE1 + 6: phase1<3, 0>(a, h.c0); break;
+    case CS_PHASE1 + 7: phase1<3, 1>(a, h.c0); break;
+    case CS_SCALAR:
 #pragma unroll
-      for (int r = 0; r < kRegs; ++r) cmul_ip(a[r], d);
+      for (int r = 0; r < kRegs; ++r) cmul_ip(a[r], h.c0);
       break;
-    }
-    case FK_PAIRG:
-      switch (op.xr) {
-        PAIRG_CASE(1) PAIRG_CASE(2) PAIRG_CASE(3) PAIRG_CASE(4) PAIRG_CASE(5) PAIRG_CASE(6) PAIRG_CASE(7)
-        PAIRG_CASE(8) PAIRG_CASE(9) PAIRG_CASE(10) PAIRG_CASE(11) PAIRG_CASE(12) PAIRG_CASE(13)
-        PAIRG_CASE(14) PAIRG_CASE(15)
-        default: break;
-      }
-      break;
-    case FK_DIAGG:
+    PAIRGX_CASE(1) PAIRGX_CASE(2) PAIRGX_CASE(3) PAIRGX_CASE(4) PAIRGX_CASE(5) PAIRGX_CASE(6) PAIRGX_CASE(7)
+    PAIRGX_CASE(8) PAIRGX_CASE(9) PAIRGX_CASE(10) PAIRGX_CASE(11) PAIRGX_CASE(12) PAIRGX_CASE(13)
+    PAIRGX_CASE(14) PAIRGX_CASE(15)
+    PAIRG_CASE(1) PAIRG_CASE(2) PAIRG_CASE(3) PAIRG_CASE(4) PAIRG_CASE(5) PAIRG_CASE(6) PAIRG_CASE(7)
+    PAIRG_CASE(8) PAIRG_CASE(9) PAIRG_CASE(10) PAIRG_CASE(11) PAIRG_CASE(12) PAIRG_CASE(13)
+    PAIRG_CASE(14) PAIRG_CASE(15)
+    case CS_DIAGG:
       if (FULL) diagg(a, op, coef, phys_base);
       break;
-    case FK_DENSE2: {
-      const double2* M = coef + op.tab;
-      if (FULL) switch (op.xr) {
-          case 0x10: dense2<0, 1>(a, M, op.cm, op.cv); break;
-          case 0x20: dense2<0, 2>(a, M, op.cm, op.cv); break;
-          case 0x30: dense2<0, 3>(a, M, op.cm, op.cv); break;
-          case 0x21: dense2<1, 2>(a, M, op.cm, op.cv); break;
-          case 0x31: dense2<1, 3>(a, M, op.cm, op.cv); break;
-          case 0x32: dense2<2, 3>(a, M, op.cm, op.cv); break;
-          default: break;
-        }
-      break;
-    }
+    case CS_DENSE2 + 0: if (FULL) dense2<0, 1>(a, coef + op.tab, h.cm, h.cv); break;
+    case CS_DENSE2 + 1: if (FULL) dense2<0, 2>(a, coef + op.tab, h.cm, h.cv); break;
+    case CS_DENSE2 + 2: if (FULL) dense2<0, 3>(a, coef + op.tab, h.cm, h.cv); break;
+    case CS_DENSE2 + 3: if (FULL) dense2<1, 2>(a, coef + op.tab, h.cm, h.cv); break;
+    case CS_DENSE2 + 4: if (FULL) dense2<1, 3>(a, coef + op.tab, h.cm, h.cv); break;
+    case CS_DENSE2 + 5: if (FULL) dense2<2, 3>(a, coef + op.tab, h.cm, h.cv); break;
     default:
       break;
   }
@@ -307,10 +313,14 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
       for (int r = 0; r < kRegs; ++r)
         a[r] = tile[s0 ^ ((r & 1) ? W0 : 0) ^ ((r & 2) ? W1 : 0) ^ ((r & 4) ? W2 : 0) ^ ((r & 8) ? W3 : 0)];
       const int oe = F.op_end;
-      for (int oi = F.op_begin; oi < oe; ++oi) {
-        const FOp& op = OPS[oi];
-        if ((phys_base & op.pm) != op.pv) continue;
-        apply_op<FULL>(a, op, coef, phys_base);
+      int oi = F.op_begin;
+      if (oi < oe) {
+        Hot h = fetch(OPS[oi]);
+        for (; oi < oe; ++oi) {
+          const Hot hn = fetch(OPS[oi + 1 < oe ? oi + 1 : oi]);   // software prefetch
+          if ((phys_base & h.pm) == h.pv) apply_op<FULL>(a, h, OPS[oi], coef, phys_base);
+          h = hn;
+        }
       }
       {
         // register r holds logical index r ^ flip: store offset = swz(sthr) ^ W(r ^ flip) (W linear)

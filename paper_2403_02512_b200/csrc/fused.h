@@ -34,9 +34,18 @@ struct __align__(16) FOp {
   uint8_t treg[6];       // DIAGG: register bit of table bit j, or 0xFF
   uint8_t tphys[6];      // DIAGG: physical position of table bit j when not a register bit
   int tab;               // offset into the coefficient array (DIAGG / DENSE2)
-  int pad[2];
+  int cs;                // dense dispatch case (see case_of() in fused_plan.cpp)
+  int pad;
   double2 c[4];          // inline coefficients (PAIR1 / PAIRG: m00 m01 m10 m11; PHASE1 / SCALAR: d)
 };
+// dense dispatch cases
+constexpr int CS_PAIR1 = 0;      // + k*4 + mtype          (0..15)
+constexpr int CS_PHASE1 = 16;    // + k*2 + v              (16..23)
+constexpr int CS_SCALAR = 24;
+constexpr int CS_PAIRGX = 25;    // + xr - 1               (25..39)
+constexpr int CS_PAIRG = 40;     // + xr - 1               (40..54)
+constexpr int CS_DIAGG = 55;
+constexpr int CS_DENSE2 = 56;    // + pair index 0..5      (56..61)
 static_assert(sizeof(FOp) == 112, "FOp layout");
 
 struct FPhase {

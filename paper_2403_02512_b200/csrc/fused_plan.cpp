@@ -226,6 +226,17 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
       op.cv &= uint8_t(~tb);
       for (auto& c : mf) prog.coef.push_back(make_double2(c.real(), c.imag()));
     }
+    switch (op.kind) {
+      case FK_PAIR1: op.cs = CS_PAIR1 + op.k * 4 + op.mtype; break;
+      case FK_PHASE1: op.cs = CS_PHASE1 + op.k * 2 + op.v; break;
+      case FK_SCALAR: op.cs = CS_SCALAR; break;
+      case FK_PAIRG: op.cs = (op.mtype == MT_X ? CS_PAIRGX : CS_PAIRG) + op.xr - 1; break;
+      case FK_DIAGG: op.cs = CS_DIAGG; break;
+      default: {
+        static const uint8_t pairs[6] = {0x10, 0x20, 0x30, 0x21, 0x31, 0x32};
+        op.cs = CS_DENSE2 + int(std::find(pairs, pairs + 6, op.xr) - pairs);
+      }
+    }
     if (op.kind != FK_DIAGG && op.kind != FK_DENSE2) {   // hot kinds carry their coefficients inline
       const int nc = (op.kind == FK_PAIR1 || op.kind == FK_PAIRG) ? 4 : 1;
       for (int j = 0; j < nc; ++j) op.c[j] = prog.coef[op.tab + j];
