@@ -33,6 +33,8 @@ def timeit(dev, ops, reps=5):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=28)
+    ap.add_argument("--case", default="")
+    ap.add_argument("--reps", type=int, default=5)
     a = ap.parse_args()
     n = a.n
     low = [n - 1, n - 2, n - 3]           # physical bits 0..2
@@ -53,8 +55,10 @@ def main():
     out = {}
     with Device(n) as d:
         for name, ops in cases.items():
+            if a.case and a.case not in name:
+                continue
             ps = plan_summary(n, ops)
-            ms, launches = timeit(d, ops)
+            ms, launches = timeit(d, ops, a.reps)
             out[name] = {"ms_per_pass": ms, "passes": ps["passes"], "phases": ps["phases"], "ops": len(ops)}
             print(f"{name:32s} passes={ps['passes']} phases={ps['phases']:3d} ops={len(ops):3d} "
                   f"ms/pass={ms:.3f} GB/s={32 * 2**n / ms / 1e6:.0f}", flush=True)

@@ -12,8 +12,12 @@
 // R, while controls and diagonal gates may sit on ANY bit (register, thread or tile-outer bit:
 // they are predicates / per-thread constants).  Switching R costs one shared-memory round trip.
 // Shared memory is XOR-swizzled so every phase's 16-byte accesses are bank-conflict free.
-// Unconditional X gates are never executed: the planner absorbs them into a per-phase flip
-// mask that relabels registers at the store.  The host planner lives in fused_plan.cpp.
+//
+// No op ever moves amplitudes between registers: X gates are register relabelings (a uniform
+// flip mask applied by the host planner, plus a per-thread flip mask `fthr` toggled by
+// thread-predicated X), honoured by the *D cases and by the phase store.  Every update is
+// written in an in-place form.  Both rules keep a[] in fixed registers across the op dispatch;
+// violating either costs ~4 register moves per amplitude per op.  Planner: fused_plan.cpp.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
@@ -35,17 +39,11 @@ __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
 // XOR swizzle of a tile index: linear over GF(2), so swz(a ^ b) == swz(a) ^ swz(b)
 __device__ __forceinline__ int swz(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
 
-// In-place friendly forms: every product that needs an OLD value is formed first, then the
-// final FMAs overwrite x0 / x1.  This lets ptxas keep a[] in fixed registers across the op
-// dispatch (the naive form costs ~4 register moves per amplitude per op at the switch merge).
+// In-place 2x2 update of (x0, x1): products needing OLD values first, then overwriting FMAs.
 template <int MT>
 __device__ __forceinline__ void pair_upd(double2& x0, double2& x1, const double2 m0, const double2 m1, const double2 m2,
                                          const double2 m3) {
-  if (MT == MT_X) {
-    const double2 t = x0;
-    x0 = x1;
-    x1 = t;
-  } else if (MT == MT_REAL) {
+  if (MT == MT_REAL) {
     const double px = m1.x * x1.x, py = m1.x * x1.y, qx = m2.x * x0.x, qy = m2.x * x0.y;
     x0.x = fma(m0.x, x0.x, px);
     x0.y = fma(m0.x, x0.y, py);
@@ -71,13 +69,10 @@ __device__ __forceinline__ void cmul_ip(double2& a, const double2 d) {
   a.y = fma(a.y, d.x, t2);
 }
 
-// fast path: every (r, r | 1<<K) pair, no register-side predicate
+// every (r, r | 1<<K) pair, no register-side predicate
 template <int K, int MT>
-__device__ __forceinline__ void pair1(double2 (&a)[kRegs], const double2* __restrict__ c) {
-  double2 m0, m1, m2, m3;
-  if (MT != MT_X) {
-    m0 = c[0]; m1 = c[1]; m2 = c[2]; m3 = c[3];
-  }
+__device__ __forceinline__ void pair1(double2 (&a)[kRegs], const double2 m0, const double2 m1, const double2 m2,
+                                      const double2 m3) {
 #pragma unroll
   for (int r = 0; r < kRegs; ++r)
     if (!((r >> K) & 1)) pair_upd<MT>(a[r], a[r | (1 << K)], m0, m1, m2, m3);
@@ -86,10 +81,7 @@ __device__ __forceinline__ void pair1(double2 (&a)[kRegs], const double2* __rest
 // general pair: xmask XR in register space, runtime register pattern (cm, cv)
 template <int XR, int MT>
 __device__ __forceinline__ void pairg(double2 (&a)[kRegs], const double2* __restrict__ c, int cm, int cv) {
-  double2 m0, m1, m2, m3;
-  if (MT != MT_X) {
-    m0 = c[0]; m1 = c[1]; m2 = c[2]; m3 = c[3];
-  }
+  const double2 m0 = c[0], m1 = c[1], m2 = c[2], m3 = c[3];
 #pragma unroll
   for (int r = 0; r < kRegs; ++r)
     if ((r & cm) == cv) pair_upd<MT>(a[r], a[r ^ XR], m0, m1, m2, m3);
@@ -103,7 +95,7 @@ __device__ __forceinline__ void phase1(double2 (&a)[kRegs], const double2 d) {
 }
 
 template <int K0, int K1>
-__device__ __forceinline__ void dense2(double2 (&a)[kRegs], const double2* __restrict__ M, int cm, int cv) {
+__device__ __forceinline__ void dense2(double2 (&a)[kRegs], const double2* __restrict__ M, int cm, int cv, int f) {
   constexpr int B0 = 1 << K0, B1 = 1 << K1;
 #pragma unroll
   for (int r = 0; r < kRegs; ++r) {
@@ -117,118 +109,115 @@ __device__ __forceinline__ void dense2(double2 (&a)[kRegs], const double2* __res
     for (int q = 0; q < 4; ++q) {
       double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
-      for (int cc = 0; cc < 4; ++cc) acc = cfma(M[q * 4 + cc], v[cc], acc);
+      for (int cc = 0; cc < 4; ++cc) acc = cfma(M[(q ^ f) * 4 + (cc ^ f)], v[cc], acc);
       a[idx[q]] = acc;
     }
   }
 }
 
 __device__ __forceinline__ void diagg(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef,
-                                      u64 phys_base) {
-  // table index = tconst | sum_k bit_k(r) * w_k   (w_k built without dynamic register indexing)
-  int tconst = 0, w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+                                      u64 phys_base, int fthr) {
+  // table index = (tconst | sum_k bit_k(r) * w_k) ^ tflip (w_k built without dynamic register indexing)
+  int tconst = 0, w0 = 0, w1 = 0, w2 = 0, w3 = 0, tflip = 0;
   const int nt = op.nt;
   for (int j = 0; j < nt; ++j) {
     const int rg = op.treg[j];
     const int bit = 1 << j;
-    if (rg == 0xFF) tconst |= int((phys_base >> op.tphys[j]) & 1ull) << j;
+    if (rg == 0xFF)
+      tconst |= int((phys_base >> op.tphys[j]) & 1ull) << j;
+    else if ((fthr >> rg) & 1)
+      tflip |= bit;
     w0 |= (rg == 0) ? bit : 0;
     w1 |= (rg == 1) ? bit : 0;
     w2 |= (rg == 2) ? bit : 0;
     w3 |= (rg == 3) ? bit : 0;
   }
-  const int cm = op.cm, cv = op.cv, tab = op.tab;
+  tconst ^= tflip;
+  const int cm = op.cm, cv = op.cv ^ (fthr & op.cm), tab = op.tab;
 #pragma unroll
   for (int r = 0; r < kRegs; ++r) {
     if ((r & cm) != cv) continue;
-    const int t = tconst | ((r & 1) ? w0 : 0) | ((r & 2) ? w1 : 0) | ((r & 4) ? w2 : 0) | ((r & 8) ? w3 : 0);
+    const int t = tconst ^ (((r & 1) ? w0 : 0) | ((r & 2) ? w1 : 0) | ((r & 4) ? w2 : 0) | ((r & 8) ? w3 : 0));
     cmul_ip(a[r], coef[tab + t]);
   }
 }
 
-#define PAIR1_CASE(K)                                            \
-  case K * 4 + MT_GENERAL: pair1<K, MT_GENERAL>(a, c); break;   \
-  case K * 4 + MT_REAL: pair1<K, MT_REAL>(a, c); break;         \
-  case K * 4 + MT_RXLIKE: pair1<K, MT_RXLIKE>(a, c); break;     \
-  case K * 4 + MT_X: pair1<K, MT_X>(a, c); break;
+#define PAIR1_CASE(K)                                                                           \
+  case CS_PAIR1 + K * 4 + MT_GENERAL: pair1<K, MT_GENERAL>(a, op.c[0], op.c[1], op.c[2], op.c[3]); break; \
+  case CS_PAIR1 + K * 4 + MT_REAL: pair1<K, MT_REAL>(a, op.c[0], op.c[1], op.c[2], op.c[3]); break;       \
+  case CS_PAIR1 + K * 4 + MT_RXLIKE: pair1<K, MT_RXLIKE>(a, op.c[0], op.c[1], op.c[2], op.c[3]); break;
+// PAIR1 on a bit whose per-thread flip is set: logical i0 sits in the bit-1 register -> swap roles
+#define PAIR1D_CASE(K)                                                                          \
+  case CS_PAIR1D + K * 4 + MT_GENERAL:                                                          \
+  case CS_PAIR1D + K * 4 + MT_REAL:                                                             \
+  case CS_PAIR1D + K * 4 + MT_RXLIKE: {                                                         \
+    const bool sw = (fthr >> K) & 1;                                                            \
+    const double2 m0 = sw ? op.c[3] : op.c[0], m1 = sw ? op.c[2] : op.c[1];                     \
+    const double2 m2 = sw ? op.c[1] : op.c[2], m3 = sw ? op.c[0] : op.c[3];                     \
+    if (op.mtype == MT_REAL) pair1<K, MT_REAL>(a, m0, m1, m2, m3);                              \
+    else if (op.mtype == MT_RXLIKE) pair1<K, MT_RXLIKE>(a, m0, m1, m2, m3);                     \
+    else pair1<K, MT_GENERAL>(a, m0, m1, m2, m3);                                               \
+    break;                                                                                      \
+  }
+#define PHASE1_CASE(K)                                                 \
+  case CS_PHASE1 + K * 2 + 0: phase1<K, 0>(a, op.c[0]); break;         \
+  case CS_PHASE1 + K * 2 + 1: phase1<K, 1>(a, op.c[0]); break;         \
+  case CS_PHASE1D + K * 2 + 0:                                         \
+  case CS_PHASE1D + K * 2 + 1:                                         \
+    if (((fthr >> K) & 1) ^ op.v) phase1<K, 1>(a, op.c[0]);            \
+    else phase1<K, 0>(a, op.c[0]);                                     \
+    break;
+#define PAIRG_CASE(XR)                                                                     \
+  case CS_PAIRGR + XR - 1: pairg<XR, MT_REAL>(a, op.c, op.cm, op.cv ^ (fthr & op.cm)); break; \
+  case CS_PAIRG + XR - 1: if (FULL) pairg<XR, MT_GENERAL>(a, op.c, op.cm, op.cv ^ (fthr & op.cm)); break;
 
-// Hot fields of an op record, prefetched one op ahead into registers (the op loop would
-// otherwise expose two dependent shared-memory latencies per op: record -> case -> coefficients).
-struct Hot {
-  u64 pm, pv;
-  int cs, cm, cv;
-  double2 c0, c1, c2, c3;
-};
-
-__device__ __forceinline__ Hot fetch(const FOp& o) {
-  Hot h;
-  h.pm = o.pm;
-  h.pv = o.pv;
-  h.cs = o.cs;
-  h.cm = o.cm;
-  h.cv = o.cv;
-  h.c0 = o.c[0];
-  h.c1 = o.c[1];
-  h.c2 = o.c[2];
-  h.c3 = o.c[3];
-  return h;
-}
-
-#undef PAIR1_CASE
-#define PAIR1_CASE(K)                                                              \
-  case CS_PAIR1 + K * 4 + MT_GENERAL: pair1<K, MT_GENERAL>(a, c); break;          \
-  case CS_PAIR1 + K * 4 + MT_REAL: pair1<K, MT_REAL>(a, c); break;                \
-  case CS_PAIR1 + K * 4 + MT_RXLIKE: pair1<K, MT_RXLIKE>(a, c); break;            \
-  case CS_PAIR1 + K * 4 + MT_X: pair1<K, MT_X>(a, c); break;
-#define PAIRGX_CASE(XR) \
-  case CS_PAIRGX + XR - 1: pairg<XR, MT_X>(a, c, h.cm, h.cv); break;
-#define PAIRG_CASE(XR) \
-  case CS_PAIRG + XR - 1: if (FULL) pairg<XR, MT_GENERAL>(a, c, h.cm, h.cv); break;
-
-// One flat switch on the dense case index (a single indirect branch).  FULL = false compiles
-// only the common kinds (fewer live registers); passes that need DIAGG / DENSE2 / general
-// PAIRG use the FULL kernel.  `op` (shared memory) is only read by the rare kinds.
+// One flat switch on the dense case index.  FULL = false compiles only the common kinds;
+// passes that need DIAGG / DENSE2 / complex PAIRG use the FULL kernel.  `op` is in shared memory.
 template <bool FULL>
-__device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const Hot& h, const FOp& op,
-                                         const double2* __restrict__ coef, u64 phys_base) {
-  const double2 c[4] = {h.c0, h.c1, h.c2, h.c3};
-  switch (h.cs) {
+__device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef,
+                                         u64 phys_base, int& fthr) {
+  switch (op.cs) {
     PAIR1_CASE(0) PAIR1_CASE(1) PAIR1_CASE(2) PAIR1_CASE(3)
-    case CS_PHASE1 + 0: phase1<0, 0>(a, h.c0); break;
-    case CS_PHASE1 + 1: phase1<0, 1>(a, h.c0); break;
-    case CS_PHASE1 + 2: phase1<1, 0>(a, h.c0); break;
-    case CS_PHASE1 + 3: phase1<1, 1>(a, h.c0); break;
-    case CS_PHASE1 + 4: phase1<2, 0>(a, h.c0); break;
-    case CS_PHASE1 + 5: phase1<2, 1>(a, h.c0); break;
-    case CS_PHASE1 + 6: phase1<3, 0>(a, h.c0); break;
-    case CS_PHASE1 + 7: phase1<3, 1>(a, h.c0); break;
-    case CS_SCALAR:
+    PAIR1D_CASE(0) PAIR1D_CASE(1) PAIR1D_CASE(2) PAIR1D_CASE(3)
+    PHASE1_CASE(0) PHASE1_CASE(1) PHASE1_CASE(2) PHASE1_CASE(3)
+    case CS_SCALAR: {
+      const double2 d = op.c[0];
 #pragma unroll
-      for (int r = 0; r < kRegs; ++r) cmul_ip(a[r], h.c0);
+      for (int r = 0; r < kRegs; ++r) cmul_ip(a[r], d);
       break;
-    PAIRGX_CASE(1) PAIRGX_CASE(2) PAIRGX_CASE(3) PAIRGX_CASE(4) PAIRGX_CASE(5) PAIRGX_CASE(6) PAIRGX_CASE(7)
-    PAIRGX_CASE(8) PAIRGX_CASE(9) PAIRGX_CASE(10) PAIRGX_CASE(11) PAIRGX_CASE(12) PAIRGX_CASE(13)
-    PAIRGX_CASE(14) PAIRGX_CASE(15)
+    }
+    case CS_XFLIP + 0: fthr ^= 1; break;
+    case CS_XFLIP + 1: fthr ^= 2; break;
+    case CS_XFLIP + 2: fthr ^= 4; break;
+    case CS_XFLIP + 3: fthr ^= 8; break;
     PAIRG_CASE(1) PAIRG_CASE(2) PAIRG_CASE(3) PAIRG_CASE(4) PAIRG_CASE(5) PAIRG_CASE(6) PAIRG_CASE(7)
     PAIRG_CASE(8) PAIRG_CASE(9) PAIRG_CASE(10) PAIRG_CASE(11) PAIRG_CASE(12) PAIRG_CASE(13)
     PAIRG_CASE(14) PAIRG_CASE(15)
     case CS_DIAGG:
-      if (FULL) diagg(a, op, coef, phys_base);
+      if (FULL) diagg(a, op, coef, phys_base, fthr);
       break;
-    case CS_DENSE2 + 0: if (FULL) dense2<0, 1>(a, coef + op.tab, h.cm, h.cv); break;
-    case CS_DENSE2 + 1: if (FULL) dense2<0, 2>(a, coef + op.tab, h.cm, h.cv); break;
-    case CS_DENSE2 + 2: if (FULL) dense2<0, 3>(a, coef + op.tab, h.cm, h.cv); break;
-    case CS_DENSE2 + 3: if (FULL) dense2<1, 2>(a, coef + op.tab, h.cm, h.cv); break;
-    case CS_DENSE2 + 4: if (FULL) dense2<1, 3>(a, coef + op.tab, h.cm, h.cv); break;
-    case CS_DENSE2 + 5: if (FULL) dense2<2, 3>(a, coef + op.tab, h.cm, h.cv); break;
     default:
+      if (FULL && op.cs >= CS_DENSE2 && op.cs < CS_DENSE2 + 6) {
+        const int k0 = op.xr & 15, k1 = op.xr >> 4;
+        const int f = ((fthr >> k0) & 1) | (((fthr >> k1) & 1) << 1);
+        const int cv = op.cv ^ (fthr & op.cm);
+        const double2* M = coef + op.tab;
+        switch (op.cs - CS_DENSE2) {
+          case 0: dense2<0, 1>(a, M, op.cm, cv, f); break;
+          case 1: dense2<0, 2>(a, M, op.cm, cv, f); break;
+          case 2: dense2<0, 3>(a, M, op.cm, cv, f); break;
+          case 3: dense2<1, 2>(a, M, op.cm, cv, f); break;
+          case 4: dense2<1, 3>(a, M, op.cm, cv, f); break;
+          default: dense2<2, 3>(a, M, op.cm, cv, f); break;
+        }
+      }
       break;
   }
 }
 
 // DB = true : one persistent CTA per SM, two tile buffers, tile t+grid prefetched during tile t.
 // DB = false: two CTAs per SM (128 registers), one buffer each; CTAs overlap each other instead.
-// Dynamic shared memory: [tile buffer(s)] [op records of the pass (if <= kMaxSmemOps)].
+// Dynamic shared memory: [tile buffer(s)] [op records of the pass].
 template <bool FULL, bool DB>
 __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__ state, const FPassArgs P,
                                                             const FPhase* __restrict__ phases,
@@ -240,15 +229,13 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
   const int nthreads = blockDim.x;            // 2^(b-4)
   const int T = 1 << P.b;
   // stage the pass's op records in shared memory (uniform broadcast reads in the op loop)
-  const int nops = P.op_end - P.op_begin;
-  const FOp* OPS = ops;                       // indexed with global op numbers
-  if (nops <= kMaxSmemOps) {
-    FOp* s_ops = reinterpret_cast<FOp*>(smem_raw + size_t(DB ? 2 : 1) * T * sizeof(double2));
+  FOp* s_ops = reinterpret_cast<FOp*>(smem_raw + size_t(DB ? 2 : 1) * T * sizeof(double2));
+  {
+    const int nops = P.op_end - P.op_begin;
     const int4* src = reinterpret_cast<const int4*>(ops + P.op_begin);
     int4* dst = reinterpret_cast<int4*>(s_ops);
     const int n16 = nops * int(sizeof(FOp) / 16);
     for (int i = tid; i < n16; i += nthreads) dst[i] = src[i];
-    OPS = s_ops - P.op_begin;
     __syncthreads();
   }
   // load slot i of this thread is tile index s = tid + nthreads * i
@@ -285,6 +272,7 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
+  const FOp* OPS = s_ops - P.op_begin;        // indexed with global op numbers
   int cur = 0;
   if (DB && blockIdx.x < P.n_tiles) issue_load(blockIdx.x, tile_mem);
   for (u64 t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
@@ -312,19 +300,15 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
 #pragma unroll
       for (int r = 0; r < kRegs; ++r)
         a[r] = tile[s0 ^ ((r & 1) ? W0 : 0) ^ ((r & 2) ? W1 : 0) ^ ((r & 4) ? W2 : 0) ^ ((r & 8) ? W3 : 0)];
+      int fthr = 0;   // per-thread register relabeling from thread-predicated X gates
       const int oe = F.op_end;
-      int oi = F.op_begin;
-      if (oi < oe) {
-        Hot h = fetch(OPS[oi]);
-        for (; oi < oe; ++oi) {
-          const Hot hn = fetch(OPS[oi + 1 < oe ? oi + 1 : oi]);   // software prefetch
-          if ((phys_base & h.pm) == h.pv) apply_op<FULL>(a, h, OPS[oi], coef, phys_base);
-          h = hn;
-        }
+      for (int oi = F.op_begin; oi < oe; ++oi) {
+        const FOp& op = OPS[oi];
+        if ((phys_base & op.pm) == op.pv) apply_op<FULL>(a, op, coef, phys_base, fthr);
       }
       {
         // register r holds logical index r ^ flip: store offset = swz(sthr) ^ W(r ^ flip) (W linear)
-        const int fl = F.flip;
+        const int fl = F.flip ^ fthr;
         const int sf = s0 ^ ((fl & 1) ? W0 : 0) ^ ((fl & 2) ? W1 : 0) ^ ((fl & 4) ? W2 : 0) ^ ((fl & 8) ? W3 : 0);
 #pragma unroll
         for (int r = 0; r < kRegs; ++r)
@@ -441,7 +425,7 @@ void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& pr
     const int threads = 1 << (A.b - kRB);
     const int nops = A.op_end - A.op_begin;
     const size_t smem = (db ? 2 : 1) * (size_t(1) << b) * sizeof(double2) +
-                        (nops <= kMaxSmemOps ? size_t(nops) * sizeof(FOp) : 0);
+                        size_t(nops) * sizeof(FOp);
     // persistent grid: one (DB) or two CTAs per SM
     const u64 grid = std::min<u64>(A.n_tiles, u64(dev_sms) * (db ? 1 : 2));
     const double bytes = 32.0 * double(h->n_local);

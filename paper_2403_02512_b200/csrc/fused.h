@@ -38,14 +38,20 @@ struct __align__(16) FOp {
   int pad;
   double2 c[4];          // inline coefficients (PAIR1 / PAIRG: m00 m01 m10 m11; PHASE1 / SCALAR: d)
 };
-// dense dispatch cases
-constexpr int CS_PAIR1 = 0;      // + k*4 + mtype          (0..15)
-constexpr int CS_PHASE1 = 16;    // + k*2 + v              (16..23)
+// Dense dispatch cases.  No case moves amplitudes between registers (data-moving swaps
+// poison register allocation for the whole op loop): X gates become register relabelings --
+// uniform ones are applied by the host (FPhase.flip), thread-predicated ones toggle a
+// per-thread flip mask (CS_XFLIP) that the *D cases and the phase store honour.
+constexpr int CS_PAIR1 = 0;      // + k*4 + mtype (mtype != MT_X)            (0..15)
+constexpr int CS_PHASE1 = 16;    // + k*2 + v                                (16..23)
 constexpr int CS_SCALAR = 24;
-constexpr int CS_PAIRGX = 25;    // + xr - 1               (25..39)
-constexpr int CS_PAIRG = 40;     // + xr - 1               (40..54)
+constexpr int CS_PAIRGR = 25;    // + xr - 1: real-matrix PAIRG (controlled X) (25..39)
+constexpr int CS_PAIRG = 40;     // + xr - 1: complex PAIRG                  (40..54)
 constexpr int CS_DIAGG = 55;
-constexpr int CS_DENSE2 = 56;    // + pair index 0..5      (56..61)
+constexpr int CS_DENSE2 = 56;    // + pair index 0..5                        (56..61)
+constexpr int CS_XFLIP = 62;     // + k: thread-predicated X on register bit k (62..65)
+constexpr int CS_PAIR1D = 66;    // + k*4 + mtype: PAIR1 on a dynamically flipped bit (66..81)
+constexpr int CS_PHASE1D = 82;   // + k*2 + v: PHASE1 on a dynamically flipped bit   (82..89)
 static_assert(sizeof(FOp) == 112, "FOp layout");
 
 struct FPhase {

@@ -58,7 +58,7 @@ std::vector<PassPlan> plan_passes(int nl, const std::vector<Prim>& prims, int b)
     for (size_t k = 0; k < remaining.size(); ++k) {
       const int i = remaining[k];
       const Req& r = req[i];
-      bool ok = k < window && r.fusable;
+      bool ok = k < window && r.fusable && int(pp.prims.size()) < kMaxSmemOps;   // op records fit in smem
       if (ok) {
         const u64 blocked = r.diag ? (r.support & def_nd) : (r.support & (def_nd | def_d));
         ok = blocked == 0 && popcount64(B | r.dense) <= b;
@@ -137,7 +137,8 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
       if (reg[k] == tp) return k;
     return -1;
   };
-  int F = 0;
+  int F = 0;   // uniform flips (applied here, on the host)
+  int D = 0;   // register bits that may carry a per-thread flip (handled by the kernel)
   for (int i : list) {
     const Prim& p = prims[i];
     FOp op;
@@ -168,6 +169,14 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
         F ^= op.xr;
         continue;
       }
+      if (single && mt == MT_X) {                 // thread-predicated X: per-thread relabel
+        op.kind = FK_PAIR1;
+        op.k = uint8_t(__builtin_ctz(op.xr));
+        op.cs = CS_XFLIP + op.k;
+        D |= op.xr;
+        prog.ops.push_back(op);
+        continue;
+      }
       std::vector<cplx> m = p.m;
       if (single && (op.cv & op.xr)) {            // i0 sits on the bit-1 register: swap roles
         m = {p.m[3], p.m[2], p.m[1], p.m[0]};
@@ -179,7 +188,7 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
         op.mtype = uint8_t(mtype_of(m));
       } else {
         op.kind = FK_PAIRG;
-        op.mtype = uint8_t(mt == MT_X ? MT_X : MT_GENERAL);
+        op.mtype = uint8_t((mt == MT_X || mt == MT_REAL) ? MT_REAL : MT_GENERAL);
       }
       for (int j = 0; j < 4; ++j) prog.coef.push_back(make_double2(m[j].real(), m[j].imag()));
     } else if (p.type == PRIM_DIAG && p.nb == 0 && popcount64(op.cm) <= 1) {
@@ -226,11 +235,12 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
       op.cv &= uint8_t(~tb);
       for (auto& c : mf) prog.coef.push_back(make_double2(c.real(), c.imag()));
     }
+    const bool dyn = ((D >> op.k) & 1) != 0;
     switch (op.kind) {
-      case FK_PAIR1: op.cs = CS_PAIR1 + op.k * 4 + op.mtype; break;
-      case FK_PHASE1: op.cs = CS_PHASE1 + op.k * 2 + op.v; break;
+      case FK_PAIR1: op.cs = (dyn ? CS_PAIR1D : CS_PAIR1) + op.k * 4 + op.mtype; break;
+      case FK_PHASE1: op.cs = (dyn ? CS_PHASE1D : CS_PHASE1) + op.k * 2 + op.v; break;
       case FK_SCALAR: op.cs = CS_SCALAR; break;
-      case FK_PAIRG: op.cs = (op.mtype == MT_X ? CS_PAIRGX : CS_PAIRG) + op.xr - 1; break;
+      case FK_PAIRG: op.cs = (op.mtype == MT_REAL ? CS_PAIRGR : CS_PAIRG) + op.xr - 1; break;
       case FK_DIAGG: op.cs = CS_DIAGG; break;
       default: {
         static const uint8_t pairs[6] = {0x10, 0x20, 0x30, 0x21, 0x31, 0x32};
@@ -338,7 +348,7 @@ Program build_program(int nl, const std::vector<Prim>& prims, std::vector<PassPl
     for (int ph = A.phase_begin; ph < A.phase_begin + A.n_phases; ++ph)
       for (int oi = prog.phases[ph].op_begin; oi < prog.phases[ph].op_end; ++oi) {
         const FOp& o = prog.ops[oi];
-        full |= o.kind == FK_DIAGG || o.kind == FK_DENSE2 || (o.kind == FK_PAIRG && o.mtype != MT_X);
+        full |= o.kind == FK_DIAGG || o.kind == FK_DENSE2 || (o.kind == FK_PAIRG && o.mtype == MT_GENERAL);
       }
     prog.full.push_back(full ? 1 : 0);
     prog.passes.push_back(A);
