@@ -137,6 +137,10 @@ int sv_reset_stats(sv_handle* h);
 /* Fusion plan summary for an op list (host-only; no GPU needed):
  * out[0]=passes, out[1]=ops, out[2]=tile bits, out[3]=phases. */
 int sv_plan_summary(int n_qubits, const sv_op* ops, int n_ops, int64_t* out4);
+/* The fused program itself, flattened (format: fused_plan.cpp serialize_program); host-only.
+ * sizes2 receives the needed int64 / double counts; buffers are filled when large enough. */
+int sv_plan_program(int n_qubits, const sv_op* ops, int n_ops, int64_t* ints, int64_t ints_cap, double* dbls,
+                    int64_t dbls_cap, int64_t* sizes2);
 
 #ifdef __cplusplus
 }

@@ -133,10 +133,13 @@ static void check_handle(const sv_handle* h) {
 static void exec_prims(sv_handle* h, const std::vector<double2*>& states, std::vector<Prim>& prims, int fuse) {
   if (prims.empty()) return;
   fold_diag_phases(prims);
-  for (double2* st : states) {
-    if (fuse)
-      apply_prims_fused(h, st, prims);
-    else
+  if (fuse) {
+    // fused passes may relabel qubits inside their tiles: the qubit at local position p ends at perm[p]
+    const std::vector<int> perm = apply_prims_fused(h, states, prims);
+    for (int o = 0; o < h->n; ++o)
+      if (h->phys[o] < h->nl) h->phys[o] = perm[h->phys[o]];
+  } else {
+    for (double2* st : states)
       for (const Prim& p : prims) launch_prim(h, st, p);
   }
   prims.clear();
@@ -705,9 +708,10 @@ int sv_reset_stats(sv_handle* h) {
   API_END
 }
 
-int sv_plan_summary(int n_qubits, const sv_op* ops, int n_ops, int64_t* out4) {
-  API_BEGIN
+// the prim list exec_prims would fuse for this op list on one GPU (identity layout)
+static std::vector<Prim> host_prims(int n_qubits, const sv_op* ops, int n_ops) {
   if (n_qubits < 1 || n_qubits > 62) sv_fail(SV_ERR_VALIDATION, "bad qubit count");
+  if (n_ops < 0 || (n_ops > 0 && !ops)) sv_fail(SV_ERR_VALIDATION, "bad op list");
   std::vector<Prim> prims;
   int col = 0;
   for (int i = 0; i < n_ops; ++i) {
@@ -715,11 +719,30 @@ int sv_plan_summary(int n_qubits, const sv_op* ops, int n_ops, int64_t* out4) {
     for (auto& pc : lower_op(ops[i], n_qubits, col, false, nullptr))
       if (!pc.fwd.skip) prims.push_back(pc.fwd);
   }
-  PlanStats s = plan_stats(n_qubits, prims);
+  fold_diag_phases(prims);
+  return prims;
+}
+
+int sv_plan_summary(int n_qubits, const sv_op* ops, int n_ops, int64_t* out4) {
+  API_BEGIN
+  PlanStats s = plan_stats(n_qubits, host_prims(n_qubits, ops, n_ops));
   out4[0] = s.passes;
   out4[1] = s.ops;
   out4[2] = s.tile_bits;
   out4[3] = s.phases;
+  API_END
+}
+
+int sv_plan_program(int n_qubits, const sv_op* ops, int n_ops, int64_t* ints, int64_t ints_cap, double* dbls,
+                    int64_t dbls_cap, int64_t* sizes2) {
+  API_BEGIN
+  std::vector<int64_t> I;
+  std::vector<double> D;
+  plan_program_serialized(n_qubits, host_prims(n_qubits, ops, n_ops), I, D);
+  sizes2[0] = int64_t(I.size());
+  sizes2[1] = int64_t(D.size());
+  if (ints && int64_t(I.size()) <= ints_cap) std::memcpy(ints, I.data(), I.size() * sizeof(int64_t));
+  if (dbls && int64_t(D.size()) <= dbls_cap) std::memcpy(dbls, D.data(), D.size() * sizeof(double));
   API_END
 }
 

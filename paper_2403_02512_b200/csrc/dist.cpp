@@ -126,8 +126,8 @@ void dist_make_local_set(sv_handle* h, const std::vector<double2*>& states, cons
   for (int o : offs) make_one_local(h, states, o, offs);
 }
 
+// Restore the identity layout (fused passes and sharded swaps leave qubits relabeled).
 void dist_canonicalize(sv_handle* h, const std::vector<double2*>& states) {
-  if (h->world == 1) return;
   // global positions first: logical offset G must sit at physical G
   for (int G = h->nl; G < h->n; ++G) {
     if (h->phys[G] == G) continue;

@@ -316,10 +316,33 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
       }
       __syncthreads();
     }
-    // shared -> global (this buffer is refilled only after the next iteration's barrier)
-    const u64 gbase = base | spread_tid;
+    // shared -> global with the pass's in-tile relabeling: store-loop slot (tid, i) covers tile
+    // index bits q[0..] and lands on physical positions tpos_st[q[..]] (q[0..2] -> bits 0..2, so
+    // 8 lanes still write 128 contiguous bytes).  Same address set as the load: in-place safe.
+    // (This buffer is refilled only after the next iteration's barrier.)
+    {
+      u64 st_tid = 0;
+      int sq_tid = 0;
+      for (int j = 0; j < P.nthr; ++j)
+        if ((tid >> j) & 1) {
+          st_tid |= 1ull << P.tpos_st[P.q[j]];
+          sq_tid |= 1 << P.q[j];
+        }
+      const u64 gb = base | st_tid;
+      const int sw_tid = swz(sq_tid);
 #pragma unroll
-    for (int i = 0; i < kRegs; ++i) state[gbase | spread_hi(i)] = tile[swz_tid ^ swz_hi(i)];
+      for (int i = 0; i < kRegs; ++i) {
+        u64 g = gb;
+        int s = 0;
+#pragma unroll
+        for (int j = 0; j < kRB; ++j)
+          if ((i >> j) & 1) {
+            g |= 1ull << P.tpos_st[P.q[P.nthr + j]];
+            s |= 1 << P.q[P.nthr + j];
+          }
+        state[g] = tile[sw_tid ^ swz(s)];
+      }
+    }
     cur ^= 1;
   }
 }
@@ -369,17 +392,21 @@ void release_fused(sv_handle* h) {
     }
 }
 
-void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& prims) {
+std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& states, const std::vector<Prim>& prims) {
   using namespace fused;
+  std::vector<int> identity(h->nl);
+  for (int p = 0; p < h->nl; ++p) identity[p] = p;
   if (h->nl < 5) {
-    for (const Prim& p : prims) launch_prim(h, state, p);
-    return;
+    for (double2* st : states)
+      for (const Prim& p : prims) launch_prim(h, st, p);
+    return identity;
   }
-  std::vector<PassPlan> plan;
-  Program prog = build_program(h->nl, prims, plan);
+  static const bool remap = !(getenv("SVB200_REMAP") && std::string(getenv("SVB200_REMAP")) == "0");
+  Program prog = build_program(h->nl, prims, remap);
   if (prog.passes.empty()) {
-    for (const Prim& p : prims) launch_prim(h, state, p);
-    return;
+    for (double2* st : states)
+      for (const Prim& p : prog.singles) launch_prim(h, st, p);
+    return identity;
   }
   // upload phases | ops | coef in one copy (the buffer is only reused after a stream sync)
   auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
@@ -409,37 +436,39 @@ void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& pr
     set_smem_attr<true, false>(tile + ops_b);
     set_smem_attr<false, false>(tile + ops_b);
     CUDA_CHECK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
-    const char* mode = getenv("SVB200_FUSED_MODE");   // "sb": single-buffer, 2 CTAs/SM
-    db = !(mode && std::string(mode) == "sb");
+    // default: single buffer, 2 CTAs/SM (measured faster: 16 warps hide the op-loop latency
+    // better than 8 warps with a prefetched tile); "db" selects the double-buffered variant
+    const char* mode = getenv("SVB200_FUSED_MODE");
+    db = mode && std::string(mode) == "db";
   });
   const int b = prog.passes[0].b;
-  size_t pi = 0;
-  for (auto& pp : plan) {
-    if (!pp.fused) {
-      launch_prim(h, state, prims[pp.single]);
-      continue;
+  for (double2* state : states) {
+    for (const Step& s : prog.steps) {
+      if (!s.fused) {
+        launch_prim(h, state, prog.singles[s.index]);
+        continue;
+      }
+      const FPassArgs& A = prog.passes[s.index];
+      const bool full = prog.full[s.index];
+      const int threads = 1 << (A.b - kRB);
+      const int nops = A.op_end - A.op_begin;
+      const size_t smem = (db ? 2 : 1) * (size_t(1) << b) * sizeof(double2) + size_t(nops) * sizeof(FOp);
+      // persistent grid: one (DB) or two CTAs per SM
+      const u64 grid = std::min<u64>(A.n_tiles, u64(dev_sms) * (db ? 1 : 2));
+      const double bytes = 32.0 * double(h->n_local);
+      cudaEvent_t ev[2];
+      stat_begin(h, KC_FUSED, bytes, ev);
+      if (db && full)
+        k_fused<true, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+      else if (db)
+        k_fused<false, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+      else if (full)
+        k_fused<true, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+      else
+        k_fused<false, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+      stat_end(h, KC_FUSED, bytes, ev);
+      CUDA_CHECK(cudaGetLastError());
     }
-    const FPassArgs& A = prog.passes[pi];
-    const bool full = prog.full[pi];
-    ++pi;
-    const int threads = 1 << (A.b - kRB);
-    const int nops = A.op_end - A.op_begin;
-    const size_t smem = (db ? 2 : 1) * (size_t(1) << b) * sizeof(double2) +
-                        size_t(nops) * sizeof(FOp);
-    // persistent grid: one (DB) or two CTAs per SM
-    const u64 grid = std::min<u64>(A.n_tiles, u64(dev_sms) * (db ? 1 : 2));
-    const double bytes = 32.0 * double(h->n_local);
-    cudaEvent_t ev[2];
-    stat_begin(h, KC_FUSED, bytes, ev);
-    if (db && full)
-      k_fused<true, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
-    else if (db)
-      k_fused<false, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
-    else if (full)
-      k_fused<true, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
-    else
-      k_fused<false, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
-    stat_end(h, KC_FUSED, bytes, ev);
-    CUDA_CHECK(cudaGetLastError());
   }
+  return prog.perm;
 }

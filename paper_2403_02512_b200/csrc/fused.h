@@ -64,28 +64,38 @@ struct FPhase {
 struct FPassArgs {
   int b;                 // tile bits
   int nthr;              // b - kRB
-  unsigned char tpos[kMaxB];   // physical positions of tile bits (ascending)
-  int n_outer_ins;
+  unsigned char tpos[kMaxB];     // physical positions of tile bits at load (ascending)
+  unsigned char tpos_st[kMaxB];  // physical position of tile bit j at store (a permutation of tpos:
+                                 // the pass relabels qubits inside its tile for free)
+  unsigned char q[kMaxB];        // store-loop order of tile bits (q[0..2] land on physical bits 0..2)
   u64 n_tiles;
   int phase_begin, n_phases;
   int op_begin, op_end;  // op records of the whole pass (contiguous)
 };
 
-struct PassPlan {
+// One step of a planned program: a fused pass (index into Program::passes) or a single
+// unfusable primitive (index into Program::singles), in execution order.
+struct Step {
   bool fused = false;
-  int single = -1;            // prim index when not fused
-  u64 tile_bits = 0;
-  std::vector<int> prims;     // in application order
+  int index = -1;
 };
 
 struct Program {
+  std::vector<Step> steps;
   std::vector<FPassArgs> passes;
   std::vector<char> full;          // pass needs the FULL kernel variant
+  std::vector<Prim> singles;       // unfusable prims, already in the layout at their step
   std::vector<FPhase> phases;
   std::vector<FOp> ops;
   std::vector<double2> coef;
+  std::vector<int> perm;           // final layout: physical position p now holds what was at p before...
+                                   // ... i.e. the qubit at p moved to perm[p]
+  int64_t n_prims_in = 0, n_prims_merged = 0;
 };
 
-Program build_program(int nl, const std::vector<Prim>& prims, std::vector<PassPlan>& plan);
+// remap = let passes relabel qubits inside their tile (moves upcoming qubits onto the low bits)
+Program build_program(int nl, const std::vector<Prim>& prims, bool remap);
+// flat int64/double serialisation of a program (tests/fused_emulator.py re-executes it on the CPU)
+void serialize_program(const Program& prog, int nl, std::vector<int64_t>& ints, std::vector<double>& dbls);
 
 }  // namespace fused

@@ -1,86 +1,114 @@
-// Host planner of the K7 fusion engine: pass construction, register-phase scheduling and
-// device-op emission (see fused.h for the program format and fused.cu for the kernel).
+// Host planner of the K7 fusion engine: pass construction, register-phase scheduling, gate
+// merging, in-tile qubit relabeling and device-op emission (program format: fused.h; kernel:
+// fused.cu).
+//
+// Commutation is decided per bit: a primitive acts on each bit of its support either Z-like
+// (diagonal: controls, diagonal-table bits), X-like (a single-target 2x2 of the form aI + bX,
+// e.g. RX or the X of a CNOT) or generally.  Two primitives commute when every shared bit is
+// Z-like in both or X-like in both -- so RZ slides past CNOT controls and RX past CNOT targets.
 #include <algorithm>
 #include <cstring>
 
 #include "fused.h"
 
 namespace fused {
+namespace {
 
 struct Req {
   u64 dense = 0;     // bits that must be register bits
   u64 support = 0;   // every bit the prim reads
+  u64 zb = 0, xb = 0;
   bool diag = false;
   bool fusable = true;
 };
+
+bool is_xlike(const std::vector<cplx>& m) { return m.size() == 4 && m[0] == m[3] && m[1] == m[2]; }
 
 Req requirements(const Prim& p) {
   Req r;
   if (p.type == PRIM_PAIR) {
     r.dense = p.xmask;
     r.support = p.fmask | p.xmask;
+    r.zb = p.fmask & ~p.xmask;
+    if (popcount64(p.xmask) == 1 && is_xlike(p.m)) r.xb = p.xmask;
     r.fusable = popcount64(p.xmask) <= kRB;
   } else if (p.type == PRIM_DIAG) {
     r.diag = true;
     r.support = p.fmask;
     for (int j = 0; j < p.nb; ++j) r.support |= 1ull << p.pos[j];
+    r.zb = r.support;
     r.fusable = p.nb <= 6;
   } else {
     for (int j = 0; j < p.nb; ++j) r.dense |= 1ull << p.pos[j];
     r.support = p.fmask | r.dense;
+    r.zb = p.fmask & ~r.dense;
     r.fusable = p.nb <= 2;
   }
   return r;
 }
 
-std::vector<PassPlan> plan_passes(int nl, const std::vector<Prim>& prims, int b) {
-  std::vector<Req> req(prims.size());
-  for (size_t i = 0; i < prims.size(); ++i) req[i] = requirements(prims[i]);
-  std::vector<int> remaining(prims.size());
-  for (size_t i = 0; i < prims.size(); ++i) remaining[i] = int(i);
-  std::vector<PassPlan> out;
-  const u64 low = (1ull << std::min(3, nl)) - 1;
-  const size_t window = 4096;
-  while (!remaining.empty()) {
-    const int p0 = remaining[0];
-    if (!req[p0].fusable || nl < 5) {
-      PassPlan s;
-      s.single = p0;
-      out.push_back(s);
-      remaining.erase(remaining.begin());
-      continue;
-    }
-    PassPlan pp;
-    pp.fused = true;
-    u64 B = low;
-    u64 def_nd = 0, def_d = 0;
-    std::vector<int> rest;
-    for (size_t k = 0; k < remaining.size(); ++k) {
-      const int i = remaining[k];
-      const Req& r = req[i];
-      bool ok = k < window && r.fusable && int(pp.prims.size()) < kMaxSmemOps;   // op records fit in smem
-      if (ok) {
-        const u64 blocked = r.diag ? (r.support & def_nd) : (r.support & (def_nd | def_d));
-        ok = blocked == 0 && popcount64(B | r.dense) <= b;
-      }
-      if (ok) {
-        B |= r.dense;
-        pp.prims.push_back(i);
-      } else {
-        if (r.diag)
-          def_d |= r.support;
-        else
-          def_nd |= r.support;
-        rest.push_back(i);
-      }
-    }
-    // fill the tile up to b bits with the lowest unused positions (longer contiguous runs)
-    for (int p = 0; p < nl && popcount64(B) < b; ++p) B |= 1ull << p;
-    pp.tile_bits = B;
-    out.push_back(pp);
-    remaining.swap(rest);
+bool commute(const Req& a, const Req& b) {
+  const u64 shared = a.support & b.support;
+  return (shared & ~((a.zb & b.zb) | (a.xb & b.xb))) == 0;
+}
+
+// union of the per-bit action classes of the prims deferred to later passes
+struct Deferred {
+  u64 z = 0, x = 0, g = 0;
+  void add(const Req& r) {
+    z |= r.zb;
+    x |= r.xb;
+    g |= r.support & ~(r.zb | r.xb);
   }
-  return out;
+  bool blocks(const Req& r) const {
+    const u64 rg = r.support & ~(r.zb | r.xb);
+    return (r.support & g) || (r.zb & x) || (r.xb & z) || (rg & (z | x));
+  }
+};
+
+u64 permute_mask(u64 m, const int* perm) {
+  u64 o = 0;
+  for (int b = 0; b < 64 && m; ++b)
+    if ((m >> b) & 1) {
+      o |= 1ull << perm[b];
+      m &= ~(1ull << b);
+    }
+  return o;
+}
+
+// relabel physical bits of a prim (positions stay ascending; tables / matrices follow)
+void relabel(Prim& p, const int* perm) {
+  p.fmask = permute_mask(p.fmask, perm);
+  p.fval = permute_mask(p.fval, perm);
+  p.xmask = permute_mask(p.xmask, perm);
+  if (p.nb == 0) return;
+  const int k = p.nb;
+  int np[16], order[16];
+  for (int j = 0; j < k; ++j) {
+    np[j] = perm[p.pos[j]];
+    order[j] = j;
+  }
+  std::sort(order, order + k, [&](int x, int y) { return np[x] < np[y]; });
+  int rank[16];   // old index bit j -> new index bit rank[j]
+  for (int i = 0; i < k; ++i) {
+    rank[order[i]] = i;
+    p.pos[i] = np[order[i]];
+  }
+  const size_t d = size_t(1) << k;
+  auto map_idx = [&](size_t r) {
+    size_t o = 0;
+    for (int j = 0; j < k; ++j)
+      if ((r >> j) & 1) o |= size_t(1) << rank[j];
+    return o;
+  };
+  std::vector<cplx> m(p.m.size());
+  if (p.type == PRIM_DIAG) {
+    for (size_t r = 0; r < d; ++r) m[map_idx(r)] = p.m[r];
+  } else {
+    for (size_t r = 0; r < d; ++r)
+      for (size_t c = 0; c < d; ++c) m[map_idx(r) * d + map_idx(c)] = p.m[r * d + c];
+  }
+  p.m = m;
 }
 
 int mtype_of(const std::vector<cplx>& m) {
@@ -126,7 +154,8 @@ void make_phase_thr(FPhase& F, const std::vector<int>& reg, int b) {
 
 // Emit the device ops of one phase.  Unconditional X on a register bit is not executed: it is
 // absorbed into a flip mask F (logical register index j lives in register j ^ F); later ops of
-// the phase are rewritten for F and the phase's store offsets apply it.  Returns F.
+// the phase are rewritten for F and the phase's store offsets apply it.  Thread-predicated X
+// becomes CS_XFLIP (per-thread relabel) and later ops on that bit use the *D cases.  Returns F.
 int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<int>& list, const int* tile_pos_of,
              const std::vector<int>& reg) {
   // phys bit -> register index (or -1)
@@ -256,32 +285,54 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
   return F;
 }
 
-// List-schedule a pass's prims into register phases.  Prims may be reordered only past prims
-// they commute with (disjoint support, or both diagonal); each phase picks up to 4 register
-// bits and runs every ready prim whose dense bits fit, to a fixpoint.
+// Can prim i be folded into prim j (j runs right before i on every bit i touches)?
+bool mergeable(const Prim& j, const Prim& i) {
+  if (j.type != i.type || j.fmask != i.fmask || j.fval != i.fval) return false;
+  if (i.type == PRIM_PAIR) return j.xmask == i.xmask && popcount64(i.xmask) == 1;
+  if (i.type == PRIM_DIAG) {
+    if (i.nb != j.nb) return false;
+    for (int t = 0; t < i.nb; ++t)
+      if (i.pos[t] != j.pos[t]) return false;
+    return true;
+  }
+  return false;
+}
+
+void merge_into(Prim& j, const Prim& i) {
+  if (i.type == PRIM_PAIR) {   // apply j then i: M = Mi * Mj
+    const std::vector<cplx> a = i.m, b = j.m;
+    j.m = {a[0] * b[0] + a[1] * b[2], a[0] * b[1] + a[1] * b[3], a[2] * b[0] + a[3] * b[2], a[2] * b[1] + a[3] * b[3]};
+  } else {
+    for (size_t t = 0; t < j.m.size(); ++t) j.m[t] *= i.m[t];
+  }
+}
+
+// List-schedule a pass's prims into register phases.  Prims are reordered only past prims
+// they commute with; each phase picks up to 4 register bits and runs every ready prim whose
+// dense bits fit, to a fixpoint.  A prim that immediately follows a compatible prim on all of
+// its bits is multiplied into it (one op instead of two).
 // Returns (register-bit mask in physical positions, prims in execution order) per phase.
-std::vector<std::pair<u64, std::vector<int>>> schedule_phases(const std::vector<Prim>& prims,
-                                                              const std::vector<int>& list) {
+std::vector<std::pair<u64, std::vector<int>>> schedule_phases(std::vector<Prim>& prims, const std::vector<int>& list,
+                                                              int64_t& merged) {
   const int L = int(list.size());
   std::vector<Req> rq(L);
   for (int i = 0; i < L; ++i) rq[i] = requirements(prims[list[i]]);
-  // remaining-predecessor counts and successor lists of the conflict DAG
   std::vector<int> npred(L, 0);
   std::vector<std::vector<int>> succ(L);
   for (int i = 0; i < L; ++i)
-    for (int j = 0; j < i; ++j) {
-      const bool commute = (rq[i].diag && rq[j].diag) || (rq[i].support & rq[j].support) == 0;
-      if (!commute) {
+    for (int j = 0; j < i; ++j)
+      if (!commute(rq[i], rq[j])) {
         succ[j].push_back(i);
         npred[i]++;
       }
-    }
   std::vector<char> done(L, 0);
   int ndone = 0;
   std::vector<std::pair<u64, std::vector<int>>> phases;
   while (ndone < L) {
     u64 R = 0;
     std::vector<int> order;
+    int last_on[64];   // per bit: index (into list) of the last op of this phase touching it
+    for (int b = 0; b < 64; ++b) last_on[b] = -1;
     for (;;) {
       bool progress = false;
       for (int i = 0; i < L; ++i) {
@@ -289,9 +340,23 @@ std::vector<std::pair<u64, std::vector<int>>> schedule_phases(const std::vector<
         if ((rq[i].dense & ~R) != 0) continue;
         done[i] = 1;
         ++ndone;
-        order.push_back(list[i]);
         for (int s : succ[i]) npred[s]--;
         progress = true;
+        // merge into the op that last touched all of this prim's bits, if compatible
+        int cand = -2;
+        for (int b = 0; b < 64; ++b)
+          if ((rq[i].support >> b) & 1) {
+            if (cand == -2) cand = last_on[b];
+            else if (cand != last_on[b]) cand = -1;
+          }
+        if (cand >= 0 && rq[cand].support == rq[i].support && mergeable(prims[list[cand]], prims[list[i]])) {
+          merge_into(prims[list[cand]], prims[list[i]]);
+          ++merged;
+          continue;
+        }
+        order.push_back(list[i]);
+        for (int b = 0; b < 64; ++b)
+          if ((rq[i].support >> b) & 1) last_on[b] = i;
       }
       if (progress) continue;
       int pick = -1;
@@ -308,12 +373,46 @@ std::vector<std::pair<u64, std::vector<int>>> schedule_phases(const std::vector<
   return phases;
 }
 
-Program build_program(int nl, const std::vector<Prim>& prims, std::vector<PassPlan>& plan) {
+}  // namespace
+
+Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap) {
   Program prog;
+  std::vector<Prim> P = prims_in;
+  prog.n_prims_in = int64_t(P.size());
   const int b = std::min(kMaxB, nl);
-  plan = plan_passes(nl, prims, b);
-  for (auto& pp : plan) {
-    if (!pp.fused) continue;
+  const u64 low = (1ull << std::min(3, nl)) - 1;
+  std::vector<int> perm_total(nl);
+  for (int p = 0; p < nl; ++p) perm_total[p] = p;
+  std::vector<Req> req(P.size());
+  for (size_t i = 0; i < P.size(); ++i) req[i] = requirements(P[i]);
+  std::vector<int> remaining(P.size());
+  for (size_t i = 0; i < P.size(); ++i) remaining[i] = int(i);
+  while (!remaining.empty()) {
+    const int p0 = remaining[0];
+    if (!req[p0].fusable || nl < 5) {
+      prog.steps.push_back({false, int(prog.singles.size())});
+      prog.singles.push_back(P[p0]);
+      remaining.erase(remaining.begin());
+      continue;
+    }
+    // ---- choose the pass: greedy over the dependency order ----
+    u64 B = low;
+    Deferred def;
+    std::vector<int> take, rest;
+    for (size_t k = 0; k < remaining.size(); ++k) {
+      const int i = remaining[k];
+      const Req& r = req[i];
+      bool ok = r.fusable && int(take.size()) < kMaxSmemOps && !def.blocks(r) && popcount64(B | r.dense) <= b;
+      if (ok) {
+        B |= r.dense;
+        take.push_back(i);
+      } else {
+        def.add(r);
+        rest.push_back(i);
+      }
+    }
+    for (int p = 0; p < nl && popcount64(B) < b; ++p) B |= 1ull << p;   // fill: longest contiguous runs
+    // ---- emit ----
     FPassArgs A;
     std::memset(&A, 0, sizeof(A));
     A.b = b;
@@ -322,13 +421,13 @@ Program build_program(int nl, const std::vector<Prim>& prims, std::vector<PassPl
     for (int i = 0; i < 64; ++i) tile_pos_of[i] = -1;
     int j = 0;
     for (int p = 0; p < nl; ++p)
-      if ((pp.tile_bits >> p) & 1) {
+      if ((B >> p) & 1) {
         A.tpos[j] = (unsigned char)p;
         tile_pos_of[p] = j++;
       }
     A.n_tiles = 1ull << (nl - b);
     A.phase_begin = int(prog.phases.size());
-    for (auto& ph : schedule_phases(prims, pp.prims)) {
+    for (auto& ph : schedule_phases(P, take, prog.n_prims_merged)) {
       std::vector<int> R;
       for (int p = 0; p < 64; ++p)
         if ((ph.first >> p) & 1) R.push_back(tile_pos_of[p]);
@@ -337,7 +436,7 @@ Program build_program(int nl, const std::vector<Prim>& prims, std::vector<PassPl
       std::memset(&F, 0, sizeof(F));
       make_phase_thr(F, R, b);
       F.op_begin = int(prog.ops.size());
-      F.flip = uint8_t(emit_ops(prog, prims, ph.second, tile_pos_of, R));
+      F.flip = uint8_t(emit_ops(prog, P, ph.second, tile_pos_of, R));
       F.op_end = int(prog.ops.size());
       prog.phases.push_back(F);
     }
@@ -345,18 +444,144 @@ Program build_program(int nl, const std::vector<Prim>& prims, std::vector<PassPl
     A.op_begin = A.n_phases ? prog.phases[A.phase_begin].op_begin : int(prog.ops.size());
     A.op_end = int(prog.ops.size());
     bool full = false;
-    for (int ph = A.phase_begin; ph < A.phase_begin + A.n_phases; ++ph)
-      for (int oi = prog.phases[ph].op_begin; oi < prog.phases[ph].op_end; ++oi) {
-        const FOp& o = prog.ops[oi];
-        full |= o.kind == FK_DIAGG || o.kind == FK_DENSE2 || (o.kind == FK_PAIRG && o.mtype == MT_GENERAL);
+    for (int oi = A.op_begin; oi < A.op_end; ++oi) {
+      const FOp& o = prog.ops[oi];
+      full |= o.kind == FK_DIAGG || o.kind == FK_DENSE2 || (o.kind == FK_PAIRG && o.mtype == MT_GENERAL);
+    }
+    // ---- in-tile relabeling: bring the qubits the next gates target onto physical bits 0..2 ----
+    int sigma[64];
+    for (int p = 0; p < 64; ++p) sigma[p] = p;
+    if (remap && !rest.empty() && b > 3) {
+      int next_use[64];
+      for (int p = 0; p < 64; ++p) next_use[p] = 1 << 30;
+      for (size_t k = 0; k < rest.size(); ++k) {
+        u64 d = req[rest[k]].dense;
+        for (int p = 0; p < 64 && d; ++p)
+          if ((d >> p) & 1) {
+            if (next_use[p] > int(k)) next_use[p] = int(k);
+            d &= ~(1ull << p);
+          }
       }
+      std::vector<int> cand;   // tile positions sorted by next use (earliest first), low bits win ties
+      for (int t = 0; t < b; ++t) cand.push_back(A.tpos[t]);
+      std::stable_sort(cand.begin(), cand.end(), [&](int x, int y) {
+        if (next_use[x] != next_use[y]) return next_use[x] < next_use[y];
+        return x < y;
+      });
+      std::vector<int> want(cand.begin(), cand.begin() + 3);   // physical positions to move onto 0..2
+      std::vector<int> out_low, in_high;
+      for (int l = 0; l < 3; ++l)
+        if (std::find(want.begin(), want.end(), l) == want.end()) out_low.push_back(l);
+      for (int x : want)
+        if (x >= 3) in_high.push_back(x);
+      for (size_t s = 0; s < in_high.size(); ++s) {   // swap(out_low[s], in_high[s])
+        sigma[in_high[s]] = out_low[s];
+        sigma[out_low[s]] = in_high[s];
+      }
+    }
+    std::vector<int> q_low, q_rest;
+    for (int t = 0; t < b; ++t) {
+      A.tpos_st[t] = (unsigned char)sigma[A.tpos[t]];
+      if (A.tpos_st[t] < 3) q_low.push_back(t);
+      else q_rest.push_back(t);
+    }
+    std::sort(q_low.begin(), q_low.end(), [&](int x, int y) { return A.tpos_st[x] < A.tpos_st[y]; });
+    int qi = 0;
+    for (int t : q_low) A.q[qi++] = (unsigned char)t;
+    for (int t : q_rest) A.q[qi++] = (unsigned char)t;
+    bool moved = false;
+    for (int p = 0; p < nl; ++p) moved |= sigma[p] != p;
+    if (moved) {
+      for (int i : rest) {
+        relabel(P[i], sigma);
+        req[i] = requirements(P[i]);
+      }
+      for (int p = 0; p < nl; ++p) perm_total[p] = sigma[perm_total[p]];
+    }
+    prog.steps.push_back({true, int(prog.passes.size())});
     prog.full.push_back(full ? 1 : 0);
     prog.passes.push_back(A);
+    remaining.swap(rest);
   }
+  prog.perm = perm_total;
   return prog;
 }
 
+void serialize_program(const Program& prog, int nl, std::vector<int64_t>& I, std::vector<double>& Dv) {
+  I.clear();
+  Dv.clear();
+  auto put_c = [&](const double2& c) {
+    Dv.push_back(c.x);
+    Dv.push_back(c.y);
+  };
+  I.push_back(1);   // format version
+  I.push_back(nl);
+  I.push_back(int64_t(prog.steps.size()));
+  for (const Step& s : prog.steps) {
+    I.push_back(s.fused ? 1 : 0);
+    if (s.fused) {
+      const FPassArgs& A = prog.passes[s.index];
+      I.push_back(A.b);
+      for (int t = 0; t < A.b; ++t) I.push_back(A.tpos[t]);
+      for (int t = 0; t < A.b; ++t) I.push_back(A.tpos_st[t]);
+      for (int t = 0; t < A.b; ++t) I.push_back(A.q[t]);
+      I.push_back(A.phase_begin);
+      I.push_back(A.n_phases);
+    } else {
+      const Prim& p = prog.singles[s.index];
+      I.push_back(p.type);
+      I.push_back(int64_t(p.fmask));
+      I.push_back(int64_t(p.fval));
+      I.push_back(int64_t(p.xmask));
+      I.push_back(p.nb);
+      for (int t = 0; t < p.nb; ++t) I.push_back(p.pos[t]);
+      I.push_back(int64_t(Dv.size()) / 2);
+      I.push_back(int64_t(p.m.size()));
+      for (auto& c : p.m) {
+        Dv.push_back(c.real());
+        Dv.push_back(c.imag());
+      }
+    }
+  }
+  I.push_back(int64_t(prog.phases.size()));
+  for (const FPhase& F : prog.phases) {
+    for (int k = 0; k < kRB; ++k) I.push_back(F.reg[k]);
+    I.push_back(F.flip);
+    for (int t = 0; t < kMaxB; ++t) I.push_back(F.thr[t]);
+    I.push_back(F.op_begin);
+    I.push_back(F.op_end);
+  }
+  I.push_back(int64_t(prog.ops.size()));
+  for (const FOp& o : prog.ops) {
+    I.push_back(int64_t(o.pm));
+    I.push_back(int64_t(o.pv));
+    I.push_back(o.cs);
+    I.push_back(o.cm);
+    I.push_back(o.cv);
+    I.push_back(o.k);
+    I.push_back(o.v);
+    I.push_back(o.xr);
+    I.push_back(o.nt);
+    I.push_back(o.mtype);
+    for (int t = 0; t < 6; ++t) I.push_back(o.treg[t]);
+    for (int t = 0; t < 6; ++t) I.push_back(o.tphys[t]);
+    I.push_back(o.tab);
+    I.push_back(int64_t(Dv.size()) / 2);   // inline coefficients
+    for (int t = 0; t < 4; ++t) put_c(o.c[t]);
+  }
+  I.push_back(int64_t(Dv.size()) / 2);     // coefficient table offset
+  I.push_back(int64_t(prog.coef.size()));
+  for (auto& c : prog.coef) put_c(c);
+  for (int p = 0; p < nl; ++p) I.push_back(prog.perm[p]);
+}
+
 }  // namespace fused
+
+void plan_program_serialized(int n_qubits, const std::vector<Prim>& prims, std::vector<int64_t>& ints,
+                             std::vector<double>& dbls) {
+  const fused::Program prog = fused::build_program(n_qubits, prims, true);
+  fused::serialize_program(prog, n_qubits, ints, dbls);
+}
 
 PlanStats plan_stats(int nl, const std::vector<Prim>& prims) {
   using namespace fused;
@@ -366,9 +591,8 @@ PlanStats plan_stats(int nl, const std::vector<Prim>& prims) {
     s.passes = s.ops;
     return s;
   }
-  std::vector<PassPlan> plan;
-  Program prog = build_program(nl, prims, plan);
-  s.passes = int64_t(plan.size());
+  Program prog = build_program(nl, prims, true);
+  s.passes = int64_t(prog.steps.size());
   s.tile_bits = std::min(kMaxB, nl);
   s.phases = int64_t(prog.phases.size());
   return s;

@@ -156,7 +156,11 @@ void ensure_partials(sv_handle* h, size_t doubles);
 void ensure_results(sv_handle* h, size_t doubles);
 
 // fused tile engine (fused.cu / planner.cpp)
-void apply_prims_fused(sv_handle* h, double2* state, const std::vector<Prim>& prims);
+// runs the fused program on every state; returns the layout change (qubit at local p -> perm[p])
+std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& states, const std::vector<Prim>& prims);
+// flat serialisation of the fused program for an op list (host only; tests re-execute it on CPU)
+void plan_program_serialized(int n_qubits, const std::vector<Prim>& prims, std::vector<int64_t>& ints,
+                             std::vector<double>& dbls);
 void release_fused(sv_handle* h);
 struct PlanStats {
   int64_t passes = 0, ops = 0, tile_bits = 0, phases = 0;

