@@ -141,6 +141,10 @@ int sv_plan_summary(int n_qubits, const sv_op* ops, int n_ops, int64_t* out4);
  * sizes2 receives the needed int64 / double counts; buffers are filled when large enough. */
 int sv_plan_program(int n_qubits, const sv_op* ops, int n_ops, int64_t* ints, int64_t ints_cap, double* dbls,
                     int64_t dbls_cap, int64_t* sizes2);
+/* The sharded driver's decisions for one rank (local primitives, global-qubit swaps, final
+ * canonicalisation), recorded without a GPU; same sizing convention. */
+int sv_plan_sharded(int n_qubits, int rank, int world, const sv_op* ops, int n_ops, int64_t* ints, int64_t ints_cap,
+                    double* dbls, int64_t dbls_cap, int64_t* sizes2);
 
 #ifdef __cplusplus
 }

@@ -133,7 +133,7 @@ static void check_handle(const sv_handle* h) {
 static void exec_prims(sv_handle* h, const std::vector<double2*>& states, std::vector<Prim>& prims, int fuse) {
   if (prims.empty()) return;
   fold_diag_phases(prims);
-  if (fuse) {
+  if (fuse && !h->recording) {
     // fused passes may relabel qubits inside their tiles: the qubit at local position p ends at perm[p]
     const std::vector<int> perm = apply_prims_fused(h, states, prims);
     for (int o = 0; o < h->n; ++o)
@@ -730,6 +730,59 @@ int sv_plan_summary(int n_qubits, const sv_op* ops, int n_ops, int64_t* out4) {
   out4[1] = s.ops;
   out4[2] = s.tile_bits;
   out4[3] = s.phases;
+  API_END
+}
+
+// Host-only: run the sharded driver for `rank` of `world` in recording mode (no device memory,
+// no NCCL) and return what it would execute -- local primitives and global-qubit swaps -- plus
+// the canonicalising swaps at the end.  tests/test_sharded_cpu.py replays it on gloo ranks.
+int sv_plan_sharded(int n_qubits, int rank, int world, const sv_op* ops, int n_ops, int64_t* ints, int64_t ints_cap,
+                    double* dbls, int64_t dbls_cap, int64_t* sizes2) {
+  API_BEGIN
+  if (world < 1 || (world & (world - 1))) sv_fail(SV_ERR_VALIDATION, "n_shards must be a power of two");
+  if (rank < 0 || rank >= world) sv_fail(SV_ERR_VALIDATION, "rank out of range");
+  if (n_qubits < 1 || n_qubits > 62) sv_fail(SV_ERR_VALIDATION, "bad qubit count");
+  sv_handle v;
+  v.recording = true;
+  v.rank = rank;
+  v.world = world;
+  v.g = __builtin_ctz(unsigned(world));
+  v.n = n_qubits;
+  v.nl = n_qubits - v.g;
+  if (v.nl < 1) sv_fail(SV_ERR_VALIDATION, "too many shards");
+  v.n_local = 1ull << v.nl;
+  v.phys.resize(n_qubits);
+  for (int o = 0; o < n_qubits; ++o) v.phys[o] = o;
+  validate_ops(&v, ops, n_ops);
+  run_ops(&v, {nullptr}, ops, n_ops, 0);
+  dist_canonicalize(&v, {nullptr});
+  std::vector<int64_t> I = {1, v.n, v.nl, v.rank, v.world, int64_t(v.rec.size())};
+  std::vector<double> D;
+  for (const RecStep& s : v.rec) {
+    I.push_back(s.kind);
+    if (s.kind == REC_GSWAP) {
+      I.push_back(s.G);
+      continue;
+    }
+    const Prim& p = s.p;
+    I.push_back(p.type);
+    I.push_back(int64_t(p.fmask));
+    I.push_back(int64_t(p.fval));
+    I.push_back(int64_t(p.xmask));
+    I.push_back(p.nb);
+    for (int t = 0; t < p.nb; ++t) I.push_back(p.pos[t]);
+    I.push_back(int64_t(D.size()) / 2);
+    I.push_back(int64_t(p.m.size()));
+    for (auto& c : p.m) {
+      D.push_back(c.real());
+      D.push_back(c.imag());
+    }
+  }
+  for (int o = 0; o < v.n; ++o) I.push_back(v.phys[o]);
+  sizes2[0] = int64_t(I.size());
+  sizes2[1] = int64_t(D.size());
+  if (ints && int64_t(I.size()) <= ints_cap) std::memcpy(ints, I.data(), I.size() * sizeof(int64_t));
+  if (dbls && int64_t(D.size()) <= dbls_cap) std::memcpy(dbls, D.data(), D.size() * sizeof(double));
   API_END
 }
 

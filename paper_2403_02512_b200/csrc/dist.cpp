@@ -42,6 +42,13 @@ void local_bit_swap(sv_handle* h, const std::vector<double2*>& states, int p, in
 
 // exchange the top local bit (nl-1) with global position G = nl + j
 void global_swap_top(sv_handle* h, const std::vector<double2*>& states, int G) {
+  if (h->recording) {
+    h->rec.push_back({REC_GSWAP, Prim(), G});
+    int ot = logical_at(h, h->nl - 1), og = logical_at(h, G);
+    h->phys[ot] = G;
+    h->phys[og] = h->nl - 1;
+    return;
+  }
   const int j = G - h->nl;
   const int partner = h->rank ^ (1 << j);
   const int b = (h->rank >> j) & 1;
@@ -131,7 +138,11 @@ void dist_canonicalize(sv_handle* h, const std::vector<double2*>& states) {
   // global positions first: logical offset G must sit at physical G
   for (int G = h->nl; G < h->n; ++G) {
     if (h->phys[G] == G) continue;
-    int p = h->phys[G];   // local (globals only ever trade with locals)
+    int p = h->phys[G];
+    if (p >= h->nl) {            // logical G sits on another global position: bring it local first
+      global_swap_top(h, states, p);
+      p = h->phys[G];            // now the top local bit
+    }
     local_bit_swap(h, states, p, h->nl - 1);
     global_swap_top(h, states, G);
   }

@@ -474,6 +474,10 @@ double prim_bytes(const sv_handle* h, const Prim& p) {
 
 void launch_prim(sv_handle* h, double2* a, const Prim& p) {
   if (p.skip) return;
+  if (h->recording) {   // host-only planning (sv_plan_sharded)
+    h->rec.push_back({REC_PRIM, p, -1});
+    return;
+  }
   const int nf = popcount64(p.fmask);
   if (nf > h->nl) sv_fail(SV_ERR_DEVICE, "internal: primitive fixes more bits than the shard has");
   const u64 count = h->n_local >> nf;

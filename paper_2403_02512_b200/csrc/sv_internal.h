@@ -74,6 +74,15 @@ enum KernelClass {
 };
 extern const char* kKernelClassNames[KC_COUNT];
 
+// Recording mode (host-only planning of a sharded run, used by sv_plan_sharded): instead of
+// launching, the executors append what they would do.
+enum RecKind { REC_PRIM = 0, REC_GSWAP = 1 };
+struct RecStep {
+  int kind;
+  Prim p;      // REC_PRIM
+  int G = -1;  // REC_GSWAP: global physical position exchanged with the top local bit
+};
+
 struct PendingTiming {
   int cls;
   double bytes;
@@ -102,6 +111,8 @@ struct sv_handle {
   size_t h_pinned_cap = 0;
   std::vector<double2*> aux;    // lambda states for the adjoint sweep
   std::mutex mu;
+  bool recording = false;       // host-only planning handle (no device memory)
+  std::vector<RecStep> rec;
   // stats
   int64_t launches = 0;
   bool profiling = false;
