@@ -7,6 +7,7 @@
 #include <new>
 
 #include "dist.h"
+#include "prim_util.h"
 #include "sv_internal.h"
 
 namespace {
@@ -147,7 +148,67 @@ static void exec_prims(sv_handle* h, const std::vector<double2*>& states, std::v
 
 // Lower and run an op list on `states` (psi, plus lambdas during the adjoint sweep all share
 // the layout).  Global-qubit targets trigger a layout swap first (dist.cpp).
+// Sharded schedule: lower everything to primitives on LOGICAL bit offsets, then repeatedly run
+// the largest batch of primitives whose dense targets are local (a primitive may only move
+// past deferred ones it commutes with); when nothing is runnable, swap the global qubit the
+// next primitive needs with the local qubit whose next dense use is furthest away (Belady).
+// Controls and diagonal bits on global qubits never need a swap (resolve_global).
+static void run_ops_sharded(sv_handle* h, const std::vector<double2*>& states, const sv_op* ops, int n_ops,
+                            int fuse) {
+  std::vector<Prim> L;
+  for (int i = 0; i < n_ops; ++i) {
+    int col = 0;
+    for (auto& pc : lower_op(ops[i], h->n, col, false, nullptr))
+      if (!pc.fwd.skip) L.push_back(pc.fwd);
+  }
+  std::vector<PrimReq> req(L.size());
+  for (size_t i = 0; i < L.size(); ++i) req[i] = prim_requirements(L[i]);
+  std::vector<int> rem(L.size());
+  for (size_t i = 0; i < L.size(); ++i) rem[i] = int(i);
+  while (!rem.empty()) {
+    DeferredSet def;
+    std::vector<int> batch, rest;
+    for (int i : rem) {
+      bool local = true;
+      for (int o = 0; o < h->n; ++o)
+        if (((req[i].dense >> o) & 1) && h->phys[o] >= h->nl) local = false;
+      if (local && !def.blocks(req[i])) {
+        batch.push_back(i);
+      } else {
+        def.add(req[i]);
+        rest.push_back(i);
+      }
+    }
+    if (!batch.empty()) {
+      std::vector<Prim> phys_prims;
+      for (int i : batch) {
+        Prim p = L[i];
+        relabel_prim(p, h->phys.data());
+        resolve_global(p, h->nl, h->rank);
+        if (!p.skip) phys_prims.push_back(p);
+      }
+      exec_prims(h, states, phys_prims, fuse);
+      rem.swap(rest);
+      continue;
+    }
+    // stuck: bring the first primitive's global dense targets local
+    std::vector<int> next_use(h->n, 1 << 30);
+    for (size_t k = 0; k < rem.size(); ++k)
+      for (int o = 0; o < h->n; ++o)
+        if (((req[rem[k]].dense >> o) & 1) && next_use[o] > int(k)) next_use[o] = int(k);
+    std::vector<int> keep;
+    for (int o = 0; o < h->n; ++o)
+      if ((req[rem[0]].dense >> o) & 1) keep.push_back(o);
+    for (int o : keep)
+      if (h->phys[o] >= h->nl) dist_swap_in(h, states, o, keep, next_use);
+  }
+}
+
 static void run_ops(sv_handle* h, const std::vector<double2*>& states, const sv_op* ops, int n_ops, int fuse) {
+  if (h->world > 1) {
+    run_ops_sharded(h, states, ops, n_ops, fuse);
+    return;
+  }
   std::vector<Prim> pending;
   for (int i = 0; i < n_ops; ++i) {
     const sv_op& op = ops[i];

@@ -121,6 +121,25 @@ bool prim_needs_swap(const Prim& p, int nl) {
   return false;
 }
 
+void dist_swap_in(sv_handle* h, const std::vector<double2*>& states, int o, const std::vector<int>& keep,
+                  const std::vector<int>& next_use) {
+  const int G = h->phys[o];
+  if (G < h->nl) return;
+  int victim = -1, best = -1;
+  for (int p = h->nl - 1; p >= 0; --p) {
+    const int lo = logical_at(h, p);
+    if (std::find(keep.begin(), keep.end(), lo) != keep.end()) continue;
+    // furthest next use wins; ties prefer the top local bit (no local swap needed)
+    if (next_use[lo] > best) {
+      best = next_use[lo];
+      victim = p;
+    }
+  }
+  if (victim < 0) sv_fail(SV_ERR_CAPACITY, "operation spans more qubits than a shard holds locally");
+  local_bit_swap(h, states, victim, h->nl - 1);
+  global_swap_top(h, states, G);
+}
+
 void dist_make_local(sv_handle* h, const std::vector<double2*>& states, const std::vector<int>& wires) {
   dist_make_local_set(h, states, wires);
 }

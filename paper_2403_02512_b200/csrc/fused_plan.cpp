@@ -7,109 +7,36 @@
 // e.g. RX or the X of a CNOT) or generally.  Two primitives commute when every shared bit is
 // Z-like in both or X-like in both -- so RZ slides past CNOT controls and RX past CNOT targets.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
+#include <string>
 
 #include "fused.h"
+#include "prim_util.h"
 
 namespace fused {
 namespace {
 
-struct Req {
-  u64 dense = 0;     // bits that must be register bits
-  u64 support = 0;   // every bit the prim reads
-  u64 zb = 0, xb = 0;
-  bool diag = false;
+// planner view of a primitive: commutation classes (prim_util.h) + fusability
+struct Req : PrimReq {
   bool fusable = true;
 };
 
-bool is_xlike(const std::vector<cplx>& m) { return m.size() == 4 && m[0] == m[3] && m[1] == m[2]; }
-
 Req requirements(const Prim& p) {
   Req r;
-  if (p.type == PRIM_PAIR) {
-    r.dense = p.xmask;
-    r.support = p.fmask | p.xmask;
-    r.zb = p.fmask & ~p.xmask;
-    if (popcount64(p.xmask) == 1 && is_xlike(p.m)) r.xb = p.xmask;
+  static_cast<PrimReq&>(r) = prim_requirements(p);
+  if (p.type == PRIM_PAIR)
     r.fusable = popcount64(p.xmask) <= kRB;
-  } else if (p.type == PRIM_DIAG) {
-    r.diag = true;
-    r.support = p.fmask;
-    for (int j = 0; j < p.nb; ++j) r.support |= 1ull << p.pos[j];
-    r.zb = r.support;
+  else if (p.type == PRIM_DIAG)
     r.fusable = p.nb <= 6;
-  } else {
-    for (int j = 0; j < p.nb; ++j) r.dense |= 1ull << p.pos[j];
-    r.support = p.fmask | r.dense;
-    r.zb = p.fmask & ~r.dense;
+  else
     r.fusable = p.nb <= 2;
-  }
   return r;
 }
 
-bool commute(const Req& a, const Req& b) {
-  const u64 shared = a.support & b.support;
-  return (shared & ~((a.zb & b.zb) | (a.xb & b.xb))) == 0;
-}
-
-// union of the per-bit action classes of the prims deferred to later passes
-struct Deferred {
-  u64 z = 0, x = 0, g = 0;
-  void add(const Req& r) {
-    z |= r.zb;
-    x |= r.xb;
-    g |= r.support & ~(r.zb | r.xb);
-  }
-  bool blocks(const Req& r) const {
-    const u64 rg = r.support & ~(r.zb | r.xb);
-    return (r.support & g) || (r.zb & x) || (r.xb & z) || (rg & (z | x));
-  }
-};
-
-u64 permute_mask(u64 m, const int* perm) {
-  u64 o = 0;
-  for (int b = 0; b < 64 && m; ++b)
-    if ((m >> b) & 1) {
-      o |= 1ull << perm[b];
-      m &= ~(1ull << b);
-    }
-  return o;
-}
-
-// relabel physical bits of a prim (positions stay ascending; tables / matrices follow)
-void relabel(Prim& p, const int* perm) {
-  p.fmask = permute_mask(p.fmask, perm);
-  p.fval = permute_mask(p.fval, perm);
-  p.xmask = permute_mask(p.xmask, perm);
-  if (p.nb == 0) return;
-  const int k = p.nb;
-  int np[16], order[16];
-  for (int j = 0; j < k; ++j) {
-    np[j] = perm[p.pos[j]];
-    order[j] = j;
-  }
-  std::sort(order, order + k, [&](int x, int y) { return np[x] < np[y]; });
-  int rank[16];   // old index bit j -> new index bit rank[j]
-  for (int i = 0; i < k; ++i) {
-    rank[order[i]] = i;
-    p.pos[i] = np[order[i]];
-  }
-  const size_t d = size_t(1) << k;
-  auto map_idx = [&](size_t r) {
-    size_t o = 0;
-    for (int j = 0; j < k; ++j)
-      if ((r >> j) & 1) o |= size_t(1) << rank[j];
-    return o;
-  };
-  std::vector<cplx> m(p.m.size());
-  if (p.type == PRIM_DIAG) {
-    for (size_t r = 0; r < d; ++r) m[map_idx(r)] = p.m[r];
-  } else {
-    for (size_t r = 0; r < d; ++r)
-      for (size_t c = 0; c < d; ++c) m[map_idx(r) * d + map_idx(c)] = p.m[r * d + c];
-  }
-  p.m = m;
-}
+inline bool commute(const Req& a, const Req& b) { return prims_commute(a, b); }
+using Deferred = DeferredSet;
+inline void relabel(Prim& p, const int* perm) { relabel_prim(p, perm); }
 
 int mtype_of(const std::vector<cplx>& m) {
   auto re = [](cplx c) { return c.imag() == 0.0; };
@@ -349,7 +276,9 @@ std::vector<std::pair<u64, std::vector<int>>> schedule_phases(std::vector<Prim>&
             if (cand == -2) cand = last_on[b];
             else if (cand != last_on[b]) cand = -1;
           }
-        if (cand >= 0 && rq[cand].support == rq[i].support && mergeable(prims[list[cand]], prims[list[i]])) {
+        static const bool merge_on = !(getenv("SVB200_MERGE") && std::string(getenv("SVB200_MERGE")) == "0");
+        if (merge_on && cand >= 0 && rq[cand].support == rq[i].support &&
+            mergeable(prims[list[cand]], prims[list[i]])) {
           merge_into(prims[list[cand]], prims[list[i]]);
           ++merged;
           continue;

@@ -1,0 +1,85 @@
+"""GPU, world_size 2 (and 4 when available): sharded state over NCCL vs the oracle.
+
+One process per GPU (SPEC.md:429-486 semantics; global qubits = top log2 P): state after
+random circuits (global-qubit swaps), expvals with X/Y/Z on global qubits, probabilities over
+global wires, and the adjoint Jacobian -- all against the monolithic oracle.
+"""
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from oracle import svoracle as O
+from paper_2403_02512_b200 import workloads
+from paper_2403_02512_b200.observables import Hamiltonian, PauliWord
+from paper_2403_02512_b200.ops import Op
+
+pytestmark = pytest.mark.gpu
+
+
+def n_gpus():
+    from paper_2403_02512_b200 import _lib
+    return _lib.device_count()
+
+
+def _worker(rank, world, nccl_ids, q):
+    try:
+        from paper_2403_02512_b200.device import Device
+        n = 12
+        rng = np.random.default_rng(5)
+        psi = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+        psi /= np.linalg.norm(psi)
+        ops = workloads.random_circuit(n, 10, seed=3)
+        ops += [Op("SWAP", (0, 11)), Op("IsingXX", (1, 0), (0.3,)), Op("CNOT", (0, 1), ctrls=(5,)),
+                Op("DoubleExcitation", (0, 1, 6, 7), (0.4,)), Op("RZ", (1,), (0.7,), ctrls=(0,))]
+        res = {}
+        for fuse in (False, True):
+            d = Device.sharded(n, rank, world, nccl_ids[int(fuse)], device=rank, fuse=fuse)
+            d.set_state(psi)
+            d.apply(ops)
+            res[f"state{int(fuse)}"] = d.get_state()
+            ham = Hamiltonian([0.5, -0.3, 0.8], [PauliWord(((0, "X"), (3, "Y"))), PauliWord(((1, "Z"), (0, "Z"))),
+                                                  PauliWord(((1, "Y"),))])
+            res[f"ev{int(fuse)}"] = d.expval(ham)
+            res[f"probs{int(fuse)}"] = d.probs([0, 7, 1])
+            res[f"norm{int(fuse)}"] = d.norm()
+            d.release()
+        sel_ops, obs = workloads.sel_config(n, 2, seed=2)
+        d = Device.sharded(n, rank, world, nccl_ids[2], device=rank)
+        res["jac"], res["jev"] = d.adjoint_jacobian(sel_ops, obs[:3], return_expvals=True)
+        d.release()
+        if rank == 0:
+            ref = O.run_circuit(n, ops, psi)
+            out = {}
+            for f in (0, 1):
+                out[f"state{f}"] = float(np.abs(res[f"state{f}"] - ref).max())
+                out[f"ev{f}"] = abs(res[f"ev{f}"] - O.expval(ref, n, ham))
+                out[f"probs{f}"] = float(np.abs(res[f"probs{f}"] - O.probabilities(ref, n, [0, 7, 1])).max())
+                out[f"norm{f}"] = abs(res[f"norm{f}"] - 1.0)
+            jref, evref = O.adjoint_jacobian(n, sel_ops, obs[:3])
+            out["jac"] = float(np.abs(res["jac"] - jref).max())
+            out["jev"] = float(np.abs(res["jev"] - evref).max())
+            q.put(("ok", out))
+    except Exception as exc:  # surface worker failures to the test
+        import traceback
+        q.put(("err", f"rank {rank}: {exc}\n{traceback.format_exc()}"))
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_nccl_matches_oracle(world):
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    from paper_2403_02512_b200.device import Device
+    nccl_ids = [Device.nccl_unique_id() for _ in range(3)]   # one id per communicator
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, nccl_ids, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    status, out = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+    assert status == "ok", out
+    for k, v in out.items():
+        tol = 1e-10 if k in ("jac", "jev") else 1e-12
+        assert v < tol, (k, v)
