@@ -390,6 +390,98 @@ static void free_aux(sv_handle* h) {
   h->aux.clear();
 }
 
+// Fused adjoint sweep (K11 on the K7 engine): psi and lambda are stored as the two halves of one
+// 2^(nl+1) array (lambda = top bit set), so "apply U^dagger to both" is a plain fused program on
+// nl+1 bits and each <lambda|G_k|psi> is a GEN op evaluated inside the tile, many gates and
+// generators per HBM pass.  Single GPU, one observable, generators on <= 2 targets; returns
+// false (and does nothing) otherwise so the caller takes the per-gate sweep.
+static bool adjoint_fused(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs* obs, int n_obs, int ncols,
+                          double* jac, double* expvals) {
+  if (h->world != 1 || n_obs != 1 || h->nl + 1 < 6) return false;
+  for (int i = 0; i < n_ops; ++i) {
+    int c = 0;
+    for (auto& pc : lower_op(ops[i], h->n, c, true, nullptr))
+      if (pc.has_gen && pc.gen.g.nb > 2) return false;
+  }
+  size_t free_b = 0, total_b = 0;
+  CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+  const size_t half = h->n_local * sizeof(double2);
+  if (2 * half + (64ull << 20) > free_b) return false;
+
+  run_ops(h, {h->state}, ops, n_ops, 1);                       // forward pass
+  const double ev = expval_impl(h, obs[0]);
+  double2* buf = nullptr;
+  CUDA_CHECK(cudaMalloc(&buf, 2 * half));
+  try {
+    launch_copy(h, buf, h->state, h->n_local);                  // psi -> low half
+    apply_observable(h, obs[0], buf, buf + h->n_local, {buf, buf + h->n_local});   // lambda = O psi
+    // reverse sweep program in the current physical layout; the psi/lambda bit is position nl
+    const int top = h->nl;
+    std::vector<Prim> prims;
+    std::vector<double> prefactor(ncols, 0.0);
+    std::vector<int> col_start(n_ops);
+    int col = 0;
+    for (int i = 0; i < n_ops; ++i) {
+      col_start[i] = col;
+      lower_op(ops[i], h->n, col, true, nullptr);
+    }
+    for (int i = n_ops - 1; i >= 0; --i) {
+      int c0 = col_start[i];
+      auto pieces = lower_op(ops[i], h->n, c0, true, h->phys.data());
+      for (int pi = int(pieces.size()) - 1; pi >= 0; --pi) {
+        Piece& pc = pieces[pi];
+        if (pc.has_gen) {
+          Prim g = pc.gen.g;
+          g.type = PRIM_GEN;
+          g.xmask = 1ull << top;
+          g.slot = pc.gen.column;
+          prefactor[pc.gen.column] = pc.gen.prefactor;
+          prims.push_back(g);
+        }
+        if (!pc.inv.skip) prims.push_back(pc.inv);
+      }
+    }
+    fold_diag_phases(prims);
+    std::vector<std::pair<int, cplx>> gens;
+    h->nl += 1;
+    h->n_local *= 2;
+    std::vector<int> perm;
+    try {
+      perm = apply_prims_fused(h, {buf}, prims, &gens);
+    } catch (...) {
+      h->nl -= 1;
+      h->n_local /= 2;
+      throw;
+    }
+    // layout bookkeeping: qubit at p moved to perm[p]; put the psi/lambda bit back on top
+    for (int o = 0; o < h->n; ++o) h->phys[o] = perm[h->phys[o]];
+    const int tpos = perm[top];
+    if (tpos != top) {
+      Prim s;   // local SWAP of physical bits tpos <-> top over the 2^(nl+1) buffer
+      s.type = PRIM_PAIR;
+      s.fmask = s.xmask = (1ull << tpos) | (1ull << top);
+      s.fval = 1ull << tpos;
+      s.m = {cplx(0), cplx(1), cplx(1), cplx(0)};
+      launch_prim(h, buf, s);
+      for (int o = 0; o < h->n; ++o)
+        if (h->phys[o] == top) h->phys[o] = tpos;
+    }
+    h->nl -= 1;
+    h->n_local /= 2;
+    launch_copy(h, h->state, buf, h->n_local);                 // swept-back psi
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    std::vector<double> im(ncols, 0.0);
+    for (auto& g : gens) im[g.first] = g.second.imag();
+    for (int c = 0; c < ncols; ++c) jac[c] = -2.0 * prefactor[c] * im[c];
+    if (expvals) expvals[0] = ev;
+  } catch (...) {
+    cudaFree(buf);
+    throw;
+  }
+  CUDA_CHECK(cudaFree(buf));
+  return true;
+}
+
 // ---------------------------------------------------------------------------
 // C-ABI
 // ---------------------------------------------------------------------------
@@ -690,6 +782,7 @@ int sv_adjoint_jacobian(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs*
   // lower once (logical layout) to learn columns and validate differentiability
   int ncols = 0;
   for (int i = 0; i < n_ops; ++i) lower_op(ops[i], h->n, ncols, true, nullptr);
+  if (fuse && adjoint_fused(h, ops, n_ops, obs, n_obs, ncols, jac, expvals)) return SV_OK;
   // capacity: one lambda per observable
   size_t free_b = 0, total_b = 0;
   CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));

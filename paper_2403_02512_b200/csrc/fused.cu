@@ -171,6 +171,83 @@ __device__ __forceinline__ void diagg(double2 (&a)[kRegs], const FOp& op, const 
   case CS_PAIRGR + XR - 1: pairg<XR, MT_REAL>(a, op.c, op.cm, op.cv ^ (fthr & op.cm)); break; \
   case CS_PAIRG + XR - 1: if (FULL) pairg<XR, MT_GENERAL>(a, op.c, op.cm, op.cv ^ (fthr & op.cm)); break;
 
+// ---- adjoint bra-kets: psi and lambda share the tile (register bit T selects lambda) --------
+__device__ __forceinline__ void cacc_conj(double& re, double& im, const double2 l, const double2 t) {
+  re = fma(l.x, t.x, fma(l.y, t.y, re));   // conj(l) * t
+  im = fma(l.x, t.y, fma(-l.y, t.x, im));
+}
+
+template <int K, int T>
+__device__ __forceinline__ void gen1(const double2 (&a)[kRegs], const FOp& op, int cv, bool sw, double& re,
+                                     double& im) {
+  const double2 g0 = sw ? op.c[3] : op.c[0], g1 = sw ? op.c[2] : op.c[1];
+  const double2 g2 = sw ? op.c[1] : op.c[2], g3 = sw ? op.c[0] : op.c[3];
+  const int cm = op.cm;
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if (((r >> K) & 1) || ((r >> T) & 1)) continue;
+    if ((r & cm) != cv) continue;
+    const double2 p0 = a[r], p1 = a[r | (1 << K)];
+    const double2 l0 = a[r | (1 << T)], l1 = a[r | (1 << K) | (1 << T)];
+    cacc_conj(re, im, l0, cfma(g0, p0, cmul(g1, p1)));
+    cacc_conj(re, im, l1, cfma(g2, p0, cmul(g3, p1)));
+  }
+}
+
+template <int K0, int K1, int T>
+__device__ __forceinline__ void gen2(const double2 (&a)[kRegs], const double2* __restrict__ M, int cm, int cv, int f,
+                                     double& re, double& im) {
+  constexpr int B0 = 1 << K0, B1 = 1 << K1, BT = 1 << T;
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if (r & (B0 | B1 | BT)) continue;
+    if ((r & cm) != cv) continue;
+    const int idx[4] = {r, r | B0, r | B1, r | B0 | B1};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc = cfma(M[(q ^ f) * 4 + (c ^ f)], a[idx[c]], acc);
+      cacc_conj(re, im, a[idx[q] | BT], acc);
+    }
+  }
+}
+
+#define GEN1_CASE(K, T) \
+  case CS_GEN1 + K * 4 + T: gen1<K, T>(a, op, cv, ((fthr >> K) & 1) != 0, re, im); break;
+#define GEN2_CASES(PI, K0, K1, TA, TB)                                              \
+  case CS_GEN2 + PI * 4 + TA: if (FULL) gen2<K0, K1, TA>(a, M, op.cm, cv, f, re, im); break; \
+  case CS_GEN2 + PI * 4 + TB: if (FULL) gen2<K0, K1, TB>(a, M, op.cm, cv, f, re, im); break;
+
+// One generator bra-ket, reduced over the warp into this warp's shared accumulator.  Every lane
+// must call it (uniform op; predicate-false lanes contribute zero).
+template <bool FULL>
+__device__ __forceinline__ void gen_op(const double2 (&a)[kRegs], const FOp& op, bool pred, int fthr,
+                                       const double2* __restrict__ coef, double2* __restrict__ acc_warp) {
+  double re = 0.0, im = 0.0;
+  if (pred) {
+    const int cv = op.cv ^ (fthr & op.cm);
+    const int k0 = op.xr & 15, k1 = op.xr >> 4;
+    const int f = ((fthr >> k0) & 1) | (((fthr >> k1) & 1) << 1);
+    const double2* M = coef + op.tab;
+    switch (op.cs) {
+      GEN1_CASE(0, 1) GEN1_CASE(0, 2) GEN1_CASE(0, 3) GEN1_CASE(1, 0) GEN1_CASE(1, 2) GEN1_CASE(1, 3)
+      GEN1_CASE(2, 0) GEN1_CASE(2, 1) GEN1_CASE(2, 3) GEN1_CASE(3, 0) GEN1_CASE(3, 1) GEN1_CASE(3, 2)
+      GEN2_CASES(0, 0, 1, 2, 3) GEN2_CASES(1, 0, 2, 1, 3) GEN2_CASES(2, 0, 3, 1, 2)
+      GEN2_CASES(3, 1, 2, 0, 3) GEN2_CASES(4, 1, 3, 0, 2) GEN2_CASES(5, 2, 3, 0, 1)
+      default: break;
+    }
+  }
+  for (int s = 16; s > 0; s >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, s);
+    im += __shfl_xor_sync(0xffffffffu, im, s);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    acc_warp[op.slot].x += re;
+    acc_warp[op.slot].y += im;
+  }
+}
+
 // One flat switch on the dense case index.  FULL = false compiles only the common kinds;
 // passes that need DIAGG / DENSE2 / complex PAIRG use the FULL kernel.  `op` is in shared memory.
 template <bool FULL>
@@ -222,7 +299,8 @@ template <bool FULL, bool DB>
 __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__ state, const FPassArgs P,
                                                             const FPhase* __restrict__ phases,
                                                             const FOp* __restrict__ ops,
-                                                            const double2* __restrict__ coef) {
+                                                            const double2* __restrict__ coef,
+                                                            double2* __restrict__ gen_partials) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* tile_mem = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x;
@@ -230,12 +308,16 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
   const int T = 1 << P.b;
   // stage the pass's op records in shared memory (uniform broadcast reads in the op loop)
   FOp* s_ops = reinterpret_cast<FOp*>(smem_raw + size_t(DB ? 2 : 1) * T * sizeof(double2));
+  const int nops = P.op_end - P.op_begin;
+  // per-warp generator accumulators (adjoint sweep): [warp][kMaxGens]
+  double2* s_gen = reinterpret_cast<double2*>(s_ops + nops);
   {
-    const int nops = P.op_end - P.op_begin;
     const int4* src = reinterpret_cast<const int4*>(ops + P.op_begin);
     int4* dst = reinterpret_cast<int4*>(s_ops);
     const int n16 = nops * int(sizeof(FOp) / 16);
     for (int i = tid; i < n16; i += nthreads) dst[i] = src[i];
+    if (P.n_gen)
+      for (int i = tid; i < (nthreads >> 5) * kMaxGens; i += nthreads) s_gen[i] = make_double2(0.0, 0.0);
     __syncthreads();
   }
   // load slot i of this thread is tile index s = tid + nthreads * i
@@ -304,7 +386,11 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
       const int oe = F.op_end;
       for (int oi = F.op_begin; oi < oe; ++oi) {
         const FOp& op = OPS[oi];
-        if ((phys_base & op.pm) == op.pv) apply_op<FULL>(a, op, coef, phys_base, fthr);
+        const bool pred = (phys_base & op.pm) == op.pv;
+        if (op.cs >= CS_GEN1)
+          gen_op<FULL>(a, op, pred, fthr, coef, s_gen + (tid >> 5) * kMaxGens);
+        else if (pred)
+          apply_op<FULL>(a, op, coef, phys_base, fthr);
       }
       {
         // register r holds logical index r ^ flip: store offset = swz(sthr) ^ W(r ^ flip) (W linear)
@@ -344,6 +430,19 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
       }
     }
     cur ^= 1;
+  }
+  // generator partials of this CTA: fixed-order sum over warps -> gen_partials[block][slot]
+  if (P.n_gen) {
+    __syncthreads();
+    const int nw = nthreads >> 5;
+    for (int g = tid; g < P.n_gen; g += nthreads) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int w = 0; w < nw; ++w) {
+        s.x += s_gen[w * kMaxGens + g].x;
+        s.y += s_gen[w * kMaxGens + g].y;
+      }
+      gen_partials[size_t(blockIdx.x) * P.n_gen_total + P.gen_base + g] = s;
+    }
   }
 }
 
@@ -392,7 +491,8 @@ void release_fused(sv_handle* h) {
     }
 }
 
-std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& states, const std::vector<Prim>& prims) {
+std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& states, const std::vector<Prim>& prims,
+                                   std::vector<std::pair<int, cplx>>* gen_out) {
   using namespace fused;
   std::vector<int> identity(h->nl);
   for (int p = 0; p < h->nl; ++p) identity[p] = p;
@@ -430,7 +530,7 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
   static bool db = true;
   std::call_once(once, [&]() {
     const int tile = int((size_t(1) << kMaxB) * sizeof(double2));
-    const int ops_b = kMaxSmemOps * int(sizeof(FOp));
+    const int ops_b = kMaxSmemOps * int(sizeof(FOp)) + 8 * kMaxGens * int(sizeof(double2));
     set_smem_attr<true, true>(2 * tile + ops_b);
     set_smem_attr<false, true>(2 * tile + ops_b);
     set_smem_attr<true, false>(tile + ops_b);
@@ -442,9 +542,18 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
     db = mode && std::string(mode) == "db";
   });
   const int b = prog.passes[0].b;
+  const u64 grid = std::min<u64>(prog.passes[0].n_tiles, u64(dev_sms) * (db ? 1 : 2));   // persistent grid
+  const int n_gen = int(prog.gen_slot_of.size());
+  double2* d_gen = nullptr;
+  if (n_gen) {
+    if (!gen_out || states.size() != 1) sv_fail(SV_ERR_DEVICE, "internal: generator ops need one combined state");
+    CUDA_CHECK(cudaMallocAsync(&d_gen, grid * n_gen * sizeof(double2), h->stream));
+    CUDA_CHECK(cudaMemsetAsync(d_gen, 0, grid * n_gen * sizeof(double2), h->stream));
+  }
   for (double2* state : states) {
     for (const Step& s : prog.steps) {
       if (!s.fused) {
+        if (prog.singles[s.index].type == PRIM_GEN) sv_fail(SV_ERR_DEVICE, "internal: unfusable generator");
         launch_prim(h, state, prog.singles[s.index]);
         continue;
       }
@@ -452,23 +561,33 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
       const bool full = prog.full[s.index];
       const int threads = 1 << (A.b - kRB);
       const int nops = A.op_end - A.op_begin;
-      const size_t smem = (db ? 2 : 1) * (size_t(1) << b) * sizeof(double2) + size_t(nops) * sizeof(FOp);
-      // persistent grid: one (DB) or two CTAs per SM
-      const u64 grid = std::min<u64>(A.n_tiles, u64(dev_sms) * (db ? 1 : 2));
+      const size_t smem = (db ? 2 : 1) * (size_t(1) << b) * sizeof(double2) + size_t(nops) * sizeof(FOp) +
+                          (A.n_gen ? size_t(threads / 32) * kMaxGens * sizeof(double2) : 0);
       const double bytes = 32.0 * double(h->n_local);
       cudaEvent_t ev[2];
       stat_begin(h, KC_FUSED, bytes, ev);
       if (db && full)
-        k_fused<true, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+        k_fused<true, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen);
       else if (db)
-        k_fused<false, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+        k_fused<false, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen);
       else if (full)
-        k_fused<true, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+        k_fused<true, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen);
       else
-        k_fused<false, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf);
+        k_fused<false, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen);
       stat_end(h, KC_FUSED, bytes, ev);
       CUDA_CHECK(cudaGetLastError());
     }
+  }
+  if (n_gen) {
+    // fixed-order reduction over the persistent CTAs -> one complex per program slot
+    ensure_results(h, size_t(2) * n_gen);
+    sum_partials(h, reinterpret_cast<const double*>(d_gen), int(grid), 2 * n_gen, h->d_results);
+    std::vector<double> z(size_t(2) * n_gen);
+    CUDA_CHECK(cudaMemcpyAsync(z.data(), h->d_results, z.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    CUDA_CHECK(cudaFreeAsync(d_gen, h->stream));
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    gen_out->clear();
+    for (int s = 0; s < n_gen; ++s) gen_out->push_back({prog.gen_slot_of[s], cplx(z[2 * s], z[2 * s + 1])});
   }
   return prog.perm;
 }

