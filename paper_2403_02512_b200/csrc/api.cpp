@@ -390,14 +390,68 @@ static void free_aux(sv_handle* h) {
   h->aux.clear();
 }
 
-// Fused adjoint sweep (K11 on the K7 engine): psi and lambda are stored as the two halves of one
-// 2^(nl+1) array (lambda = top bit set), so "apply U^dagger to both" is a plain fused program on
-// nl+1 bits and each <lambda|G_k|psi> is a GEN op evaluated inside the tile, many gates and
-// generators per HBM pass.  Single GPU, one observable, generators on <= 2 targets; returns
-// false (and does nothing) otherwise so the caller takes the per-gate sweep.
+// Fused adjoint sweep (K11 on the K7 engine): psi (h->state) and lambda (its own array) are
+// treated as one 2^(nl+1) state whose top bit -- pinned, never relabeled -- selects the array, so
+// "apply U^dagger to both" is a plain fused program on nl+1 bits and each <lambda|G_k|psi> is a
+// GEN op evaluated inside the tile: many gates and generators per HBM pass, no state copies.
+// One sweep per observable from the saved final state.  Single GPU, generators on <= 2 targets;
+// returns false (and does nothing) otherwise so the caller takes the per-gate sweep.
+static void adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs& obs, int ncols, double2* lam,
+                              double* jac_row) {
+  apply_observable(h, obs, h->state, lam, {h->state, lam});                      // lambda = O psi
+  // reverse sweep program in the current physical layout; the psi/lambda bit is position nl
+  const int top = h->nl;
+  std::vector<Prim> prims;
+  std::vector<double> prefactor(ncols, 0.0);
+  std::vector<int> col_start(n_ops);
+  int col = 0;
+  for (int i = 0; i < n_ops; ++i) {
+    col_start[i] = col;
+    lower_op(ops[i], h->n, col, true, nullptr);
+  }
+  for (int i = n_ops - 1; i >= 0; --i) {
+    int c0 = col_start[i];
+    auto pieces = lower_op(ops[i], h->n, c0, true, h->phys.data());
+    for (int pi = int(pieces.size()) - 1; pi >= 0; --pi) {
+      Piece& pc = pieces[pi];
+      if (pc.has_gen) {
+        Prim g = pc.gen.g;
+        g.type = PRIM_GEN;
+        g.xmask = 1ull << top;
+        g.slot = pc.gen.column;
+        prefactor[pc.gen.column] = pc.gen.prefactor;
+        prims.push_back(g);
+      }
+      if (!pc.inv.skip) prims.push_back(pc.inv);
+    }
+  }
+  fold_diag_phases(prims);
+  std::vector<std::pair<int, cplx>> gens;
+  h->nl += 1;
+  h->n_local *= 2;
+  std::vector<int> perm;
+  try {
+    // psi = h->state, lambda = lam: one logical 2^(nl+1) state whose top bit (pinned) picks the array
+    perm = apply_prims_fused(h, {h->state}, prims, &gens, lam);
+  } catch (...) {
+    h->nl -= 1;
+    h->n_local /= 2;
+    throw;
+  }
+  h->nl -= 1;
+  h->n_local /= 2;
+  if (perm[top] != top) sv_fail(SV_ERR_DEVICE, "internal: the psi/lambda bit was relabeled");
+  for (int o = 0; o < h->n; ++o) h->phys[o] = perm[h->phys[o]];   // qubit at p moved to perm[p]
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  std::vector<double> im(ncols, 0.0);
+  for (auto& g : gens) im[g.first] = g.second.imag();
+  for (int c = 0; c < ncols; ++c) jac_row[c] = -2.0 * prefactor[c] * im[c];
+}
+
 static bool adjoint_fused(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs* obs, int n_obs, int ncols,
                           double* jac, double* expvals) {
-  if (h->world != 1 || n_obs != 1 || h->nl + 1 < 6) return false;
+  // tiles need >= 32 threads (2^(b-4)) for the warp-level generator reduction: nl + 1 >= 9
+  if (h->world != 1 || n_obs < 1 || h->nl + 1 < 9) return false;
   for (int i = 0; i < n_ops; ++i) {
     int c = 0;
     for (auto& pc : lower_op(ops[i], h->n, c, true, nullptr))
@@ -406,79 +460,35 @@ static bool adjoint_fused(sv_handle* h, const sv_op* ops, int n_ops, const sv_ob
   size_t free_b = 0, total_b = 0;
   CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
   const size_t half = h->n_local * sizeof(double2);
-  if (2 * half + (64ull << 20) > free_b) return false;
+  if ((n_obs > 1 ? 2 : 1) * half + (64ull << 20) > free_b) return false;   // lambda (+ saved psi)
 
-  run_ops(h, {h->state}, ops, n_ops, 1);                       // forward pass
-  const double ev = expval_impl(h, obs[0]);
-  double2* buf = nullptr;
-  CUDA_CHECK(cudaMalloc(&buf, 2 * half));
+  run_ops(h, {h->state}, ops, n_ops, 1);                       // forward pass (once)
+  std::vector<double> ev(n_obs);
+  for (int k = 0; k < n_obs; ++k) ev[k] = expval_impl(h, obs[k]);
+  double2 *buf = nullptr, *saved = nullptr;   // buf = lambda
+  CUDA_CHECK(cudaMalloc(&buf, half));
   try {
-    launch_copy(h, buf, h->state, h->n_local);                  // psi -> low half
-    apply_observable(h, obs[0], buf, buf + h->n_local, {buf, buf + h->n_local});   // lambda = O psi
-    // reverse sweep program in the current physical layout; the psi/lambda bit is position nl
-    const int top = h->nl;
-    std::vector<Prim> prims;
-    std::vector<double> prefactor(ncols, 0.0);
-    std::vector<int> col_start(n_ops);
-    int col = 0;
-    for (int i = 0; i < n_ops; ++i) {
-      col_start[i] = col;
-      lower_op(ops[i], h->n, col, true, nullptr);
+    const std::vector<int> phys_final = h->phys;
+    if (n_obs > 1) {
+      CUDA_CHECK(cudaMalloc(&saved, half));
+      launch_copy(h, saved, h->state, h->n_local);
     }
-    for (int i = n_ops - 1; i >= 0; --i) {
-      int c0 = col_start[i];
-      auto pieces = lower_op(ops[i], h->n, c0, true, h->phys.data());
-      for (int pi = int(pieces.size()) - 1; pi >= 0; --pi) {
-        Piece& pc = pieces[pi];
-        if (pc.has_gen) {
-          Prim g = pc.gen.g;
-          g.type = PRIM_GEN;
-          g.xmask = 1ull << top;
-          g.slot = pc.gen.column;
-          prefactor[pc.gen.column] = pc.gen.prefactor;
-          prims.push_back(g);
-        }
-        if (!pc.inv.skip) prims.push_back(pc.inv);
+    for (int k = 0; k < n_obs; ++k) {
+      if (k > 0) {                                             // restart from the final state
+        launch_copy(h, h->state, saved, h->n_local);
+        h->phys = phys_final;
       }
+      adjoint_fused_row(h, ops, n_ops, obs[k], ncols, buf, jac + size_t(k) * ncols);
     }
-    fold_diag_phases(prims);
-    std::vector<std::pair<int, cplx>> gens;
-    h->nl += 1;
-    h->n_local *= 2;
-    std::vector<int> perm;
-    try {
-      perm = apply_prims_fused(h, {buf}, prims, &gens);
-    } catch (...) {
-      h->nl -= 1;
-      h->n_local /= 2;
-      throw;
-    }
-    // layout bookkeeping: qubit at p moved to perm[p]; put the psi/lambda bit back on top
-    for (int o = 0; o < h->n; ++o) h->phys[o] = perm[h->phys[o]];
-    const int tpos = perm[top];
-    if (tpos != top) {
-      Prim s;   // local SWAP of physical bits tpos <-> top over the 2^(nl+1) buffer
-      s.type = PRIM_PAIR;
-      s.fmask = s.xmask = (1ull << tpos) | (1ull << top);
-      s.fval = 1ull << tpos;
-      s.m = {cplx(0), cplx(1), cplx(1), cplx(0)};
-      launch_prim(h, buf, s);
-      for (int o = 0; o < h->n; ++o)
-        if (h->phys[o] == top) h->phys[o] = tpos;
-    }
-    h->nl -= 1;
-    h->n_local /= 2;
-    launch_copy(h, h->state, buf, h->n_local);                 // swept-back psi
-    CUDA_CHECK(cudaStreamSynchronize(h->stream));
-    std::vector<double> im(ncols, 0.0);
-    for (auto& g : gens) im[g.first] = g.second.imag();
-    for (int c = 0; c < ncols; ++c) jac[c] = -2.0 * prefactor[c] * im[c];
-    if (expvals) expvals[0] = ev;
+    if (expvals)
+      for (int k = 0; k < n_obs; ++k) expvals[k] = ev[k];
   } catch (...) {
     cudaFree(buf);
+    if (saved) cudaFree(saved);
     throw;
   }
   CUDA_CHECK(cudaFree(buf));
+  if (saved) CUDA_CHECK(cudaFree(saved));
   return true;
 }
 

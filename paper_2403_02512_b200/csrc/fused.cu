@@ -300,7 +300,12 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
                                                             const FPhase* __restrict__ phases,
                                                             const FOp* __restrict__ ops,
                                                             const double2* __restrict__ coef,
-                                                            double2* __restrict__ gen_partials) {
+                                                            double2* __restrict__ gen_partials,
+                                                            double2* __restrict__ state_hi) {
+  // two-array states (adjoint sweep): indices with bit P.hi_mask live in state_hi
+  auto gptr = [&](u64 idx) -> double2* {
+    return (idx & P.hi_mask) ? state_hi + (idx ^ P.hi_mask) : state + idx;
+  };
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* tile_mem = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x;
@@ -348,7 +353,7 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
     const u64 gb = tile_base(t) | spread_tid;
 #pragma unroll
     for (int i = 0; i < kRegs; ++i) {
-      const double2* src = state + (gb | spread_hi(i));
+      const double2* src = gptr(gb | spread_hi(i));
       const unsigned dst = (unsigned)__cvta_generic_to_shared(&dst_buf[swz_tid ^ swz_hi(i)]);
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
     }
@@ -426,7 +431,7 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
             g |= 1ull << P.tpos_st[P.q[P.nthr + j]];
             s |= 1 << P.q[P.nthr + j];
           }
-        state[g] = tile[sw_tid ^ swz(s)];
+        *gptr(g) = tile[sw_tid ^ swz(s)];
       }
     }
     cur ^= 1;
@@ -492,20 +497,35 @@ void release_fused(sv_handle* h) {
 }
 
 std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& states, const std::vector<Prim>& prims,
-                                   std::vector<std::pair<int, cplx>>* gen_out) {
+                                   std::vector<std::pair<int, cplx>>* gen_out, double2* state_hi) {
   using namespace fused;
   std::vector<int> identity(h->nl);
   for (int p = 0; p < h->nl; ++p) identity[p] = p;
+  // two-array state (state_hi): the top bit selects the array; singles run on each half
+  auto run_single = [&](double2* st, const Prim& p) {
+    if (!state_hi) {
+      launch_prim(h, st, p);
+      return;
+    }
+    h->nl -= 1;
+    h->n_local /= 2;
+    launch_prim(h, st, p);
+    launch_prim(h, state_hi, p);
+    h->nl += 1;
+    h->n_local *= 2;
+  };
   if (h->nl < 5) {
     for (double2* st : states)
-      for (const Prim& p : prims) launch_prim(h, st, p);
+      for (const Prim& p : prims) run_single(st, p);
     return identity;
   }
   static const bool remap = !(getenv("SVB200_REMAP") && std::string(getenv("SVB200_REMAP")) == "0");
-  Program prog = build_program(h->nl, prims, remap);
+  Program prog = build_program(h->nl, prims, remap, state_hi != nullptr);
+  if (state_hi)
+    for (auto& A : prog.passes) A.hi_mask = 1ull << (h->nl - 1);
   if (prog.passes.empty()) {
     for (double2* st : states)
-      for (const Prim& p : prog.singles) launch_prim(h, st, p);
+      for (const Prim& p : prog.singles) run_single(st, p);
     return identity;
   }
   // upload phases | ops | coef in one copy (the buffer is only reused after a stream sync)
@@ -554,7 +574,7 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
     for (const Step& s : prog.steps) {
       if (!s.fused) {
         if (prog.singles[s.index].type == PRIM_GEN) sv_fail(SV_ERR_DEVICE, "internal: unfusable generator");
-        launch_prim(h, state, prog.singles[s.index]);
+        run_single(state, prog.singles[s.index]);
         continue;
       }
       const FPassArgs& A = prog.passes[s.index];
@@ -567,13 +587,13 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
       cudaEvent_t ev[2];
       stat_begin(h, KC_FUSED, bytes, ev);
       if (db && full)
-        k_fused<true, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen);
+        k_fused<true, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen, state_hi);
       else if (db)
-        k_fused<false, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen);
+        k_fused<false, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen, state_hi);
       else if (full)
-        k_fused<true, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen);
+        k_fused<true, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen, state_hi);
       else
-        k_fused<false, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen);
+        k_fused<false, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen, state_hi);
       stat_end(h, KC_FUSED, bytes, ev);
       CUDA_CHECK(cudaGetLastError());
     }

@@ -75,6 +75,7 @@ struct FPassArgs {
   u64 n_tiles;
   int phase_begin, n_phases;
   int op_begin, op_end;  // op records of the whole pass (contiguous)
+  u64 hi_mask;           // two-array state: indices with this bit live in the second array
   int n_gen;             // GEN slots used by this pass
   int gen_base;          // first global result slot of this pass
   int n_gen_total;       // result slots of the whole program (row length of the partials)
@@ -102,7 +103,8 @@ struct Program {
 };
 
 // remap = let passes relabel qubits inside their tile (moves upcoming qubits onto the low bits)
-Program build_program(int nl, const std::vector<Prim>& prims, bool remap);
+// pin_top = never relabel bit nl-1 (the psi/lambda selector of the adjoint sweep's two arrays)
+Program build_program(int nl, const std::vector<Prim>& prims, bool remap, bool pin_top = false);
 // flat int64/double serialisation of a program (tests/fused_emulator.py re-executes it on the CPU)
 void serialize_program(const Program& prog, int nl, std::vector<int64_t>& ints, std::vector<double>& dbls);
 

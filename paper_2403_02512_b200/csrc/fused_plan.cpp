@@ -352,7 +352,7 @@ std::vector<std::pair<u64, std::vector<int>>> schedule_phases(std::vector<Prim>&
 
 }  // namespace
 
-Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap) {
+Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, bool pin_top) {
   Program prog;
   std::vector<Prim> P = prims_in;
   prog.n_prims_in = int64_t(P.size());
@@ -449,7 +449,8 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap) {
           }
       }
       std::vector<int> cand;   // tile positions sorted by next use (earliest first), low bits win ties
-      for (int t = 0; t < b; ++t) cand.push_back(A.tpos[t]);
+      for (int t = 0; t < b; ++t)
+        if (!(pin_top && A.tpos[t] == nl - 1)) cand.push_back(A.tpos[t]);
       std::stable_sort(cand.begin(), cand.end(), [&](int x, int y) {
         if (next_use[x] != next_use[y]) return next_use[x] < next_use[y];
         return x < y;

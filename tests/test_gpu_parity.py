@@ -325,7 +325,7 @@ def test_fused_equals_unfused_mid_size():
 def test_fused_adjoint_single_observable(seed):
     """One observable -> the fused sweep (psi/lambda in one array, GEN bra-kets in the tile)."""
     rng = np.random.default_rng(300 + seed)
-    n = [7, 9, 12, 15][seed]
+    n = [8, 9, 12, 15][seed]
     kinds = ["RX", "RY", "RZ", "Phase", "Rot", "IsingXX", "IsingXY", "IsingYY", "IsingZZ",
              "SingleExcitation", "CNOT", "H", "CZ", "SWAP", "T", "X", "Y"]
     ops = []
