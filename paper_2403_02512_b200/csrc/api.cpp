@@ -381,8 +381,9 @@ static void apply_observable(sv_handle* h, const sv_obs& o, const double2* psi, 
     CUDA_CHECK(cudaMemsetAsync(lam, 0, h->n_local * sizeof(double2), h->stream));
     return;
   }
-  for (size_t gi = 0; gi < groups.size(); ++gi)
-    pauli_group_apply(h, psi, lam, groups[gi].x, groups[gi].terms, gi > 0);
+  std::vector<std::pair<u64, std::vector<PauliTerm>>> gl;
+  for (auto& g : groups) gl.push_back({g.x, g.terms});
+  pauli_groups_apply(h, psi, lam, gl);
 }
 
 static void free_aux(sv_handle* h) {
@@ -396,9 +397,11 @@ static void free_aux(sv_handle* h) {
 // GEN op evaluated inside the tile: many gates and generators per HBM pass, no state copies.
 // One sweep per observable from the saved final state.  Single GPU, generators on <= 2 targets;
 // returns false (and does nothing) otherwise so the caller takes the per-gate sweep.
-static void adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs& obs, int ncols, double2* lam,
-                              double* jac_row) {
+static double adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs& obs, int ncols, double2* lam,
+                                double* jac_row) {
   apply_observable(h, obs, h->state, lam, {h->state, lam});                      // lambda = O psi
+  const double ev = reduce_dot_re(h, h->state, lam);                             // <psi|O|psi> = Re<psi|lambda>
+  // (local part; the fused sweep is single-GPU)
   // reverse sweep program in the current physical layout; the psi/lambda bit is position nl
   const int top = h->nl;
   std::vector<Prim> prims;
@@ -446,6 +449,7 @@ static void adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const s
   std::vector<double> im(ncols, 0.0);
   for (auto& g : gens) im[g.first] = g.second.imag();
   for (int c = 0; c < ncols; ++c) jac_row[c] = -2.0 * prefactor[c] * im[c];
+  return ev;
 }
 
 static bool adjoint_fused(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs* obs, int n_obs, int ncols,
@@ -464,7 +468,6 @@ static bool adjoint_fused(sv_handle* h, const sv_op* ops, int n_ops, const sv_ob
 
   run_ops(h, {h->state}, ops, n_ops, 1);                       // forward pass (once)
   std::vector<double> ev(n_obs);
-  for (int k = 0; k < n_obs; ++k) ev[k] = expval_impl(h, obs[k]);
   double2 *buf = nullptr, *saved = nullptr;   // buf = lambda
   CUDA_CHECK(cudaMalloc(&buf, half));
   try {
@@ -478,7 +481,7 @@ static bool adjoint_fused(sv_handle* h, const sv_op* ops, int n_ops, const sv_ob
         launch_copy(h, h->state, saved, h->n_local);
         h->phys = phys_final;
       }
-      adjoint_fused_row(h, ops, n_ops, obs[k], ncols, buf, jac + size_t(k) * ncols);
+      ev[k] = adjoint_fused_row(h, ops, n_ops, obs[k], ncols, buf, jac + size_t(k) * ncols);
     }
     if (expvals)
       for (int k = 0; k < n_obs; ++k) expvals[k] = ev[k];

@@ -222,6 +222,12 @@ __global__ void __launch_bounds__(kThreads) k_sum_partials(const double* __restr
   }
 }
 
+// Pauli-sum term for K10 (observable application): coefficient * i^{nY} and the z-mask
+struct PauliApplyTermDev {
+  u64 z;
+  double2 cc;
+};
+
 __global__ void __launch_bounds__(kThreads) k_norm2(const double2* __restrict__ a, u64 n, double* __restrict__ partials) {
   double v[1] = {0.0};
   for (u64 i = u64(blockIdx.x) * kThreads + threadIdx.x; i < n; i += u64(gridDim.x) * kThreads) {
@@ -229,6 +235,50 @@ __global__ void __launch_bounds__(kThreads) k_norm2(const double2* __restrict__ 
     v[0] = fma(x.x, x.x, fma(x.y, x.y, v[0]));
   }
   block_reduce_store<1>(v, partials);
+}
+
+// Re <a|b> partials (K12)
+__global__ void __launch_bounds__(kThreads) k_dot_re(const double2* __restrict__ a, const double2* __restrict__ b, u64 n,
+                                                     double* __restrict__ partials) {
+  double v[1] = {0.0};
+  for (u64 i = u64(blockIdx.x) * kThreads + threadIdx.x; i < n; i += u64(gridDim.x) * kThreads) {
+    const double2 x = a[i], y = b[i];
+    v[0] = fma(x.x, y.x, fma(x.y, y.y, v[0]));
+  }
+  block_reduce_store<1>(v, partials);
+}
+
+// K10 batched: lam = sum over up to kMaxXG x-groups of sum_t cc_t (-1)^{pc((i^x_g) & z_t)} psi_{i^x_g};
+// psi is read once per group, lam written once (instead of a read-modify-write per group).
+constexpr int kMaxXG = 16;
+struct PauliGroupsArgs {
+  u64 x[kMaxXG];
+  int t_begin[kMaxXG + 1];   // term ranges per group in the shared term array
+  int ng;
+};
+
+__global__ void __launch_bounds__(kThreads) k_pauli_apply_multi(const double2* __restrict__ psi, double2* __restrict__ lam,
+                                                                u64 n, const PauliGroupsArgs G,
+                                                                const PauliApplyTermDev* __restrict__ terms, int nterms,
+                                                                int accumulate) {
+  extern __shared__ PauliApplyTermDev sat2[];
+  for (int t = threadIdx.x; t < nterms; t += kThreads) sat2[t] = terms[t];
+  __syncthreads();
+  for (u64 i = u64(blockIdx.x) * kThreads + threadIdx.x; i < n; i += u64(gridDim.x) * kThreads) {
+    double2 o = accumulate ? lam[i] : make_double2(0.0, 0.0);
+    for (int g = 0; g < G.ng; ++g) {
+      const u64 j = i ^ G.x[g];
+      const double2 b = psi[j];
+      double2 s = make_double2(0.0, 0.0);
+      for (int t = G.t_begin[g]; t < G.t_begin[g + 1]; ++t) {
+        const double sg = (__popcll(j & sat2[t].z) & 1) ? -1.0 : 1.0;
+        s.x = fma(sg, sat2[t].cc.x, s.x);
+        s.y = fma(sg, sat2[t].cc.y, s.y);
+      }
+      o = cfma(s, b, o);
+    }
+    lam[i] = o;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -273,11 +323,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_expval(const double2* __rest
   block_reduce_store<1>(v, partials);
 }
 
-// K10: lambda (+)= sum_t cc_t (-1)^{pc((i^x) & z_t)} psi_{i^x}
-struct PauliApplyTermDev {
-  u64 z;
-  double2 cc;
-};
+// K10: lambda (+)= sum_t cc_t (-1)^{pc((i^x) & z_t)} psi_{i^x}   (PauliApplyTermDev: see above)
 
 __global__ void __launch_bounds__(kThreads) k_pauli_apply(const double2* __restrict__ psi, double2* __restrict__ lam, u64 xmask,
                                                           u64 n, const PauliApplyTermDev* __restrict__ terms, int nterms,
@@ -621,6 +667,49 @@ void pauli_group_apply(sv_handle* h, const double2* psi, double2* lam, u64 xmask
   k_pauli_apply<<<g, kThreads, smem, h->stream>>>(psi, lam, xmask, h->n_local, d_terms, int(dt.size()), accumulate ? 1 : 0);
   stat_end(h, KC_APPLY_OBS, bytes, ev);
   CUDA_CHECK(cudaGetLastError());
+}
+
+void pauli_groups_apply(sv_handle* h, const double2* psi, double2* lam,
+                        const std::vector<std::pair<u64, std::vector<PauliTerm>>>& groups) {
+  const unsigned g = unsigned(std::min<u64>(grid_for(h->n_local, kThreads * 4), 148ull * 64));
+  for (size_t g0 = 0; g0 < groups.size(); g0 += kMaxXG) {
+    PauliGroupsArgs G;
+    std::vector<PauliApplyTermDev> dt;
+    G.ng = int(std::min<size_t>(kMaxXG, groups.size() - g0));
+    for (int k = 0; k < G.ng; ++k) {
+      G.x[k] = groups[g0 + k].first;
+      G.t_begin[k] = int(dt.size());
+      for (const auto& t : groups[g0 + k].second) dt.push_back({t.zmask, d2(t.cc)});
+    }
+    G.t_begin[G.ng] = int(dt.size());
+    auto* d_terms = (const PauliApplyTermDev*)scratch_upload(h, dt.data(), dt.size() * sizeof(PauliApplyTermDev));
+    const size_t smem = dt.size() * sizeof(PauliApplyTermDev);
+    if (smem > 48 * 1024)
+      CUDA_CHECK(cudaFuncSetAttribute(k_pauli_apply_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const int acc = g0 > 0;
+    const double bytes = (16.0 * G.ng + 16.0 + (acc ? 16.0 : 0.0)) * double(h->n_local);
+    cudaEvent_t ev[2];
+    stat_begin(h, KC_APPLY_OBS, bytes, ev);
+    k_pauli_apply_multi<<<g, kThreads, smem, h->stream>>>(psi, lam, h->n_local, G, d_terms, int(dt.size()), acc);
+    stat_end(h, KC_APPLY_OBS, bytes, ev);
+    CUDA_CHECK(cudaGetLastError());
+  }
+}
+
+double reduce_dot_re(sv_handle* h, const double2* a, const double2* b) {
+  const unsigned g = red_grid(h->n_local);
+  ensure_partials(h, g);
+  ensure_results(h, 1);
+  cudaEvent_t ev[2];
+  stat_begin(h, KC_REDUCE, 32.0 * double(h->n_local), ev);
+  k_dot_re<<<g, kThreads, 0, h->stream>>>(a, b, h->n_local, h->d_partials);
+  stat_end(h, KC_REDUCE, 32.0 * double(h->n_local), ev);
+  CUDA_CHECK(cudaGetLastError());
+  sum_partials(h, h->d_partials, g, 1, h->d_results);
+  double out = 0;
+  CUDA_CHECK(cudaMemcpyAsync(&out, h->d_results, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  return out;
 }
 
 void braket_prim_async(sv_handle* h, const double2* bra, const double2* ket, const Prim& gp, double* d_out) {

@@ -160,6 +160,10 @@ void pauli_group_expval_async(sv_handle* h, const double2* state, u64 xmask, con
                               double* d_out);
 void pauli_group_apply(sv_handle* h, const double2* psi, double2* lam, u64 xmask,
                        const std::vector<PauliTerm>& terms, bool accumulate);
+// lam = sum over x-groups (batched: psi read once per group, lam written once per batch of 16)
+void pauli_groups_apply(sv_handle* h, const double2* psi, double2* lam,
+                        const std::vector<std::pair<u64, std::vector<PauliTerm>>>& groups);
+double reduce_dot_re(sv_handle* h, const double2* a, const double2* b);   // Re <a|b> (local part)
 // <bra| P_f (G) |ket> complex, written to d_out[0..1]
 void braket_prim_async(sv_handle* h, const double2* bra, const double2* ket, const Prim& g, double* d_out);
 void probs_async(sv_handle* h, const double2* state, const std::vector<int>& pos_msb_first, double* d_out);
