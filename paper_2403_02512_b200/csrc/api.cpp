@@ -422,6 +422,22 @@ static double adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const
         g.type = PRIM_GEN;
         g.xmask = 1ull << top;
         g.slot = pc.gen.column;
+        // diagonal generators (Z, ZZ, |1><1|) become table bra-kets: targets need not be in registers
+        const size_t d = size_t(1) << g.nb;
+        bool diag = true;
+        for (size_t r = 0; r < d && diag; ++r)
+          for (size_t c = 0; c < d; ++c)
+            if (r != c && g.m[r * d + c] != 0.0) diag = false;
+        if (diag) {
+          std::vector<cplx> t(d);
+          for (size_t r = 0; r < d; ++r) t[r] = g.m[r * d + r];
+          u64 tb = 0;
+          for (int j = 0; j < g.nb; ++j) tb |= 1ull << g.pos[j];
+          g.type = PRIM_GEND;
+          g.fmask &= ~tb;
+          g.fval &= ~tb;
+          g.m = t;
+        }
         prefactor[pc.gen.column] = pc.gen.prefactor;
         prims.push_back(g);
       }

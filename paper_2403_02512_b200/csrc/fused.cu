@@ -219,10 +219,37 @@ __device__ __forceinline__ void gen2(const double2 (&a)[kRegs], const double2* _
   case CS_GEN2 + PI * 4 + TA: if (FULL) gen2<K0, K1, TA>(a, M, op.cm, cv, f, re, im); break; \
   case CS_GEN2 + PI * 4 + TB: if (FULL) gen2<K0, K1, TB>(a, M, op.cm, cv, f, re, im); break;
 
+// diagonal generator: sum_r conj(lambda_r) g(bits of r) psi_r, table bits anywhere (like diagg)
+template <int T>
+__device__ __forceinline__ void gen_diag(const double2 (&a)[kRegs], const FOp& op, int cv, int fthr, u64 phys_base,
+                                         const double2* __restrict__ coef, double& re, double& im) {
+  int tconst = 0, w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+  for (int j = 0; j < op.nt; ++j) {
+    const int rg = op.treg[j];
+    const int bit = 1 << j;
+    if (rg == 0xFF)
+      tconst |= int((phys_base >> op.tphys[j]) & 1ull) << j;
+    else if ((fthr >> rg) & 1)
+      tconst ^= bit;
+    w0 |= (rg == 0) ? bit : 0;
+    w1 |= (rg == 1) ? bit : 0;
+    w2 |= (rg == 2) ? bit : 0;
+    w3 |= (rg == 3) ? bit : 0;
+  }
+  const int cm = op.cm, tab = op.tab;
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if ((r >> T) & 1) continue;
+    if ((r & cm) != cv) continue;
+    const int t = tconst ^ (((r & 1) ? w0 : 0) | ((r & 2) ? w1 : 0) | ((r & 4) ? w2 : 0) | ((r & 8) ? w3 : 0));
+    cacc_conj(re, im, a[r | (1 << T)], cmul(coef[tab + t], a[r]));
+  }
+}
+
 // One generator bra-ket, reduced over the warp into this warp's shared accumulator.  Every lane
 // must call it (uniform op; predicate-false lanes contribute zero).
 template <bool FULL>
-__device__ __forceinline__ void gen_op(const double2 (&a)[kRegs], const FOp& op, bool pred, int fthr,
+__device__ __forceinline__ void gen_op(const double2 (&a)[kRegs], const FOp& op, bool pred, int fthr, u64 phys_base,
                                        const double2* __restrict__ coef, double2* __restrict__ acc_warp) {
   double re = 0.0, im = 0.0;
   if (pred) {
@@ -235,6 +262,10 @@ __device__ __forceinline__ void gen_op(const double2 (&a)[kRegs], const FOp& op,
       GEN1_CASE(2, 0) GEN1_CASE(2, 1) GEN1_CASE(2, 3) GEN1_CASE(3, 0) GEN1_CASE(3, 1) GEN1_CASE(3, 2)
       GEN2_CASES(0, 0, 1, 2, 3) GEN2_CASES(1, 0, 2, 1, 3) GEN2_CASES(2, 0, 3, 1, 2)
       GEN2_CASES(3, 1, 2, 0, 3) GEN2_CASES(4, 1, 3, 0, 2) GEN2_CASES(5, 2, 3, 0, 1)
+      case CS_GEND + 0: gen_diag<0>(a, op, cv, fthr, phys_base, coef, re, im); break;
+      case CS_GEND + 1: gen_diag<1>(a, op, cv, fthr, phys_base, coef, re, im); break;
+      case CS_GEND + 2: gen_diag<2>(a, op, cv, fthr, phys_base, coef, re, im); break;
+      case CS_GEND + 3: gen_diag<3>(a, op, cv, fthr, phys_base, coef, re, im); break;
       default: break;
     }
   }
@@ -393,7 +424,7 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
         const FOp& op = OPS[oi];
         const bool pred = (phys_base & op.pm) == op.pv;
         if (op.cs >= CS_GEN1)
-          gen_op<FULL>(a, op, pred, fthr, coef, s_gen + (tid >> 5) * kMaxGens);
+          gen_op<FULL>(a, op, pred, fthr, phys_base, coef, s_gen + (tid >> 5) * kMaxGens);
         else if (pred)
           apply_op<FULL>(a, op, coef, phys_base, fthr);
       }
@@ -573,7 +604,7 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
   for (double2* state : states) {
     for (const Step& s : prog.steps) {
       if (!s.fused) {
-        if (prog.singles[s.index].type == PRIM_GEN) sv_fail(SV_ERR_DEVICE, "internal: unfusable generator");
+        if (prog.singles[s.index].type >= PRIM_GEN) sv_fail(SV_ERR_DEVICE, "internal: unfusable generator");
         run_single(state, prog.singles[s.index]);
         continue;
       }

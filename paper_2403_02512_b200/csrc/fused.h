@@ -55,6 +55,7 @@ constexpr int CS_PHASE1D = 82;   // + k*2 + v: PHASE1 on a dynamically flipped b
 // adjoint bra-kets (psi and lambda share the tile; t = register bit selecting lambda)
 constexpr int CS_GEN1 = 90;      // + k*4 + t: 2x2 generator on register bit k        (90..105)
 constexpr int CS_GEN2 = 106;     // + pair*4 + t: 4x4 generator on register bits pair (106..129)
+constexpr int CS_GEND = 130;     // + t: diagonal generator (table on any bits; only t in registers) (130..133)
 constexpr int kMaxGens = 64;     // generator slots per pass (per-warp shared-memory accumulators)
 static_assert(sizeof(FOp) == 112, "FOp layout");
 

@@ -27,7 +27,7 @@ Req requirements(const Prim& p) {
   static_cast<PrimReq&>(r) = prim_requirements(p);
   if (p.type == PRIM_PAIR)
     r.fusable = popcount64(p.xmask) <= kRB;
-  else if (p.type == PRIM_DIAG)
+  else if (p.type == PRIM_DIAG || p.type == PRIM_GEND)
     r.fusable = p.nb <= 6;
   else
     r.fusable = p.nb <= 2;   // DENSE (<= 2 targets) and GEN (<= 2 targets + the psi/lambda bit)
@@ -116,6 +116,30 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
     }
     op.cv ^= uint8_t(F & op.cm);   // physical register = logical ^ F
     op.tab = int(prog.coef.size());
+    if (p.type == PRIM_GEND) {
+      // diagonal generator: table bits anywhere (like DIAGG), only the psi/lambda bit t in registers
+      int t = -1;
+      for (int bpos = 0; bpos < 64; ++bpos)
+        if ((p.xmask >> bpos) & 1) t = reg_of_phys(bpos);
+      op.slot = int(prog.gen_slot_of.size());
+      prog.gen_slot_of.push_back(p.slot);
+      op.nt = uint8_t(p.nb);
+      int tflip = 0;
+      for (int j = 0; j < p.nb; ++j) {
+        const int k = reg_of_phys(p.pos[j]);
+        op.treg[j] = k >= 0 ? uint8_t(k) : uint8_t(0xFF);
+        op.tphys[j] = uint8_t(p.pos[j]);
+        if (k >= 0 && ((F >> k) & 1)) tflip |= 1 << j;
+      }
+      for (size_t tt = 0; tt < p.m.size(); ++tt) {
+        const cplx c = p.m[tt ^ size_t(tflip)];
+        prog.coef.push_back(make_double2(c.real(), c.imag()));
+      }
+      op.v = uint8_t(t);
+      op.cs = CS_GEND + t;
+      prog.ops.push_back(op);
+      continue;
+    }
     if (p.type == PRIM_GEN) {
       // adjoint bra-ket: targets and the psi/lambda bit t are register bits; the slot is assigned
       // by build_program (op.slot = index into prog.gen_slot_of, rebased per pass)
@@ -380,7 +404,7 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
     for (size_t k = 0; k < remaining.size(); ++k) {
       const int i = remaining[k];
       const Req& r = req[i];
-      const bool gen = P[i].type == PRIM_GEN;
+      const bool gen = P[i].type == PRIM_GEN || P[i].type == PRIM_GEND;
       bool ok = r.fusable && int(take.size()) < kMaxSmemOps && !def.blocks(r) && popcount64(B | r.dense) <= b &&
                 (!gen || ngen < kMaxGens);
       if (ok) {
@@ -432,7 +456,7 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
       if (o.cs >= CS_GEN1) o.slot -= A.gen_base;   // pass-local accumulator slot
       full |= (o.cs < CS_GEN1 && (o.kind == FK_DIAGG || o.kind == FK_DENSE2 ||
                                   (o.kind == FK_PAIRG && o.mtype == MT_GENERAL))) ||
-              o.cs >= CS_GEN2;
+              (o.cs >= CS_GEN2 && o.cs < CS_GEND);
     }
     // ---- in-tile relabeling: bring the qubits the next gates target onto physical bits 0..2 ----
     int sigma[64];

@@ -33,6 +33,12 @@ inline PrimReq prim_requirements(const Prim& p) {
     r.support = p.fmask;
     for (int j = 0; j < p.nb; ++j) r.support |= 1ull << p.pos[j];
     r.zb = r.support;
+  } else if (p.type == PRIM_GEND) {
+    // diagonal generator: Z-like everywhere except the psi/lambda bit it reads across
+    r.support = p.fmask | p.xmask;
+    for (int j = 0; j < p.nb; ++j) r.support |= 1ull << p.pos[j];
+    r.dense = p.xmask;
+    r.zb = r.support & ~p.xmask;
   } else if (p.type == PRIM_GEN) {
     // reads psi and lambda on its targets (general) across the psi/lambda bit; controls Z-like
     for (int j = 0; j < p.nb; ++j) r.dense |= 1ull << p.pos[j];
@@ -103,7 +109,7 @@ inline void relabel_prim(Prim& p, const int* perm) {
     return o;
   };
   std::vector<cplx> m(p.m.size());
-  if (p.type == PRIM_DIAG) {
+  if (p.type == PRIM_DIAG || p.type == PRIM_GEND) {
     for (size_t r = 0; r < d; ++r) m[map_idx(r)] = p.m[r];
   } else {
     for (size_t r = 0; r < d; ++r)

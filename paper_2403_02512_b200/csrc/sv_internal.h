@@ -41,7 +41,9 @@ void sv_nccl_check(ncclResult_t r, const char* what);
 //          one array: lambda is the half whose bit `xmask` (one bit) is set.  G is a 2^nb x 2^nb
 //          matrix on pos[] (targets, fmask includes them with value 0 plus the controls);
 //          the result accumulates into Jacobian slot `slot`.
-enum PrimType { PRIM_PAIR = 0, PRIM_DIAG = 1, PRIM_DENSE = 2, PRIM_GEN = 3 };
+//   GEND : GEN with a diagonal G given as a table over pos[] (like DIAG; pos need not be local to
+//          a register), restricted by fmask/fval.
+enum PrimType { PRIM_PAIR = 0, PRIM_DIAG = 1, PRIM_DENSE = 2, PRIM_GEN = 3, PRIM_GEND = 4 };
 
 struct Prim {
   int type = PRIM_PAIR;
