@@ -14,7 +14,8 @@ from .errors import raise_for_status
 from .observables import DenseHermitian, Hamiltonian, PauliWord, as_observable
 from .ops import KIND_CODE, Op
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libsvb200.so")
+# SVB200_LIB selects another in-tree build of the same library (A/B kernel experiments)
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), os.environ.get("SVB200_LIB", "libsvb200.so"))
 
 # Every symbol include/svb200.h declares (checked by tests/test_boundary.py).
 EXPORTS = (

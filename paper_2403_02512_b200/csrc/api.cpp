@@ -3,6 +3,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <new>
 
@@ -153,14 +154,10 @@ static void exec_prims(sv_handle* h, const std::vector<double2*>& states, std::v
 // past deferred ones it commutes with); when nothing is runnable, swap the global qubit the
 // next primitive needs with the local qubit whose next dense use is furthest away (Belady).
 // Controls and diagonal bits on global qubits never need a swap (resolve_global).
-static void run_ops_sharded(sv_handle* h, const std::vector<double2*>& states, const sv_op* ops, int n_ops,
-                            int fuse) {
-  std::vector<Prim> L;
-  for (int i = 0; i < n_ops; ++i) {
-    int col = 0;
-    for (auto& pc : lower_op(ops[i], h->n, col, false, nullptr))
-      if (!pc.fwd.skip) L.push_back(pc.fwd);
-  }
+// `exec` receives each batch already relabeled to physical positions and resolved against
+// this rank's global bits (the forward pass and the fused adjoint sweep share this schedule).
+static void schedule_sharded(sv_handle* h, const std::vector<double2*>& states, const std::vector<Prim>& L,
+                             const std::function<void(std::vector<Prim>&)>& exec) {
   std::vector<PrimReq> req(L.size());
   for (size_t i = 0; i < L.size(); ++i) req[i] = prim_requirements(L[i]);
   std::vector<int> rem(L.size());
@@ -187,7 +184,7 @@ static void run_ops_sharded(sv_handle* h, const std::vector<double2*>& states, c
         resolve_global(p, h->nl, h->rank);
         if (!p.skip) phys_prims.push_back(p);
       }
-      exec_prims(h, states, phys_prims, fuse);
+      exec(phys_prims);
       rem.swap(rest);
       continue;
     }
@@ -202,6 +199,17 @@ static void run_ops_sharded(sv_handle* h, const std::vector<double2*>& states, c
     for (int o : keep)
       if (h->phys[o] >= h->nl) dist_swap_in(h, states, o, keep, next_use);
   }
+}
+
+static void run_ops_sharded(sv_handle* h, const std::vector<double2*>& states, const sv_op* ops, int n_ops,
+                            int fuse) {
+  std::vector<Prim> L;
+  for (int i = 0; i < n_ops; ++i) {
+    int col = 0;
+    for (auto& pc : lower_op(ops[i], h->n, col, false, nullptr))
+      if (!pc.fwd.skip) L.push_back(pc.fwd);
+  }
+  schedule_sharded(h, states, L, [&](std::vector<Prim>& batch) { exec_prims(h, states, batch, fuse); });
 }
 
 static void run_ops(sv_handle* h, const std::vector<double2*>& states, const sv_op* ops, int n_ops, int fuse) {
@@ -395,15 +403,15 @@ static void free_aux(sv_handle* h) {
 // treated as one 2^(nl+1) state whose top bit -- pinned, never relabeled -- selects the array, so
 // "apply U^dagger to both" is a plain fused program on nl+1 bits and each <lambda|G_k|psi> is a
 // GEN op evaluated inside the tile: many gates and generators per HBM pass, no state copies.
-// One sweep per observable from the saved final state.  Single GPU, generators on <= 2 targets;
-// returns false (and does nothing) otherwise so the caller takes the per-gate sweep.
+// One sweep per observable from the saved final state.  Sharded handles run the same sweep
+// through the sharded schedule (both arrays swap together; controls and diagonal tables on global
+// bits resolve per rank) and sum the per-rank bra-kets with one allreduce.  Generators on <= 2
+// targets (adjoint_fused checks).
 static double adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs& obs, int ncols, double2* lam,
                                 double* jac_row) {
   apply_observable(h, obs, h->state, lam, {h->state, lam});                      // lambda = O psi
-  const double ev = reduce_dot_re(h, h->state, lam);                             // <psi|O|psi> = Re<psi|lambda>
-  // (local part; the fused sweep is single-GPU)
-  // reverse sweep program in the current physical layout; the psi/lambda bit is position nl
-  const int top = h->nl;
+  // reverse sweep on LOGICAL bit offsets; generators become bra-kets whose psi/lambda selector
+  // (xmask) is set per batch to the top bit of the two-array state
   std::vector<Prim> prims;
   std::vector<double> prefactor(ncols, 0.0);
   std::vector<int> col_start(n_ops);
@@ -414,13 +422,13 @@ static double adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const
   }
   for (int i = n_ops - 1; i >= 0; --i) {
     int c0 = col_start[i];
-    auto pieces = lower_op(ops[i], h->n, c0, true, h->phys.data());
+    auto pieces = lower_op(ops[i], h->n, c0, true, nullptr);
     for (int pi = int(pieces.size()) - 1; pi >= 0; --pi) {
       Piece& pc = pieces[pi];
       if (pc.has_gen) {
         Prim g = pc.gen.g;
         g.type = PRIM_GEN;
-        g.xmask = 1ull << top;
+        g.xmask = 0;
         g.slot = pc.gen.column;
         // diagonal generators (Z, ZZ, |1><1|) become table bra-kets: targets need not be in registers
         const size_t d = size_t(1) << g.nb;
@@ -444,34 +452,45 @@ static double adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const
       if (!pc.inv.skip) prims.push_back(pc.inv);
     }
   }
-  fold_diag_phases(prims);
-  std::vector<std::pair<int, cplx>> gens;
-  h->nl += 1;
-  h->n_local *= 2;
-  std::vector<int> perm;
-  try {
-    // psi = h->state, lambda = lam: one logical 2^(nl+1) state whose top bit (pinned) picks the array
-    perm = apply_prims_fused(h, {h->state}, prims, &gens, lam);
-  } catch (...) {
+  // im[0..ncols) = Im<lambda_k|G_k|psi_k> (this rank's part), im[ncols] = Re<psi|lambda> = <O>
+  std::vector<double> im(ncols + 1, 0.0);
+  im[ncols] = reduce_dot_re(h, h->state, lam);
+  const std::vector<double2*> both = {h->state, lam};
+  schedule_sharded(h, both, prims, [&](std::vector<Prim>& batch) {
+    const int top = h->nl;
+    for (Prim& p : batch)
+      if (p.type == PRIM_GEN || p.type == PRIM_GEND) p.xmask = 1ull << top;
+    fold_diag_phases(batch);
+    std::vector<std::pair<int, cplx>> gens;
+    h->nl += 1;
+    h->n_local *= 2;
+    std::vector<int> perm;
+    try {
+      // psi = h->state, lambda = lam: one logical 2^(nl+1) state whose top bit (pinned) picks the array
+      perm = apply_prims_fused(h, {h->state}, batch, &gens, lam);
+    } catch (...) {
+      h->nl -= 1;
+      h->n_local /= 2;
+      throw;
+    }
     h->nl -= 1;
     h->n_local /= 2;
-    throw;
-  }
-  h->nl -= 1;
-  h->n_local /= 2;
-  if (perm[top] != top) sv_fail(SV_ERR_DEVICE, "internal: the psi/lambda bit was relabeled");
-  for (int o = 0; o < h->n; ++o) h->phys[o] = perm[h->phys[o]];   // qubit at p moved to perm[p]
+    if (perm[top] != top) sv_fail(SV_ERR_DEVICE, "internal: the psi/lambda bit was relabeled");
+    for (int o = 0; o < h->n; ++o)
+      if (h->phys[o] < top) h->phys[o] = perm[h->phys[o]];   // qubit at p moved to perm[p]
+    for (auto& g : gens) im[g.first] += g.second.imag();
+    batch.clear();
+  });
   CUDA_CHECK(cudaStreamSynchronize(h->stream));
-  std::vector<double> im(ncols, 0.0);
-  for (auto& g : gens) im[g.first] = g.second.imag();
+  dist_allreduce_sum(h, im.data(), im.size());
   for (int c = 0; c < ncols; ++c) jac_row[c] = -2.0 * prefactor[c] * im[c];
-  return ev;
+  return im[ncols];
 }
 
 static bool adjoint_fused(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs* obs, int n_obs, int ncols,
                           double* jac, double* expvals) {
   // tiles need >= 32 threads (2^(b-4)) for the warp-level generator reduction: nl + 1 >= 9
-  if (h->world != 1 || n_obs < 1 || h->nl + 1 < 9) return false;
+  if (n_obs < 1 || h->nl + 1 < 9) return false;
   for (int i = 0; i < n_ops; ++i) {
     int c = 0;
     for (auto& pc : lower_op(ops[i], h->n, c, true, nullptr))
@@ -480,7 +499,9 @@ static bool adjoint_fused(sv_handle* h, const sv_op* ops, int n_ops, const sv_ob
   size_t free_b = 0, total_b = 0;
   CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
   const size_t half = h->n_local * sizeof(double2);
-  if ((n_obs > 1 ? 2 : 1) * half + (64ull << 20) > free_b) return false;   // lambda (+ saved psi)
+  double lacking = ((n_obs > 1 ? 2 : 1) * half + (64ull << 20) > free_b) ? 1.0 : 0.0;   // lambda (+ saved psi)
+  dist_allreduce_sum(h, &lacking, 1);   // every rank must take the same path (collectives inside)
+  if (lacking > 0) return false;
 
   run_ops(h, {h->state}, ops, n_ops, 1);                       // forward pass (once)
   std::vector<double> ev(n_obs);

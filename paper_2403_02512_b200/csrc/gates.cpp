@@ -468,11 +468,11 @@ void resolve_global(Prim& p, int nl, int rank) {
   p.fmask &= local;
   p.fval &= local;
   if (p.type == PRIM_PAIR && (p.xmask & ~local)) sv_fail(SV_ERR_DEVICE, "internal: pair target on a global qubit");
-  if (p.type == PRIM_DENSE) {
+  if (p.type == PRIM_DENSE || p.type == PRIM_GEN) {
     for (int j = 0; j < p.nb; ++j)
       if (p.pos[j] >= nl) sv_fail(SV_ERR_DEVICE, "internal: dense target on a global qubit");
   }
-  if (p.type == PRIM_DIAG && p.nb > 0) {
+  if ((p.type == PRIM_DIAG || p.type == PRIM_GEND) && p.nb > 0) {
     int keep[16], nk = 0;
     int fixed_bits = 0;  // table index bits pinned by the rank
     int fixed_vals = 0;

@@ -45,9 +45,15 @@ def _worker(rank, world, nccl_ids, q):
             res[f"norm{int(fuse)}"] = d.norm()
             d.release()
         sel_ops, obs = workloads.sel_config(n, 2, seed=2)
-        d = Device.sharded(n, rank, world, nccl_ids[2], device=rank)
-        res["jac"], res["jev"] = d.adjoint_jacobian(sel_ops, obs[:3], return_expvals=True)
-        d.release()
+        qaoa_ops, qaoa_h, _ = workloads.qaoa_maxcut(n, p=2, seed=1)
+        hea_ops = workloads.hardware_efficient_ansatz(n, layers=3, n_trainable=60, seed=2)
+        hea_h = workloads.random_pauli_hamiltonian(n, 12, seed=4)
+        for fuse in (False, True):
+            d = Device.sharded(n, rank, world, nccl_ids[2 + int(fuse)], device=rank, fuse=fuse)
+            res[f"jac{int(fuse)}"], res[f"jev{int(fuse)}"] = d.adjoint_jacobian(sel_ops, obs[:3], return_expvals=True)
+            res[f"qjac{int(fuse)}"], res[f"qjev{int(fuse)}"] = d.adjoint_jacobian(qaoa_ops, [qaoa_h], return_expvals=True)
+            res[f"hjac{int(fuse)}"], res[f"hjev{int(fuse)}"] = d.adjoint_jacobian(hea_ops, [hea_h], return_expvals=True)
+            d.release()
         if rank == 0:
             ref = O.run_circuit(n, ops, psi)
             out = {}
@@ -56,9 +62,13 @@ def _worker(rank, world, nccl_ids, q):
                 out[f"ev{f}"] = abs(res[f"ev{f}"] - O.expval(ref, n, ham))
                 out[f"probs{f}"] = float(np.abs(res[f"probs{f}"] - O.probabilities(ref, n, [0, 7, 1])).max())
                 out[f"norm{f}"] = abs(res[f"norm{f}"] - 1.0)
-            jref, evref = O.adjoint_jacobian(n, sel_ops, obs[:3])
-            out["jac"] = float(np.abs(res["jac"] - jref).max())
-            out["jev"] = float(np.abs(res["jev"] - evref).max())
+            refs = {"": O.adjoint_jacobian(n, sel_ops, obs[:3]), "q": O.adjoint_jacobian(n, qaoa_ops, [qaoa_h]),
+                    "h": O.adjoint_jacobian(n, hea_ops, [hea_h])}
+            for key, (jref, evref) in refs.items():
+                for f in (0, 1):
+                    scale = max(1.0, float(np.abs(jref).max()))
+                    out[f"{key}jac{f}"] = float(np.abs(res[f"{key}jac{f}"] - jref).max()) / scale
+                    out[f"{key}jev{f}"] = float(np.abs(np.asarray(res[f"{key}jev{f}"]) - evref).max()) / scale
             q.put(("ok", out))
     except Exception as exc:  # surface worker failures to the test
         import traceback
@@ -70,7 +80,7 @@ def test_sharded_nccl_matches_oracle(world):
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
     from paper_2403_02512_b200.device import Device
-    nccl_ids = [Device.nccl_unique_id() for _ in range(3)]   # one id per communicator
+    nccl_ids = [Device.nccl_unique_id() for _ in range(4)]   # one id per communicator
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     procs = [ctx.Process(target=_worker, args=(r, world, nccl_ids, q)) for r in range(world)]
@@ -81,5 +91,5 @@ def test_sharded_nccl_matches_oracle(world):
         p.join(timeout=120)
     assert status == "ok", out
     for k, v in out.items():
-        tol = 1e-10 if k in ("jac", "jev") else 1e-12
+        tol = 1e-10 if "j" in k else 1e-12
         assert v < tol, (k, v)
