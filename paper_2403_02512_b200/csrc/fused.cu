@@ -323,97 +323,133 @@ __device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const FOp& op, con
   }
 }
 
+// Launch-time records derived from the planned program: every per-pass / per-phase quantity the
+// kernel would otherwise recompute per tile or per phase (swizzled shared-memory offsets, spread
+// physical bit masks) is computed once on the host.  Shared-memory offsets compose by XOR because
+// swz is GF(2)-linear.
+constexpr int kTB = kMaxB - kRB;   // max thread-index bits
+// The thread-index -> (swizzled shared offset, physical bits) maps of a phase are GF(2)-linear in
+// the thread index (<= 8 bits), so each is two 16-entry nibble tables: s0 = s_lo[tid & 15] ^
+// s_hi[tid >> 4].
+struct __align__(16) DPhase {
+  int W[kRB];        // swz(1 << reg[k]): offset of register bit k
+  int s_lo[16], s_hi[16];   // swizzled shared offset of the thread's slot, per tid nibble
+  u64 g_lo[16], g_hi[16];   // physical bits of the thread's slot, per tid nibble
+  int op_begin, op_end;     // pass-local op range
+  int flip, pad;
+};
+static_assert(sizeof(DPhase) == 416, "DPhase layout");
+static_assert(kTB <= 8, "two tid nibbles");
+
+struct DPass {
+  u64 n_tiles;
+  u64 outer;           // physical bits NOT in the tile (the tile index deposits into these)
+  u64 grid_step;       // deposit(gridDim.x): tile t -> t + grid is a masked add
+  u64 hi;              // two-array state: indices with this bit live in state_hi
+  u64 ld_off[kRegs];   // load slot i: physical offset of its register-slot bits (without hi)
+  u64 st_off[kRegs];   // store slot i: the same after the pass's in-tile relabeling
+  u64 ld_tb[kTB];      // physical bit of thread-index bit j at load (may be hi)
+  u64 st_tb[kTB];      // ... at store
+  int ld_sm[kRegs];    // swizzled shared offset of load slot i
+  int st_sm[kRegs];    // swizzled shared offset of store slot i
+  int st_tsm[kTB];     // swizzled shared offset of thread-index bit j at store
+  unsigned ld_hsel, st_hsel;   // slots whose index carries the hi bit
+  int b, nthr, n_phases, n_ops, n_gen, gen_base, n_gen_total, pad;
+};
+
 // DB = true : one persistent CTA per SM, two tile buffers, tile t+grid prefetched during tile t.
 // DB = false: two CTAs per SM (128 registers), one buffer each; CTAs overlap each other instead.
-// Dynamic shared memory: [tile buffer(s)] [op records of the pass].
-template <bool FULL, bool DB>
-__global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__ state, const FPassArgs P,
-                                                            const FPhase* __restrict__ phases,
+// TWO = the adjoint sweep's two-array state (psi | lambda selected by bit P.hi).
+// Dynamic shared memory: [tile buffer(s)] [phase records] [op records] [generator accumulators].
+template <bool FULL, bool DB, bool TWO>
+__global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__ state, const DPass P,
+                                                            const DPhase* __restrict__ phases,
                                                             const FOp* __restrict__ ops,
                                                             const double2* __restrict__ coef,
                                                             double2* __restrict__ gen_partials,
                                                             double2* __restrict__ state_hi) {
-  // two-array states (adjoint sweep): indices with bit P.hi_mask live in state_hi
-  auto gptr = [&](u64 idx) -> double2* {
-    return (idx & P.hi_mask) ? state_hi + (idx ^ P.hi_mask) : state + idx;
-  };
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* tile_mem = reinterpret_cast<double2*>(smem_raw);
   const int tid = threadIdx.x;
   const int nthreads = blockDim.x;            // 2^(b-4)
   const int T = 1 << P.b;
-  // stage the pass's op records in shared memory (uniform broadcast reads in the op loop)
-  FOp* s_ops = reinterpret_cast<FOp*>(smem_raw + size_t(DB ? 2 : 1) * T * sizeof(double2));
-  const int nops = P.op_end - P.op_begin;
-  // per-warp generator accumulators (adjoint sweep): [warp][kMaxGens]
-  double2* s_gen = reinterpret_cast<double2*>(s_ops + nops);
+  DPhase* s_ph = reinterpret_cast<DPhase*>(smem_raw + size_t(DB ? 2 : 1) * T * sizeof(double2));
+  FOp* s_ops = reinterpret_cast<FOp*>(s_ph + P.n_phases);
+  double2* s_gen = reinterpret_cast<double2*>(s_ops + P.n_ops);   // per-warp accumulators [warp][kMaxGens]
   {
-    const int4* src = reinterpret_cast<const int4*>(ops + P.op_begin);
-    int4* dst = reinterpret_cast<int4*>(s_ops);
-    const int n16 = nops * int(sizeof(FOp) / 16);
+    // stage the pass's phase and op records (uniform broadcast reads in the phase / op loops)
+    const int4* src = reinterpret_cast<const int4*>(phases);
+    int4* dst = reinterpret_cast<int4*>(s_ph);
+    const int n16p = P.n_phases * int(sizeof(DPhase) / 16);
+    for (int i = tid; i < n16p; i += nthreads) dst[i] = src[i];
+    src = reinterpret_cast<const int4*>(ops);
+    dst = reinterpret_cast<int4*>(s_ops);
+    const int n16 = P.n_ops * int(sizeof(FOp) / 16);
     for (int i = tid; i < n16; i += nthreads) dst[i] = src[i];
     if (P.n_gen)
       for (int i = tid; i < (nthreads >> 5) * kMaxGens; i += nthreads) s_gen[i] = make_double2(0.0, 0.0);
     __syncthreads();
   }
-  // load slot i of this thread is tile index s = tid + nthreads * i
-  u64 spread_tid = 0;
-  for (int j = 0; j < P.nthr; ++j)
-    if ((tid >> j) & 1) spread_tid |= 1ull << P.tpos[j];
-  const int swz_tid = swz(tid);
-  auto spread_hi = [&](int i) {
-    u64 s = 0;
+  // per-thread constants of the pass
+  u64 ld_tid = 0, st_tid = 0;
+  int st_sw = 0;
 #pragma unroll
-    for (int j = 0; j < kRB; ++j)
-      if ((i >> j) & 1) s |= 1ull << P.tpos[P.nthr + j];
-    return s;
-  };
-  auto swz_hi = [&](int i) { return swz(nthreads * i); };
-  // tile index -> global base (insert zero bits at the tile positions)
-  auto tile_base = [&](u64 t) {
-    u64 base = t;
-    for (int j = 0; j < P.b; ++j) {
-      const int p = P.tpos[j];
-      const u64 lo = base & ((1ull << p) - 1ull);
-      base = ((base ^ lo) << 1) | lo;
+  for (int j = 0; j < kTB; ++j)
+    if (j < P.nthr && ((tid >> j) & 1)) {
+      ld_tid |= P.ld_tb[j];
+      st_tid |= P.st_tb[j];
+      st_sw ^= P.st_tsm[j];
     }
-    return base;
+  const int ld_sw = swz(tid);
+  // slot i of a thread whose index bits are g lives at (g | off_i); the bits are disjoint, so the
+  // address is a pointer computed once per tile plus a per-slot constant.  Two-array states pick
+  // the array by the hi bit (off_i never carries it; hsel says which slots do).
+  auto slot_ptrs = [&](u64 g, double2*& p_lo, double2*& p_hi) {
+    if (!TWO) {
+      p_lo = p_hi = state + g;
+      return;
+    }
+    const u64 gl = g & ~P.hi;
+    p_hi = state_hi + gl;
+    p_lo = (g & P.hi) ? p_hi : state + gl;
   };
   // global -> shared (cp.async 16 B per amplitude, conflict-free through the swizzle), one group
-  auto issue_load = [&](u64 t, double2* dst_buf) {
-    const u64 gb = tile_base(t) | spread_tid;
+  auto issue_load = [&](u64 base, double2* dst_buf) {
+    double2 *p_lo, *p_hi;
+    slot_ptrs(base | ld_tid, p_lo, p_hi);
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(dst_buf);
 #pragma unroll
     for (int i = 0; i < kRegs; ++i) {
-      const double2* src = gptr(gb | spread_hi(i));
-      const unsigned dst = (unsigned)__cvta_generic_to_shared(&dst_buf[swz_tid ^ swz_hi(i)]);
+      const double2* src = (TWO && ((P.ld_hsel >> i) & 1) ? p_hi : p_lo) + P.ld_off[i];
+      const unsigned dst = sb + unsigned(ld_sw ^ P.ld_sm[i]) * 16u;
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
-  const FOp* OPS = s_ops - P.op_begin;        // indexed with global op numbers
+  // first tile's base: deposit blockIdx.x into the outer bits; later tiles: masked add
+  u64 base = 0;
+  {
+    u64 m = P.outer;
+    for (u64 v = blockIdx.x; m && v; m &= m - 1, v >>= 1)
+      if (v & 1) base |= m & (~m + 1);
+  }
   int cur = 0;
-  if (DB && blockIdx.x < P.n_tiles) issue_load(blockIdx.x, tile_mem);
+  if (DB && blockIdx.x < P.n_tiles) issue_load(base, tile_mem);
   for (u64 t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
     double2* tile = tile_mem + (DB ? cur * T : 0);
+    const u64 nbase = ((base | ~P.outer) + P.grid_step) & P.outer;
     if (!DB) {
       __syncthreads();   // previous tile fully stored before the buffer is refilled
-      issue_load(t, tile_mem);
+      issue_load(base, tile_mem);
     }
     asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
-    if (DB && t + gridDim.x < P.n_tiles) issue_load(t + gridDim.x, tile_mem + (cur ^ 1) * T);
-    const u64 base = tile_base(t);
+    if (DB && t + gridDim.x < P.n_tiles) issue_load(nbase, tile_mem + (cur ^ 1) * T);
     for (int ph = 0; ph < P.n_phases; ++ph) {
-      const FPhase& F = phases[P.phase_begin + ph];
-      int sthr = 0;
-      u64 phys_base = base;
-      for (int j = 0; j < P.nthr; ++j)
-        if ((tid >> j) & 1) {
-          sthr |= 1 << F.thr[j];
-          phys_base |= 1ull << P.tpos[F.thr[j]];
-        }
-      const int s0 = swz(sthr);
-      const int W0 = swz(1 << F.reg[0]), W1 = swz(1 << F.reg[1]), W2 = swz(1 << F.reg[2]), W3 = swz(1 << F.reg[3]);
+      const DPhase& F = s_ph[ph];
+      const int s0 = F.s_lo[tid & 15] ^ F.s_hi[tid >> 4];
+      const u64 phys_base = base | F.g_lo[tid & 15] | F.g_hi[tid >> 4];
+      const int W0 = F.W[0], W1 = F.W[1], W2 = F.W[2], W3 = F.W[3];
       double2 a[kRegs];
 #pragma unroll
       for (int r = 0; r < kRegs; ++r)
@@ -421,7 +457,7 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
       int fthr = 0;   // per-thread register relabeling from thread-predicated X gates
       const int oe = F.op_end;
       for (int oi = F.op_begin; oi < oe; ++oi) {
-        const FOp& op = OPS[oi];
+        const FOp& op = s_ops[oi];
         const bool pred = (phys_base & op.pm) == op.pv;
         if (op.cs >= CS_GEN1)
           gen_op<FULL>(a, op, pred, fthr, phys_base, coef, s_gen + (tid >> 5) * kMaxGens);
@@ -429,7 +465,7 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
           apply_op<FULL>(a, op, coef, phys_base, fthr);
       }
       {
-        // register r holds logical index r ^ flip: store offset = swz(sthr) ^ W(r ^ flip) (W linear)
+        // register r holds logical index r ^ flip: store offset = s0 ^ W(r ^ flip) (W linear)
         const int fl = F.flip ^ fthr;
         const int sf = s0 ^ ((fl & 1) ? W0 : 0) ^ ((fl & 2) ? W1 : 0) ^ ((fl & 4) ? W2 : 0) ^ ((fl & 8) ? W3 : 0);
 #pragma unroll
@@ -438,33 +474,18 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
       }
       __syncthreads();
     }
-    // shared -> global with the pass's in-tile relabeling: store-loop slot (tid, i) covers tile
-    // index bits q[0..] and lands on physical positions tpos_st[q[..]] (q[0..2] -> bits 0..2, so
-    // 8 lanes still write 128 contiguous bytes).  Same address set as the load: in-place safe.
-    // (This buffer is refilled only after the next iteration's barrier.)
+    // shared -> global with the pass's in-tile relabeling (store slot offsets precomputed; the
+    // three lowest tile bits still land on physical bits 0..2, so 8 lanes write 128 contiguous
+    // bytes).  Same address set as the load: in-place safe.  (The buffer is refilled only after
+    // the next iteration's barrier.)
     {
-      u64 st_tid = 0;
-      int sq_tid = 0;
-      for (int j = 0; j < P.nthr; ++j)
-        if ((tid >> j) & 1) {
-          st_tid |= 1ull << P.tpos_st[P.q[j]];
-          sq_tid |= 1 << P.q[j];
-        }
-      const u64 gb = base | st_tid;
-      const int sw_tid = swz(sq_tid);
+      double2 *p_lo, *p_hi;
+      slot_ptrs(base | st_tid, p_lo, p_hi);
 #pragma unroll
-      for (int i = 0; i < kRegs; ++i) {
-        u64 g = gb;
-        int s = 0;
-#pragma unroll
-        for (int j = 0; j < kRB; ++j)
-          if ((i >> j) & 1) {
-            g |= 1ull << P.tpos_st[P.q[P.nthr + j]];
-            s |= 1 << P.q[P.nthr + j];
-          }
-        *gptr(g) = tile[sw_tid ^ swz(s)];
-      }
+      for (int i = 0; i < kRegs; ++i)
+        (TWO && ((P.st_hsel >> i) & 1) ? p_hi : p_lo)[P.st_off[i]] = tile[st_sw ^ P.st_sm[i]];
     }
+    base = nbase;
     cur ^= 1;
   }
   // generator partials of this CTA: fixed-order sum over warps -> gen_partials[block][slot]
@@ -480,6 +501,79 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
       gen_partials[size_t(blockIdx.x) * P.n_gen_total + P.gen_base + g] = s;
     }
   }
+}
+
+inline int swz_host(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
+
+inline u64 deposit_host(u64 v, u64 m) {
+  u64 r = 0;
+  for (; m && v; m &= m - 1, v >>= 1)
+    if (v & 1) r |= m & (~m + 1);
+  return r;
+}
+
+DPass make_dpass(const FPassArgs& A, int nl, u64 grid) {
+  DPass D;
+  std::memset(&D, 0, sizeof(D));
+  D.n_tiles = A.n_tiles;
+  u64 tilemask = 0;
+  for (int j = 0; j < A.b; ++j) tilemask |= 1ull << A.tpos[j];
+  D.outer = ((nl >= 64) ? ~0ull : ((1ull << nl) - 1)) & ~tilemask;
+  D.grid_step = deposit_host(grid, D.outer);
+  D.hi = A.hi_mask;
+  const int nthr = A.nthr, nthreads = 1 << nthr;
+  for (int j = 0; j < nthr; ++j) {
+    D.ld_tb[j] = 1ull << A.tpos[j];
+    D.st_tb[j] = 1ull << A.tpos_st[A.q[j]];
+    D.st_tsm[j] = swz_host(1 << A.q[j]);
+  }
+  for (int i = 0; i < kRegs; ++i) {
+    u64 lo = 0, so = 0;
+    int ss = 0;
+    for (int k = 0; k < kRB; ++k)
+      if ((i >> k) & 1) {
+        lo |= 1ull << A.tpos[nthr + k];
+        so |= 1ull << A.tpos_st[A.q[nthr + k]];
+        ss |= 1 << A.q[nthr + k];
+      }
+    D.ld_off[i] = lo & ~D.hi;
+    D.st_off[i] = so & ~D.hi;
+    if (lo & D.hi) D.ld_hsel |= 1u << i;
+    if (so & D.hi) D.st_hsel |= 1u << i;
+    D.ld_sm[i] = swz_host(nthreads * i);
+    D.st_sm[i] = swz_host(ss);
+  }
+  D.b = A.b;
+  D.nthr = nthr;
+  D.n_phases = A.n_phases;
+  D.n_ops = A.op_end - A.op_begin;
+  D.n_gen = A.n_gen;
+  D.gen_base = A.gen_base;
+  D.n_gen_total = A.n_gen_total;
+  return D;
+}
+
+DPhase make_dphase(const FPhase& F, const FPassArgs& A) {
+  DPhase D;
+  std::memset(&D, 0, sizeof(D));
+  for (int k = 0; k < kRB; ++k) D.W[k] = swz_host(1 << F.reg[k]);
+  for (int v = 0; v < 16; ++v)
+    for (int j = 0; j < 4; ++j) {
+      if ((v >> j) & 1) {
+        if (j < A.nthr) {
+          D.s_lo[v] ^= swz_host(1 << F.thr[j]);
+          D.g_lo[v] |= 1ull << A.tpos[F.thr[j]];
+        }
+        if (j + 4 < A.nthr) {
+          D.s_hi[v] ^= swz_host(1 << F.thr[j + 4]);
+          D.g_hi[v] |= 1ull << A.tpos[F.thr[j + 4]];
+        }
+      }
+    }
+  D.op_begin = F.op_begin - A.op_begin;
+  D.op_end = F.op_end - A.op_begin;
+  D.flip = F.flip;
+  return D;
 }
 
 struct DevProgram {
@@ -508,9 +602,15 @@ void* program_buffer(sv_handle* h, size_t bytes) {
   return d.buf;
 }
 
-template <bool FULL, bool DB>
+template <bool FULL, bool DB, bool TWO>
 void set_smem_attr(int bytes) {
-  CUDA_CHECK(cudaFuncSetAttribute(k_fused<FULL, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  CUDA_CHECK(cudaFuncSetAttribute(k_fused<FULL, DB, TWO>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+template <bool FULL, bool DB, bool TWO>
+void launch_fused(unsigned grid, int threads, size_t smem, cudaStream_t st, double2* state, const DPass& D,
+                  const DPhase* ph, const FOp* op, const double2* cf, double2* gen, double2* state_hi) {
+  k_fused<FULL, DB, TWO><<<grid, threads, smem, st>>>(state, D, ph, op, cf, gen, state_hi);
 }
 
 }  // namespace
@@ -559,33 +659,21 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
       for (const Prim& p : prog.singles) run_single(st, p);
     return identity;
   }
-  // upload phases | ops | coef in one copy (the buffer is only reused after a stream sync)
-  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
-  const size_t b_ph = prog.phases.size() * sizeof(FPhase);
-  const size_t b_op = prog.ops.size() * sizeof(FOp);
-  const size_t b_cf = prog.coef.size() * sizeof(double2);
-  const size_t total = align(b_ph) + align(b_op) + align(b_cf);
-  std::vector<char> host(total);
-  std::memcpy(host.data(), prog.phases.data(), b_ph);
-  std::memcpy(host.data() + align(b_ph), prog.ops.data(), b_op);
-  std::memcpy(host.data() + align(b_ph) + align(b_op), prog.coef.data(), b_cf);
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));   // previous program may still be in use
-  char* dbuf = (char*)program_buffer(h, total);
-  CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), total, cudaMemcpyHostToDevice, h->stream));
-  const FPhase* d_ph = (const FPhase*)dbuf;
-  const FOp* d_op = (const FOp*)(dbuf + align(b_ph));
-  const double2* d_cf = (const double2*)(dbuf + align(b_ph) + align(b_op));
-
   static std::once_flag once;
   static int dev_sms = 148;
   static bool db = true;
   std::call_once(once, [&]() {
+    // the attribute is an upper bound; a launch's real footprint sets its occupancy
     const int tile = int((size_t(1) << kMaxB) * sizeof(double2));
-    const int ops_b = kMaxSmemOps * int(sizeof(FOp)) + 8 * kMaxGens * int(sizeof(double2));
-    set_smem_attr<true, true>(2 * tile + ops_b);
-    set_smem_attr<false, true>(2 * tile + ops_b);
-    set_smem_attr<true, false>(tile + ops_b);
-    set_smem_attr<false, false>(tile + ops_b);
+    const int recs = 200 * 1024 - 2 * tile;
+    set_smem_attr<true, true, false>(2 * tile + recs);
+    set_smem_attr<false, true, false>(2 * tile + recs);
+    set_smem_attr<true, false, false>(tile + recs);
+    set_smem_attr<false, false, false>(tile + recs);
+    set_smem_attr<true, true, true>(2 * tile + recs);
+    set_smem_attr<false, true, true>(2 * tile + recs);
+    set_smem_attr<true, false, true>(tile + recs);
+    set_smem_attr<false, false, true>(tile + recs);
     CUDA_CHECK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
     // default: single buffer, 2 CTAs/SM (measured faster: 16 warps hide the op-loop latency
     // better than 8 warps with a prefetched tile); "db" selects the double-buffered variant
@@ -594,6 +682,27 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
   });
   const int b = prog.passes[0].b;
   const u64 grid = std::min<u64>(prog.passes[0].n_tiles, u64(dev_sms) * (db ? 1 : 2));   // persistent grid
+
+  // launch records + upload phases | ops | coef in one copy (the buffer is only reused after a sync)
+  std::vector<DPhase> dph(prog.phases.size());
+  for (const FPassArgs& A : prog.passes)
+    for (int ph = 0; ph < A.n_phases; ++ph) dph[A.phase_begin + ph] = make_dphase(prog.phases[A.phase_begin + ph], A);
+  auto align = [](size_t x) { return (x + 255) & ~size_t(255); };
+  const size_t b_ph = dph.size() * sizeof(DPhase);
+  const size_t b_op = prog.ops.size() * sizeof(FOp);
+  const size_t b_cf = prog.coef.size() * sizeof(double2);
+  const size_t total = align(b_ph) + align(b_op) + align(b_cf);
+  std::vector<char> host(total);
+  std::memcpy(host.data(), dph.data(), b_ph);
+  std::memcpy(host.data() + align(b_ph), prog.ops.data(), b_op);
+  std::memcpy(host.data() + align(b_ph) + align(b_op), prog.coef.data(), b_cf);
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));   // previous program may still be in use
+  char* dbuf = (char*)program_buffer(h, total);
+  CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), total, cudaMemcpyHostToDevice, h->stream));
+  const DPhase* d_ph = (const DPhase*)dbuf;
+  const FOp* d_op = (const FOp*)(dbuf + align(b_ph));
+  const double2* d_cf = (const double2*)(dbuf + align(b_ph) + align(b_op));
+
   const int n_gen = int(prog.gen_slot_of.size());
   double2* d_gen = nullptr;
   if (n_gen) {
@@ -601,6 +710,7 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
     CUDA_CHECK(cudaMallocAsync(&d_gen, grid * n_gen * sizeof(double2), h->stream));
     CUDA_CHECK(cudaMemsetAsync(d_gen, 0, grid * n_gen * sizeof(double2), h->stream));
   }
+  const bool two = state_hi != nullptr;
   for (double2* state : states) {
     for (const Step& s : prog.steps) {
       if (!s.fused) {
@@ -609,22 +719,29 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
         continue;
       }
       const FPassArgs& A = prog.passes[s.index];
+      const DPass D = make_dpass(A, h->nl, grid);
       const bool full = prog.full[s.index];
       const int threads = 1 << (A.b - kRB);
-      const int nops = A.op_end - A.op_begin;
-      const size_t smem = (db ? 2 : 1) * (size_t(1) << b) * sizeof(double2) + size_t(nops) * sizeof(FOp) +
-                          (A.n_gen ? size_t(threads / 32) * kMaxGens * sizeof(double2) : 0);
+      const size_t smem = (db ? 2 : 1) * (size_t(1) << b) * sizeof(double2) + size_t(D.n_phases) * sizeof(DPhase) +
+                          size_t(D.n_ops) * sizeof(FOp) + (A.n_gen ? size_t(threads / 32) * kMaxGens * sizeof(double2) : 0);
+      const DPhase* ph = d_ph + A.phase_begin;
+      const FOp* op = d_op + A.op_begin;
       const double bytes = 32.0 * double(h->n_local);
       cudaEvent_t ev[2];
       stat_begin(h, KC_FUSED, bytes, ev);
-      if (db && full)
-        k_fused<true, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen, state_hi);
-      else if (db)
-        k_fused<false, true><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen, state_hi);
-      else if (full)
-        k_fused<true, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen, state_hi);
-      else
-        k_fused<false, false><<<unsigned(grid), threads, smem, h->stream>>>(state, A, d_ph, d_op, d_cf, d_gen, state_hi);
+      const unsigned g = unsigned(grid);
+      cudaStream_t st = h->stream;
+      if (two) {
+        if (db && full) launch_fused<true, true, true>(g, threads, smem, st, state, D, ph, op, d_cf, d_gen, state_hi);
+        else if (db) launch_fused<false, true, true>(g, threads, smem, st, state, D, ph, op, d_cf, d_gen, state_hi);
+        else if (full) launch_fused<true, false, true>(g, threads, smem, st, state, D, ph, op, d_cf, d_gen, state_hi);
+        else launch_fused<false, false, true>(g, threads, smem, st, state, D, ph, op, d_cf, d_gen, state_hi);
+      } else {
+        if (db && full) launch_fused<true, true, false>(g, threads, smem, st, state, D, ph, op, d_cf, d_gen, state_hi);
+        else if (db) launch_fused<false, true, false>(g, threads, smem, st, state, D, ph, op, d_cf, d_gen, state_hi);
+        else if (full) launch_fused<true, false, false>(g, threads, smem, st, state, D, ph, op, d_cf, d_gen, state_hi);
+        else launch_fused<false, false, false>(g, threads, smem, st, state, D, ph, op, d_cf, d_gen, state_hi);
+      }
       stat_end(h, KC_FUSED, bytes, ev);
       CUDA_CHECK(cudaGetLastError());
     }

@@ -64,18 +64,26 @@ void fill_regs(std::vector<int>& reg, int b) {
     if (std::find(reg.begin(), reg.end(), p) == reg.end()) reg.push_back(p);
 }
 
-void make_phase_thr(FPhase& F, const std::vector<int>& reg, int b) {
+// Thread-index bits of a phase.  Lanes 0..2 take one non-register position of each residue class
+// mod 3 (the swizzle then spreads a 16-byte wavefront over all banks); among the candidates, and
+// for the remaining bits, positions the phase's ops test as predicates (controls, diagonal
+// patterns: `use`) go to the high, warp-uniform thread bits, so those predicates -- and the
+// per-thread X flips they drive -- do not split warps.
+void make_phase_thr(FPhase& F, const std::vector<int>& reg, int b, const int* use) {
   for (int k = 0; k < kRB; ++k) F.reg[k] = (uint8_t)reg[k];
+  auto is_reg = [&](int p) { return std::find(reg.begin(), reg.end(), p) != reg.end(); };
   std::vector<int> thr;
-  for (int c = 0; c < 3; ++c)
+  for (int c = 0; c < 3; ++c) {
+    int best = -1;
     for (int p = c; p < b; p += 3)
-      if (std::find(reg.begin(), reg.end(), p) == reg.end()) {
-        thr.push_back(p);
-        break;
-      }
+      if (!is_reg(p) && (best < 0 || use[p] < use[best])) best = p;
+    if (best >= 0) thr.push_back(best);
+  }
+  std::vector<int> rest;
   for (int p = 0; p < b; ++p)
-    if (std::find(reg.begin(), reg.end(), p) == reg.end() && std::find(thr.begin(), thr.end(), p) == thr.end())
-      thr.push_back(p);
+    if (!is_reg(p) && std::find(thr.begin(), thr.end(), p) == thr.end()) rest.push_back(p);
+  std::stable_sort(rest.begin(), rest.end(), [&](int x, int y) { return use[x] < use[y]; });
+  thr.insert(thr.end(), rest.begin(), rest.end());
   for (int j = 0; j < b - kRB; ++j) F.thr[j] = (uint8_t)thr[j];
 }
 
@@ -438,9 +446,13 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
       for (int p = 0; p < 64; ++p)
         if ((ph.first >> p) & 1) R.push_back(tile_pos_of[p]);
       fill_regs(R, b);
+      int use[kMaxB] = {0};   // predicate tests per tile position in this phase
+      for (int i : ph.second)
+        for (int p = 0; p < 64; ++p)
+          if (((P[i].fmask >> p) & 1) && tile_pos_of[p] >= 0) ++use[tile_pos_of[p]];
       FPhase F;
       std::memset(&F, 0, sizeof(F));
-      make_phase_thr(F, R, b);
+      make_phase_thr(F, R, b, use);
       F.op_begin = int(prog.ops.size());
       F.flip = uint8_t(emit_ops(prog, P, ph.second, tile_pos_of, R));
       F.op_end = int(prog.ops.size());
