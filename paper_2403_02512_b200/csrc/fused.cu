@@ -87,6 +87,33 @@ __device__ __forceinline__ void pairg(double2 (&a)[kRegs], const double2* __rest
     if ((r & cm) == cv) pair_upd<MT>(a[r], a[r ^ XR], m0, m1, m2, m3);
 }
 
+// rotation R(phi) of every (x0, x1) pair on register bit K as shears u += t v; v += s u; u += t v
+// (RY type: on (re0, re1) and (im0, im1); RX type: R(-phi) on (re0, im1), R(phi) on (im0, re1))
+template <int K, bool RX>
+__device__ __forceinline__ void pair_shear(double2 (&a)[kRegs], const double t, const double s) {
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if ((r >> K) & 1) continue;
+    double2& x0 = a[r];
+    double2& x1 = a[r | (1 << K)];
+    if (RX) {
+      x0.x = fma(-t, x1.y, x0.x);
+      x0.y = fma(t, x1.x, x0.y);
+      x1.y = fma(-s, x0.x, x1.y);
+      x1.x = fma(s, x0.y, x1.x);
+      x0.x = fma(-t, x1.y, x0.x);
+      x0.y = fma(t, x1.x, x0.y);
+    } else {
+      x0.x = fma(t, x1.x, x0.x);
+      x0.y = fma(t, x1.y, x0.y);
+      x1.x = fma(s, x0.x, x1.x);
+      x1.y = fma(s, x0.y, x1.y);
+      x0.x = fma(t, x1.x, x0.x);
+      x0.y = fma(t, x1.y, x0.y);
+    }
+  }
+}
+
 template <int K, int V>
 __device__ __forceinline__ void phase1(double2 (&a)[kRegs], const double2 d) {
 #pragma unroll
@@ -167,6 +194,14 @@ __device__ __forceinline__ void diagg(double2 (&a)[kRegs], const FOp& op, const 
     if (((fthr >> K) & 1) ^ op.v) phase1<K, 1>(a, op.c[0]);            \
     else phase1<K, 0>(a, op.c[0]);                                     \
     break;
+#define SHEAR_CASE(K)                                                                       \
+  case CS_SHEAR + K * 4 + SH_RY: pair_shear<K, false>(a, op.c[0].x, op.c[0].y); break;         \
+  case CS_SHEAR + K * 4 + SH_RX: pair_shear<K, true>(a, op.c[0].x, op.c[0].y); break;          \
+  case CS_SHEAR + K * 4 + SH_RYD: {   /* flipped roles: R(-phi) */                            \
+    const bool sw = (fthr >> K) & 1;                                                          \
+    pair_shear<K, false>(a, sw ? -op.c[0].x : op.c[0].x, sw ? -op.c[0].y : op.c[0].y);       \
+    break;                                                                                    \
+  }
 #define PAIRG_CASE(XR)                                                                     \
   case CS_PAIRGR + XR - 1: pairg<XR, MT_REAL>(a, op.c, op.cm, op.cv ^ (fthr & op.cm)); break; \
   case CS_PAIRG + XR - 1: if (FULL) pairg<XR, MT_GENERAL>(a, op.c, op.cm, op.cv ^ (fthr & op.cm)); break;
@@ -288,6 +323,7 @@ __device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const FOp& op, con
     PAIR1_CASE(0) PAIR1_CASE(1) PAIR1_CASE(2) PAIR1_CASE(3)
     PAIR1D_CASE(0) PAIR1D_CASE(1) PAIR1D_CASE(2) PAIR1D_CASE(3)
     PHASE1_CASE(0) PHASE1_CASE(1) PHASE1_CASE(2) PHASE1_CASE(3)
+    SHEAR_CASE(0) SHEAR_CASE(1) SHEAR_CASE(2) SHEAR_CASE(3)
     case CS_SCALAR: {
       const double2 d = op.c[0];
 #pragma unroll

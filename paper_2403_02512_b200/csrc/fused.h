@@ -52,10 +52,14 @@ constexpr int CS_DENSE2 = 56;    // + pair index 0..5                        (56
 constexpr int CS_XFLIP = 62;     // + k: thread-predicated X on register bit k (62..65)
 constexpr int CS_PAIR1D = 66;    // + k*4 + mtype: PAIR1 on a dynamically flipped bit (66..81)
 constexpr int CS_PHASE1D = 82;   // + k*2 + v: PHASE1 on a dynamically flipped bit   (82..89)
+// unconditioned rotations as three in-place shears per real pair (6 FMAs instead of 4 DMUL +
+// 4 DFMA); c[0] = (t, s) = (-tan(phi/2), sin(phi)), |phi| <= pi/2
+constexpr int CS_SHEAR = 90;     // + k*4 + {0: RY-type, 1: RX-type, 2: RY-type on a flipped bit} (90..105)
+constexpr int SH_RY = 0, SH_RX = 1, SH_RYD = 2;
 // adjoint bra-kets (psi and lambda share the tile; t = register bit selecting lambda)
-constexpr int CS_GEN1 = 90;      // + k*4 + t: 2x2 generator on register bit k        (90..105)
-constexpr int CS_GEN2 = 106;     // + pair*4 + t: 4x4 generator on register bits pair (106..129)
-constexpr int CS_GEND = 130;     // + t: diagonal generator (table on any bits; only t in registers) (130..133)
+constexpr int CS_GEN1 = 106;     // + k*4 + t: 2x2 generator on register bit k        (106..121)
+constexpr int CS_GEN2 = 122;     // + pair*4 + t: 4x4 generator on register bits pair (122..145)
+constexpr int CS_GEND = 146;     // + t: diagonal generator (table on any bits; only t in registers) (146..149)
 constexpr int kMaxGens = 64;     // generator slots per pass (per-warp shared-memory accumulators)
 static_assert(sizeof(FOp) == 112, "FOp layout");
 

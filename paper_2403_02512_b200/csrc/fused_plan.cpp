@@ -7,6 +7,7 @@
 // e.g. RX or the X of a CNOT) or generally.  Two primitives commute when every shared bit is
 // Z-like in both or X-like in both -- so RZ slides past CNOT controls and RX past CNOT targets.
 #include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -103,6 +104,9 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
   };
   int F = 0;   // uniform flips (applied here, on the host)
   int D = 0;   // register bits that may carry a per-thread flip (handled by the kernel)
+  static const bool shear_on = !(getenv("SVB200_SHEAR") && std::string(getenv("SVB200_SHEAR")) == "0");
+  const int op_first = int(prog.ops.size());
+  int neg = 0;   // unconditioned rotations emitted as -R(phi'): the phase owes the state a factor (-1)^neg
   for (int i : list) {
     const Prim& p = prims[i];
     FOp op;
@@ -272,6 +276,27 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
       for (auto& c : mf) prog.coef.push_back(make_double2(c.real(), c.imag()));
     }
     const bool dyn = ((D >> op.k) & 1) != 0;
+    if (shear_on && op.kind == FK_PAIR1 && (op.mtype == MT_REAL || op.mtype == MT_RXLIKE)) {
+      // rotation R(phi) = [[c, -s], [s, c]] (RY type) or [[c, -is], [-is, c]] (RX type)?
+      cplx m[4];
+      for (int j = 0; j < 4; ++j) m[j] = cplx(prog.coef[op.tab + j].x, prog.coef[op.tab + j].y);
+      const bool rx = op.mtype == MT_RXLIKE;
+      const bool rot = rx ? (m[0] == m[3] && m[1] == m[2]) : (m[0] == m[3] && m[1] == -m[2]);
+      double c = m[0].real(), sn = rx ? -m[1].imag() : m[2].real();
+      if (rot && (c >= 0.0 || op.pm == 0)) {
+        if (c < 0.0) {   // R(phi) = -R(phi -+ pi): the sign is global for an unconditioned op
+          c = -c;
+          sn = -sn;
+          neg ^= 1;
+        }
+        op.cs = CS_SHEAR + op.k * 4 + (rx ? SH_RX : (dyn ? SH_RYD : SH_RY));   // RX is symmetric under flips
+        op.c[0] = make_double2(-sn / (1.0 + c), sn);
+        op.c[1] = make_double2(c, 0.0);   // (c, s) kept for a later conversion back to the 2x2 form
+        op.c[2] = make_double2(sn, rx ? 1.0 : 0.0);
+        prog.ops.push_back(op);
+        continue;
+      }
+    }
     switch (op.kind) {
       case FK_PAIR1: op.cs = (dyn ? CS_PAIR1D : CS_PAIR1) + op.k * 4 + op.mtype; break;
       case FK_PHASE1: op.cs = (dyn ? CS_PHASE1D : CS_PHASE1) + op.k * 2 + op.v; break;
@@ -288,6 +313,51 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
       for (int j = 0; j < nc; ++j) op.c[j] = prog.coef[op.tab + j];
     }
     prog.ops.push_back(op);
+  }
+  if (neg) {
+    // absorb the owed -1 into an unconditioned 2x2 / scalar op of the phase, else turn one
+    // unconditioned shear back into its 2x2 form carrying the sign
+    auto negate = [&](FOp& o, int nc) {
+      for (int j = 0; j < nc; ++j) {
+        o.c[j] = make_double2(-o.c[j].x, -o.c[j].y);
+        prog.coef[o.tab + j] = o.c[j];
+      }
+    };
+    int conv = -1;
+    for (int oi = int(prog.ops.size()) - 1; oi >= op_first && neg; --oi) {
+      FOp& o = prog.ops[oi];
+      if (o.pm != 0) continue;
+      const bool pair1 = (o.cs >= CS_PAIR1 && o.cs < CS_PAIR1 + 16) || (o.cs >= CS_PAIR1D && o.cs < CS_PAIR1D + 16);
+      if (pair1) {
+        negate(o, 4);
+        neg = 0;
+      } else if (o.cs == CS_SCALAR) {
+        negate(o, 1);
+        neg = 0;
+      } else if (conv < 0 && o.cs >= CS_SHEAR && o.cs < CS_SHEAR + 16) {
+        conv = oi;
+      }
+    }
+    if (neg) {
+      if (conv < 0) sv_fail(SV_ERR_DEVICE, "internal: unabsorbed rotation sign");
+      FOp& o = prog.ops[conv];
+      const double c = o.c[1].x, sn = o.c[2].x;
+      const bool rx = o.c[2].y != 0.0;
+      const int k = (o.cs - CS_SHEAR) / 4;
+      const bool dyn = ((D >> k) & 1) != 0;
+      std::array<cplx, 4> mm;
+      if (rx)
+        mm = {cplx(-c, 0), cplx(0, sn), cplx(0, sn), cplx(-c, 0)};      // -[[c, -is], [-is, c]]
+      else
+        mm = {cplx(-c, 0), cplx(sn, 0), cplx(-sn, 0), cplx(-c, 0)};     // -[[c, -s], [s, c]]
+      o.tab = int(prog.coef.size());
+      for (int j = 0; j < 4; ++j) {
+        prog.coef.push_back(make_double2(mm[j].real(), mm[j].imag()));
+        o.c[j] = prog.coef.back();
+      }
+      o.mtype = uint8_t(rx ? MT_RXLIKE : MT_REAL);
+      o.cs = (dyn ? CS_PAIR1D : CS_PAIR1) + k * 4 + o.mtype;
+    }
   }
   return F;
 }

@@ -17,6 +17,7 @@ from paper_2403_02512_b200 import _lib
 # dispatch cases (fused.h)
 CS_PAIR1, CS_PHASE1, CS_SCALAR, CS_PAIRGR, CS_PAIRG = 0, 16, 24, 25, 40
 CS_DIAGG, CS_DENSE2, CS_XFLIP, CS_PAIR1D, CS_PHASE1D = 55, 56, 62, 66, 82
+CS_SHEAR = 90   # + k*4 + {0: RY-type, 1: RX-type, 2: RY-type on a flipped bit}
 KRB = 4
 KMAXB = 12
 
@@ -178,6 +179,32 @@ def _apply(a, op, pred, fthr, phys_base, coef):
         for r in range(16):
             if not (r >> k) & 1:
                 pair(r, r | (1 << k), m, pred)
+    elif CS_SHEAR <= cs < CS_SHEAR + 16:
+        k, kind = (cs - CS_SHEAR) // 4, (cs - CS_SHEAR) % 4
+        t, s = c[0].real, c[0].imag
+        if kind == 2:
+            sg = np.where(((fthr >> k) & 1).astype(bool), -1.0, 1.0)
+            t, s = sg * t, sg * s
+
+        def shear(u, v, t, s):   # u += t v; v += s u; u += t v   (same rounding as the kernel's FMAs)
+            u = u + t * v
+            v = v + s * u
+            return u + t * v, v
+
+        for r in range(16):
+            if (r >> k) & 1:
+                continue
+            x0, x1 = a[..., r].copy(), a[..., r | (1 << k)].copy()
+            if kind == 1:
+                ure, vim = shear(x0.real, x1.imag, -t, -s)
+                uim, vre = shear(x0.imag, x1.real, t, s)
+                n0, n1 = ure + 1j * uim, vre + 1j * vim
+            else:
+                r0, r1 = shear(x0.real, x1.real, t, s)
+                i0, i1 = shear(x0.imag, x1.imag, t, s)
+                n0, n1 = r0 + 1j * i0, r1 + 1j * i1
+            a[..., r] = np.where(pred, n0, x0)
+            a[..., r | (1 << k)] = np.where(pred, n1, x1)
     elif CS_PHASE1 <= cs < CS_PHASE1 + 8 or CS_PHASE1D <= cs < CS_PHASE1D + 8:
         k = op["k"]
         v = op["v"] ^ (((fthr >> k) & 1) if cs >= CS_PHASE1D else 0)
