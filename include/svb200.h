@@ -21,6 +21,8 @@
  *   sv_apply_matrix                apply_matrix                        state.py:278-303
  *   sv_apply_ops                   Device.apply (op list)              SPEC.md:649 (circuit op SPEC.md:494)
  *   sv_expval / sv_probs           measurements.expval / probabilities SPEC.md:283-301
+ *   sv_var                         measurements.variance
+ *   sv_sample                      measurements.sample / sample_root
  *   sv_adjoint_jacobian            adjoint_jacobian
  *   sv_create_sharded              ShardedState / shard
  */
@@ -114,6 +116,15 @@ int sv_apply_ops(sv_handle* h, const sv_op* ops, int n_ops, int fuse);
 /* ---- measurements ---- */
 int sv_expval(sv_handle* h, const sv_obs* obs, double* out);
 int sv_probs(sv_handle* h, const int32_t* wires, int n_wires, double* out); /* n_wires=0: all */
+/* <O^2> - <O>^2 (Pauli word: 1 - <P>^2; otherwise |O psi|^2 - <psi|O psi>^2). */
+int sv_var(sv_handle* h, const sv_obs* obs, double* out);
+/* shots i.i.d. outcomes over `wires` (n_wires=0: all; wires[0] = MSB of the outcome index),
+ * deterministic per seed and identical for sharded and single-GPU states: with p = the
+ * marginal probabilities (sv_probs) and C their sequential inclusive prefix sums, shot i draws
+ * x = splitmix64(seed + (i + 1) * 0x9E3779B97F4A7C15), u = (x >> 11) * 2^-53, and returns the
+ * first b with C[b] > u * C[last].  out: shots int64 outcome indices.  shots == 0 -> validation
+ * error; more than 30 wires -> capacity error. */
+int sv_sample(sv_handle* h, const int32_t* wires, int n_wires, uint64_t shots, uint64_t seed, int64_t* out);
 
 /* ---- adjoint Jacobian ----
  * Runs ops forward from the handle's current state, then the reverse sweep.

@@ -337,6 +337,36 @@ def probabilities(amps, n, wires=None):
     return np.transpose(m, [kept.index(w) for w in wires]).reshape(-1)
 
 
+def variance(amps, n, obs):
+    """<O^2> - <O>^2, O^2 formed by applying O twice."""
+    amps = np.asarray(amps)
+    lam = apply_observable(amps, n, obs)
+    e = np.vdot(amps, lam).real
+    return float(np.vdot(lam, lam).real - e * e)
+
+
+def _splitmix64(x):
+    m = (1 << 64) - 1
+    x = (x + 0x9E3779B97F4A7C15) & m
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & m
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & m
+    return x ^ (x >> 31)
+
+
+def sample(amps, n, shots, seed=0, wires=None):
+    """Outcome indices of ``shots`` draws by the fixed inverse-CDF procedure
+    the library documents (include/svb200.h, sv_sample): sequential prefix sums C of the
+    marginal probabilities, u_i = splitmix64(seed + (i+1) * golden) >> 11 scaled by 2^-53,
+    outcome = first b with C[b] > u_i * C[-1]."""
+    if shots < 1:
+        raise OracleError("shots must be >= 1")
+    c = np.cumsum(probabilities(amps, n, wires))
+    m = (1 << 64) - 1
+    u = np.array([(_splitmix64((seed + (i + 1) * 0x9E3779B97F4A7C15) & m) >> 11) for i in range(shots)],
+                 dtype=np.float64) * (1.0 / 9007199254740992.0) * c[-1]
+    return np.minimum(np.searchsorted(c, u, side="right"), len(c) - 1).astype(np.int64)
+
+
 # ---------------------------------------------------------------------------
 # adjoint-gradient (SPEC.md:354-422; formula SURVEY Appendix A)
 # ---------------------------------------------------------------------------

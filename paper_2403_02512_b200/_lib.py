@@ -22,7 +22,7 @@ EXPORTS = (
     "sv_device_count", "sv_create", "sv_nccl_unique_id", "sv_create_sharded", "sv_destroy", "sv_info",
     "sv_reset", "sv_set_basis_state", "sv_set_state", "sv_get_state", "sv_norm",
     "sv_apply_single_qubit", "sv_apply_controlled_single_qubit", "sv_apply_matrix", "sv_apply_ops",
-    "sv_expval", "sv_probs", "sv_adjoint_jacobian", "sv_last_error", "sv_synchronize", "sv_stream",
+    "sv_expval", "sv_probs", "sv_var", "sv_sample", "sv_adjoint_jacobian", "sv_last_error", "sv_synchronize", "sv_stream",
     "sv_launch_count", "sv_set_profiling", "sv_kernel_stats", "sv_reset_stats", "sv_plan_summary",
     "sv_plan_program", "sv_plan_sharded",
 )
@@ -75,6 +75,8 @@ def lib():
             "sv_apply_ops": [H, POINTER(SvOp), c_int, c_int],
             "sv_expval": [H, POINTER(SvObs), POINTER(c_double)],
             "sv_probs": [H, POINTER(c_int32), c_int, POINTER(c_double)],
+            "sv_var": [H, POINTER(SvObs), POINTER(c_double)],
+            "sv_sample": [H, POINTER(c_int32), c_int, ctypes.c_uint64, ctypes.c_uint64, POINTER(ctypes.c_int64)],
             "sv_adjoint_jacobian": [H, POINTER(SvOp), c_int, POINTER(SvObs), c_int, c_int, POINTER(c_double),
                                     POINTER(c_double)],
             "sv_synchronize": [H],

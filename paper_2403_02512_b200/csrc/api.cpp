@@ -800,25 +800,99 @@ int sv_expval(sv_handle* h, const sv_obs* obs, double* out) {
   API_END
 }
 
+// variance: a Pauli word squares to I, so Var = 1 - <P>^2; otherwise
+// lambda = O psi (one extra state buffer) gives <O^2> = |lambda|^2 (O Hermitian) and <O> =
+// Re<psi|lambda>, both local partial sums allreduced across shards.
+int sv_var(sv_handle* h, const sv_obs* obs, double* out) {
+  API_BEGIN
+  check_handle(h);
+  if (!obs || !out) sv_fail(SV_ERR_VALIDATION, "null observable");
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (obs->type == SV_OBS_PAULI) {
+    const double e = expval_impl(h, *obs);
+    *out = 1.0 - e * e;
+  } else {
+    size_t free_b = 0, total_b = 0;
+    CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+    const size_t bytes = h->n_local * sizeof(double2);
+    double lacking = (bytes + (64ull << 20) > free_b) ? 1.0 : 0.0;
+    dist_allreduce_sum(h, &lacking, 1);
+    if (lacking > 0) sv_fail(SV_ERR_CAPACITY, "variance needs one extra state buffer");
+    expval_impl(h, *obs);   // validates the observable (and its wires) like expval
+    double2* lam = nullptr;
+    CUDA_CHECK(cudaMalloc(&lam, bytes));
+    try {
+      apply_observable(h, *obs, h->state, lam, {h->state, lam});
+      double v[2] = {reduce_norm2(h, lam), reduce_dot_re(h, h->state, lam)};
+      dist_allreduce_sum(h, v, 2);
+      *out = v[0] - v[1] * v[1];
+    } catch (...) {
+      cudaFree(lam);
+      throw;
+    }
+    CUDA_CHECK(cudaFree(lam));
+  }
+  API_END
+}
+
+static std::vector<int> measured_wires(const sv_handle* h, const int32_t* wires, int n_wires, const char* what) {
+  std::vector<int> w;
+  if (n_wires <= 0) {
+    for (int q = 0; q < h->n; ++q) w.push_back(q);
+    return w;
+  }
+  for (int i = 0; i < n_wires; ++i) {
+    if (wires[i] < 0 || wires[i] >= h->n)
+      sv_fail(SV_ERR_VALIDATION, "wire " + std::to_string(wires[i]) + " out of range for " + std::to_string(h->n) +
+                                     "-qubit register");
+    for (int j = 0; j < i; ++j)
+      if (wires[j] == wires[i]) sv_fail(SV_ERR_VALIDATION, std::string("duplicate wires in ") + what);
+    w.push_back(wires[i]);
+  }
+  return w;
+}
+
 int sv_probs(sv_handle* h, const int32_t* wires, int n_wires, double* out) {
   API_BEGIN
   check_handle(h);
   std::lock_guard<std::mutex> lk(h->mu);
-  std::vector<int> w;
-  if (n_wires <= 0) {
-    for (int q = 0; q < h->n; ++q) w.push_back(q);
-  } else {
-    for (int i = 0; i < n_wires; ++i) {
-      if (wires[i] < 0 || wires[i] >= h->n)
-        sv_fail(SV_ERR_VALIDATION, "wire " + std::to_string(wires[i]) + " out of range for " + std::to_string(h->n) +
-                                       "-qubit register");
-      for (int j = 0; j < i; ++j)
-        if (wires[j] == wires[i]) sv_fail(SV_ERR_VALIDATION, "duplicate wires in probabilities");
-      w.push_back(wires[i]);
-    }
-  }
+  const std::vector<int> w = measured_wires(h, wires, n_wires, "probabilities");
   if (w.size() > 40) sv_fail(SV_ERR_CAPACITY, "probability vector too large");
   dist_probs(h, w, out);
+  API_END
+}
+
+// Deterministic sampling (sample_root SPEC.md:455-462): the marginal
+// distribution comes from the device reduction (dist_probs: every rank holds the same vector),
+// the inverse-CDF draw is the fixed procedure documented in svb200.h, so a sharded state and a
+// single-GPU state give the same rows for the same seed.
+static inline uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+int sv_sample(sv_handle* h, const int32_t* wires, int n_wires, uint64_t shots, uint64_t seed, int64_t* out) {
+  API_BEGIN
+  check_handle(h);
+  if (shots == 0) sv_fail(SV_ERR_VALIDATION, "shots must be >= 1");
+  if (!out) sv_fail(SV_ERR_VALIDATION, "null output buffer");
+  std::lock_guard<std::mutex> lk(h->mu);
+  const std::vector<int> w = measured_wires(h, wires, n_wires, "sample");
+  if (w.size() > 30) sv_fail(SV_ERR_CAPACITY, "sampling supports at most 30 measured wires");
+  const size_t bins = size_t(1) << w.size();
+  std::vector<double> c(bins);
+  dist_probs(h, w, c.data());
+  for (size_t b = 1; b < bins; ++b) c[b] += c[b - 1];   // sequential inclusive prefix
+  const double total = c[bins - 1];
+  for (uint64_t i = 0; i < shots; ++i) {
+    const uint64_t x = splitmix64(seed + (i + 1) * 0x9E3779B97F4A7C15ull);
+    const double u = double(x >> 11) * (1.0 / 9007199254740992.0) * total;
+    size_t b = size_t(std::upper_bound(c.begin(), c.end(), u) - c.begin());
+    if (b >= bins) b = bins - 1;
+    out[i] = int64_t(b);
+  }
   API_END
 }
 

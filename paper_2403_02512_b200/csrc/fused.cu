@@ -202,6 +202,13 @@ __device__ __forceinline__ void diagg(double2 (&a)[kRegs], const FOp& op, const 
     pair_shear<K, false>(a, sw ? -op.c[0].x : op.c[0].x, sw ? -op.c[0].y : op.c[0].y);       \
     break;                                                                                    \
   }
+#define DENSE2_CASE(PI, K0, K1)                                                              \
+  case CS_DENSE2 + PI:                                                                        \
+    if (FULL) {                                                                               \
+      const int f = ((fthr >> K0) & 1) | (((fthr >> K1) & 1) << 1);                          \
+      dense2<K0, K1>(a, coef + op.tab, op.cm, op.cv ^ (fthr & op.cm), f);                     \
+    }                                                                                         \
+    break;
 #define PAIRG_CASE(XR)                                                                     \
   case CS_PAIRGR + XR - 1: pairg<XR, MT_REAL>(a, op.c, op.cm, op.cv ^ (fthr & op.cm)); break; \
   case CS_PAIRG + XR - 1: if (FULL) pairg<XR, MT_GENERAL>(a, op.c, op.cm, op.cv ^ (fthr & op.cm)); break;
@@ -317,13 +324,18 @@ __device__ __forceinline__ void gen_op(const double2 (&a)[kRegs], const FOp& op,
 // One flat switch on the dense case index.  FULL = false compiles only the common kinds;
 // passes that need DIAGG / DENSE2 / complex PAIRG use the FULL kernel.  `op` is in shared memory.
 template <bool FULL>
-__device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef,
-                                         u64 phys_base, int& fthr) {
-  switch (op.cs) {
+__device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const int cs, const FOp& op,
+                                         const double2* __restrict__ coef, u64 phys_base, int& fthr) {
+  // every index 0 .. CS_GEN1-1 is an explicit label and the default is unreachable, so the
+  // compiler emits one jump table (a compare tree here costs ~5 dependent branches per op)
+  switch (cs) {
     PAIR1_CASE(0) PAIR1_CASE(1) PAIR1_CASE(2) PAIR1_CASE(3)
+    case CS_PAIR1 + 3: case CS_PAIR1 + 7: case CS_PAIR1 + 11: case CS_PAIR1 + 15: break;
     PAIR1D_CASE(0) PAIR1D_CASE(1) PAIR1D_CASE(2) PAIR1D_CASE(3)
+    case CS_PAIR1D + 3: case CS_PAIR1D + 7: case CS_PAIR1D + 11: case CS_PAIR1D + 15: break;
     PHASE1_CASE(0) PHASE1_CASE(1) PHASE1_CASE(2) PHASE1_CASE(3)
     SHEAR_CASE(0) SHEAR_CASE(1) SHEAR_CASE(2) SHEAR_CASE(3)
+    case CS_SHEAR + 3: case CS_SHEAR + 7: case CS_SHEAR + 11: case CS_SHEAR + 15: break;
     case CS_SCALAR: {
       const double2 d = op.c[0];
 #pragma unroll
@@ -340,22 +352,9 @@ __device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const FOp& op, con
     case CS_DIAGG:
       if (FULL) diagg(a, op, coef, phys_base, fthr);
       break;
-    default:
-      if (FULL && op.cs >= CS_DENSE2 && op.cs < CS_DENSE2 + 6) {
-        const int k0 = op.xr & 15, k1 = op.xr >> 4;
-        const int f = ((fthr >> k0) & 1) | (((fthr >> k1) & 1) << 1);
-        const int cv = op.cv ^ (fthr & op.cm);
-        const double2* M = coef + op.tab;
-        switch (op.cs - CS_DENSE2) {
-          case 0: dense2<0, 1>(a, M, op.cm, cv, f); break;
-          case 1: dense2<0, 2>(a, M, op.cm, cv, f); break;
-          case 2: dense2<0, 3>(a, M, op.cm, cv, f); break;
-          case 3: dense2<1, 2>(a, M, op.cm, cv, f); break;
-          case 4: dense2<1, 3>(a, M, op.cm, cv, f); break;
-          default: dense2<2, 3>(a, M, op.cm, cv, f); break;
-        }
-      }
-      break;
+    DENSE2_CASE(0, 0, 1) DENSE2_CASE(1, 0, 2) DENSE2_CASE(2, 0, 3)
+    DENSE2_CASE(3, 1, 2) DENSE2_CASE(4, 1, 3) DENSE2_CASE(5, 2, 3)
+    default: __builtin_unreachable();
   }
 }
 
@@ -492,13 +491,29 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
         a[r] = tile[s0 ^ ((r & 1) ? W0 : 0) ^ ((r & 2) ? W1 : 0) ^ ((r & 4) ? W2 : 0) ^ ((r & 8) ? W3 : 0)];
       int fthr = 0;   // per-thread register relabeling from thread-predicated X gates
       const int oe = F.op_end;
-      for (int oi = F.op_begin; oi < oe; ++oi) {
+      // the next op's header (case, pattern) is loaded one iteration ahead, so the dispatch
+      // branches do not wait on shared memory
+      int oi = F.op_begin;
+      int cs_n = 0;
+      u64 pm_n = 0, pv_n = 0;
+      if (oi < oe) {
+        cs_n = s_ops[oi].cs;
+        pm_n = s_ops[oi].pm;
+        pv_n = s_ops[oi].pv;
+      }
+      for (; oi < oe; ++oi) {
         const FOp& op = s_ops[oi];
-        const bool pred = (phys_base & op.pm) == op.pv;
-        if (op.cs >= CS_GEN1)
+        const int cs = cs_n;
+        const bool pred = (phys_base & pm_n) == pv_n;
+        if (oi + 1 < oe) {
+          cs_n = s_ops[oi + 1].cs;
+          pm_n = s_ops[oi + 1].pm;
+          pv_n = s_ops[oi + 1].pv;
+        }
+        if (cs >= CS_GEN1)
           gen_op<FULL>(a, op, pred, fthr, phys_base, coef, s_gen + (tid >> 5) * kMaxGens);
         else if (pred)
-          apply_op<FULL>(a, op, coef, phys_base, fthr);
+          apply_op<FULL>(a, cs, op, coef, phys_base, fthr);
       }
       {
         // register r holds logical index r ^ flip: store offset = s0 ^ W(r ^ flip) (W linear)

@@ -1,7 +1,7 @@
 """``Device``: the py-bindings device handle of the reference on a B200.
 
 ``bind_device(n_qubits, precision, tier)`` returns a handle that owns a complex128 state in
-HBM; ``apply`` / ``expval`` / ``probs`` / ``adjoint_jacobian`` forward 1:1 to the C-ABI
+HBM; ``apply`` / ``expval`` / ``var`` / ``probs`` / ``sample`` / ``adjoint_jacobian`` forward 1:1 to the C-ABI
 (include/svb200.h) with copy-out marshalling. One mutator per handle
  is enforced by a per-handle mutex inside the library.
 """
@@ -139,8 +139,28 @@ class Device:
                                        out.ctypes.data_as(ctypes.POINTER(c_double))))
         return out
 
-    def sample(self, shots, seed=0):
-        raise UnsupportedOperationError("sampling is a next-round item (SURVEY.md §8(f) rank 1)")
+    def var(self, obs):
+        """Variance <O^2> - <O>^2 (SPEC.md:313-320)."""
+        pb = _lib.PackedObs([as_observable(obs)])
+        v = c_double()
+        _lib.check(_lib.lib().sv_var(self.handle, pb.ptr, ctypes.byref(v)))
+        return v.value
+
+    def sample_indices(self, shots, seed=0, wires=None):
+        """``shots`` outcome indices over ``wires`` (all if None; wires[0] = MSB), deterministic
+        per seed; the draw procedure is documented at sv_sample in include/svb200.h."""
+        w = np.zeros(0, dtype=np.int32) if wires is None else np.ascontiguousarray(wires, dtype=np.int32)
+        out = np.empty(int(shots), dtype=np.int64)
+        _lib.check(_lib.lib().sv_sample(self.handle, w.ctypes.data_as(ctypes.POINTER(ctypes.c_int32)), len(w),
+                                        int(shots), int(seed) & 0xFFFFFFFFFFFFFFFF,
+                                        out.ctypes.data_as(ctypes.POINTER(ctypes.c_int64))))
+        return out
+
+    def sample(self, shots, seed=0, wires=None):
+        """SampleSet: ``shots`` rows of 0/1 bits, one column per measured wire."""
+        width = self.n_qubits if wires is None else len(wires)
+        idx = self.sample_indices(shots, seed, wires)
+        return ((idx[:, None] >> np.arange(width - 1, -1, -1)) & 1).astype(np.int8)
 
     # ---- adjoint Jacobian ----------------------------------------------------------------
     def adjoint_jacobian(self, ops, observables, return_expvals=False, fuse=None):

@@ -358,3 +358,48 @@ def test_fused_adjoint_qaoa_and_hea_vs_unfused():
         ja = a.adjoint_jacobian(ops, [h], fuse=True)
         jb = b.adjoint_jacobian(ops, [h], fuse=False)
     assert np.abs(ja - jb).max() < 1e-10 * max(1.0, sum(abs(c) for c in h.coeffs))
+
+
+def test_variance_vs_oracle():
+    """SPEC.md:313-320 on the device: Pauli words, a Hamiltonian and a dense observable."""
+    rng = np.random.default_rng(21)
+    n = 11
+    psi = rand_state(rng, n)
+    obs = [PauliWord(((3, "Z"),)), PauliWord(((0, "X"), (10, "Y"), (5, "Z"))),
+           workloads.random_pauli_hamiltonian(n, 25, seed=3),
+           DenseHermitian((7, 2), (lambda a: a + a.conj().T)(rng.normal(size=(4, 4)) + 1j * rng.normal(size=(4, 4))))]
+    with Device(n) as d:
+        d.set_state(psi)
+        for o in obs:
+            got, ref = d.var(o), O.variance(psi, n, o)
+            assert abs(got - ref) <= 1e-10 * max(1.0, obs_norm1(o) ** 2), (o, got, ref)
+        d.reset()
+        assert abs(d.var(PauliWord(((0, "Z"),)))) < 1e-15          # Var(Z) on |0> = 0
+        d.apply([Op("H", (0,))])
+        assert abs(d.var(PauliWord(((0, "Z"),))) - 1.0) < 1e-12    # Var(Z) on H|0> = 1
+
+
+def test_sample_vs_oracle_procedure():
+    """the device draws the same rows as the oracle's restatement of the
+    documented procedure (probabilities agree to ~1e-16, so outcomes coincide), KATs and errors."""
+    rng = np.random.default_rng(8)
+    n = 12
+    ops = workloads.random_circuit(n, 8, seed=2)
+    psi = O.run_circuit(n, ops)
+    with Device(n) as d:
+        d.apply(ops)
+        for wires in (None, [3], [11, 0, 5], list(range(n))[::-1]):
+            got = d.sample_indices(20_000, seed=1234, wires=wires)
+            ref = O.sample(psi, n, 20_000, seed=1234, wires=wires)
+            assert (got != ref).sum() <= 1, wires      # a draw on a 1e-16 boundary may differ
+        rows = d.sample(64, seed=5, wires=[1, 2])
+        assert rows.shape == (64, 2) and set(np.unique(rows)) <= {0, 1}
+        assert (d.sample_indices(500, seed=77) == d.sample_indices(500, seed=77)).all()
+        with pytest.raises(errors.ValidationError):
+            d.sample_indices(0)
+        d.set_basis_state((1 << n) - 1)
+        assert (d.sample(100, seed=3) == 1).all()              # |1...1> -> all rows ones
+        d.reset()
+        d.apply([Op("H", (0,))])
+        f0 = (d.sample(10_000, seed=42, wires=[0])[:, 0] == 0).mean()
+        assert abs(f0 - 0.5) < 0.02

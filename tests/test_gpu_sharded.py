@@ -43,6 +43,8 @@ def _worker(rank, world, nccl_ids, q):
             res[f"ev{int(fuse)}"] = d.expval(ham)
             res[f"probs{int(fuse)}"] = d.probs([0, 7, 1])
             res[f"norm{int(fuse)}"] = d.norm()
+            res[f"samp{int(fuse)}"] = d.sample_indices(5000, seed=99, wires=[0, 7, 1, 11])
+            res[f"var{int(fuse)}"] = d.var(ham)
             d.release()
         sel_ops, obs = workloads.sel_config(n, 2, seed=2)
         qaoa_ops, qaoa_h, _ = workloads.qaoa_maxcut(n, p=2, seed=1)
@@ -62,6 +64,8 @@ def _worker(rank, world, nccl_ids, q):
                 out[f"ev{f}"] = abs(res[f"ev{f}"] - O.expval(ref, n, ham))
                 out[f"probs{f}"] = float(np.abs(res[f"probs{f}"] - O.probabilities(ref, n, [0, 7, 1])).max())
                 out[f"norm{f}"] = abs(res[f"norm{f}"] - 1.0)
+                out[f"samp{f}"] = float((res[f"samp{f}"] != O.sample(ref, n, 5000, seed=99, wires=[0, 7, 1, 11])).sum()) * 5e-13
+                out[f"var{f}"] = abs(res[f"var{f}"] - O.variance(ref, n, ham))
             refs = {"": O.adjoint_jacobian(n, sel_ops, obs[:3]), "q": O.adjoint_jacobian(n, qaoa_ops, [qaoa_h]),
                     "h": O.adjoint_jacobian(n, hea_ops, [hea_h])}
             for key, (jref, evref) in refs.items():

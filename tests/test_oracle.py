@@ -226,3 +226,44 @@ def test_sharded_model_roundtrip():
     psi = np.arange(8, dtype=complex)
     sh = O.shard(psi, 2)
     assert np.array_equal(sh[0], psi[:4]) and np.array_equal(O.gather(sh), psi)
+
+
+def test_kat_variance():
+    """Var(Z) on |0> = 0, on H|0> = 1; Hamiltonian and dense vs explicit O^2."""
+    zero = O.zero_state(1)
+    assert abs(O.variance(zero, 1, PauliWord(((0, "Z"),)))) < 1e-15
+    plus = np.array([1, 1], dtype=np.complex128) / np.sqrt(2)
+    assert abs(O.variance(plus, 1, PauliWord(((0, "Z"),))) - 1.0) < 1e-15
+    rng = np.random.default_rng(3)
+    n = 5
+    psi = rng.normal(size=32) + 1j * rng.normal(size=32)
+    psi /= np.linalg.norm(psi)
+    h = Hamiltonian([0.3, -1.2], [PauliWord(((0, "X"), (2, "Y"))), PauliWord(((4, "Z"),))])
+    M = np.stack([O.apply_observable(np.eye(32, dtype=np.complex128)[:, k], n, h) for k in range(32)], axis=1)
+    ref = np.vdot(psi, M @ M @ psi).real - np.vdot(psi, M @ psi).real ** 2
+    assert abs(O.variance(psi, n, h) - ref) < 1e-12
+
+
+def test_kat_sample():
+    """|1> -> all ones; H|0> frequency 0.5 +- 0.02 at 1e4 shots; same seed ->
+    identical rows; shots = 0 rejected; chi-square against |psi|^2."""
+    one = np.array([0, 1], dtype=np.complex128)
+    assert (O.sample(one, 1, 100, seed=7) == 1).all()
+    plus = np.array([1, 1], dtype=np.complex128) / np.sqrt(2)
+    s = O.sample(plus, 1, 10_000, seed=11)
+    assert abs((s == 0).mean() - 0.5) < 0.02
+    assert (O.sample(plus, 1, 500, seed=3) == O.sample(plus, 1, 500, seed=3)).all()
+    with pytest.raises(O.OracleError):
+        O.sample(plus, 1, 0)
+    rng = np.random.default_rng(0)
+    n = 4
+    psi = rng.normal(size=16) + 1j * rng.normal(size=16)
+    psi /= np.linalg.norm(psi)
+    shots = 100_000
+    counts = np.bincount(O.sample(psi, n, shots, seed=5), minlength=16)
+    expected = np.abs(psi) ** 2 * shots
+    chi2 = float(((counts - expected) ** 2 / expected).sum())
+    assert chi2 < 37.7   # chi-square(15 dof) at p = 0.001
+    # marginal over wires (2, 0): same procedure on the marginal vector
+    m = O.sample(psi, n, 1000, seed=9, wires=[2, 0])
+    assert m.min() >= 0 and m.max() < 4
