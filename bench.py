@@ -275,6 +275,16 @@ def main():
                         "circuit's effective GB/s (value) is a multiple of the HBM peak"
                 if dom == "fused_tile" else None}
 
+    # global-qubit swaps (rank-0 view): NCCL send/recv of half a shard per swap over NVLink
+    comm = None
+    if world > 1 and "swap" in stats:
+        sw = stats["swap"]
+        sent = sw["bytes"] / 2.0   # stats count 32 B per swapped amplitude (read + write); NVLink carries 16 B
+        comm = {"swaps_per_step": sw["launches"] / args.steps, "bytes_sent_per_rank_per_step": sent / args.steps,
+                "ms_per_step": sw["ms"] / args.steps, "share_of_step": sw["ms"] / ms if ms else None,
+                "nvlink_GBps_per_direction": sent / (sw["ms"] / 1e3) / 1e9 if sw["ms"] > 0 else None,
+                "nvlink_peak_GBps_per_direction": 900.0}
+
     # e2e through the public API: host op list in, <Z_0> out, every step
     obs = PauliWord(((0, "Z"),))
     packed = _lib.PackedOps(ops)
@@ -318,7 +328,7 @@ def main():
                        "parallelism": f"sharded over {world} GPU(s), {g} global qubit(s)" if world > 1 else "1 GPU",
                        "l2": f"state {16 * (1 << (n - g)) / 2**30:.0f} GiB per GPU >> 126 MB L2 (no flush needed)"},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "clocks": clocks, "expval_check": ev,
+            "clocks": clocks, "expval_check": ev, "comm": comm,
         }
         print(json.dumps(line), flush=True)
     dev.release()

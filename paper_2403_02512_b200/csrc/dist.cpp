@@ -11,7 +11,7 @@
 #include "dist.h"
 
 namespace {
-constexpr u64 kStagingAmps = 1ull << 24;   // 256 MiB staging ring for chunked half-shard swaps
+constexpr u64 kStagingAmps = 1ull << 27;   // 2 GiB staging: two 1 GiB slots (NCCL p2p reaches ~600 GB/s only at >= 512 MiB messages, benchmarks/p2p_bw.py)
 
 struct DistState {
   SwapStats stats;
@@ -55,17 +55,30 @@ void global_swap_top(sv_handle* h, const std::vector<double2*>& states, int G) {
   const u64 half = h->n_local >> 1;
   // we send our (top bit = 1-b) half and receive the partner's (top bit = b) half into it
   const u64 my_off = (1 - b) ? half : 0;
+  // Chunk k: send our chunk k and receive the partner's into staging slot k&1 (main stream), then
+  // copy the slot over our chunk k on the copy stream -- so the copy of chunk k overlaps the
+  // transfer of chunk k+1.  A slot is reused only after its previous copy finished; chunk k+1's
+  // send reads a region no copy has touched yet.
+  const u64 chunk = h->staging_amps / 2;
   cudaEvent_t ev[2];
   for (double2* st : states) {
     stat_begin(h, KC_SWAP, 32.0 * double(half), ev);
-    for (u64 c = 0; c < half; c += h->staging_amps) {
-      const u64 len = std::min<u64>(h->staging_amps, half - c);
+    int k = 0;
+    for (u64 c = 0; c < half; c += chunk, ++k) {
+      const u64 len = std::min<u64>(chunk, half - c);
+      double2* slot = h->staging + (k & 1) * chunk;
+      if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_copy[k & 1], 0));
       NCCL_CHECK(ncclGroupStart());
       NCCL_CHECK(ncclSend(st + my_off + c, len * 2, ncclDouble, partner, h->comm, h->stream));
-      NCCL_CHECK(ncclRecv(h->staging, len * 2, ncclDouble, partner, h->comm, h->stream));
+      NCCL_CHECK(ncclRecv(slot, len * 2, ncclDouble, partner, h->comm, h->stream));
       NCCL_CHECK(ncclGroupEnd());
-      CUDA_CHECK(cudaMemcpyAsync(st + my_off + c, h->staging, len * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream));
+      CUDA_CHECK(cudaEventRecord(h->ev_recv[k & 1], h->stream));
+      CUDA_CHECK(cudaStreamWaitEvent(h->copy_stream, h->ev_recv[k & 1], 0));
+      CUDA_CHECK(cudaMemcpyAsync(st + my_off + c, slot, len * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                 h->copy_stream));
+      CUDA_CHECK(cudaEventRecord(h->ev_copy[k & 1], h->copy_stream));
     }
+    for (int s = 0; s < std::min(k, 2); ++s) CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_copy[s], 0));
     stat_end(h, KC_SWAP, 32.0 * double(half), ev);
   }
   int ot = logical_at(h, h->nl - 1), og = logical_at(h, G);
@@ -97,8 +110,13 @@ void dist_init(sv_handle* h, const void* nccl_id) {
   ncclUniqueId id;
   std::memcpy(&id, nccl_id, sizeof(id));
   NCCL_CHECK(ncclCommInitRank(&h->comm, h->world, id, h->rank));
-  h->staging_amps = std::min<u64>(kStagingAmps, std::max<u64>(h->n_local >> 1, 1));
+  h->staging_amps = std::min<u64>(kStagingAmps, std::max<u64>(h->n_local >> 1, 2));
   CUDA_CHECK(cudaMalloc(&h->staging, h->staging_amps * sizeof(double2)));
+  CUDA_CHECK(cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking));
+  for (int i = 0; i < 2; ++i) {
+    CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_recv[i], cudaEventDisableTiming));
+    CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_copy[i], cudaEventDisableTiming));
+  }
 }
 
 void dist_destroy(sv_handle* h) {
@@ -109,6 +127,15 @@ void dist_destroy(sv_handle* h) {
   if (h->staging) {
     cudaFree(h->staging);
     h->staging = nullptr;
+  }
+  for (int i = 0; i < 2; ++i) {
+    if (h->ev_recv[i]) cudaEventDestroy(h->ev_recv[i]);
+    if (h->ev_copy[i]) cudaEventDestroy(h->ev_copy[i]);
+    h->ev_recv[i] = h->ev_copy[i] = nullptr;
+  }
+  if (h->copy_stream) {
+    cudaStreamDestroy(h->copy_stream);
+    h->copy_stream = nullptr;
   }
 }
 

@@ -109,6 +109,9 @@ struct sv_handle {
   ncclComm_t comm = nullptr;
   double2* staging = nullptr;
   u64 staging_amps = 0;
+  cudaStream_t copy_stream = nullptr;          // swap pipeline: staging -> state copies
+  cudaEvent_t ev_recv[2] = {nullptr, nullptr};
+  cudaEvent_t ev_copy[2] = {nullptr, nullptr};
   // reduction scratch
   double* d_partials = nullptr;
   size_t partials_cap = 0;      // doubles
