@@ -114,6 +114,20 @@ __device__ __forceinline__ void pair_shear(double2 (&a)[kRegs], const double t, 
   }
 }
 
+// a[r] *= d for registers r with parity(r & M) == 1 ^ tp (tp: the thread's parity part)
+template <int M>
+__device__ __forceinline__ void parity_phase(double2 (&a)[kRegs], const double2 d, const int tp) {
+  if (tp) {
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r)
+      if (!(__builtin_popcount(r & M) & 1)) cmul_ip(a[r], d);
+  } else {
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r)
+      if (__builtin_popcount(r & M) & 1) cmul_ip(a[r], d);
+  }
+}
+
 template <int K, int V>
 __device__ __forceinline__ void phase1(double2 (&a)[kRegs], const double2 d) {
 #pragma unroll
@@ -208,6 +222,10 @@ __device__ __forceinline__ void diagg(double2 (&a)[kRegs], const FOp& op, const 
       const int f = ((fthr >> K0) & 1) | (((fthr >> K1) & 1) << 1);                          \
       dense2<K0, K1>(a, coef + op.tab, op.cm, op.cv ^ (fthr & op.cm), f);                     \
     }                                                                                         \
+    break;
+#define PARITY_CASE(M)                                                                          \
+  case CS_PARITY + M:                                                                           \
+    parity_phase<M>(a, op.c[0], (__popcll(phys_base & op.xm) + __popc(fthr & M) + op.v) & 1);   \
     break;
 #define PAIRG_CASE(XR)                                                                     \
   case CS_PAIRGR + XR - 1: pairg<XR, MT_REAL>(a, op.c, op.cm, op.cv ^ (fthr & op.cm)); break; \
@@ -336,6 +354,9 @@ __device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const int cs, cons
     PHASE1_CASE(0) PHASE1_CASE(1) PHASE1_CASE(2) PHASE1_CASE(3)
     SHEAR_CASE(0) SHEAR_CASE(1) SHEAR_CASE(2) SHEAR_CASE(3)
     case CS_SHEAR + 3: case CS_SHEAR + 7: case CS_SHEAR + 11: case CS_SHEAR + 15: break;
+    PARITY_CASE(0) PARITY_CASE(1) PARITY_CASE(2) PARITY_CASE(3) PARITY_CASE(4) PARITY_CASE(5)
+    PARITY_CASE(6) PARITY_CASE(7) PARITY_CASE(8) PARITY_CASE(9) PARITY_CASE(10) PARITY_CASE(11)
+    PARITY_CASE(12) PARITY_CASE(13) PARITY_CASE(14) PARITY_CASE(15)
     case CS_SCALAR: {
       const double2 d = op.c[0];
 #pragma unroll

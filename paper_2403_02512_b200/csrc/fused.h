@@ -21,11 +21,13 @@ enum FKind : uint8_t {
   FK_SCALAR = 3,  // a *= d on all 16 amplitudes (pattern only on thread / outer bits)
   FK_DIAGG = 4,   // table lookup diagonal, general
   FK_DENSE2 = 5,  // 4x4 on register bits (k0 < k1) = xr & 15, xr >> 4
+  FK_PARITY = 6,  // diagonal phase on the parity of its bits (IsingZZ, Z-string phases)
 };
 enum MType : uint8_t { MT_GENERAL = 0, MT_REAL = 1, MT_RXLIKE = 2, MT_X = 3 };
 
 struct __align__(16) FOp {
   u64 pm, pv;            // fixed pattern on non-register bits (tested on the thread's physical base)
+  u64 xm;                // PARITY: non-register bits whose parity (on the physical base) enters the phase
   uint8_t kind, mtype;
   uint8_t xr;            // PAIRG: register-space xmask; DENSE2: k0 | (k1 << 4)
   uint8_t cm, cv;        // register-space pattern (PAIRG includes i0's pattern on xr)
@@ -36,6 +38,7 @@ struct __align__(16) FOp {
   int tab;               // offset into the coefficient array (DIAGG / DENSE2)
   int cs;                // dense dispatch case (CS_* below)
   int slot;              // GEN: accumulator slot within the pass
+  int pad_;
   double2 c[4];          // inline coefficients (PAIR1 / PAIRG: m00 m01 m10 m11; PHASE1 / SCALAR: d)
 };
 // Dense dispatch cases.  No case moves amplitudes between registers (data-moving swaps
@@ -56,12 +59,15 @@ constexpr int CS_PHASE1D = 82;   // + k*2 + v: PHASE1 on a dynamically flipped b
 // 4 DFMA); c[0] = (t, s) = (-tan(phi/2), sin(phi)), |phi| <= pi/2
 constexpr int CS_SHEAR = 90;     // + k*4 + {0: RY-type, 1: RX-type, 2: RY-type on a flipped bit} (90..105)
 constexpr int SH_RY = 0, SH_RX = 1, SH_RYD = 2;
+// parity phase (IsingZZ / ZZ..Z-string phases): a *= d where parity(register bits M of r) ^
+// parity(physical base & xm) ^ parity(fthr & M) ^ v == 1
+constexpr int CS_PARITY = 106;   // + M (register mask, 0..15)                        (106..121)
 // adjoint bra-kets (psi and lambda share the tile; t = register bit selecting lambda)
-constexpr int CS_GEN1 = 106;     // + k*4 + t: 2x2 generator on register bit k        (106..121)
-constexpr int CS_GEN2 = 122;     // + pair*4 + t: 4x4 generator on register bits pair (122..145)
-constexpr int CS_GEND = 146;     // + t: diagonal generator (table on any bits; only t in registers) (146..149)
+constexpr int CS_GEN1 = 122;     // + k*4 + t: 2x2 generator on register bit k        (122..137)
+constexpr int CS_GEN2 = 138;     // + pair*4 + t: 4x4 generator on register bits pair (138..161)
+constexpr int CS_GEND = 162;     // + t: diagonal generator (table on any bits; only t in registers) (162..165)
 constexpr int kMaxGens = 64;     // generator slots per pass (per-warp shared-memory accumulators)
-static_assert(sizeof(FOp) == 112, "FOp layout");
+static_assert(sizeof(FOp) == 128, "FOp layout");
 
 struct FPhase {
   uint8_t reg[kRB];      // tile positions held in registers

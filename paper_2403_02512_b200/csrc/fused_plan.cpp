@@ -88,6 +88,16 @@ void make_phase_thr(FPhase& F, const std::vector<int>& reg, int b, const int* us
   for (int j = 0; j < b - kRB; ++j) F.thr[j] = (uint8_t)thr[j];
 }
 
+// A diagonal table that is 1 on even-parity indices and one constant d on odd ones (IsingZZ
+// after phase folding, Z..Z-string rotations).
+bool parity_table(const Prim& p) {
+  if (p.nb < 1 || p.m.size() != (size_t(1) << p.nb) || p.m[0] != cplx(1.0, 0.0)) return false;
+  const cplx d = p.m[1];
+  for (size_t i = 0; i < p.m.size(); ++i)
+    if (p.m[i] != ((__builtin_popcountll(i) & 1) ? d : cplx(1.0, 0.0))) return false;
+  return true;
+}
+
 // Emit the device ops of one phase.  Unconditional X on a register bit is not executed: it is
 // absorbed into a flip mask F (logical register index j lives in register j ^ F); later ops of
 // the phase are rewritten for F and the phase's store offsets apply it.  Thread-predicated X
@@ -240,6 +250,26 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
         op.v = uint8_t(op.cv ? 1 : 0);
       }
       prog.coef.push_back(make_double2(p.m[0].real(), p.m[0].imag()));
+    } else if (p.type == PRIM_DIAG && op.cm == 0 && parity_table(p)) {
+      // phase d on the odd-parity half of the table bits: register bits form the case mask,
+      // the rest enter through the thread's physical base (xm); uniform flips fix the offset v
+      op.kind = FK_PARITY;
+      int M = 0, v = 0;
+      for (int j = 0; j < p.nb; ++j) {
+        const int k = reg_of_phys(p.pos[j]);
+        if (k >= 0) {
+          M |= 1 << k;
+          v ^= (F >> k) & 1;
+        } else {
+          op.xm |= 1ull << p.pos[j];
+        }
+      }
+      op.v = uint8_t(v);
+      op.cs = CS_PARITY + M;
+      prog.coef.push_back(make_double2(p.m[1].real(), p.m[1].imag()));
+      op.c[0] = prog.coef.back();
+      prog.ops.push_back(op);
+      continue;
     } else if (p.type == PRIM_DIAG) {
       op.kind = FK_DIAGG;
       op.nt = uint8_t(p.nb);
@@ -517,9 +547,13 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
         if ((ph.first >> p) & 1) R.push_back(tile_pos_of[p]);
       fill_regs(R, b);
       int use[kMaxB] = {0};   // predicate tests per tile position in this phase
-      for (int i : ph.second)
+      for (int i : ph.second) {
         for (int p = 0; p < 64; ++p)
           if (((P[i].fmask >> p) & 1) && tile_pos_of[p] >= 0) ++use[tile_pos_of[p]];
+        if (P[i].type == PRIM_DIAG)   // table bits off the registers are per-thread inputs too
+          for (int j = 0; j < P[i].nb; ++j)
+            if (tile_pos_of[P[i].pos[j]] >= 0) ++use[tile_pos_of[P[i].pos[j]]];
+      }
       FPhase F;
       std::memset(&F, 0, sizeof(F));
       make_phase_thr(F, R, b, use);
@@ -649,6 +683,7 @@ void serialize_program(const Program& prog, int nl, std::vector<int64_t>& I, std
   for (const FOp& o : prog.ops) {
     I.push_back(int64_t(o.pm));
     I.push_back(int64_t(o.pv));
+    I.push_back(int64_t(o.xm));
     I.push_back(o.cs);
     I.push_back(o.cm);
     I.push_back(o.cv);

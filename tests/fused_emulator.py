@@ -18,6 +18,7 @@ from paper_2403_02512_b200 import _lib
 CS_PAIR1, CS_PHASE1, CS_SCALAR, CS_PAIRGR, CS_PAIRG = 0, 16, 24, 25, 40
 CS_DIAGG, CS_DENSE2, CS_XFLIP, CS_PAIR1D, CS_PHASE1D = 55, 56, 62, 66, 82
 CS_SHEAR = 90   # + k*4 + {0: RY-type, 1: RX-type, 2: RY-type on a flipped bit}
+CS_PARITY = 106  # + register mask M
 KRB = 4
 KMAXB = 12
 
@@ -68,11 +69,11 @@ def parse(I, D):
         phases.append(dict(reg=reg, flip=flip, thr=thr, op_begin=nxt(), op_end=nxt()))
     ops = []
     for _ in range(nxt()):
-        pm, pv, cs, cm, cv, k, v, xr, nt, mtype = (nxt() for _ in range(10))
+        pm, pv, xm, cs, cm, cv, k, v, xr, nt, mtype = (nxt() for _ in range(11))
         treg = [nxt() for _ in range(6)]
         tphys = [nxt() for _ in range(6)]
         tab, coff = nxt(), nxt()
-        ops.append(dict(pm=pm, pv=pv, cs=cs, cm=cm, cv=cv, k=k, v=v, xr=xr, nt=nt, mtype=mtype, treg=treg,
+        ops.append(dict(pm=pm, pv=pv, xm=xm & 0xFFFFFFFFFFFFFFFF, cs=cs, cm=cm, cv=cv, k=k, v=v, xr=xr, nt=nt, mtype=mtype, treg=treg,
                         tphys=tphys, tab=tab, c=C[coff:coff + 4]))
     coef_off, ncoef = nxt(), nxt()
     coef = C[coef_off:coef_off + ncoef]
@@ -205,6 +206,13 @@ def _apply(a, op, pred, fthr, phys_base, coef):
                 n0, n1 = r0 + 1j * i0, r1 + 1j * i1
             a[..., r] = np.where(pred, n0, x0)
             a[..., r | (1 << k)] = np.where(pred, n1, x1)
+    elif CS_PARITY <= cs < CS_PARITY + 16:
+        M = cs - CS_PARITY
+        popc = np.vectorize(lambda x: bin(int(x)).count("1"))
+        tp = (popc(phys_base & op["xm"]) + popc(fthr & M) + op["v"]) & 1
+        for r in range(16):
+            hit = pred & (((bin(r & M).count("1") & 1) ^ tp) == 1)
+            a[..., r] = np.where(hit, c[0] * a[..., r], a[..., r])
     elif CS_PHASE1 <= cs < CS_PHASE1 + 8 or CS_PHASE1D <= cs < CS_PHASE1D + 8:
         k = op["k"]
         v = op["v"] ^ (((fthr >> k) & 1) if cs >= CS_PHASE1D else 0)

@@ -75,3 +75,22 @@ def test_structured_workloads_program():
     ops, _, _ = workloads.qaoa_maxcut(12, p=2, seed=2)
     check(12, ops)
     check(13, workloads.hardware_efficient_ansatz(13, layers=4, n_trainable=100, seed=4))
+
+
+def test_parity_and_shear_cases_are_exercised():
+    """IsingZZ becomes a parity phase (register mask + per-thread parity), unconditioned
+    rotations become shears -- both re-executed against the oracle."""
+    rng = np.random.default_rng(11)
+    n = 14
+    ops = [Op("H", (q,)) for q in range(n)]
+    for _ in range(60):
+        a, b = rng.choice(n, size=2, replace=False)
+        ops.append(Op("IsingZZ", (int(a), int(b)), (float(rng.uniform(-3, 3)),)))
+        ops.append(Op(("RX", "RY")[int(rng.integers(2))], (int(rng.integers(n)),), (float(rng.uniform(-6, 6)),)))
+        if rng.random() < 0.3:
+            ops.append(Op("CNOT", (int(a), int(b))))
+    prog = check(n, ops)
+    cases = [op["cs"] for op in prog["ops"]]
+    assert any(106 <= c < 122 for c in cases), "IsingZZ should plan to CS_PARITY"
+    assert any(90 <= c < 106 for c in cases), "rotations should plan to CS_SHEAR"
+    assert any(106 <= op["cs"] < 122 and op["xm"] for op in prog["ops"]), "some parity bits off the registers"
