@@ -268,10 +268,10 @@ def main():
                 "traffic": traffic, "kernel": dom, "algorithmic_bytes_per_launch": per_launch,
                 "launches": st["launches"], "share_of_step": st["ms"] / ms if ms else None, "peak_source": peak_src,
                 "frac_of_8000": achieved / 8000.0,
-                "traffic_source": "profiles/traffic.json (ncu dram bytes / algorithmic, 26-qubit capture)"
+                "traffic_source": "profiles/traffic.json (ncu dram bytes / algorithmic, 30-qubit capture)"
                 if traffic else None,
                 "note": "fused_tile does one HBM read+write per pass but many gates per pass; it is bound by "
-                        "its FP64/issue stream (profiles/r1_ncu_fused_pass.md), so frac < 1 while the "
+                        "its FP64/issue stream (profiles/r1_ncu_fused_pass_v14.md), so frac < 1 while the "
                         "circuit's effective GB/s (value) is a multiple of the HBM peak"
                 if dom == "fused_tile" else None}
 
