@@ -128,8 +128,11 @@ static void drain_timings(sv_handle* h) {
 // ---------------------------------------------------------------------------
 // op execution
 // ---------------------------------------------------------------------------
+// Every entry point makes the handle's GPU current for the calling thread, so handles on
+// different GPUs can be driven from worker threads of one process (observable batching).
 static void check_handle(const sv_handle* h) {
   if (!h) sv_fail(SV_ERR_VALIDATION, "null device handle (released?)");
+  if (!h->recording) CUDA_CHECK(cudaSetDevice(h->device));
 }
 
 static void exec_prims(sv_handle* h, const std::vector<double2*>& states, std::vector<Prim>& prims, int fuse) {
@@ -643,6 +646,7 @@ int sv_create_sharded(int n_qubits, int rank, int world, int device, const void*
 
 int sv_destroy(sv_handle* h) {
   API_BEGIN
+  if (h && !h->recording) CUDA_CHECK(cudaSetDevice(h->device));
   destroy_handle(h);
   API_END
 }

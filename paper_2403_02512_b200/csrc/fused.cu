@@ -731,10 +731,12 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
       for (const Prim& p : prog.singles) run_single(st, p);
     return identity;
   }
-  static std::once_flag once;
-  static int dev_sms = 148;
-  static bool db = true;
-  std::call_once(once, [&]() {
+  // kernel attributes are per device: one-time setup for each device this process uses
+  static std::once_flag once_dev[64];
+  static int sms_dev[64];
+  static bool db = false;
+  if (h->device < 0 || h->device >= 64) sv_fail(SV_ERR_DEVICE, "device ordinal out of range");
+  std::call_once(once_dev[h->device], [&]() {
     // the attribute is an upper bound; a launch's real footprint sets its occupancy
     const int tile = int((size_t(1) << kMaxB) * sizeof(double2));
     const int recs = 200 * 1024 - 2 * tile;
@@ -746,14 +748,14 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
     set_smem_attr<false, true, true>(2 * tile + recs);
     set_smem_attr<true, false, true>(tile + recs);
     set_smem_attr<false, false, true>(tile + recs);
-    CUDA_CHECK(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, h->device));
+    CUDA_CHECK(cudaDeviceGetAttribute(&sms_dev[h->device], cudaDevAttrMultiProcessorCount, h->device));
     // default: single buffer, 2 CTAs/SM (measured faster: 16 warps hide the op-loop latency
     // better than 8 warps with a prefetched tile); "db" selects the double-buffered variant
     const char* mode = getenv("SVB200_FUSED_MODE");
     db = mode && std::string(mode) == "db";
   });
   const int b = prog.passes[0].b;
-  const u64 grid = std::min<u64>(prog.passes[0].n_tiles, u64(dev_sms) * (db ? 1 : 2));   // persistent grid
+  const u64 grid = std::min<u64>(prog.passes[0].n_tiles, u64(sms_dev[h->device]) * (db ? 1 : 2));   // persistent grid
 
   // launch records + upload phases | ops | coef in one copy (the buffer is only reused after a sync)
   std::vector<DPhase> dph(prog.phases.size());
