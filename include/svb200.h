@@ -73,6 +73,7 @@ typedef struct sv_op {
 #define SV_OBS_PAULI 0        /* one Pauli word, coefficient 1 */
 #define SV_OBS_HAMILTONIAN 1  /* sum_t coeffs[t] * P_t */
 #define SV_OBS_DENSE 2        /* dense Hermitian on wires */
+#define SV_OBS_SPARSE 3       /* CSR Hermitian on the whole register (single-GPU states) */
 typedef struct sv_obs {
   int32_t type;
   int32_t n_terms;             /* PAULI: 1 */
@@ -83,6 +84,12 @@ typedef struct sv_obs {
   int32_t n_wires;             /* DENSE */
   const int32_t* wires;        /* DENSE */
   const double* matrix;        /* DENSE: interleaved complex 2^w x 2^w */
+  /* SPARSE: CSR over logical basis indices, dim = 2^n_qubits */
+  int64_t csr_dim;
+  int64_t csr_nnz;
+  const int64_t* csr_indptr;   /* dim + 1, monotone, [0] = 0, [dim] = nnz */
+  const int64_t* csr_indices;  /* nnz columns in [0, dim) */
+  const double* csr_data;      /* nnz interleaved complex values */
 } sv_obs;
 
 typedef struct sv_handle sv_handle;

@@ -305,6 +305,13 @@ def apply_pauli_word(amps, n, factors):
 
 def apply_observable(amps, n, obs):
     """Out-of-place O|psi> (the lambda = O psi step of SPEC.md:373)."""
+    if hasattr(obs, "indptr"):   # SparseHermitian: CSR over logical indices (SPEC.md:303-311)
+        amps = np.asarray(amps)
+        out = np.zeros_like(amps)
+        for r in range(len(obs.indptr) - 1):
+            lo, hi = obs.indptr[r], obs.indptr[r + 1]
+            out[r] = np.dot(obs.data[lo:hi], amps[obs.indices[lo:hi]])
+        return out
     if hasattr(obs, "factors"):
         return apply_pauli_word(amps, n, obs.factors)
     if hasattr(obs, "coeffs"):

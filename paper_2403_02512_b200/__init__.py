@@ -8,7 +8,7 @@ it is missing -- there is no CPU fallback.
 
 from .errors import (CapacityError, DeviceError, SvkitError, UnsupportedOperationError,  # noqa: F401
                      ValidationError)
-from .observables import DenseHermitian, Hamiltonian, PauliWord  # noqa: F401
+from .observables import DenseHermitian, Hamiltonian, PauliWord, SparseHermitian  # noqa: F401
 from .ops import GATE_KINDS, Op, gate  # noqa: F401
 
 __version__ = "0.1.0"

@@ -11,7 +11,7 @@ from ctypes import POINTER, c_char, c_char_p, c_double, c_int, c_int32, c_int64,
 import numpy as np
 
 from .errors import raise_for_status
-from .observables import DenseHermitian, Hamiltonian, PauliWord, as_observable
+from .observables import DenseHermitian, Hamiltonian, PauliWord, SparseHermitian, as_observable
 from .ops import KIND_CODE, Op
 
 # SVB200_LIB selects another in-tree build of the same library (A/B kernel experiments)
@@ -42,6 +42,8 @@ class SvObs(ctypes.Structure):
         ("type", c_int32), ("n_terms", c_int32), ("coeffs", POINTER(c_double)),
         ("term_len", POINTER(c_int32)), ("term_wires", POINTER(c_int32)), ("term_paulis", c_char_p),
         ("n_wires", c_int32), ("wires", POINTER(c_int32)), ("matrix", POINTER(c_double)),
+        ("csr_dim", ctypes.c_int64), ("csr_nnz", ctypes.c_int64), ("csr_indptr", POINTER(ctypes.c_int64)),
+        ("csr_indices", POINTER(ctypes.c_int64)), ("csr_data", POINTER(c_double)),
     ]
 
 
@@ -170,6 +172,16 @@ class PackedObs:
         self._keep = []
         for i, o in enumerate(obs):
             rec = self.arr[i]
+            if isinstance(o, SparseHermitian):
+                rec.type = 3
+                ip, ix = o.indptr, o.indices
+                dv = o.data.view(np.float64)
+                rec.csr_dim, rec.csr_nnz = o.dim, len(ix)
+                rec.csr_indptr = ip.ctypes.data_as(POINTER(ctypes.c_int64))
+                rec.csr_indices = ix.ctypes.data_as(POINTER(ctypes.c_int64))
+                rec.csr_data = _dptr(dv)
+                self._keep += [ip, ix, dv]
+                continue
             if isinstance(o, DenseHermitian):
                 rec.type = 2
                 w = np.ascontiguousarray(o.wires, dtype=np.int32)

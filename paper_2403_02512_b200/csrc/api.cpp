@@ -332,7 +332,28 @@ static std::vector<PauliGroup> pauli_groups(sv_handle* h, const sv_obs& o, const
 }
 
 // <psi|O|psi> summed on the host in fixed group order (device partials are deterministic)
+// CSR structure checks (SPEC.md:273 invariants; malformed CSR -> validation error)
+static void validate_csr(const sv_handle* h, const sv_obs& o) {
+  if (o.csr_dim != (int64_t(1) << h->n))
+    sv_fail(SV_ERR_VALIDATION, "CSR dimension " + std::to_string(o.csr_dim) + " != 2^" + std::to_string(h->n));
+  if (!o.csr_indptr || o.csr_nnz < 0 || (o.csr_nnz > 0 && (!o.csr_indices || !o.csr_data)))
+    sv_fail(SV_ERR_VALIDATION, "malformed CSR: missing arrays");
+  if (o.csr_indptr[0] != 0 || o.csr_indptr[o.csr_dim] != o.csr_nnz)
+    sv_fail(SV_ERR_VALIDATION, "malformed CSR: row pointers must start at 0 and end at nnz");
+  for (int64_t r = 0; r < o.csr_dim; ++r)
+    if (o.csr_indptr[r + 1] < o.csr_indptr[r]) sv_fail(SV_ERR_VALIDATION, "malformed CSR: row pointers not monotone");
+  for (int64_t k = 0; k < o.csr_nnz; ++k)
+    if (o.csr_indices[k] < 0 || o.csr_indices[k] >= o.csr_dim)
+      sv_fail(SV_ERR_VALIDATION, "malformed CSR: column index out of range");
+  if (h->world != 1)
+    sv_fail(SV_ERR_UNSUPPORTED, "sparse observables on sharded states are not supported (single-GPU states only)");
+}
+
 static double expval_impl(sv_handle* h, const sv_obs& o) {
+  if (o.type == SV_OBS_SPARSE) {
+    validate_csr(h, o);
+    return csr_apply_or_expval(h, o, h->state, nullptr);
+  }
   if (o.type == SV_OBS_DENSE) {
     if (o.n_wires < 1 || !o.wires || !o.matrix) sv_fail(SV_ERR_VALIDATION, "malformed dense observable");
     sv_op op{};
@@ -377,6 +398,11 @@ static double expval_impl(sv_handle* h, const sv_obs& o) {
 // lam = O psi (out of place), the lambda initialisation of the adjoint sweep
 static void apply_observable(sv_handle* h, const sv_obs& o, const double2* psi, double2* lam,
                              const std::vector<double2*>& all_states) {
+  if (o.type == SV_OBS_SPARSE) {
+    validate_csr(h, o);
+    csr_apply_or_expval(h, o, psi, lam);
+    return;
+  }
   if (o.type == SV_OBS_DENSE) {
     std::vector<int> tw(o.wires, o.wires + o.n_wires);
     dist_make_local_set(h, all_states, tw);

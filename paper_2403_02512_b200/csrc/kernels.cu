@@ -248,6 +248,55 @@ __global__ void __launch_bounds__(kThreads) k_dot_re(const double2* __restrict__
   block_reduce_store<1>(v, partials);
 }
 
+// ---- sparse (CSR) observables ---------------------------------------
+// Row i / column j are LOGICAL basis indices; the state is addressed through the layout
+// permutation (logical bit o -> physical bit phys[o]) as five byte-wise lookup tables.
+struct CsrArgs {
+  const int64_t* indptr;
+  const int64_t* indices;
+  const double2* data;
+  const u64* perm_tab;   // [5][256]: physical bits of logical byte b with value v (nullptr: identity)
+  u64 rows;
+};
+
+__device__ __forceinline__ u64 to_phys(u64 i, const u64* __restrict__ t) {
+  if (!t) return i;
+  return t[i & 255] | t[256 + ((i >> 8) & 255)] | t[512 + ((i >> 16) & 255)] | t[768 + ((i >> 24) & 255)] |
+         t[1024 + ((i >> 32) & 255)];
+}
+
+// one warp per row: acc = sum_k A[i, j_k] psi_j; expval partial += Re(conj(psi_i) acc), or lam_i = acc
+template <bool APPLY>
+__global__ void __launch_bounds__(kThreads) k_csr(const double2* __restrict__ psi, const CsrArgs A,
+                                                  double2* __restrict__ lam, double* __restrict__ partials) {
+  const int lane = threadIdx.x & 31;
+  const u64 warps = u64(gridDim.x) * (kThreads / 32);
+  double v[1] = {0.0};
+  for (u64 row = u64(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5); row < A.rows; row += warps) {
+    double ax = 0.0, ay = 0.0;
+    for (int64_t k = A.indptr[row] + lane; k < A.indptr[row + 1]; k += 32) {
+      const double2 m = A.data[k];
+      const double2 x = psi[to_phys(u64(A.indices[k]), A.perm_tab)];
+      ax = fma(m.x, x.x, fma(-m.y, x.y, ax));
+      ay = fma(m.x, x.y, fma(m.y, x.x, ay));
+    }
+    for (int s = 16; s > 0; s >>= 1) {
+      ax += __shfl_xor_sync(0xffffffffu, ax, s);
+      ay += __shfl_xor_sync(0xffffffffu, ay, s);
+    }
+    if (lane == 0) {
+      const u64 pr = to_phys(row, A.perm_tab);
+      if (APPLY) {
+        lam[pr] = make_double2(ax, ay);
+      } else {
+        const double2 p = psi[pr];
+        v[0] += p.x * ax + p.y * ay;   // Re(conj(p) * acc)
+      }
+    }
+  }
+  if (!APPLY) block_reduce_store<1>(v, partials);
+}
+
 // K10 batched: lam = sum over up to kMaxXG x-groups of sum_t cc_t (-1)^{pc((i^x_g) & z_t)} psi_{i^x_g};
 // psi is read once per group, lam written once (instead of a read-modify-write per group).
 constexpr int kMaxXG = 16;
@@ -694,6 +743,64 @@ void pauli_groups_apply(sv_handle* h, const double2* psi, double2* lam,
     stat_end(h, KC_APPLY_OBS, bytes, ev);
     CUDA_CHECK(cudaGetLastError());
   }
+}
+
+// Sparse observable on a single-GPU state: expval (lam == nullptr) or lam = A psi.  The CSR
+// arrays are staged in device memory for the call (validated by the caller).
+double csr_apply_or_expval(sv_handle* h, const sv_obs& o, const double2* psi, double2* lam) {
+  const u64 rows = u64(o.csr_dim), nnz = u64(o.csr_nnz);
+  bool ident = true;
+  for (int b = 0; b < h->n; ++b) ident &= h->phys[b] == b;
+  std::vector<u64> tab;
+  if (!ident) {
+    tab.assign(5 * 256, 0);
+    for (int byte = 0; byte < 5; ++byte)
+      for (int v = 0; v < 256; ++v)
+        for (int j = 0; j < 8; ++j) {
+          const int o_bit = byte * 8 + j;
+          if (((v >> j) & 1) && o_bit < h->n) tab[byte * 256 + v] |= 1ull << h->phys[o_bit];
+        }
+  }
+  const size_t b_ptr = (rows + 1) * sizeof(int64_t), b_idx = nnz * sizeof(int64_t), b_dat = nnz * sizeof(double2);
+  const size_t b_tab = tab.size() * sizeof(u64);
+  char* buf = nullptr;
+  CUDA_CHECK(cudaMallocAsync(&buf, b_ptr + b_idx + b_dat + b_tab + 64, h->stream));
+  auto al = [](size_t x) { return (x + 15) & ~size_t(15); };
+  CsrArgs A;
+  A.indptr = (const int64_t*)buf;
+  A.indices = (const int64_t*)(buf + al(b_ptr));
+  A.data = (const double2*)(buf + al(b_ptr) + al(b_idx));
+  A.perm_tab = ident ? nullptr : (const u64*)(buf + al(b_ptr) + al(b_idx) + al(b_dat));
+  A.rows = rows;
+  CUDA_CHECK(cudaMemcpyAsync((void*)A.indptr, o.csr_indptr, b_ptr, cudaMemcpyHostToDevice, h->stream));
+  if (nnz) {
+    CUDA_CHECK(cudaMemcpyAsync((void*)A.indices, o.csr_indices, b_idx, cudaMemcpyHostToDevice, h->stream));
+    CUDA_CHECK(cudaMemcpyAsync((void*)A.data, o.csr_data, b_dat, cudaMemcpyHostToDevice, h->stream));
+  }
+  if (!ident) CUDA_CHECK(cudaMemcpyAsync((void*)A.perm_tab, tab.data(), b_tab, cudaMemcpyHostToDevice, h->stream));
+  const unsigned g = red_grid(rows * 32);
+  double out = 0.0;
+  cudaEvent_t ev[2];
+  const double bytes = 16.0 * double(h->n_local) + 24.0 * double(nnz);
+  if (lam) {
+    CUDA_CHECK(cudaMemsetAsync(lam, 0, h->n_local * sizeof(double2), h->stream));
+    stat_begin(h, KC_APPLY_OBS, bytes, ev);
+    k_csr<true><<<g, kThreads, 0, h->stream>>>(psi, A, lam, nullptr);
+    stat_end(h, KC_APPLY_OBS, bytes, ev);
+    CUDA_CHECK(cudaGetLastError());
+  } else {
+    ensure_partials(h, g);
+    ensure_results(h, 1);
+    stat_begin(h, KC_REDUCE, bytes, ev);
+    k_csr<false><<<g, kThreads, 0, h->stream>>>(psi, A, nullptr, h->d_partials);
+    stat_end(h, KC_REDUCE, bytes, ev);
+    CUDA_CHECK(cudaGetLastError());
+    sum_partials(h, h->d_partials, g, 1, h->d_results);
+    CUDA_CHECK(cudaMemcpyAsync(&out, h->d_results, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  }
+  CUDA_CHECK(cudaFreeAsync(buf, h->stream));
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  return out;
 }
 
 double reduce_dot_re(sv_handle* h, const double2* a, const double2* b) {

@@ -169,6 +169,8 @@ void pauli_group_apply(sv_handle* h, const double2* psi, double2* lam, u64 xmask
 void pauli_groups_apply(sv_handle* h, const double2* psi, double2* lam,
                         const std::vector<std::pair<u64, std::vector<PauliTerm>>>& groups);
 double reduce_dot_re(sv_handle* h, const double2* a, const double2* b);   // Re <a|b> (local part)
+// CSR observable on a single-GPU state: <psi|A|psi> (lam == nullptr) or lam = A psi
+double csr_apply_or_expval(sv_handle* h, const sv_obs& o, const double2* psi, double2* lam);
 // <bra| P_f (G) |ket> complex, written to d_out[0..1]
 void braket_prim_async(sv_handle* h, const double2* bra, const double2* ket, const Prim& g, double* d_out);
 void probs_async(sv_handle* h, const double2* state, const std::vector<int>& pos_msb_first, double* d_out);

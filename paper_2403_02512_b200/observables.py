@@ -87,8 +87,58 @@ class DenseHermitian:
         return max(self.wires, default=-1)
 
 
+@dataclass
+class SparseHermitian:
+    """CSR observable over the whole register: row pointers, column indices and
+    complex values over LOGICAL basis indices (qubit 0 = MSB). The structure is validated here
+    (monotone row pointers, in-range columns) and again behind the C-ABI."""
+
+    indptr: np.ndarray = field(repr=False)
+    indices: np.ndarray = field(repr=False)
+    data: np.ndarray = field(repr=False)
+
+    def __post_init__(self):
+        self.indptr = np.ascontiguousarray(self.indptr, dtype=np.int64)
+        self.indices = np.ascontiguousarray(self.indices, dtype=np.int64)
+        self.data = np.ascontiguousarray(self.data, dtype=np.complex128)
+        dim = len(self.indptr) - 1
+        if dim < 1 or self.indptr[0] != 0 or np.any(np.diff(self.indptr) < 0):
+            raise ValidationError("malformed CSR: row pointers must start at 0 and be monotone")
+        if self.indptr[-1] != len(self.indices) or len(self.indices) != len(self.data):
+            raise ValidationError("malformed CSR: nnz mismatch between row pointers, columns and values")
+        if len(self.indices) and (self.indices.min() < 0 or self.indices.max() >= dim):
+            raise ValidationError("malformed CSR: column index out of range")
+
+    @property
+    def dim(self):
+        return len(self.indptr) - 1
+
+    @classmethod
+    def from_dense(cls, matrix):
+        m = np.asarray(matrix, dtype=np.complex128)
+        rows, cols = np.nonzero(m)
+        indptr = np.zeros(m.shape[0] + 1, dtype=np.int64)
+        np.add.at(indptr, rows + 1, 1)
+        return cls(np.cumsum(indptr), cols, m[rows, cols])
+
+    @classmethod
+    def from_scipy(cls, a):
+        a = a.tocsr()
+        return cls(a.indptr, a.indices, a.data)
+
+    def to_dense(self):
+        m = np.zeros((self.dim, self.dim), dtype=np.complex128)
+        for r in range(self.dim):
+            for k in range(self.indptr[r], self.indptr[r + 1]):
+                m[r, self.indices[k]] += self.data[k]
+        return m
+
+    def max_wire(self):
+        return self.dim.bit_length() - 2
+
+
 def as_observable(obs):
-    """Accept a PauliWord/Hamiltonian/DenseHermitian or a ``[(wire, P), ...]`` list."""
-    if isinstance(obs, (PauliWord, Hamiltonian, DenseHermitian)):
+    """Accept a PauliWord/Hamiltonian/DenseHermitian/SparseHermitian or a ``[(wire, P), ...]`` list."""
+    if isinstance(obs, (PauliWord, Hamiltonian, DenseHermitian, SparseHermitian)):
         return obs
     return PauliWord(tuple(obs))

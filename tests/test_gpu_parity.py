@@ -403,3 +403,33 @@ def test_sample_vs_oracle_procedure():
         d.apply([Op("H", (0,))])
         f0 = (d.sample(10_000, seed=42, wires=[0])[:, 0] == 0).mean()
         assert abs(f0 - 0.5) < 0.02
+
+
+def test_sparse_observable_vs_oracle():
+    """SPEC.md:303-311 through the C-ABI: expval, variance and the adjoint Jacobian with a CSR
+    observable, on a state whose layout was relabeled by fused passes; structure errors."""
+    from paper_2403_02512_b200.observables import SparseHermitian
+    rng = np.random.default_rng(17)
+    n = 10
+    dim = 1 << n
+    m = np.zeros((dim, dim), dtype=np.complex128)
+    mask = rng.random((dim, dim)) < 0.01
+    m[mask] = rng.normal(size=mask.sum()) + 1j * rng.normal(size=mask.sum())
+    m = m + m.conj().T
+    sp = SparseHermitian.from_dense(m)
+    ops = workloads.hardware_efficient_ansatz(n, layers=3, n_trainable=40, seed=3)
+    psi = O.run_circuit(n, ops)
+    scale = float(np.abs(m).sum(axis=1).max())
+    with Device(n) as d:
+        d.apply(ops)
+        assert abs(d.expval(sp) - np.vdot(psi, m @ psi).real) <= 1e-10 * scale
+        assert abs(d.var(sp) - O.variance(psi, n, sp)) <= 1e-10 * scale ** 2
+        for fuse in (True, False):
+            d.reset()
+            jac, ev = d.adjoint_jacobian(ops, [sp], return_expvals=True, fuse=fuse)
+            jref, evref = O.adjoint_jacobian(n, ops, [sp])
+            assert np.abs(jac - jref).max() <= 1e-10 * scale, fuse
+            assert abs(ev[0] - evref[0]) <= 1e-10 * scale
+        d.reset()
+        with pytest.raises(errors.ValidationError):
+            d.expval(SparseHermitian.from_dense(np.eye(8)))      # dimension != 2^n

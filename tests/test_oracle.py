@@ -267,3 +267,35 @@ def test_kat_sample():
     # marginal over wires (2, 0): same procedure on the marginal vector
     m = O.sample(psi, n, 1000, seed=9, wires=[2, 0])
     assert m.min() >= 0 and m.max() < 4
+
+
+def rand_sparse_herm(rng, n, density=0.08):
+    dim = 1 << n
+    m = np.zeros((dim, dim), dtype=np.complex128)
+    mask = rng.random((dim, dim)) < density
+    m[mask] = rng.normal(size=mask.sum()) + 1j * rng.normal(size=mask.sum())
+    return m + m.conj().T
+
+
+def test_kat_sparse_expval():
+    """CSR identity -> 1; CSR of Z on |1> -> -1; random sparse Hermitian (n=6)
+    vs the dense contraction; malformed CSR -> validation error."""
+    from paper_2403_02512_b200.errors import ValidationError
+    from paper_2403_02512_b200.observables import SparseHermitian
+    rng = np.random.default_rng(4)
+    psi = rng.normal(size=8) + 1j * rng.normal(size=8)
+    psi /= np.linalg.norm(psi)
+    assert abs(O.expval(psi, 3, SparseHermitian.from_dense(np.eye(8))) - 1.0) < 1e-14
+    one = np.array([0, 1], dtype=np.complex128)
+    assert abs(O.expval(one, 1, SparseHermitian.from_dense(np.diag([1.0, -1.0]))) + 1.0) < 1e-15
+    n = 6
+    m = rand_sparse_herm(rng, n)
+    psi = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    psi /= np.linalg.norm(psi)
+    sp = SparseHermitian.from_dense(m)
+    assert np.allclose(sp.to_dense(), m)
+    assert abs(O.expval(psi, n, sp) - np.vdot(psi, m @ psi).real) < 1e-10
+    with pytest.raises(ValidationError):
+        SparseHermitian([0, 2, 1], [0, 1], [1.0, 1.0])          # non-monotone row pointers
+    with pytest.raises(ValidationError):
+        SparseHermitian([0, 1, 2], [0, 5], [1.0, 1.0])          # column out of range
