@@ -103,7 +103,8 @@ class Device:
 
     # ---- gates -------------------------------------------------------------------------
     def apply(self, ops, fuse=None):
-        """Apply an op list in order (Device.apply)."""
+        """Apply an op list (or a circuit_ir.Circuit) in order (Device.apply)."""
+        ops = getattr(ops, "ops", ops)
         ops = [o if isinstance(o, Op) else Op(*o) for o in ops]
         packed = _lib.PackedOps(ops)
         f = self.fuse if fuse is None else fuse
@@ -169,7 +170,7 @@ class Device:
         Starts from the handle's current state; on return the handle holds the state swept back
         to the input (fp64 round-off).
         """
-        ops = [o if isinstance(o, Op) else Op(*o) for o in ops]
+        ops = [o if isinstance(o, Op) else Op(*o) for o in getattr(ops, "ops", ops)]
         obs = [as_observable(o) for o in observables]
         ncols = sum(op.n_trainable for op in ops)
         po, pb = _lib.PackedOps(ops), _lib.PackedObs(obs)

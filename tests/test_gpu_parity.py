@@ -433,3 +433,21 @@ def test_sparse_observable_vs_oracle():
         d.reset()
         with pytest.raises(errors.ValidationError):
             d.expval(SparseHermitian.from_dense(np.eye(8)))      # dimension != 2^n
+
+
+def test_h2_vqe_energy_and_gradient():
+    """circuit-ir end to end on the device: the H2 fixture + singles/doubles ansatz (the
+    DoubleExcitation generator takes the per-gate adjoint path), batched and unbatched."""
+    import os
+    from paper_2403_02512_b200 import circuit_ir as C
+    from paper_2403_02512_b200.batching import batched_expval_and_grad
+    h2 = C.parse_hamiltonian(open(os.path.join(os.path.dirname(__file__), "fixtures", "h2.ham")).read())
+    theta = np.array([0.01, -0.02, 0.21])
+    c = C.singles_doubles_ansatz(4, 2, theta)
+    jref, evref = O.adjoint_jacobian(4, c.ops, [h2])
+    with Device(4) as d:
+        jac, ev = d.adjoint_jacobian(c, [h2], return_expvals=True)
+    assert abs(ev[0] - evref[0]) < 1e-12 and np.abs(jac - jref).max() < 1e-12
+    e, g = batched_expval_and_grad(c.ops, h2, n_workers=3, n_qubits=4)
+    assert abs(e - evref[0]) < 1e-12 and np.abs(g - jref[0]).max() < 1e-12
+    assert abs(e - (-1.1361894540)) < 2e-3
