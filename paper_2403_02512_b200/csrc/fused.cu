@@ -309,15 +309,16 @@ __device__ __forceinline__ void gen_diag(const double2 (&a)[kRegs], const FOp& o
 // One generator bra-ket, reduced over the warp into this warp's shared accumulator.  Every lane
 // must call it (uniform op; predicate-false lanes contribute zero).
 template <bool FULL>
-__device__ __forceinline__ void gen_op(const double2 (&a)[kRegs], const FOp& op, bool pred, int fthr, u64 phys_base,
-                                       const double2* __restrict__ coef, double2* __restrict__ acc_warp) {
+__device__ __forceinline__ void gen_op(const double2 (&a)[kRegs], const int cs, const FOp& op, bool pred, int fthr,
+                                       u64 phys_base, const double2* __restrict__ coef,
+                                       double2* __restrict__ acc_warp) {
   double re = 0.0, im = 0.0;
   if (pred) {
     const int cv = op.cv ^ (fthr & op.cm);
     const int k0 = op.xr & 15, k1 = op.xr >> 4;
     const int f = ((fthr >> k0) & 1) | (((fthr >> k1) & 1) << 1);
     const double2* M = coef + op.tab;
-    switch (op.cs) {
+    switch (cs) {
       GEN1_CASE(0, 1) GEN1_CASE(0, 2) GEN1_CASE(0, 3) GEN1_CASE(1, 0) GEN1_CASE(1, 2) GEN1_CASE(1, 3)
       GEN1_CASE(2, 0) GEN1_CASE(2, 1) GEN1_CASE(2, 3) GEN1_CASE(3, 0) GEN1_CASE(3, 1) GEN1_CASE(3, 2)
       GEN2_CASES(0, 0, 1, 2, 3) GEN2_CASES(1, 0, 2, 1, 3) GEN2_CASES(2, 0, 3, 1, 2)
@@ -524,7 +525,10 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
       }
       for (; oi < oe; ++oi) {
         const FOp& op = s_ops[oi];
-        const int cs = cs_n;
+        const int cs = cs_n & 0xFFFF;
+        if (cs_n >> 16) {   // attached thread-predicated X (host: FOp.fk)
+          if ((phys_base & op.fpm) == op.fpv) fthr ^= cs_n >> 16;
+        }
         const bool pred = (phys_base & pm_n) == pv_n;
         if (oi + 1 < oe) {
           cs_n = s_ops[oi + 1].cs;
@@ -532,7 +536,7 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
           pv_n = s_ops[oi + 1].pv;
         }
         if (cs >= CS_GEN1)
-          gen_op<FULL>(a, op, pred, fthr, phys_base, coef, s_gen + (tid >> 5) * kMaxGens);
+          gen_op<FULL>(a, cs, op, pred, fthr, phys_base, coef, s_gen + (tid >> 5) * kMaxGens);
         else if (pred)
           apply_op<FULL>(a, cs, op, coef, phys_base, fthr);
       }
@@ -769,6 +773,10 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
   std::vector<char> host(total);
   std::memcpy(host.data(), dph.data(), b_ph);
   std::memcpy(host.data() + align(b_ph), prog.ops.data(), b_op);
+  {
+    FOp* dev_ops = reinterpret_cast<FOp*>(host.data() + align(b_ph));
+    for (size_t i = 0; i < prog.ops.size(); ++i) dev_ops[i].cs |= dev_ops[i].fk << 16;   // one prefetched word
+  }
   std::memcpy(host.data() + align(b_ph) + align(b_op), prog.coef.data(), b_cf);
   CUDA_CHECK(cudaStreamSynchronize(h->stream));   // previous program may still be in use
   char* dbuf = (char*)program_buffer(h, total);

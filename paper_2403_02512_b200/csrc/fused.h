@@ -28,6 +28,7 @@ enum MType : uint8_t { MT_GENERAL = 0, MT_REAL = 1, MT_RXLIKE = 2, MT_X = 3 };
 struct __align__(16) FOp {
   u64 pm, pv;            // fixed pattern on non-register bits (tested on the thread's physical base)
   u64 xm;                // PARITY: non-register bits whose parity (on the physical base) enters the phase
+  u64 fpm, fpv;          // attached thread-predicated X (applied before the op): pattern ...
   uint8_t kind, mtype;
   uint8_t xr;            // PAIRG: register-space xmask; DENSE2: k0 | (k1 << 4)
   uint8_t cm, cv;        // register-space pattern (PAIRG includes i0's pattern on xr)
@@ -38,7 +39,7 @@ struct __align__(16) FOp {
   int tab;               // offset into the coefficient array (DIAGG / DENSE2)
   int cs;                // dense dispatch case (CS_* below)
   int slot;              // GEN: accumulator slot within the pass
-  int pad_;
+  int fk;                // ... and register-flip mask (0: none).  The device copy carries fk in cs >> 16
   double2 c[4];          // inline coefficients (PAIR1 / PAIRG: m00 m01 m10 m11; PHASE1 / SCALAR: d)
 };
 // Dense dispatch cases.  No case moves amplitudes between registers (data-moving swaps
@@ -67,7 +68,7 @@ constexpr int CS_GEN1 = 122;     // + k*4 + t: 2x2 generator on register bit k  
 constexpr int CS_GEN2 = 138;     // + pair*4 + t: 4x4 generator on register bits pair (138..161)
 constexpr int CS_GEND = 162;     // + t: diagonal generator (table on any bits; only t in registers) (162..165)
 constexpr int kMaxGens = 64;     // generator slots per pass (per-warp shared-memory accumulators)
-static_assert(sizeof(FOp) == 128, "FOp layout");
+static_assert(sizeof(FOp) == 144, "FOp layout");
 
 struct FPhase {
   uint8_t reg[kRB];      // tile positions held in registers

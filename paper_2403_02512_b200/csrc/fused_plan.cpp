@@ -116,6 +116,24 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
   int D = 0;   // register bits that may carry a per-thread flip (handled by the kernel)
   static const bool shear_on = !(getenv("SVB200_SHEAR") && std::string(getenv("SVB200_SHEAR")) == "0");
   const int op_first = int(prog.ops.size());
+  // A thread-predicated X is not an op of its own: it rides on the next op of the phase (the
+  // kernel toggles the flip before that op), saving one dispatch; only a second X arriving
+  // before that op, or one left at the end of the phase, is emitted standalone (CS_XFLIP).
+  bool pend = false;
+  FOp pend_op;
+  auto push_op = [&](FOp& o) {
+    if (pend && o.cs >= CS_XFLIP && o.cs < CS_XFLIP + 4) {
+      prog.ops.push_back(pend_op);   // two flips in a row: the first stands alone
+      pend = false;
+    }
+    if (pend) {
+      o.fpm = pend_op.pm;
+      o.fpv = pend_op.pv;
+      o.fk = 1 << pend_op.k;
+      pend = false;
+    }
+    prog.ops.push_back(o);
+  };
   int neg = 0;   // unconditioned rotations emitted as -R(phi'): the phase owes the state a factor (-1)^neg
   for (int i : list) {
     const Prim& p = prims[i];
@@ -159,7 +177,7 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
       }
       op.v = uint8_t(t);
       op.cs = CS_GEND + t;
-      prog.ops.push_back(op);
+      push_op(op);
       continue;
     }
     if (p.type == PRIM_GEN) {
@@ -207,7 +225,7 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
             prog.coef.push_back(make_double2(v.real(), v.imag()));
           }
       }
-      prog.ops.push_back(op);
+      push_op(op);
       continue;
     }
     if (p.type == PRIM_PAIR) {
@@ -224,7 +242,9 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
         op.k = uint8_t(__builtin_ctz(op.xr));
         op.cs = CS_XFLIP + op.k;
         D |= op.xr;
-        prog.ops.push_back(op);
+        if (pend) prog.ops.push_back(pend_op);
+        pend_op = op;
+        pend = true;
         continue;
       }
       std::vector<cplx> m = p.m;
@@ -268,7 +288,7 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
       op.cs = CS_PARITY + M;
       prog.coef.push_back(make_double2(p.m[1].real(), p.m[1].imag()));
       op.c[0] = prog.coef.back();
-      prog.ops.push_back(op);
+      push_op(op);
       continue;
     } else if (p.type == PRIM_DIAG) {
       op.kind = FK_DIAGG;
@@ -323,7 +343,7 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
         op.c[0] = make_double2(-sn / (1.0 + c), sn);
         op.c[1] = make_double2(c, 0.0);   // (c, s) kept for a later conversion back to the 2x2 form
         op.c[2] = make_double2(sn, rx ? 1.0 : 0.0);
-        prog.ops.push_back(op);
+        push_op(op);
         continue;
       }
     }
@@ -342,8 +362,9 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
       const int nc = (op.kind == FK_PAIR1 || op.kind == FK_PAIRG) ? 4 : 1;
       for (int j = 0; j < nc; ++j) op.c[j] = prog.coef[op.tab + j];
     }
-    prog.ops.push_back(op);
+    push_op(op);
   }
+  if (pend) prog.ops.push_back(pend_op);
   if (neg) {
     // absorb the owed -1 into an unconditioned 2x2 / scalar op of the phase, else turn one
     // unconditioned shear back into its 2x2 form carrying the sign
@@ -684,6 +705,9 @@ void serialize_program(const Program& prog, int nl, std::vector<int64_t>& I, std
     I.push_back(int64_t(o.pm));
     I.push_back(int64_t(o.pv));
     I.push_back(int64_t(o.xm));
+    I.push_back(int64_t(o.fpm));
+    I.push_back(int64_t(o.fpv));
+    I.push_back(o.fk);
     I.push_back(o.cs);
     I.push_back(o.cm);
     I.push_back(o.cv);

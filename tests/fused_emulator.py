@@ -69,11 +69,11 @@ def parse(I, D):
         phases.append(dict(reg=reg, flip=flip, thr=thr, op_begin=nxt(), op_end=nxt()))
     ops = []
     for _ in range(nxt()):
-        pm, pv, xm, cs, cm, cv, k, v, xr, nt, mtype = (nxt() for _ in range(11))
+        pm, pv, xm, fpm, fpv, fk, cs, cm, cv, k, v, xr, nt, mtype = (nxt() for _ in range(14))
         treg = [nxt() for _ in range(6)]
         tphys = [nxt() for _ in range(6)]
         tab, coff = nxt(), nxt()
-        ops.append(dict(pm=pm, pv=pv, xm=xm & 0xFFFFFFFFFFFFFFFF, cs=cs, cm=cm, cv=cv, k=k, v=v, xr=xr, nt=nt, mtype=mtype, treg=treg,
+        ops.append(dict(pm=pm, pv=pv, xm=xm & 0xFFFFFFFFFFFFFFFF, fpm=fpm, fpv=fpv, fk=fk, cs=cs, cm=cm, cv=cv, k=k, v=v, xr=xr, nt=nt, mtype=mtype, treg=treg,
                         tphys=tphys, tab=tab, c=C[coff:coff + 4]))
     coef_off, ncoef = nxt(), nxt()
     coef = C[coef_off:coef_off + ncoef]
@@ -141,6 +141,8 @@ def _run_pass(state, P, prog, nl):
         a = tile[:, sthr[:, None] | regoff[None, :]]                     # (n_tiles, nthreads, 16)
         fthr = np.zeros(phys_base.shape, dtype=np.int64)
         for op in prog["ops"][ph["op_begin"]:ph["op_end"]]:
+            if op["fk"]:   # attached thread-predicated X: toggle the flip before the op
+                fthr ^= np.where((phys_base & op["fpm"]) == op["fpv"], op["fk"], 0)
             pred = (phys_base & op["pm"]) == op["pv"]
             _apply(a, op, pred, fthr, phys_base, prog["coef"])
         fl = ph["flip"] ^ fthr                                           # per thread
