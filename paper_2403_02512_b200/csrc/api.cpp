@@ -525,23 +525,27 @@ static bool adjoint_fused(sv_handle* h, const sv_op* ops, int n_ops, const sv_ob
     for (auto& pc : lower_op(ops[i], h->n, c, true, nullptr))
       if (pc.has_gen && pc.gen.g.nb > 2) return false;
   }
+  // lambda (+ the saved final psi for several observables) are allocated once per handle and
+  // kept (the SPEC's "preallocation of all required memory"), so repeated Jacobians do not pay
+  // for mapping tens of GiB each call
+  const size_t half = h->n_local * sizeof(double2);
+  const int need = n_obs > 1 ? 2 : 1;
   size_t free_b = 0, total_b = 0;
   CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-  const size_t half = h->n_local * sizeof(double2);
-  double lacking = ((n_obs > 1 ? 2 : 1) * half + (64ull << 20) > free_b) ? 1.0 : 0.0;   // lambda (+ saved psi)
+  const int have = (h->adj_lam ? 1 : 0) + (h->adj_saved ? 1 : 0);
+  double lacking = (size_t(std::max(0, need - have)) * half + (64ull << 20) > free_b) ? 1.0 : 0.0;
   dist_allreduce_sum(h, &lacking, 1);   // every rank must take the same path (collectives inside)
   if (lacking > 0) return false;
+  if (!h->adj_lam) CUDA_CHECK(cudaMalloc(&h->adj_lam, half));
+  if (need > 1 && !h->adj_saved) CUDA_CHECK(cudaMalloc(&h->adj_saved, half));
 
   run_ops(h, {h->state}, ops, n_ops, 1);                       // forward pass (once)
   std::vector<double> ev(n_obs);
-  double2 *buf = nullptr, *saved = nullptr;   // buf = lambda
-  CUDA_CHECK(cudaMalloc(&buf, half));
-  try {
+  double2* buf = h->adj_lam;   // lambda
+  double2* saved = h->adj_saved;
+  {
     const std::vector<int> phys_final = h->phys;
-    if (n_obs > 1) {
-      CUDA_CHECK(cudaMalloc(&saved, half));
-      launch_copy(h, saved, h->state, h->n_local);
-    }
+    if (n_obs > 1) launch_copy(h, saved, h->state, h->n_local);
     for (int k = 0; k < n_obs; ++k) {
       if (k > 0) {                                             // restart from the final state
         launch_copy(h, h->state, saved, h->n_local);
@@ -551,13 +555,7 @@ static bool adjoint_fused(sv_handle* h, const sv_op* ops, int n_ops, const sv_ob
     }
     if (expvals)
       for (int k = 0; k < n_obs; ++k) expvals[k] = ev[k];
-  } catch (...) {
-    cudaFree(buf);
-    if (saved) cudaFree(saved);
-    throw;
   }
-  CUDA_CHECK(cudaFree(buf));
-  if (saved) CUDA_CHECK(cudaFree(saved));
   return true;
 }
 
@@ -604,10 +602,17 @@ static void create_common(sv_handle* h, int n_qubits, int device) {
   CUDA_CHECK(cudaStreamSynchronize(h->stream));
 }
 
+static void release_adjoint_buffers(sv_handle* h) {
+  if (h->adj_lam) cudaFree(h->adj_lam);
+  if (h->adj_saved) cudaFree(h->adj_saved);
+  h->adj_lam = h->adj_saved = nullptr;
+}
+
 static void destroy_handle(sv_handle* h) {
   if (!h) return;
   if (h->stream) cudaStreamSynchronize(h->stream);
   free_aux(h);
+  release_adjoint_buffers(h);
   release_scratch(h);
   release_fused(h);
   dist_destroy(h);
@@ -842,6 +847,7 @@ int sv_var(sv_handle* h, const sv_obs* obs, double* out) {
     const double e = expval_impl(h, *obs);
     *out = 1.0 - e * e;
   } else {
+    release_adjoint_buffers(h);
     size_t free_b = 0, total_b = 0;
     CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
     const size_t bytes = h->n_local * sizeof(double2);
@@ -937,7 +943,8 @@ int sv_adjoint_jacobian(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs*
   int ncols = 0;
   for (int i = 0; i < n_ops; ++i) lower_op(ops[i], h->n, ncols, true, nullptr);
   if (fuse && adjoint_fused(h, ops, n_ops, obs, n_obs, ncols, jac, expvals)) return SV_OK;
-  // capacity: one lambda per observable
+  // capacity: one lambda per observable; the fused path's kept buffers go first
+  release_adjoint_buffers(h);
   size_t free_b = 0, total_b = 0;
   CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
   const double need = double(n_obs) * double(h->n_local) * sizeof(double2);

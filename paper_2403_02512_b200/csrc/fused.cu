@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
 
@@ -659,6 +660,54 @@ struct DevProgram {
 std::mutex g_prog_mu;
 std::vector<std::pair<sv_handle*, DevProgram>> g_progs;
 
+// Plan cache: the same primitive list on the same layout plans to the same program (repeated
+// circuits, and every observable row of a multi-observable adjoint sweep), so the host planner
+// runs once.  A few entries per handle, exact comparison of the inputs.
+struct PlanKey {
+  int nl;
+  bool remap, pin;
+  std::vector<Prim> prims;
+};
+bool same_prim(const Prim& a, const Prim& b) {
+  if (a.type != b.type || a.fmask != b.fmask || a.fval != b.fval || a.xmask != b.xmask || a.nb != b.nb ||
+      a.skip != b.skip || a.slot != b.slot || a.m != b.m)
+    return false;
+  for (int j = 0; j < a.nb; ++j)
+    if (a.pos[j] != b.pos[j]) return false;
+  return true;
+}
+std::mutex g_plan_mu;
+std::vector<std::pair<sv_handle*, std::vector<std::pair<PlanKey, std::shared_ptr<Program>>>>> g_plans;
+
+std::shared_ptr<Program> cached_program(sv_handle* h, const std::vector<Prim>& prims, bool remap, bool pin) {
+  static const bool off = getenv("SVB200_PLAN_CACHE") && std::string(getenv("SVB200_PLAN_CACHE")) == "0";
+  if (off) return std::make_shared<Program>(build_program(h->nl, prims, remap, pin));
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  std::vector<std::pair<PlanKey, std::shared_ptr<Program>>>* lst = nullptr;
+  for (auto& e : g_plans)
+    if (e.first == h) lst = &e.second;
+  if (!lst) {
+    g_plans.push_back({h, {}});
+    lst = &g_plans.back().second;
+  }
+  for (size_t i = 0; i < lst->size(); ++i) {
+    const PlanKey& k = (*lst)[i].first;
+    if (k.nl != h->nl || k.remap != remap || k.pin != pin || k.prims.size() != prims.size()) continue;
+    bool eq = true;
+    for (size_t j = 0; j < prims.size() && eq; ++j) eq = same_prim(k.prims[j], prims[j]);
+    if (eq) {
+      auto hit = (*lst)[i];
+      lst->erase(lst->begin() + i);
+      lst->insert(lst->begin(), hit);   // most recent first
+      return hit.second;
+    }
+  }
+  auto prog = std::make_shared<Program>(build_program(h->nl, prims, remap, pin));
+  lst->insert(lst->begin(), {PlanKey{h->nl, remap, pin, prims}, prog});
+  if (lst->size() > 4) lst->pop_back();
+  return prog;
+}
+
 void* program_buffer(sv_handle* h, size_t bytes) {
   std::lock_guard<std::mutex> lk(g_prog_mu);
   for (auto& e : g_progs)
@@ -694,6 +743,14 @@ void launch_fused(unsigned grid, int threads, size_t smem, cudaStream_t st, doub
 
 void release_fused(sv_handle* h) {
   using namespace fused;
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    for (size_t i = 0; i < g_plans.size(); ++i)
+      if (g_plans[i].first == h) {
+        g_plans.erase(g_plans.begin() + i);
+        break;
+      }
+  }
   std::lock_guard<std::mutex> lk(g_prog_mu);
   for (size_t i = 0; i < g_progs.size(); ++i)
     if (g_progs[i].first == h) {
@@ -727,7 +784,8 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
     return identity;
   }
   static const bool remap = !(getenv("SVB200_REMAP") && std::string(getenv("SVB200_REMAP")) == "0");
-  Program prog = build_program(h->nl, prims, remap, state_hi != nullptr);
+  const std::shared_ptr<Program> prog_ptr = cached_program(h, prims, remap, state_hi != nullptr);
+  Program& prog = *prog_ptr;
   if (state_hi)
     for (auto& A : prog.passes) A.hi_mask = 1ull << (h->nl - 1);
   if (prog.passes.empty()) {

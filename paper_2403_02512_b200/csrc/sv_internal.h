@@ -120,6 +120,8 @@ struct sv_handle {
   double* h_pinned = nullptr;
   size_t h_pinned_cap = 0;
   std::vector<double2*> aux;    // lambda states for the adjoint sweep
+  double2* adj_lam = nullptr;   // fused adjoint: lambda, kept across calls
+  double2* adj_saved = nullptr; // fused adjoint: saved final psi (several observables)
   std::mutex mu;
   bool recording = false;       // host-only planning handle (no device memory)
   std::vector<RecStep> rec;
