@@ -230,7 +230,10 @@ def main():
         if pg:
             pg.barrier()
 
+    # one step = |0...0> + the whole circuit (reset also restores the canonical qubit layout, so
+    # every step runs the same planned program: fused passes relabel qubits inside their tiles)
     for _ in range(args.warmup):
+        dev.reset()
         dev.apply(ops)
     barrier()
     dev.reset_stats()
@@ -242,6 +245,7 @@ def main():
     barrier()
     e0.record(stream)
     for _ in range(args.steps):
+        dev.reset()
         dev.apply(ops)
     e1.record(stream)
     e1.synchronize()

@@ -159,6 +159,12 @@ int sv_plan_summary(int n_qubits, const sv_op* ops, int n_ops, int64_t* out4);
  * sizes2 receives the needed int64 / double counts; buffers are filled when large enough. */
 int sv_plan_program(int n_qubits, const sv_op* ops, int n_ops, int64_t* ints, int64_t ints_cap, double* dbls,
                     int64_t dbls_cap, int64_t* sizes2);
+/* Runtime pass compiler (host-only, no GPU needed): plan the op list and compile every fused pass
+ * into its own sm_100a kernel with NVRTC (the kernels the device path launches; cached
+ * process-wide by pass structure).  two_array = plan for the adjoint sweep's psi|lambda state.
+ * out[0]=passes, out[1]=passes with a generated kernel, out[2]=kernels compiled so far in this
+ * process, out[3]=their total compile time in microseconds. */
+int sv_plan_compile(int n_qubits, const sv_op* ops, int n_ops, int two_array, int64_t* out4);
 /* The sharded driver's decisions for one rank (local primitives, global-qubit swaps, final
  * canonicalisation), recorded without a GPU; same sizing convention. */
 int sv_plan_sharded(int n_qubits, int rank, int world, const sv_op* ops, int n_ops, int64_t* ints, int64_t ints_cap,

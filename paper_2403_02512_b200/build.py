@@ -36,6 +36,22 @@ def nvcc():
     raise RuntimeError("nvcc not found")
 
 
+def cuda_home():
+    return os.path.dirname(os.path.dirname(os.path.realpath(nvcc())))
+
+
+def gen_dev_inc():
+    """fused_dev.cuh as a C++ raw string: the device helpers the runtime pass compiler (fused_jit.cpp,
+    NVRTC) prepends to every generated pass kernel -- the same source the prebuilt kernel includes."""
+    with open(os.path.join(CSRC, "fused_dev.cuh")) as f:
+        body = f.read()
+    text = 'R"SVB200DEV(' + body + ')SVB200DEV"\n'
+    out = os.path.join(BUILD, "fused_dev_src.inc")
+    if not os.path.exists(out) or open(out).read() != text:
+        with open(out, "w") as f:
+            f.write(text)
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
@@ -44,7 +60,7 @@ def needs_build():
     if not os.path.exists(OUT):
         return True
     t = os.path.getmtime(OUT)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + [os.path.join(HERE, "..", "include", "svb200.h")]
+    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + [os.path.join(HERE, "..", "include", "svb200.h")]
     return any(os.path.getmtime(s) > t for s in deps)
 
 
@@ -54,7 +70,10 @@ def build(force=False, verbose=False):
     inc, lib = nccl_dirs()
     os.makedirs(BUILD, exist_ok=True)
     objs = []
-    common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", inc, "-I", os.path.join(HERE, "..", "include")]
+    common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", inc, "-I", os.path.join(HERE, "..", "include"),
+              "-I", BUILD]
+    gen_dev_inc()
+    cmds = []
     for src in sources():
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         cmd = [nvcc(), *ARCH, "-lineinfo", *common, "-c", src, "-o", obj]
@@ -62,17 +81,23 @@ def build(force=False, verbose=False):
             cmd += ["-Xptxas", "-v"] if verbose else []
             cmd += ["--expt-relaxed-constexpr"]
         else:
-            cmd = [nvcc(), *common, "-x", "c++", "-c", src, "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+            cmd = [nvcc(), *common, "-I", os.path.join(cuda_home(), "include"), "-x", "c++", "-c", src, "-o", obj]
+        cmds.append((src, cmd))
+        objs.append(obj)
+    # compile the translation units in parallel (fused.cu alone takes ~2 min)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+        results = list(ex.map(lambda sc: (sc[0], subprocess.run(sc[1], capture_output=True, text=True)), cmds))
+    for src, r in results:
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose and r.stderr:
             sys.stderr.write(r.stderr)
-        objs.append(obj)
     tmp = OUT + ".tmp"
     link = [nvcc(), *ARCH, "-shared", "-o", tmp, *objs, "-L", lib, "-l:libnccl.so.2",
-            "-Xlinker", "-rpath", "-Xlinker", lib, "-cudart", "static"]
+            "-Xlinker", "-rpath", "-Xlinker", lib, "-cudart", "static",
+            "-L", os.path.join(cuda_home(), "lib64"), "-lnvrtc", "-Xlinker", "-rpath", "-Xlinker", os.path.join(cuda_home(), "lib64")]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)

@@ -1048,6 +1048,13 @@ int sv_plan_summary(int n_qubits, const sv_op* ops, int n_ops, int64_t* out4) {
   API_END
 }
 
+int sv_plan_compile(int n_qubits, const sv_op* ops, int n_ops, int two_array, int64_t* out4) {
+  API_BEGIN
+  if (n_qubits < 5 || n_qubits > 62) sv_fail(SV_ERR_VALIDATION, "bad qubit count");
+  plan_compile(n_qubits, host_prims(n_qubits, ops, n_ops), two_array != 0, out4);
+  API_END
+}
+
 // Host-only: run the sharded driver for `rank` of `world` in recording mode (no device memory,
 // no NCCL) and return what it would execute -- local primitives and global-qubit swaps -- plus
 // the canonicalising swaps at the end.  tests/test_sharded_cpu.py replays it on gloo ranks.

@@ -26,136 +26,26 @@
 #include <string>
 
 #include "fused.h"
+#include "fused_dev.cuh"
 
 namespace fused {
 namespace {
 
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
-__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
-  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
-}
-
-// XOR swizzle of a tile index: linear over GF(2), so swz(a ^ b) == swz(a) ^ swz(b)
-__device__ __forceinline__ int swz(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
-
-// In-place 2x2 update of (x0, x1): products needing OLD values first, then overwriting FMAs.
-template <int MT>
-__device__ __forceinline__ void pair_upd(double2& x0, double2& x1, const double2 m0, const double2 m1, const double2 m2,
-                                         const double2 m3) {
-  if (MT == MT_REAL) {
-    const double px = m1.x * x1.x, py = m1.x * x1.y, qx = m2.x * x0.x, qy = m2.x * x0.y;
-    x0.x = fma(m0.x, x0.x, px);
-    x0.y = fma(m0.x, x0.y, py);
-    x1.x = fma(m3.x, x1.x, qx);
-    x1.y = fma(m3.x, x1.y, qy);
-  } else if (MT == MT_RXLIKE) {   // m0, m3 real; m1, m2 imaginary: (i b)(x + i y) = -b y + i b x
-    const double px = -m1.y * x1.y, py = m1.y * x1.x, qx = -m2.y * x0.y, qy = m2.y * x0.x;
-    x0.x = fma(m0.x, x0.x, px);
-    x0.y = fma(m0.x, x0.y, py);
-    x1.x = fma(m3.x, x1.x, qx);
-    x1.y = fma(m3.x, x1.y, qy);
-  } else {
-    const double2 p = cmul(m1, x1), q = cmul(m2, x0);
-    x0 = cfma(m0, x0, p);
-    x1 = cfma(m3, x1, q);
-  }
-}
-
-// a *= d in place (cross products first)
-__device__ __forceinline__ void cmul_ip(double2& a, const double2 d) {
-  const double t1 = a.y * d.y, t2 = a.x * d.y;
-  a.x = fma(a.x, d.x, -t1);
-  a.y = fma(a.y, d.x, t2);
-}
-
-// every (r, r | 1<<K) pair, no register-side predicate
-template <int K, int MT>
-__device__ __forceinline__ void pair1(double2 (&a)[kRegs], const double2 m0, const double2 m1, const double2 m2,
-                                      const double2 m3) {
-#pragma unroll
-  for (int r = 0; r < kRegs; ++r)
-    if (!((r >> K) & 1)) pair_upd<MT>(a[r], a[r | (1 << K)], m0, m1, m2, m3);
-}
-
-// general pair: xmask XR in register space, runtime register pattern (cm, cv)
-template <int XR, int MT>
-__device__ __forceinline__ void pairg(double2 (&a)[kRegs], const double2* __restrict__ c, int cm, int cv) {
-  const double2 m0 = c[0], m1 = c[1], m2 = c[2], m3 = c[3];
-#pragma unroll
-  for (int r = 0; r < kRegs; ++r)
-    if ((r & cm) == cv) pair_upd<MT>(a[r], a[r ^ XR], m0, m1, m2, m3);
-}
-
-// rotation R(phi) of every (x0, x1) pair on register bit K as shears u += t v; v += s u; u += t v
-// (RY type: on (re0, re1) and (im0, im1); RX type: R(-phi) on (re0, im1), R(phi) on (im0, re1))
-template <int K, bool RX>
-__device__ __forceinline__ void pair_shear(double2 (&a)[kRegs], const double t, const double s) {
-#pragma unroll
-  for (int r = 0; r < kRegs; ++r) {
-    if ((r >> K) & 1) continue;
-    double2& x0 = a[r];
-    double2& x1 = a[r | (1 << K)];
-    if (RX) {
-      x0.x = fma(-t, x1.y, x0.x);
-      x0.y = fma(t, x1.x, x0.y);
-      x1.y = fma(-s, x0.x, x1.y);
-      x1.x = fma(s, x0.y, x1.x);
-      x0.x = fma(-t, x1.y, x0.x);
-      x0.y = fma(t, x1.x, x0.y);
-    } else {
-      x0.x = fma(t, x1.x, x0.x);
-      x0.y = fma(t, x1.y, x0.y);
-      x1.x = fma(s, x0.x, x1.x);
-      x1.y = fma(s, x0.y, x1.y);
-      x0.x = fma(t, x1.x, x0.x);
-      x0.y = fma(t, x1.y, x0.y);
-    }
-  }
-}
-
-// a[r] *= d for registers r with parity(r & M) == 1 ^ tp (tp: the thread's parity part)
-template <int M>
-__device__ __forceinline__ void parity_phase(double2 (&a)[kRegs], const double2 d, const int tp) {
-  if (tp) {
-#pragma unroll
-    for (int r = 0; r < kRegs; ++r)
-      if (!(__builtin_popcount(r & M) & 1)) cmul_ip(a[r], d);
-  } else {
-#pragma unroll
-    for (int r = 0; r < kRegs; ++r)
-      if (__builtin_popcount(r & M) & 1) cmul_ip(a[r], d);
-  }
-}
-
-template <int K, int V>
-__device__ __forceinline__ void phase1(double2 (&a)[kRegs], const double2 d) {
-#pragma unroll
-  for (int r = 0; r < kRegs; ++r)
-    if (((r >> K) & 1) == V) cmul_ip(a[r], d);
-}
-
-template <int K0, int K1>
-__device__ __forceinline__ void dense2(double2 (&a)[kRegs], const double2* __restrict__ M, int cm, int cv, int f) {
-  constexpr int B0 = 1 << K0, B1 = 1 << K1;
-#pragma unroll
-  for (int r = 0; r < kRegs; ++r) {
-    if ((r & (B0 | B1)) != 0) continue;
-    if ((r & cm) != cv) continue;
-    const int idx[4] = {r, r | B0, r | B1, r | B0 | B1};   // matrix index bit 0 <-> K0, bit 1 <-> K1
-    double2 v[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) v[q] = a[idx[q]];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) acc = cfma(M[(q ^ f) * 4 + (cc ^ f)], v[cc], acc);
-      a[idx[q]] = acc;
-    }
-  }
-}
+using fdev::cacc_conj;
+using fdev::cfma;
+using fdev::cmul;
+using fdev::cmul_ip;
+using fdev::dense2;
+using fdev::DPass;
+using fdev::DPhase;
+using fdev::gen2;
+using fdev::pair1;
+using fdev::pair_shear;
+using fdev::pairg;
+using fdev::parity_phase;
+using fdev::phase1;
+using fdev::swz;
+using fdev::kTB;
 
 __device__ __forceinline__ void diagg(double2 (&a)[kRegs], const FOp& op, const double2* __restrict__ coef,
                                       u64 phys_base, int fthr) {
@@ -229,53 +119,16 @@ __device__ __forceinline__ void diagg(double2 (&a)[kRegs], const FOp& op, const 
     parity_phase<M>(a, op.c[0], (__popcll(phys_base & op.xm) + __popc(fthr & M) + op.v) & 1);   \
     break;
 #define PAIRG_CASE(XR)                                                                     \
-  case CS_PAIRGR + XR - 1: pairg<XR, MT_REAL>(a, op.c, op.cm, op.cv ^ (fthr & op.cm)); break; \
-  case CS_PAIRG + XR - 1: if (FULL) pairg<XR, MT_GENERAL>(a, op.c, op.cm, op.cv ^ (fthr & op.cm)); break;
-
-// ---- adjoint bra-kets: psi and lambda share the tile (register bit T selects lambda) --------
-__device__ __forceinline__ void cacc_conj(double& re, double& im, const double2 l, const double2 t) {
-  re = fma(l.x, t.x, fma(l.y, t.y, re));   // conj(l) * t
-  im = fma(l.x, t.y, fma(-l.y, t.x, im));
-}
-
-template <int K, int T>
-__device__ __forceinline__ void gen1(const double2 (&a)[kRegs], const FOp& op, int cv, bool sw, double& re,
-                                     double& im) {
-  const double2 g0 = sw ? op.c[3] : op.c[0], g1 = sw ? op.c[2] : op.c[1];
-  const double2 g2 = sw ? op.c[1] : op.c[2], g3 = sw ? op.c[0] : op.c[3];
-  const int cm = op.cm;
-#pragma unroll
-  for (int r = 0; r < kRegs; ++r) {
-    if (((r >> K) & 1) || ((r >> T) & 1)) continue;
-    if ((r & cm) != cv) continue;
-    const double2 p0 = a[r], p1 = a[r | (1 << K)];
-    const double2 l0 = a[r | (1 << T)], l1 = a[r | (1 << K) | (1 << T)];
-    cacc_conj(re, im, l0, cfma(g0, p0, cmul(g1, p1)));
-    cacc_conj(re, im, l1, cfma(g2, p0, cmul(g3, p1)));
-  }
-}
-
-template <int K0, int K1, int T>
-__device__ __forceinline__ void gen2(const double2 (&a)[kRegs], const double2* __restrict__ M, int cm, int cv, int f,
-                                     double& re, double& im) {
-  constexpr int B0 = 1 << K0, B1 = 1 << K1, BT = 1 << T;
-#pragma unroll
-  for (int r = 0; r < kRegs; ++r) {
-    if (r & (B0 | B1 | BT)) continue;
-    if ((r & cm) != cv) continue;
-    const int idx[4] = {r, r | B0, r | B1, r | B0 | B1};
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double2 acc = make_double2(0.0, 0.0);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc = cfma(M[(q ^ f) * 4 + (c ^ f)], a[idx[c]], acc);
-      cacc_conj(re, im, a[idx[q] | BT], acc);
-    }
-  }
-}
+  case CS_PAIRGR + XR - 1: pairg<XR, MT_REAL>(a, op.c[0], op.c[1], op.c[2], op.c[3], op.cm, op.cv ^ (fthr & op.cm)); break; \
+  case CS_PAIRG + XR - 1: if (FULL) pairg<XR, MT_GENERAL>(a, op.c[0], op.c[1], op.c[2], op.c[3], op.cm, op.cv ^ (fthr & op.cm)); break;
 
 #define GEN1_CASE(K, T) \
-  case CS_GEN1 + K * 4 + T: gen1<K, T>(a, op, cv, ((fthr >> K) & 1) != 0, re, im); break;
+  case CS_GEN1 + K * 4 + T: {                                                                  \
+    const bool sw = ((fthr >> K) & 1) != 0;                                                      \
+    fdev::gen1<K, T>(a, sw ? op.c[3] : op.c[0], sw ? op.c[2] : op.c[1], sw ? op.c[1] : op.c[2],  \
+                     sw ? op.c[0] : op.c[3], op.cm, cv, re, im);                                  \
+    break;                                                                                       \
+  }
 #define GEN2_CASES(PI, K0, K1, TA, TB)                                              \
   case CS_GEN2 + PI * 4 + TA: if (FULL) gen2<K0, K1, TA>(a, M, op.cm, cv, f, re, im); break; \
   case CS_GEN2 + PI * 4 + TB: if (FULL) gen2<K0, K1, TB>(a, M, op.cm, cv, f, re, im); break;
@@ -381,39 +234,10 @@ __device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const int cs, cons
   }
 }
 
-// Launch-time records derived from the planned program: every per-pass / per-phase quantity the
+// Launch-time records (DPass / DPhase, fused_dev.cuh): every per-pass / per-phase quantity the
 // kernel would otherwise recompute per tile or per phase (swizzled shared-memory offsets, spread
 // physical bit masks) is computed once on the host.  Shared-memory offsets compose by XOR because
 // swz is GF(2)-linear.
-constexpr int kTB = kMaxB - kRB;   // max thread-index bits
-// The thread-index -> (swizzled shared offset, physical bits) maps of a phase are GF(2)-linear in
-// the thread index (<= 8 bits), so each is two 16-entry nibble tables: s0 = s_lo[tid & 15] ^
-// s_hi[tid >> 4].
-struct __align__(16) DPhase {
-  int W[kRB];        // swz(1 << reg[k]): offset of register bit k
-  int s_lo[16], s_hi[16];   // swizzled shared offset of the thread's slot, per tid nibble
-  u64 g_lo[16], g_hi[16];   // physical bits of the thread's slot, per tid nibble
-  int op_begin, op_end;     // pass-local op range
-  int flip, pad;
-};
-static_assert(sizeof(DPhase) == 416, "DPhase layout");
-static_assert(kTB <= 8, "two tid nibbles");
-
-struct DPass {
-  u64 n_tiles;
-  u64 outer;           // physical bits NOT in the tile (the tile index deposits into these)
-  u64 grid_step;       // deposit(gridDim.x): tile t -> t + grid is a masked add
-  u64 hi;              // two-array state: indices with this bit live in state_hi
-  u64 ld_off[kRegs];   // load slot i: physical offset of its register-slot bits (without hi)
-  u64 st_off[kRegs];   // store slot i: the same after the pass's in-tile relabeling
-  u64 ld_tb[kTB];      // physical bit of thread-index bit j at load (may be hi)
-  u64 st_tb[kTB];      // ... at store
-  int ld_sm[kRegs];    // swizzled shared offset of load slot i
-  int st_sm[kRegs];    // swizzled shared offset of store slot i
-  int st_tsm[kTB];     // swizzled shared offset of thread-index bit j at store
-  unsigned ld_hsel, st_hsel;   // slots whose index carries the hi bit
-  int b, nthr, n_phases, n_ops, n_gen, gen_base, n_gen_total, pad;
-};
 
 // DB = true : one persistent CTA per SM, two tile buffers, tile t+grid prefetched during tile t.
 // DB = false: two CTAs per SM (128 registers), one buffer each; CTAs overlap each other instead.
@@ -817,7 +641,8 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
     db = mode && std::string(mode) == "db";
   });
   const int b = prog.passes[0].b;
-  const u64 grid = std::min<u64>(prog.passes[0].n_tiles, u64(sms_dev[h->device]) * (db ? 1 : 2));   // persistent grid
+  const bool jdb = !db && jit_db();   // generated kernels in their double-buffered 1-CTA/SM form
+  const u64 grid = std::min<u64>(prog.passes[0].n_tiles, u64(sms_dev[h->device]) * ((db || jdb) ? 1 : 2));   // persistent grid
 
   // launch records + upload phases | ops | coef in one copy (the buffer is only reused after a sync)
   std::vector<DPhase> dph(prog.phases.size());
@@ -827,7 +652,10 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
   const size_t b_ph = dph.size() * sizeof(DPhase);
   const size_t b_op = prog.ops.size() * sizeof(FOp);
   const size_t b_cf = prog.coef.size() * sizeof(double2);
-  const size_t total = align(b_ph) + align(b_op) + align(b_cf);
+  const bool two = state_hi != nullptr;
+  if (!db) jit_prepare(prog, two);   // per-pass compiled kernels (cached by structure)
+  const size_t b_jt = prog.jit_tabs.size() * sizeof(double2);
+  const size_t total = align(b_ph) + align(b_op) + align(b_cf) + align(b_jt);
   std::vector<char> host(total);
   std::memcpy(host.data(), dph.data(), b_ph);
   std::memcpy(host.data() + align(b_ph), prog.ops.data(), b_op);
@@ -836,12 +664,14 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
     for (size_t i = 0; i < prog.ops.size(); ++i) dev_ops[i].cs |= dev_ops[i].fk << 16;   // one prefetched word
   }
   std::memcpy(host.data() + align(b_ph) + align(b_op), prog.coef.data(), b_cf);
+  if (b_jt) std::memcpy(host.data() + align(b_ph) + align(b_op) + align(b_cf), prog.jit_tabs.data(), b_jt);
   CUDA_CHECK(cudaStreamSynchronize(h->stream));   // previous program may still be in use
   char* dbuf = (char*)program_buffer(h, total);
   CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), total, cudaMemcpyHostToDevice, h->stream));
   const DPhase* d_ph = (const DPhase*)dbuf;
   const FOp* d_op = (const FOp*)(dbuf + align(b_ph));
   const double2* d_cf = (const double2*)(dbuf + align(b_ph) + align(b_op));
+  const double2* d_jt = (const double2*)(dbuf + align(b_ph) + align(b_op) + align(b_cf));
 
   const int n_gen = int(prog.gen_slot_of.size());
   double2* d_gen = nullptr;
@@ -850,7 +680,6 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
     CUDA_CHECK(cudaMallocAsync(&d_gen, grid * n_gen * sizeof(double2), h->stream));
     CUDA_CHECK(cudaMemsetAsync(d_gen, 0, grid * n_gen * sizeof(double2), h->stream));
   }
-  const bool two = state_hi != nullptr;
   for (double2* state : states) {
     for (const Step& s : prog.steps) {
       if (!s.fused) {
@@ -871,7 +700,13 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
       stat_begin(h, KC_FUSED, bytes, ev);
       const unsigned g = unsigned(grid);
       cudaStream_t st = h->stream;
-      if (two) {
+      const JitPass* jp = (!db && s.index < int(prog.jit.size()) && prog.jit[s.index].kernel) ? &prog.jit[s.index] : nullptr;
+      if (jp) {
+        // generated kernel of this pass: [tile] [phase records] [generator accumulators]
+        const size_t jsmem = (jdb ? 2 : 1) * (size_t(1) << b) * sizeof(double2) + size_t(D.n_phases) * sizeof(DPhase) +
+                             (A.n_gen ? size_t(threads / 32) * kMaxGens * sizeof(double2) : 0);
+        jit_launch(*jp, h->device, g, threads, jsmem, st, state, state_hi, &D, ph, d_jt, d_gen);
+      } else if (two) {
         if (db && full) launch_fused<true, true, true>(g, threads, smem, st, state, D, ph, op, d_cf, d_gen, state_hi);
         else if (db) launch_fused<false, true, true>(g, threads, smem, st, state, D, ph, op, d_cf, d_gen, state_hi);
         else if (full) launch_fused<true, false, true>(g, threads, smem, st, state, D, ph, op, d_cf, d_gen, state_hi);

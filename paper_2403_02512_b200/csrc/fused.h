@@ -4,6 +4,7 @@
 
 #include <vector>
 
+#include "fused_jit.h"
 #include "sv_internal.h"
 
 namespace fused {
@@ -112,6 +113,10 @@ struct Program {
                                    // ... i.e. the qubit at p moved to perm[p]
   std::vector<int> gen_slot_of;    // program result slot -> Prim::slot (the caller's Jacobian slot)
   int64_t n_prims_in = 0, n_prims_merged = 0;
+  // runtime pass compiler (fused_jit.cpp): per-pass kernels and their parameter blocks
+  bool jit_ready = false, jit_two = false;
+  std::vector<JitPass> jit;
+  std::vector<double2> jit_tabs;   // coefficient tables of the generated kernels, all passes
 };
 
 // remap = let passes relabel qubits inside their tile (moves upcoming qubits onto the low bits)

@@ -1,0 +1,379 @@
+// K7 device-side building blocks, shared by the prebuilt op-interpreting tile kernel (fused.cu)
+// and the per-pass specialised kernels the runtime pass compiler generates (fused_jit.cpp hands
+// this file, verbatim, to NVRTC in front of every generated kernel).  Self-contained: no host
+// headers, nothing but CUDA built-ins.
+//
+// Register model (see fused.cu): a thread holds 16 amplitudes a[r] of its tile, r = the 4
+// "register bits".  Every update below is in place (a[] never moves between registers).
+#pragma once
+
+typedef unsigned long long u64;
+
+namespace fdev {
+
+constexpr int kMaxB = 12;        // tile bits (2^12 amplitudes = 64 KiB)
+constexpr int kRB = 4;           // register bits per thread
+constexpr int kRegs = 1 << kRB;  // amplitudes per thread
+constexpr int kTB = kMaxB - kRB; // max thread-index bits
+constexpr int kMaxGens = 64;     // generator slots per pass (per-warp shared accumulators)
+constexpr int kMtGeneral = 0, kMtReal = 1, kMtRxLike = 2;
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+
+// XOR swizzle of a tile index: linear over GF(2), so swz(a ^ b) == swz(a) ^ swz(b)
+__device__ __forceinline__ int swz(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
+
+// In-place 2x2 update of (x0, x1): products needing OLD values first, then overwriting FMAs.
+template <int MT>
+__device__ __forceinline__ void pair_upd(double2& x0, double2& x1, const double2 m0, const double2 m1, const double2 m2,
+                                         const double2 m3) {
+  if (MT == kMtReal) {
+    const double px = m1.x * x1.x, py = m1.x * x1.y, qx = m2.x * x0.x, qy = m2.x * x0.y;
+    x0.x = fma(m0.x, x0.x, px);
+    x0.y = fma(m0.x, x0.y, py);
+    x1.x = fma(m3.x, x1.x, qx);
+    x1.y = fma(m3.x, x1.y, qy);
+  } else if (MT == kMtRxLike) {   // m0, m3 real; m1, m2 imaginary: (i b)(x + i y) = -b y + i b x
+    const double px = -m1.y * x1.y, py = m1.y * x1.x, qx = -m2.y * x0.y, qy = m2.y * x0.x;
+    x0.x = fma(m0.x, x0.x, px);
+    x0.y = fma(m0.x, x0.y, py);
+    x1.x = fma(m3.x, x1.x, qx);
+    x1.y = fma(m3.x, x1.y, qy);
+  } else {
+    const double2 p = cmul(m1, x1), q = cmul(m2, x0);
+    x0 = cfma(m0, x0, p);
+    x1 = cfma(m3, x1, q);
+  }
+}
+
+// a *= d in place (cross products first)
+__device__ __forceinline__ void cmul_ip(double2& a, const double2 d) {
+  const double t1 = a.y * d.y, t2 = a.x * d.y;
+  a.x = fma(a.x, d.x, -t1);
+  a.y = fma(a.y, d.x, t2);
+}
+
+// every (r, r | 1<<K) pair, no register-side predicate
+template <int K, int MT>
+__device__ __forceinline__ void pair1(double2 (&a)[kRegs], const double2 m0, const double2 m1, const double2 m2,
+                                      const double2 m3) {
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r)
+    if (!((r >> K) & 1)) pair_upd<MT>(a[r], a[r | (1 << K)], m0, m1, m2, m3);
+}
+
+// general pair: xmask XR in register space, runtime register pattern (cm, cv)
+template <int XR, int MT>
+__device__ __forceinline__ void pairg(double2 (&a)[kRegs], const double2 m0, const double2 m1, const double2 m2,
+                                      const double2 m3, int cm, int cv) {
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r)
+    if ((r & cm) == cv) pair_upd<MT>(a[r], a[r ^ XR], m0, m1, m2, m3);
+}
+
+// rotation R(phi) of every (x0, x1) pair on register bit K as shears u += t v; v += s u; u += t v
+// (RY type: on (re0, re1) and (im0, im1); RX type: R(-phi) on (re0, im1), R(phi) on (im0, re1))
+template <int K, bool RX>
+__device__ __forceinline__ void pair_shear(double2 (&a)[kRegs], const double t, const double s) {
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if ((r >> K) & 1) continue;
+    double2& x0 = a[r];
+    double2& x1 = a[r | (1 << K)];
+    if (RX) {
+      x0.x = fma(-t, x1.y, x0.x);
+      x0.y = fma(t, x1.x, x0.y);
+      x1.y = fma(-s, x0.x, x1.y);
+      x1.x = fma(s, x0.y, x1.x);
+      x0.x = fma(-t, x1.y, x0.x);
+      x0.y = fma(t, x1.x, x0.y);
+    } else {
+      x0.x = fma(t, x1.x, x0.x);
+      x0.y = fma(t, x1.y, x0.y);
+      x1.x = fma(s, x0.x, x1.x);
+      x1.y = fma(s, x0.y, x1.y);
+      x0.x = fma(t, x1.x, x0.x);
+      x0.y = fma(t, x1.y, x0.y);
+    }
+  }
+}
+
+// a[r] *= d for registers r with parity(r & M) == 1 ^ tp (tp: the thread's parity part)
+template <int M>
+__device__ __forceinline__ void parity_phase(double2 (&a)[kRegs], const double2 d, const int tp) {
+  if (tp) {
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r)
+      if (!(__popc(r & M) & 1)) cmul_ip(a[r], d);
+  } else {
+#pragma unroll
+    for (int r = 0; r < kRegs; ++r)
+      if (__popc(r & M) & 1) cmul_ip(a[r], d);
+  }
+}
+
+template <int K, int V>
+__device__ __forceinline__ void phase1(double2 (&a)[kRegs], const double2 d) {
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r)
+    if (((r >> K) & 1) == V) cmul_ip(a[r], d);
+}
+
+template <int K0, int K1>
+__device__ __forceinline__ void dense2(double2 (&a)[kRegs], const double2* __restrict__ M, int cm, int cv, int f) {
+  constexpr int B0 = 1 << K0, B1 = 1 << K1;
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if ((r & (B0 | B1)) != 0) continue;
+    if ((r & cm) != cv) continue;
+    const int idx[4] = {r, r | B0, r | B1, r | B0 | B1};   // matrix index bit 0 <-> K0, bit 1 <-> K1
+    double2 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = a[idx[q]];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) acc = cfma(M[(q ^ f) * 4 + (cc ^ f)], v[cc], acc);
+      a[idx[q]] = acc;
+    }
+  }
+}
+
+// diagonal table: a[r] *= tab[tconst ^ W(r)], W(r) = the table bits register r carries (compile-time
+// when the planner's table layout is known, i.e. in generated pass kernels)
+template <int W0, int W1, int W2, int W3>
+__device__ __forceinline__ void diag_tab(double2 (&a)[kRegs], const double2* __restrict__ tab, int tconst, int cm,
+                                         int cv) {
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if ((r & cm) != cv) continue;
+    const int t = tconst ^ (((r & 1) ? W0 : 0) | ((r & 2) ? W1 : 0) | ((r & 4) ? W2 : 0) | ((r & 8) ? W3 : 0));
+    cmul_ip(a[r], tab[t]);
+  }
+}
+
+// ---- adjoint bra-kets: psi and lambda share the tile (register bit T selects lambda) --------
+__device__ __forceinline__ void cacc_conj(double& re, double& im, const double2 l, const double2 t) {
+  re = fma(l.x, t.x, fma(l.y, t.y, re));   // conj(l) * t
+  im = fma(l.x, t.y, fma(-l.y, t.x, im));
+}
+
+template <int K, int T>
+__device__ __forceinline__ void gen1(const double2 (&a)[kRegs], const double2 g0, const double2 g1, const double2 g2,
+                                     const double2 g3, int cm, int cv, double& re, double& im) {
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if (((r >> K) & 1) || ((r >> T) & 1)) continue;
+    if ((r & cm) != cv) continue;
+    const double2 p0 = a[r], p1 = a[r | (1 << K)];
+    const double2 l0 = a[r | (1 << T)], l1 = a[r | (1 << K) | (1 << T)];
+    cacc_conj(re, im, l0, cfma(g0, p0, cmul(g1, p1)));
+    cacc_conj(re, im, l1, cfma(g2, p0, cmul(g3, p1)));
+  }
+}
+
+template <int K0, int K1, int T>
+__device__ __forceinline__ void gen2(const double2 (&a)[kRegs], const double2* __restrict__ M, int cm, int cv, int f,
+                                     double& re, double& im) {
+  constexpr int B0 = 1 << K0, B1 = 1 << K1, BT = 1 << T;
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if (r & (B0 | B1 | BT)) continue;
+    if ((r & cm) != cv) continue;
+    const int idx[4] = {r, r | B0, r | B1, r | B0 | B1};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc = cfma(M[(q ^ f) * 4 + (c ^ f)], a[idx[c]], acc);
+      cacc_conj(re, im, a[idx[q] | BT], acc);
+    }
+  }
+}
+
+// diagonal generator over a table (like diag_tab): sum_r conj(lambda_r) g[t(r)] psi_r
+template <int T, int W0, int W1, int W2, int W3>
+__device__ __forceinline__ void gen_diag_tab(const double2 (&a)[kRegs], const double2* __restrict__ tab, int tconst,
+                                             int cm, int cv, double& re, double& im) {
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if ((r >> T) & 1) continue;
+    if ((r & cm) != cv) continue;
+    const int t = tconst ^ (((r & 1) ? W0 : 0) | ((r & 2) ? W1 : 0) | ((r & 4) ? W2 : 0) | ((r & 8) ? W3 : 0));
+    cacc_conj(re, im, a[r | (1 << T)], cmul(tab[t], a[r]));
+  }
+}
+
+// warp-reduce one bra-ket and add it to this warp's shared accumulator (every lane calls)
+__device__ __forceinline__ void gen_commit(double re, double im, double2* __restrict__ acc_warp, int slot) {
+  for (int s = 16; s > 0; s >>= 1) {
+    re += __shfl_xor_sync(0xffffffffu, re, s);
+    im += __shfl_xor_sync(0xffffffffu, im, s);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    acc_warp[slot].x += re;
+    acc_warp[slot].y += im;
+  }
+}
+
+// Launch-time records derived from the planned program (computed once on the host): see fused.cu.
+// The thread-index -> (swizzled shared offset, physical bits) maps of a phase are GF(2)-linear in
+// the thread index (<= 8 bits), so each is two 16-entry nibble tables: s0 = s_lo[tid & 15] ^
+// s_hi[tid >> 4].
+struct __align__(16) DPhase {
+  int W[kRB];        // swz(1 << reg[k]): offset of register bit k
+  int s_lo[16], s_hi[16];   // swizzled shared offset of the thread's slot, per tid nibble
+  u64 g_lo[16], g_hi[16];   // physical bits of the thread's slot, per tid nibble
+  int op_begin, op_end;     // pass-local op range
+  int flip, pad;
+};
+static_assert(sizeof(DPhase) == 416, "DPhase layout");
+static_assert(kTB <= 8, "two tid nibbles");
+
+struct DPass {
+  u64 n_tiles;
+  u64 outer;           // physical bits NOT in the tile (the tile index deposits into these)
+  u64 grid_step;       // deposit(gridDim.x): tile t -> t + grid is a masked add
+  u64 hi;              // two-array state: indices with this bit live in state_hi
+  u64 ld_off[kRegs];   // load slot i: physical offset of its register-slot bits (without hi)
+  u64 st_off[kRegs];   // store slot i: the same after the pass's in-tile relabeling
+  u64 ld_tb[kTB];      // physical bit of thread-index bit j at load (may be hi)
+  u64 st_tb[kTB];      // ... at store
+  int ld_sm[kRegs];    // swizzled shared offset of load slot i
+  int st_sm[kRegs];    // swizzled shared offset of store slot i
+  int st_tsm[kTB];     // swizzled shared offset of thread-index bit j at store
+  unsigned ld_hsel, st_hsel;   // slots whose index carries the hi bit
+  int b, nthr, n_phases, n_ops, n_gen, gen_base, n_gen_total, pad;
+};
+
+// The tile loop of one pass for the generated (per-pass specialised) kernels: persistent CTAs;
+// stage -> body(tile, phase records, tile base, warp accumulators) -> store with the pass's in-tile
+// relabeling -> next tile.  Same data movement as k_fused<*, DB, TWO>:
+//   DB = false: 2 CTAs per SM, one tile buffer each (the two CTAs overlap each other);
+//   DB = true : 1 CTA per SM, two tile buffers: tile t + grid streams in while tile t is computed.
+// Dynamic shared memory: [tile buffer(s)] [phase records] [generator accumulators].
+template <bool TWO, bool DB, class Body>
+__device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* __restrict__ state_hi, const DPass& P,
+                                         const DPhase* __restrict__ phases, double2* __restrict__ gen_partials,
+                                         Body body) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* tile = reinterpret_cast<double2*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int nthreads = blockDim.x;
+  const int T = 1 << P.b;
+  DPhase* s_ph = reinterpret_cast<DPhase*>(smem_raw + size_t(DB ? 2 : 1) * T * sizeof(double2));
+  double2* s_gen = reinterpret_cast<double2*>(s_ph + P.n_phases);
+  {
+    const int4* src = reinterpret_cast<const int4*>(phases);
+    int4* dst = reinterpret_cast<int4*>(s_ph);
+    const int n16p = P.n_phases * int(sizeof(DPhase) / 16);
+    for (int i = tid; i < n16p; i += nthreads) dst[i] = src[i];
+    if (P.n_gen)
+      for (int i = tid; i < (nthreads >> 5) * kMaxGens; i += nthreads) s_gen[i] = make_double2(0.0, 0.0);
+  }
+  u64 ld_tid = 0, st_tid = 0;
+  int st_sw = 0;
+#pragma unroll
+  for (int j = 0; j < kTB; ++j)
+    if (j < P.nthr && ((tid >> j) & 1)) {
+      ld_tid |= P.ld_tb[j];
+      st_tid |= P.st_tb[j];
+      st_sw ^= P.st_tsm[j];
+    }
+  const int ld_sw = swz(tid);
+  auto slot_ptrs = [&](u64 g, double2*& p_lo, double2*& p_hi) {
+    if (!TWO) {
+      p_lo = p_hi = state + g;
+      return;
+    }
+    const u64 gl = g & ~P.hi;
+    p_hi = state_hi + gl;
+    p_lo = (g & P.hi) ? p_hi : state + gl;
+  };
+  u64 base = 0;
+  {
+    u64 m = P.outer;
+    for (u64 v = blockIdx.x; m && v; m &= m - 1, v >>= 1)
+      if (v & 1) base |= m & (~m + 1);
+  }
+  double2* acc_warp = s_gen + (tid >> 5) * kMaxGens;
+  auto issue_load = [&](u64 b0, double2* buf) {
+    double2 *p_lo, *p_hi;
+    slot_ptrs(b0 | ld_tid, p_lo, p_hi);
+    const unsigned sb = (unsigned)__cvta_generic_to_shared(buf);
+#pragma unroll
+    for (int i = 0; i < kRegs; ++i) {
+      const double2* src = (TWO && ((P.ld_hsel >> i) & 1) ? p_hi : p_lo) + P.ld_off[i];
+      const unsigned dst = sb + unsigned(ld_sw ^ P.ld_sm[i]) * 16u;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  int cur = 0;
+  if (DB && blockIdx.x < P.n_tiles) {
+    __syncthreads();   // phase records staged
+    issue_load(base, tile);
+  }
+  for (u64 t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+    const u64 nbase = ((base | ~P.outer) + P.grid_step) & P.outer;
+    double2* tl = tile + (DB ? cur * T : 0);
+    if (!DB) {
+      __syncthreads();   // previous tile stored (and phase records staged) before the buffer is refilled
+      issue_load(base, tile);
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncthreads();
+    // DB: the other buffer's previous tile was fully read by the store loop before this barrier
+    if (DB && t + gridDim.x < P.n_tiles) issue_load(nbase, tile + (cur ^ 1) * T);
+    body(tl, s_ph, base, acc_warp);   // every phase, each ending with __syncthreads()
+    {
+      double2 *p_lo, *p_hi;
+      slot_ptrs(base | st_tid, p_lo, p_hi);
+#pragma unroll
+      for (int i = 0; i < kRegs; ++i)
+        (TWO && ((P.st_hsel >> i) & 1) ? p_hi : p_lo)[P.st_off[i]] = tl[st_sw ^ P.st_sm[i]];
+    }
+    base = nbase;
+    cur ^= 1;
+  }
+  if (P.n_gen) {
+    __syncthreads();
+    const int nw = nthreads >> 5;
+    for (int g = tid; g < P.n_gen; g += nthreads) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int w = 0; w < nw; ++w) {
+        s.x += s_gen[w * kMaxGens + g].x;
+        s.y += s_gen[w * kMaxGens + g].y;
+      }
+      gen_partials[size_t(blockIdx.x) * P.n_gen_total + P.gen_base + g] = s;
+    }
+  }
+}
+
+// phase entry / exit for generated kernels: registers <- tile (offsets s0 ^ W(r)), and the store
+// honouring the phase's uniform flip and the thread's dynamic flips
+#define FDEV_PHASE_LOAD(F, W0, W1, W2, W3)                                                                       \
+  const int s0 = (F).s_lo[threadIdx.x & 15] ^ (F).s_hi[threadIdx.x >> 4];                                      \
+  const u64 pb = base | (F).g_lo[threadIdx.x & 15] | (F).g_hi[threadIdx.x >> 4];                                \
+  double2 a[fdev::kRegs];                                                                                       \
+  _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r) a[r] =                                                \
+      tile[s0 ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)];     \
+  int fthr = 0;                                                                                                 \
+  (void)pb;                                                                                                     \
+  (void)fthr;
+#define FDEV_PHASE_STORE(FLIP, W0, W1, W2, W3)                                                                   \
+  {                                                                                                             \
+    const int fl = (FLIP) ^ fthr;                                                                               \
+    const int sf = s0 ^ ((fl & 1) ? (W0) : 0) ^ ((fl & 2) ? (W1) : 0) ^ ((fl & 4) ? (W2) : 0) ^ ((fl & 8) ? (W3) : 0); \
+    _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r)                                                     \
+      tile[sf ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)] = a[r]; \
+  }                                                                                                             \
+  __syncthreads();
+
+}  // namespace fdev

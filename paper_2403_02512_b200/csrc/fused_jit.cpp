@@ -1,0 +1,397 @@
+// Runtime pass compiler for the K7 fusion engine.
+//
+// The prebuilt tile kernel (fused.cu, k_fused) interprets a pass's op records: per op it loads
+// the record from shared memory, tests the predicate and dispatches through a jump table.  That
+// interpretation is ~2/3 of the instructions the kernel issues (profiles/r1_ncu_fused_pass_v14.md:
+// FP64 34.8 %, BRA + UISETP + LOP3 + LDS + IMAD + LEA ~43 %), and the dispatch boundaries stop the
+// compiler from overlapping one gate's FMAs with the next gate's.
+//
+// Here every planned pass becomes its own kernel: the pass's op sequence is emitted as straight-line
+// CUDA (the same fused_dev.cuh building blocks, with register bits, masks and patterns as literals)
+// and compiled for sm_100a with NVRTC at plan time.  Gate coefficients are NOT in the source: they
+// travel as a by-value kernel parameter block (constant bank 0, read directly by the DFMAs), and
+// diagonal / 4x4 tables through a small device table, so a kernel depends only on the pass's
+// *structure* -- circuits re-run with new parameters (VQE / QAOA optimisation loops, the rows of a
+// multi-observable adjoint sweep) reuse the compiled kernels.  Kernels are cached process-wide by
+// their source text; distinct passes compile in parallel.
+//
+// Data movement, tiles, phases and results are exactly those of k_fused<*, false, *>; the pass
+// compiler only removes the interpreter.  SVB200_JIT=0 selects the interpreter (A/B timing).
+#include <nvrtc.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <sstream>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "fused.h"
+#include "fused_jit.h"
+
+namespace fused {
+namespace {
+
+const char* kDevSrc =
+#include "fused_dev_src.inc"
+    ;
+
+std::string hex64(u64 v) {
+  char b[32];
+  std::snprintf(b, sizeof(b), "0x%llxull", v);
+  return b;
+}
+
+int swz_h(int s) { return s ^ (((s >> 3) ^ (s >> 6) ^ (s >> 9)) & 7); }
+
+const int kPairK0[6] = {0, 0, 0, 1, 1, 2};
+const int kPairK1[6] = {1, 2, 3, 2, 3, 3};
+
+// Source generator for one pass.  Records, in emission order, which op coefficients go into the
+// parameter block (cf_refs) and which coefficient tables go into the device table (tab_refs).
+struct Gen {
+  std::ostringstream o;
+  std::vector<std::pair<int, int>> cf_refs;   // (pass-local op, c[] index)
+  std::vector<std::pair<int, int>> tab_refs;  // (pass-local op, table length)
+  int tab_len = 0;
+
+  std::string C(int op, int j) {
+    cf_refs.push_back({op, j});
+    return "cf.v[" + std::to_string(cf_refs.size() - 1) + "]";
+  }
+  std::string T(int op, int len) {
+    tab_refs.push_back({op, len});
+    const int off = tab_len;
+    tab_len += len;
+    return "(tabs + " + std::to_string(off) + ")";
+  }
+};
+
+// table index constant of a DIAGG / GEND op: off-register table bits from the thread's physical
+// base, register table bits carrying a dynamic flip toggle their table bit
+std::string tconst_expr(const FOp& op, int W[4]) {
+  std::string e = "0";
+  for (int k = 0; k < 4; ++k) W[k] = 0;
+  for (int j = 0; j < op.nt; ++j) {
+    const int rg = op.treg[j];
+    if (rg == 0xFF) {
+      e += " | (int((pb >> " + std::to_string(op.tphys[j]) + ") & 1ull) << " + std::to_string(j) + ")";
+    } else {
+      W[rg] |= 1 << j;
+      e = "(" + e + ") ^ (((fthr >> " + std::to_string(rg) + ") & 1) << " + std::to_string(j) + ")";
+    }
+  }
+  return e;
+}
+
+bool emit_op(Gen& g, int i, const FOp& op) {
+  std::ostringstream& o = g.o;
+  const int cs = op.cs;
+  o << "    {\n";
+  if (op.fk) o << "      if ((pb & " << hex64(op.fpm) << ") == " << hex64(op.fpv) << ") fthr ^= " << op.fk << ";\n";
+  const bool has_pred = op.pm != 0 || op.pv != 0;
+  const std::string pred = "((pb & " + hex64(op.pm) + ") == " + hex64(op.pv) + ")";
+  const std::string cm = std::to_string(int(op.cm));
+  const std::string cvd = "(" + std::to_string(int(op.cv)) + " ^ (fthr & " + cm + "))";
+  if (cs >= CS_GEN1) {
+    o << "      double re = 0.0, im = 0.0;\n";
+    o << "      if (" << (has_pred ? pred : std::string("true")) << ") {\n";
+    if (cs < CS_GEN2) {
+      const int k = (cs - CS_GEN1) / 4, t = (cs - CS_GEN1) % 4;
+      const std::string c0 = g.C(i, 0), c1 = g.C(i, 1), c2 = g.C(i, 2), c3 = g.C(i, 3);
+      o << "        const bool sw = (fthr >> " << k << ") & 1;\n";
+      o << "        fdev::gen1<" << k << ", " << t << ">(a, sw ? " << c3 << " : " << c0 << ", sw ? " << c2 << " : " << c1
+        << ", sw ? " << c1 << " : " << c2 << ", sw ? " << c0 << " : " << c3 << ", " << cm << ", " << cvd
+        << ", re, im);\n";
+    } else if (cs < CS_GEND) {
+      const int pi = (cs - CS_GEN2) / 4, t = (cs - CS_GEN2) % 4;
+      const int k0 = kPairK0[pi], k1 = kPairK1[pi];
+      o << "        const int f = ((fthr >> " << k0 << ") & 1) | (((fthr >> " << k1 << ") & 1) << 1);\n";
+      o << "        fdev::gen2<" << k0 << ", " << k1 << ", " << t << ">(a, " << g.T(i, 16) << ", " << cm << ", " << cvd
+        << ", f, re, im);\n";
+    } else if (cs < CS_GEND + 4) {
+      const int t = cs - CS_GEND;
+      int W[4];
+      const std::string tc = tconst_expr(op, W);
+      o << "        fdev::gen_diag_tab<" << t << ", " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ">(a, "
+        << g.T(i, 1 << op.nt) << ", " << tc << ", " << cm << ", " << cvd << ", re, im);\n";
+    } else {
+      return false;
+    }
+    o << "      }\n";
+    o << "      fdev::gen_commit(re, im, acc_warp, " << op.slot << ");\n";
+    o << "    }\n";
+    return true;
+  }
+  if (has_pred) o << "      if " << pred << " {\n";
+  if (cs >= CS_PAIR1 && cs < CS_PAIR1 + 16) {
+    const int k = cs / 4, mt = cs % 4;
+    if (mt != MT_X)
+      o << "      fdev::pair1<" << k << ", " << mt << ">(a, " << g.C(i, 0) << ", " << g.C(i, 1) << ", " << g.C(i, 2)
+        << ", " << g.C(i, 3) << ");\n";
+  } else if (cs >= CS_PAIR1D && cs < CS_PAIR1D + 16) {
+    const int k = (cs - CS_PAIR1D) / 4, mt = op.mtype;
+    if (mt != MT_X) {
+      const std::string c0 = g.C(i, 0), c1 = g.C(i, 1), c2 = g.C(i, 2), c3 = g.C(i, 3);
+      o << "      if ((fthr >> " << k << ") & 1) fdev::pair1<" << k << ", " << mt << ">(a, " << c3 << ", " << c2 << ", "
+        << c1 << ", " << c0 << ");\n";
+      o << "      else fdev::pair1<" << k << ", " << mt << ">(a, " << c0 << ", " << c1 << ", " << c2 << ", " << c3
+        << ");\n";
+    }
+  } else if (cs >= CS_PHASE1 && cs < CS_PHASE1 + 8) {
+    o << "      fdev::phase1<" << (cs - CS_PHASE1) / 2 << ", " << (cs - CS_PHASE1) % 2 << ">(a, " << g.C(i, 0) << ");\n";
+  } else if (cs >= CS_PHASE1D && cs < CS_PHASE1D + 8) {
+    const int k = (cs - CS_PHASE1D) / 2;
+    const std::string c0 = g.C(i, 0);
+    o << "      if (((fthr >> " << k << ") & 1) ^ " << int(op.v) << ") fdev::phase1<" << k << ", 1>(a, " << c0 << ");\n";
+    o << "      else fdev::phase1<" << k << ", 0>(a, " << c0 << ");\n";
+  } else if (cs == CS_SCALAR) {
+    o << "      _Pragma(\"unroll\") for (int r = 0; r < fdev::kRegs; ++r) fdev::cmul_ip(a[r], " << g.C(i, 0) << ");\n";
+  } else if (cs >= CS_XFLIP && cs < CS_XFLIP + 4) {
+    o << "      fthr ^= " << (1 << (cs - CS_XFLIP)) << ";\n";
+  } else if (cs >= CS_SHEAR && cs < CS_SHEAR + 16) {
+    const int k = (cs - CS_SHEAR) / 4, sub = (cs - CS_SHEAR) % 4;
+    const std::string c0 = g.C(i, 0);
+    if (sub == SH_RY) o << "      fdev::pair_shear<" << k << ", false>(a, " << c0 << ".x, " << c0 << ".y);\n";
+    if (sub == SH_RX) o << "      fdev::pair_shear<" << k << ", true>(a, " << c0 << ".x, " << c0 << ".y);\n";
+    if (sub == SH_RYD) {
+      o << "      if ((fthr >> " << k << ") & 1) fdev::pair_shear<" << k << ", false>(a, -" << c0 << ".x, -" << c0
+        << ".y);\n";
+      o << "      else fdev::pair_shear<" << k << ", false>(a, " << c0 << ".x, " << c0 << ".y);\n";
+    }
+  } else if (cs >= CS_PARITY && cs < CS_PARITY + 16) {
+    const int M = cs - CS_PARITY;
+    std::string tp = "(__popc(fthr & " + std::to_string(M) + ") + " + std::to_string(int(op.v));
+    if (op.xm) tp += " + __popcll(pb & " + hex64(op.xm) + ")";
+    tp += ") & 1";
+    o << "      fdev::parity_phase<" << M << ">(a, " << g.C(i, 0) << ", " << tp << ");\n";
+  } else if (cs >= CS_PAIRGR && cs < CS_PAIRGR + 15) {
+    o << "      fdev::pairg<" << (cs - CS_PAIRGR + 1) << ", fdev::kMtReal>(a, " << g.C(i, 0) << ", " << g.C(i, 1) << ", "
+      << g.C(i, 2) << ", " << g.C(i, 3) << ", " << cm << ", " << cvd << ");\n";
+  } else if (cs >= CS_PAIRG && cs < CS_PAIRG + 15) {
+    o << "      fdev::pairg<" << (cs - CS_PAIRG + 1) << ", fdev::kMtGeneral>(a, " << g.C(i, 0) << ", " << g.C(i, 1)
+      << ", " << g.C(i, 2) << ", " << g.C(i, 3) << ", " << cm << ", " << cvd << ");\n";
+  } else if (cs == CS_DIAGG) {
+    int W[4];
+    const std::string tc = tconst_expr(op, W);
+    o << "      fdev::diag_tab<" << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ">(a, " << g.T(i, 1 << op.nt)
+      << ", " << tc << ", " << cm << ", " << cvd << ");\n";
+  } else if (cs >= CS_DENSE2 && cs < CS_DENSE2 + 6) {
+    const int k0 = kPairK0[cs - CS_DENSE2], k1 = kPairK1[cs - CS_DENSE2];
+    o << "      {\n        const int f = ((fthr >> " << k0 << ") & 1) | (((fthr >> " << k1 << ") & 1) << 1);\n";
+    o << "        fdev::dense2<" << k0 << ", " << k1 << ">(a, " << g.T(i, 16) << ", " << cm << ", " << cvd
+      << ", f);\n      }\n";
+  } else {
+    return false;
+  }
+  if (has_pred) o << "      }\n";
+  o << "    }\n";
+  return true;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+// compiled-kernel cache (process-wide, keyed by the generated source)
+// ---------------------------------------------------------------------------------------------
+struct JitKernel {
+  std::string src;
+  bool ok = false;
+  std::string log;
+  std::vector<char> cubin;
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kern = nullptr;
+  int smem_set[64] = {0};   // per device: dynamic shared memory attribute already set
+  std::mutex mu;
+};
+
+namespace {
+std::mutex g_jit_mu;
+std::map<std::string, std::shared_ptr<JitKernel>> g_jit;
+std::atomic<int64_t> g_jit_compiled{0};
+std::atomic<int64_t> g_jit_compile_us{0};
+
+void compile_kernel(JitKernel& k) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const std::string full = std::string(kDevSrc) + "\n" + k.src;
+  nvrtcProgram prog;
+  if (nvrtcCreateProgram(&prog, full.c_str(), "svb200_pass.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    k.log = "nvrtcCreateProgram failed";
+    return;
+  }
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--restrict"};
+  const nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
+  size_t ls = 0;
+  nvrtcGetProgramLogSize(prog, &ls);
+  if (ls > 1) {
+    k.log.resize(ls);
+    nvrtcGetProgramLog(prog, &k.log[0]);
+  }
+  if (r == NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetCUBINSize(prog, &n);
+    k.cubin.resize(n);
+    nvrtcGetCUBIN(prog, k.cubin.data());
+    k.ok = n > 0;
+  }
+  nvrtcDestroyProgram(&prog);
+  g_jit_compiled += 1;
+  g_jit_compile_us += std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count();
+}
+
+}  // namespace
+
+bool jit_enabled() {
+  static const bool on = !(getenv("SVB200_JIT") && std::string(getenv("SVB200_JIT")) == "0");
+  return on;
+}
+
+// SVB200_JIT_MODE=db: one CTA per SM with two tile buffers (the next tile streams in during the
+// current one's phases) instead of two single-buffer CTAs per SM
+bool jit_db() {
+  static const bool db = getenv("SVB200_JIT_MODE") && std::string(getenv("SVB200_JIT_MODE")) == "db";
+  return db;
+}
+
+std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, std::vector<std::pair<int, int>>* cf_refs,
+                            std::vector<std::pair<int, int>>* tab_refs) {
+  const FPassArgs& A = prog.passes[pass];
+  Gen g;
+  std::ostringstream& o = g.o;
+  std::ostringstream body;
+  for (int ph = 0; ph < A.n_phases; ++ph) {
+    const FPhase& F = prog.phases[A.phase_begin + ph];
+    int W[4];
+    for (int k = 0; k < 4; ++k) W[k] = swz_h(1 << F.reg[k]);
+    o << "  {   // phase " << ph << "\n";
+    o << "    FDEV_PHASE_LOAD(s_ph[" << ph << "], " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ")\n";
+    for (int oi = F.op_begin; oi < F.op_end; ++oi)
+      if (!emit_op(g, oi - A.op_begin, prog.ops[oi])) return std::string();
+    o << "    FDEV_PHASE_STORE(" << int(F.flip) << ", " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ")\n";
+    o << "  }\n";
+  }
+  const size_t ncf = std::max<size_t>(g.cf_refs.size(), 1);
+  // kernel parameter space: 32764 bytes (sm_70+, CUDA 12.1+); the fixed arguments use < 1 KiB
+  if (ncf * sizeof(double2) + sizeof(void*) * 5 + 1024 > 32000) return std::string();
+  std::ostringstream k;
+  k << "struct SvCf { double2 v[" << ncf << "]; };\n";
+  k << "extern \"C\" __global__ void __launch_bounds__(256, " << (db ? 1 : 2) << ")\n";
+  k << "svb200_pass(double2* __restrict__ state, double2* __restrict__ state_hi, const fdev::DPass P,\n"
+       "            const fdev::DPhase* __restrict__ phases, const double2* __restrict__ tabs,\n"
+       "            double2* __restrict__ gen_partials, const SvCf cf) {\n";
+  k << "  fdev::run_pass<" << (two ? "true" : "false") << ", " << (db ? "true" : "false")
+    << ">(state, state_hi, P, phases, gen_partials,\n"
+       "      [&](double2* __restrict__ tile, const fdev::DPhase* __restrict__ s_ph, const u64 base,\n"
+       "          double2* __restrict__ acc_warp) {\n";
+  k << "  (void)acc_warp; (void)tabs;\n";
+  k << o.str();
+  k << "  });\n}\n";
+  if (cf_refs) *cf_refs = g.cf_refs;
+  if (tab_refs) *tab_refs = g.tab_refs;
+  return k.str();
+}
+
+// Compile (or find) the kernels of every pass of a program; fills prog.jit (nullptr = interpreter).
+void jit_prepare(Program& prog, bool two) {
+  if (prog.jit_ready && prog.jit_two == two) return;
+  prog.jit.assign(prog.passes.size(), JitPass());
+  prog.jit_tabs.clear();
+  prog.jit_ready = true;
+  prog.jit_two = two;
+  if (!jit_enabled()) return;
+  std::vector<std::shared_ptr<JitKernel>> todo;
+  for (size_t p = 0; p < prog.passes.size(); ++p) {
+    JitPass& jp = prog.jit[p];
+    std::string src = jit_pass_source(prog, int(p), two, jit_db(), &jp.cf_refs, &jp.tab_refs);
+    if (src.empty()) continue;
+    std::lock_guard<std::mutex> lk(g_jit_mu);
+    auto it = g_jit.find(src);
+    if (it == g_jit.end()) {
+      auto k = std::make_shared<JitKernel>();
+      k->src = src;
+      it = g_jit.emplace(src, k).first;
+      todo.push_back(k);
+    }
+    jp.kernel = it->second;
+  }
+  if (const char* dump = getenv("SVB200_JIT_DUMP")) {   // debugging: write the generated sources
+    for (size_t i = 0; i < todo.size(); ++i) {
+      const std::string fn = std::string(dump) + "/pass_" + std::to_string(g_jit_compiled.load() + int64_t(i)) + ".cu";
+      if (FILE* f = std::fopen(fn.c_str(), "w")) {
+        std::fputs(kDevSrc, f);
+        std::fputs(todo[i]->src.c_str(), f);
+        std::fclose(f);
+      }
+    }
+  }
+  if (!todo.empty()) {
+    // distinct pass structures compile in parallel (NVRTC programs are independent)
+    const int nth = std::max(1, std::min<int>(int(todo.size()), int(std::thread::hardware_concurrency())));
+    std::atomic<size_t> next{0};
+    std::vector<std::thread> ths;
+    for (int t = 0; t < nth; ++t)
+      ths.emplace_back([&]() {
+        for (size_t i = next++; i < todo.size(); i = next++) compile_kernel(*todo[i]);
+      });
+    for (auto& th : ths) th.join();
+    for (auto& k : todo)
+      if (!k->ok) {
+        std::lock_guard<std::mutex> lk(g_jit_mu);
+        g_jit.erase(k->src);
+        sv_fail(SV_ERR_DEVICE, "pass compiler (NVRTC) failed:\n" + k->log.substr(0, 4000));
+      }
+  }
+  // per-pass parameter blocks and the device table layout (values are fixed per program)
+  for (size_t p = 0; p < prog.passes.size(); ++p) {
+    JitPass& jp = prog.jit[p];
+    if (!jp.kernel) continue;
+    const FPassArgs& A = prog.passes[p];
+    jp.cf.assign(std::max<size_t>(jp.cf_refs.size(), 1), make_double2(0.0, 0.0));
+    for (size_t r = 0; r < jp.cf_refs.size(); ++r)
+      jp.cf[r] = prog.ops[A.op_begin + jp.cf_refs[r].first].c[jp.cf_refs[r].second];
+    jp.tab_base = int(prog.jit_tabs.size());
+    for (const auto& tr : jp.tab_refs) {
+      const FOp& op = prog.ops[A.op_begin + tr.first];
+      for (int j = 0; j < tr.second; ++j) prog.jit_tabs.push_back(prog.coef[op.tab + j]);
+    }
+  }
+}
+
+bool jit_launch(const JitPass& jp, int device, unsigned grid, int threads, size_t smem, cudaStream_t st, double2* state,
+                double2* state_hi, const void* dpass, const void* phases, const double2* tabs, double2* gen) {
+  JitKernel& k = *jp.kernel;
+  {
+    std::lock_guard<std::mutex> lk(k.mu);
+    if (!k.lib) {
+      CUDA_CHECK(cudaLibraryLoadData(&k.lib, k.cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0));
+      CUDA_CHECK(cudaLibraryGetKernel(&k.kern, k.lib, "svb200_pass"));
+    }
+    if (device < 0 || device >= 64) sv_fail(SV_ERR_DEVICE, "device ordinal out of range");
+    if (k.smem_set[device] < int(smem)) {
+      CUDA_CHECK(cudaFuncSetAttribute(reinterpret_cast<const void*>(k.kern),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      k.smem_set[device] = int(smem);
+    }
+  }
+  const double2* tb = tabs + jp.tab_base;
+  void* args[] = {&state, &state_hi, const_cast<void*>(dpass), const_cast<void**>(&phases),
+                  const_cast<const double2**>(&tb), &gen, const_cast<double2*>(jp.cf.data())};
+  CUDA_CHECK(cudaLaunchKernel(reinterpret_cast<const void*>(k.kern), dim3(grid), dim3(threads), args, smem, st));
+  return true;
+}
+
+void jit_stats(int64_t* compiled, int64_t* compile_us, int64_t* cached) {
+  *compiled = g_jit_compiled.load();
+  *compile_us = g_jit_compile_us.load();
+  std::lock_guard<std::mutex> lk(g_jit_mu);
+  *cached = int64_t(g_jit.size());
+}
+
+}  // namespace fused

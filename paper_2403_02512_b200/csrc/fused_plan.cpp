@@ -115,6 +115,7 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
   int F = 0;   // uniform flips (applied here, on the host)
   int D = 0;   // register bits that may carry a per-thread flip (handled by the kernel)
   static const bool shear_on = !(getenv("SVB200_SHEAR") && std::string(getenv("SVB200_SHEAR")) == "0");
+  const bool stable = jit_enabled();
   const int op_first = int(prog.ops.size());
   // A thread-predicated X is not an op of its own: it rides on the next op of the phase (the
   // kernel toggles the flip before that op), saving one dispatch; only a second X arriving
@@ -333,7 +334,9 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
       const bool rx = op.mtype == MT_RXLIKE;
       const bool rot = rx ? (m[0] == m[3] && m[1] == m[2]) : (m[0] == m[3] && m[1] == -m[2]);
       double c = m[0].real(), sn = rx ? -m[1].imag() : m[2].real();
-      if (rot && (c >= 0.0 || op.pm == 0)) {
+      // the runtime pass compiler keys kernels on structure, so there the choice may not depend on
+      // the angle: conditioned rotations always keep the 2x2 form
+      if (rot && (op.pm == 0 || (c >= 0.0 && !stable))) {
         if (c < 0.0) {   // R(phi) = -R(phi -+ pi): the sign is global for an unconditioned op
           c = -c;
           sn = -sn;
@@ -365,10 +368,19 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
     push_op(op);
   }
   if (pend) prog.ops.push_back(pend_op);
-  if (neg) {
+  // value-independent structure (runtime pass compiler): the sign is always "absorbed", +1 or -1
+  const bool any_shear = [&]() {
+    for (int oi = op_first; oi < int(prog.ops.size()); ++oi)
+      if (prog.ops[oi].pm == 0 && prog.ops[oi].cs >= CS_SHEAR && prog.ops[oi].cs < CS_SHEAR + 16) return true;
+    return false;
+  }();
+  if (neg || (stable && any_shear)) {
     // absorb the owed -1 into an unconditioned 2x2 / scalar op of the phase, else turn one
     // unconditioned shear back into its 2x2 form carrying the sign
+    const double sg = neg ? -1.0 : 1.0;
+    neg = 1;
     auto negate = [&](FOp& o, int nc) {
+      if (sg > 0) return;
       for (int j = 0; j < nc; ++j) {
         o.c[j] = make_double2(-o.c[j].x, -o.c[j].y);
         prog.coef[o.tab + j] = o.c[j];
@@ -401,6 +413,8 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
         mm = {cplx(-c, 0), cplx(0, sn), cplx(0, sn), cplx(-c, 0)};      // -[[c, -is], [-is, c]]
       else
         mm = {cplx(-c, 0), cplx(sn, 0), cplx(-sn, 0), cplx(-c, 0)};     // -[[c, -s], [s, c]]
+      if (sg > 0)
+        for (auto& z : mm) z = -z;
       o.tab = int(prog.coef.size());
       for (int j = 0; j < 4; ++j) {
         prog.coef.push_back(make_double2(mm[j].real(), mm[j].imag()));
@@ -734,6 +748,23 @@ void plan_program_serialized(int n_qubits, const std::vector<Prim>& prims, std::
                              std::vector<double>& dbls) {
   const fused::Program prog = fused::build_program(n_qubits, prims, true);
   fused::serialize_program(prog, n_qubits, ints, dbls);
+}
+
+// Host-only: plan, then compile every pass with the runtime pass compiler (no GPU needed: NVRTC
+// emits sm_100a cubins; they are loaded on first launch).  out4 = {passes, passes with a generated
+// kernel, kernels compiled so far in this process, their total compile time in microseconds}.
+void plan_compile(int nl, const std::vector<Prim>& prims, bool two, int64_t* out4) {
+  using namespace fused;
+  Program prog = build_program(nl, prims, true, two);
+  jit_prepare(prog, two);
+  int64_t with = 0;
+  for (const JitPass& jp : prog.jit) with += jp.kernel ? 1 : 0;
+  int64_t compiled = 0, us = 0, cached = 0;
+  jit_stats(&compiled, &us, &cached);
+  out4[0] = int64_t(prog.passes.size());
+  out4[1] = with;
+  out4[2] = compiled;
+  out4[3] = us;
 }
 
 PlanStats plan_stats(int nl, const std::vector<Prim>& prims) {

@@ -198,5 +198,6 @@ struct PlanStats {
   int64_t passes = 0, ops = 0, tile_bits = 0, phases = 0;
 };
 PlanStats plan_stats(int nl, const std::vector<Prim>& prims);
+void plan_compile(int nl, const std::vector<Prim>& prims, bool two, int64_t* out4);
 
 inline int popcount64(u64 x) { return __builtin_popcountll(x); }

@@ -224,3 +224,14 @@ def plan_summary(n_qubits, ops):
     out = (c_int64 * 4)()
     _lib.check(_lib.lib().sv_plan_summary(int(n_qubits), packed.ptr, packed.n, out))
     return {"passes": out[0], "ops": out[1], "tile_bits": out[2], "phases": out[3]}
+
+
+def plan_compile(n_qubits, ops, two_array=False):
+    """Host-only: plan the op list and compile every fused pass into its own sm_100a kernel with
+    the runtime pass compiler (NVRTC; no GPU needed).  Returns {passes, compiled_passes,
+    kernels_compiled_total, compile_s_total} (the last two are process-wide counters)."""
+    packed = _lib.PackedOps(ops)
+    out = (c_int64 * 4)()
+    _lib.check(_lib.lib().sv_plan_compile(int(n_qubits), packed.ptr, packed.n, int(bool(two_array)), out))
+    return {"passes": out[0], "compiled_passes": out[1], "kernels_compiled_total": out[2],
+            "compile_s_total": out[3] * 1e-6}
