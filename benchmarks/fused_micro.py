@@ -19,10 +19,13 @@ from paper_2403_02512_b200.ops import Op  # noqa: E402
 
 
 def timeit(dev, ops, reps=5):
+    # reset before every apply: the canonical layout plans (and compiles) one program for all reps
+    dev.reset()
     dev.apply(ops)
     dev.reset_stats()
     dev.set_profiling(True)
     for _ in range(reps):
+        dev.reset()
         dev.apply(ops)
     st = dev.kernel_stats()
     dev.set_profiling(False)

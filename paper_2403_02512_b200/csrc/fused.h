@@ -92,6 +92,7 @@ struct FPassArgs {
   int n_gen;             // GEN slots used by this pass
   int gen_base;          // first global result slot of this pass
   int n_gen_total;       // result slots of the whole program (row length of the partials)
+  int direct = 0;        // last phase's lane bits = the tile bits stored to physical 0..2
 };
 
 // One step of a planned program: a fused pass (index into Program::passes) or a single
@@ -113,6 +114,7 @@ struct Program {
                                    // ... i.e. the qubit at p moved to perm[p]
   std::vector<int> gen_slot_of;    // program result slot -> Prim::slot (the caller's Jacobian slot)
   int64_t n_prims_in = 0, n_prims_merged = 0;
+  int owed_neg = 0;                // global -1 owed by rotations emitted as -R(phi') (planner only)
   // runtime pass compiler (fused_jit.cpp): per-pass kernels and their parameter blocks
   bool jit_ready = false, jit_two = false;
   std::vector<JitPass> jit;

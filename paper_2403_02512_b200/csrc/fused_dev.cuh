@@ -258,7 +258,10 @@ struct DPass {
 //   DB = false: 2 CTAs per SM, one tile buffer each (the two CTAs overlap each other);
 //   DB = true : 1 CTA per SM, two tile buffers: tile t + grid streams in while tile t is computed.
 // Dynamic shared memory: [tile buffer(s)] [phase records] [generator accumulators].
-template <bool TWO, bool DB, class Body>
+//   DIRECT (single buffer, one array): the body's last phase stores its registers straight to HBM
+//   and calls next_load() once it has read the tile, so the next tile streams into the buffer while
+//   the last phase computes; the loop itself then has no store.
+template <bool TWO, bool DB, bool DIRECT, class Body>
 __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* __restrict__ state_hi, const DPass& P,
                                          const DPhase* __restrict__ phases, double2* __restrict__ gen_partials,
                                          Body body) {
@@ -316,6 +319,22 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     asm volatile("cp.async.commit_group;\n" ::);
   };
   int cur = 0;
+  if (DIRECT) {
+    for (u64 t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+      const u64 nbase = ((base | ~P.outer) + P.grid_step) & P.outer;
+      if (t == blockIdx.x) {
+        __syncthreads();   // phase records staged
+        issue_load(base, tile);
+      }
+      asm volatile("cp.async.wait_all;\n" ::);
+      __syncthreads();
+      const bool more = t + gridDim.x < P.n_tiles;
+      body(tile, s_ph, base, acc_warp, [&]() {
+        if (more) issue_load(nbase, tile);
+      });
+      base = nbase;
+    }
+  } else {
   if (DB && blockIdx.x < P.n_tiles) {
     __syncthreads();   // phase records staged
     issue_load(base, tile);
@@ -331,7 +350,7 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     __syncthreads();
     // DB: the other buffer's previous tile was fully read by the store loop before this barrier
     if (DB && t + gridDim.x < P.n_tiles) issue_load(nbase, tile + (cur ^ 1) * T);
-    body(tl, s_ph, base, acc_warp);   // every phase, each ending with __syncthreads()
+    body(tl, s_ph, base, acc_warp, []() {});   // every phase, each ending with __syncthreads()
     {
       double2 *p_lo, *p_hi;
       slot_ptrs(base | st_tid, p_lo, p_hi);
@@ -341,6 +360,7 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     }
     base = nbase;
     cur ^= 1;
+  }
   }
   if (P.n_gen) {
     __syncthreads();
@@ -375,5 +395,19 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
       tile[sf ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)] = a[r]; \
   }                                                                                                             \
   __syncthreads();
+
+// last phase of a DIRECT pass: after reading the tile into registers (barrier: every warp has
+// read it), start the next tile's load, compute, then store each register to HBM at
+// gb | WOFF(r ^ fl) (gb = tile base | the thread's store bits, WOFF(r) = register r's store bits)
+#define FDEV_PHASE_STORE_GLOBAL(FLIP, O0, O1, O2, O3)                                                            \
+  {                                                                                                             \
+    const int fl = (FLIP) ^ fthr;                                                                               \
+    const u64 wf = ((fl & 1) ? (O0) : 0ull) | ((fl & 2) ? (O1) : 0ull) | ((fl & 4) ? (O2) : 0ull) |             \
+                   ((fl & 8) ? (O3) : 0ull);                                                                    \
+    double2* __restrict__ gp = state + (base | st_thr);                                                         \
+    _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r)                                                     \
+      __stcs(gp + ((((r & 1) ? (O0) : 0ull) | ((r & 2) ? (O1) : 0ull) | ((r & 4) ? (O2) : 0ull) |                \
+                   ((r & 8) ? (O3) : 0ull)) ^ wf), a[r]);                                                       \
+  }
 
 }  // namespace fdev

@@ -220,14 +220,16 @@ std::atomic<int64_t> g_jit_compile_us{0};
 
 void compile_kernel(JitKernel& k) {
   const auto t0 = std::chrono::steady_clock::now();
-  const std::string full = std::string(kDevSrc) + "\n" + k.src;
+  // configuration #defines lead the generated text; they must precede the shared header
+  const size_t cut = k.src.find("struct SvCf");
+  const std::string full = k.src.substr(0, cut) + std::string(kDevSrc) + "\n" + k.src.substr(cut);
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, full.c_str(), "svb200_pass.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     k.log = "nvrtcCreateProgram failed";
     return;
   }
-  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--restrict"};
-  const nvrtcResult r = nvrtcCompileProgram(prog, 4, opts);
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--std=c++17", "-lineinfo", "--restrict", "-default-device"};
+  const nvrtcResult r = nvrtcCompileProgram(prog, 5, opts);
   size_t ls = 0;
   nvrtcGetProgramLogSize(prog, &ls);
   if (ls > 1) {
@@ -260,21 +262,44 @@ bool jit_db() {
   return db;
 }
 
+// resident CTAs per SM of the single-buffer form (SVB200_JIT_CTAS, default 2)
+int jit_ctas_per_sm() {
+  static const int n = getenv("SVB200_JIT_CTAS") ? std::max(1, std::min(3, atoi(getenv("SVB200_JIT_CTAS")))) : 2;
+  return n;
+}
+
 std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, std::vector<std::pair<int, int>>* cf_refs,
                             std::vector<std::pair<int, int>>* tab_refs) {
   const FPassArgs& A = prog.passes[pass];
   Gen g;
   std::ostringstream& o = g.o;
   std::ostringstream body;
+  static const bool direct_on = !(getenv("SVB200_JIT_DIRECT") && std::string(getenv("SVB200_JIT_DIRECT")) == "0");
+  const bool direct = direct_on && A.direct && !two && !db && A.n_phases > 0;
+  if (direct) {
+    // the thread's physical store bits in the last phase (its lane bits land on physical 0..2)
+    const FPhase& L = prog.phases[A.phase_begin + A.n_phases - 1];
+    o << "  u64 st_thr = 0;\n";
+    for (int j = 0; j < A.nthr; ++j)
+      o << "  if ((threadIdx.x >> " << j << ") & 1) st_thr |= " << hex64(1ull << A.tpos_st[L.thr[j]]) << ";\n";
+  }
   for (int ph = 0; ph < A.n_phases; ++ph) {
     const FPhase& F = prog.phases[A.phase_begin + ph];
+    const bool last_direct = direct && ph == A.n_phases - 1;
     int W[4];
     for (int k = 0; k < 4; ++k) W[k] = swz_h(1 << F.reg[k]);
-    o << "  {   // phase " << ph << "\n";
+    o << "  {   // phase " << ph << (last_direct ? " (direct store)" : "") << "\n";
     o << "    FDEV_PHASE_LOAD(s_ph[" << ph << "], " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ")\n";
+    if (last_direct) o << "    __syncthreads();\n    next_load();\n";
     for (int oi = F.op_begin; oi < F.op_end; ++oi)
       if (!emit_op(g, oi - A.op_begin, prog.ops[oi])) return std::string();
-    o << "    FDEV_PHASE_STORE(" << int(F.flip) << ", " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ")\n";
+    if (last_direct) {
+      o << "    FDEV_PHASE_STORE_GLOBAL(" << int(F.flip);
+      for (int k = 0; k < 4; ++k) o << ", " << hex64(1ull << A.tpos_st[F.reg[k]]);
+      o << ")\n";
+    } else {
+      o << "    FDEV_PHASE_STORE(" << int(F.flip) << ", " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ")\n";
+    }
     o << "  }\n";
   }
   const size_t ncf = std::max<size_t>(g.cf_refs.size(), 1);
@@ -282,15 +307,16 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
   if (ncf * sizeof(double2) + sizeof(void*) * 5 + 1024 > 32000) return std::string();
   std::ostringstream k;
   k << "struct SvCf { double2 v[" << ncf << "]; };\n";
-  k << "extern \"C\" __global__ void __launch_bounds__(256, " << (db ? 1 : 2) << ")\n";
+  k << "extern \"C\" __global__ void __launch_bounds__(256, " << (db ? 1 : jit_ctas_per_sm()) << ")\n";
   k << "svb200_pass(double2* __restrict__ state, double2* __restrict__ state_hi, const fdev::DPass P,\n"
        "            const fdev::DPhase* __restrict__ phases, const double2* __restrict__ tabs,\n"
        "            double2* __restrict__ gen_partials, const SvCf cf) {\n";
-  k << "  fdev::run_pass<" << (two ? "true" : "false") << ", " << (db ? "true" : "false")
+  k << "  fdev::run_pass<" << (two ? "true" : "false") << ", " << (db ? "true" : "false") << ", "
+    << (direct ? "true" : "false")
     << ">(state, state_hi, P, phases, gen_partials,\n"
        "      [&](double2* __restrict__ tile, const fdev::DPhase* __restrict__ s_ph, const u64 base,\n"
-       "          double2* __restrict__ acc_warp) {\n";
-  k << "  (void)acc_warp; (void)tabs;\n";
+       "          double2* __restrict__ acc_warp, auto next_load) {\n";
+  k << "  (void)acc_warp; (void)tabs; (void)next_load;\n";
   k << o.str();
   k << "  });\n}\n";
   if (cf_refs) *cf_refs = g.cf_refs;

@@ -25,7 +25,8 @@ struct JitPass {
 
 // generated source of one pass (empty: not expressible, e.g. parameter block too large)
 bool jit_enabled();   // SVB200_JIT != 0: passes run as generated kernels (planner keeps structure value-free)
-bool jit_db();   // generated kernels use the double-buffered 1-CTA-per-SM tile loop
+bool jit_db();
+int jit_ctas_per_sm();   // generated kernels use the double-buffered 1-CTA-per-SM tile loop
 std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, std::vector<std::pair<int, int>>* cf_refs,
                             std::vector<std::pair<int, int>>* tab_refs);
 // compile / look up every pass kernel of prog (no-op when already prepared); throws SvError on failure

@@ -368,63 +368,63 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
     push_op(op);
   }
   if (pend) prog.ops.push_back(pend_op);
-  // value-independent structure (runtime pass compiler): the sign is always "absorbed", +1 or -1
-  const bool any_shear = [&]() {
-    for (int oi = op_first; oi < int(prog.ops.size()); ++oi)
-      if (prog.ops[oi].pm == 0 && prog.ops[oi].cs >= CS_SHEAR && prog.ops[oi].cs < CS_SHEAR + 16) return true;
-    return false;
-  }();
-  if (neg || (stable && any_shear)) {
-    // absorb the owed -1 into an unconditioned 2x2 / scalar op of the phase, else turn one
-    // unconditioned shear back into its 2x2 form carrying the sign
-    const double sg = neg ? -1.0 : 1.0;
-    neg = 1;
-    auto negate = [&](FOp& o, int nc) {
-      if (sg > 0) return;
-      for (int j = 0; j < nc; ++j) {
-        o.c[j] = make_double2(-o.c[j].x, -o.c[j].y);
-        prog.coef[o.tab + j] = o.c[j];
-      }
-    };
-    int conv = -1;
-    for (int oi = int(prog.ops.size()) - 1; oi >= op_first && neg; --oi) {
-      FOp& o = prog.ops[oi];
-      if (o.pm != 0) continue;
-      const bool pair1 = (o.cs >= CS_PAIR1 && o.cs < CS_PAIR1 + 16) || (o.cs >= CS_PAIR1D && o.cs < CS_PAIR1D + 16);
-      if (pair1) {
-        negate(o, 4);
-        neg = 0;
-      } else if (o.cs == CS_SCALAR) {
-        negate(o, 1);
-        neg = 0;
-      } else if (conv < 0 && o.cs >= CS_SHEAR && o.cs < CS_SHEAR + 16) {
-        conv = oi;
-      }
-    }
-    if (neg) {
-      if (conv < 0) sv_fail(SV_ERR_DEVICE, "internal: unabsorbed rotation sign");
-      FOp& o = prog.ops[conv];
-      const double c = o.c[1].x, sn = o.c[2].x;
-      const bool rx = o.c[2].y != 0.0;
-      const int k = (o.cs - CS_SHEAR) / 4;
-      const bool dyn = ((D >> k) & 1) != 0;
-      std::array<cplx, 4> mm;
-      if (rx)
-        mm = {cplx(-c, 0), cplx(0, sn), cplx(0, sn), cplx(-c, 0)};      // -[[c, -is], [-is, c]]
-      else
-        mm = {cplx(-c, 0), cplx(sn, 0), cplx(-sn, 0), cplx(-c, 0)};     // -[[c, -s], [s, c]]
-      if (sg > 0)
-        for (auto& z : mm) z = -z;
-      o.tab = int(prog.coef.size());
-      for (int j = 0; j < 4; ++j) {
-        prog.coef.push_back(make_double2(mm[j].real(), mm[j].imag()));
-        o.c[j] = prog.coef.back();
-      }
-      o.mtype = uint8_t(rx ? MT_RXLIKE : MT_REAL);
-      o.cs = (dyn ? CS_PAIR1D : CS_PAIR1) + k * 4 + o.mtype;
-    }
-  }
+  prog.owed_neg ^= neg;   // resolved once per program (absorb_rotation_signs)
   return F;
+}
+
+// Unconditioned rotations emitted as -R(phi') leave the state owing a global factor -1 per such
+// rotation.  A global sign commutes with everything (and cancels in every psi/lambda bra-ket, both
+// halves carry it), so the program's net sign is absorbed ONCE, into the coefficients of any
+// unconditioned 2x2 / scalar op of the program; only a program without one turns its last
+// unconditioned shear back into a 2x2 carrying the sign.  With the runtime pass compiler the
+// choice must not depend on the angles (kernels are keyed on structure), so the conversion then
+// happens whether the owed sign is +1 or -1.
+void absorb_rotation_signs(Program& prog, bool stable) {
+  const double sg = prog.owed_neg ? -1.0 : 1.0;
+  auto absorber = [](const FOp& o) {
+    if (o.pm != 0) return false;
+    if (o.cs == CS_SCALAR) return true;
+    const bool p1 = (o.cs >= CS_PAIR1 && o.cs < CS_PAIR1 + 16) || (o.cs >= CS_PAIR1D && o.cs < CS_PAIR1D + 16);
+    return p1 && o.mtype != MT_X && (o.cs % 4) != 3;
+  };
+  for (FOp& o : prog.ops)
+    if (absorber(o)) {
+      if (sg < 0) {
+        const int nc = o.cs == CS_SCALAR ? 1 : 4;
+        for (int j = 0; j < nc; ++j) {
+          o.c[j] = make_double2(-o.c[j].x, -o.c[j].y);
+          prog.coef[o.tab + j] = o.c[j];
+        }
+      }
+      prog.owed_neg = 0;
+      return;
+    }
+  if (!(sg < 0 || stable)) return;
+  for (int oi = int(prog.ops.size()) - 1; oi >= 0; --oi) {
+    FOp& o = prog.ops[oi];
+    if (o.pm != 0 || o.cs < CS_SHEAR || o.cs >= CS_SHEAR + 16) continue;
+    const double c = o.c[1].x, sn = o.c[2].x;
+    const bool rx = o.c[2].y != 0.0;
+    const int k = (o.cs - CS_SHEAR) / 4;
+    // RX-type 2x2s are symmetric under a per-thread flip of their bit; RY-type ones on a flipped
+    // bit (SH_RYD) need the *D form
+    const bool dyn = (o.cs - CS_SHEAR) % 4 == SH_RYD;
+    std::array<cplx, 4> mm;
+    if (rx)
+      mm = {cplx(c, 0), cplx(0, -sn), cplx(0, -sn), cplx(c, 0)};     // [[c, -is], [-is, c]]
+    else
+      mm = {cplx(c, 0), cplx(-sn, 0), cplx(sn, 0), cplx(c, 0)};      // [[c, -s], [s, c]]
+    o.tab = int(prog.coef.size());
+    for (int j = 0; j < 4; ++j) {
+      prog.coef.push_back(make_double2(sg * mm[j].real(), sg * mm[j].imag()));
+      o.c[j] = prog.coef.back();
+    }
+    o.mtype = uint8_t(rx ? MT_RXLIKE : MT_REAL);
+    o.cs = (dyn ? CS_PAIR1D : CS_PAIR1) + k * 4 + o.mtype;
+    prog.owed_neg = 0;
+    return;
+  }
+  if (sg < 0) sv_fail(SV_ERR_DEVICE, "internal: unabsorbed rotation sign");
 }
 
 // Can prim i be folded into prim j (j runs right before i on every bit i touches)?
@@ -651,6 +651,34 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
     int qi = 0;
     for (int t : q_low) A.q[qi++] = (unsigned char)t;
     for (int t : q_rest) A.q[qi++] = (unsigned char)t;
+    // Direct store: when the tile positions that land on physical bits 0..2 are thread bits of
+    // the last phase (and carry none of its predicates), make them its lane bits.  Each 8-lane
+    // group then holds one 128-byte run, so the generated kernel stores the last phase's registers
+    // straight to HBM (no shared-memory round trip) and refills the tile buffer with the next
+    // tile while the last phase computes (fused_jit.cpp).
+    A.direct = 0;
+    if (A.n_phases > 0 && q_low.size() == 3) {
+      FPhase& L = prog.phases[A.phase_begin + A.n_phases - 1];
+      bool ok = true;
+      u64 lowld = 0;
+      for (int t : q_low) {
+        lowld |= 1ull << A.tpos[t];
+        for (int k = 0; k < kRB; ++k) ok &= L.reg[k] != t;
+      }
+      for (int oi = L.op_begin; oi < L.op_end && ok; ++oi) {
+        const FOp& o = prog.ops[oi];
+        if ((o.pm | o.fpm | o.xm) & lowld) ok = false;
+        for (int j = 0; j < o.nt; ++j)
+          if (o.treg[j] == 0xFF && ((lowld >> o.tphys[j]) & 1)) ok = false;
+      }
+      if (ok) {
+        std::vector<int> thr(q_low.begin(), q_low.end());
+        for (int j = 0; j < b - kRB; ++j)
+          if (std::find(q_low.begin(), q_low.end(), int(L.thr[j])) == q_low.end()) thr.push_back(L.thr[j]);
+        for (int j = 0; j < b - kRB; ++j) L.thr[j] = uint8_t(thr[j]);
+        A.direct = 1;
+      }
+    }
     bool moved = false;
     for (int p = 0; p < nl; ++p) moved |= sigma[p] != p;
     if (moved) {
@@ -667,6 +695,7 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
   }
   prog.perm = perm_total;
   for (auto& A : prog.passes) A.n_gen_total = int(prog.gen_slot_of.size());
+  absorb_rotation_signs(prog, jit_enabled());
   return prog;
 }
 
