@@ -8,6 +8,7 @@
 // Z-like in both or X-like in both -- so RZ slides past CNOT controls and RX past CNOT targets.
 #include <algorithm>
 #include <array>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -651,9 +652,10 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
     int qi = 0;
     for (int t : q_low) A.q[qi++] = (unsigned char)t;
     for (int t : q_rest) A.q[qi++] = (unsigned char)t;
-    // Direct store: when the tile positions that land on physical bits 0..2 are thread bits of
-    // the last phase (and carry none of its predicates), make them its lane bits.  Each 8-lane
-    // group then holds one 128-byte run, so the generated kernel stores the last phase's registers
+    // Direct store: the tile positions that land on physical bits 0..2 become the last phase's
+    // lane bits (those that are not its register bits; none may carry one of its predicates, which
+    // would split warps).  An 8-lane group then holds one 128-byte run (or a run split over two
+    // registers), so the generated kernel stores the last phase's registers
     // straight to HBM (no shared-memory round trip) and refills the tile buffer with the next
     // tile while the last phase computes (fused_jit.cpp).
     A.direct = 0;
@@ -661,9 +663,12 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
       FPhase& L = prog.phases[A.phase_begin + A.n_phases - 1];
       bool ok = true;
       u64 lowld = 0;
+      std::vector<int> lanes;   // q_low positions that are thread bits of the last phase
       for (int t : q_low) {
         lowld |= 1ull << A.tpos[t];
-        for (int k = 0; k < kRB; ++k) ok &= L.reg[k] != t;
+        bool reg = false;
+        for (int k = 0; k < kRB; ++k) reg |= L.reg[k] == t;
+        if (!reg) lanes.push_back(t);
       }
       for (int oi = L.op_begin; oi < L.op_end && ok; ++oi) {
         const FOp& o = prog.ops[oi];
@@ -672,9 +677,11 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
           if (o.treg[j] == 0xFF && ((lowld >> o.tphys[j]) & 1)) ok = false;
       }
       if (ok) {
-        std::vector<int> thr(q_low.begin(), q_low.end());
+        // a low store bit held in a register splits the thread's 128-byte run over two stores of
+        // full 32-byte sectors (still merged in L2); lanes carry the others
+        std::vector<int> thr(lanes.begin(), lanes.end());
         for (int j = 0; j < b - kRB; ++j)
-          if (std::find(q_low.begin(), q_low.end(), int(L.thr[j])) == q_low.end()) thr.push_back(L.thr[j]);
+          if (std::find(lanes.begin(), lanes.end(), int(L.thr[j])) == lanes.end()) thr.push_back(L.thr[j]);
         for (int j = 0; j < b - kRB; ++j) L.thr[j] = uint8_t(thr[j]);
         A.direct = 1;
       }
