@@ -36,7 +36,7 @@ def make_device(n, dist):
     return Device.sharded(n, rank, world, nid[0], device=local)
 
 
-def gpu_time(n, ops, obs, fuse, reps=2, dist=None):
+def gpu_time(n, ops, obs, fuse, reps=3, dist=None):
     with make_device(n, dist) as d:
         d.adjoint_jacobian(ops, obs, fuse=fuse)      # warm-up (plans, allocations)
         ts = []

@@ -410,4 +410,18 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
                    ((r & 8) ? (O3) : 0ull)) ^ wf), a[r]);                                                       \
   }
 
+// ... two-array state (adjoint sweep): indices carrying the selector bit P.hi live in state_hi
+#define FDEV_PHASE_STORE_GLOBAL2(FLIP, O0, O1, O2, O3)                                                           \
+  {                                                                                                             \
+    const int fl = (FLIP) ^ fthr;                                                                               \
+    const u64 wf = ((fl & 1) ? (O0) : 0ull) | ((fl & 2) ? (O1) : 0ull) | ((fl & 4) ? (O2) : 0ull) |             \
+                   ((fl & 8) ? (O3) : 0ull);                                                                    \
+    const u64 gb = base | st_thr;                                                                               \
+    _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r) {                                                   \
+      const u64 g = gb | ((((r & 1) ? (O0) : 0ull) | ((r & 2) ? (O1) : 0ull) | ((r & 4) ? (O2) : 0ull) |          \
+                          ((r & 8) ? (O3) : 0ull)) ^ wf);                                                        \
+      __stcs(((g & P.hi) ? state_hi : state) + (g & ~P.hi), a[r]);                                             \
+    }                                                                                                           \
+  }
+
 }  // namespace fdev

@@ -275,7 +275,7 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
   std::ostringstream& o = g.o;
   std::ostringstream body;
   static const bool direct_on = !(getenv("SVB200_JIT_DIRECT") && std::string(getenv("SVB200_JIT_DIRECT")) == "0");
-  const bool direct = direct_on && A.direct && !two && !db && A.n_phases > 0;
+  const bool direct = direct_on && A.direct && !db && A.n_phases > 0;
   if (direct) {
     // the thread's physical store bits in the last phase (its lane bits land on physical 0..2)
     const FPhase& L = prog.phases[A.phase_begin + A.n_phases - 1];
@@ -294,7 +294,7 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
     for (int oi = F.op_begin; oi < F.op_end; ++oi)
       if (!emit_op(g, oi - A.op_begin, prog.ops[oi])) return std::string();
     if (last_direct) {
-      o << "    FDEV_PHASE_STORE_GLOBAL(" << int(F.flip);
+      o << "    FDEV_PHASE_STORE_GLOBAL" << (two ? "2(" : "(") << int(F.flip);
       for (int k = 0; k < 4; ++k) o << ", " << hex64(1ull << A.tpos_st[F.reg[k]]);
       o << ")\n";
     } else {
