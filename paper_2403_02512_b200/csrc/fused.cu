@@ -642,7 +642,8 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
   });
   const int b = prog.passes[0].b;
   const bool jdb = !db && jit_db();   // generated kernels in their double-buffered 1-CTA/SM form
-  const u64 grid = std::min<u64>(prog.passes[0].n_tiles, u64(sms_dev[h->device]) * ((db || jdb) ? 1 : (jit_enabled() ? jit_ctas_per_sm() : 2)));   // persistent grid
+  const u64 grid = std::min<u64>(prog.passes[0].n_tiles, u64(sms_dev[h->device]) * ((db || jdb) ? 1 : (jit_enabled() ? jit_ctas_per_sm() : 2)) *
+                                                    (u64(1) << (kMaxB - std::min(kMaxB, prog.passes[0].b))));   // persistent grid
 
   // launch records + upload phases | ops | coef in one copy (the buffer is only reused after a sync)
   std::vector<DPhase> dph(prog.phases.size());

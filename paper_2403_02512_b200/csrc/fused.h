@@ -123,6 +123,7 @@ struct Program {
 
 // remap = let passes relabel qubits inside their tile (moves upcoming qubits onto the low bits)
 // pin_top = never relabel bit nl-1 (the psi/lambda selector of the adjoint sweep's two arrays)
+int tile_bits();   // tile bits of a fused pass (default kMaxB)
 Program build_program(int nl, const std::vector<Prim>& prims, bool remap, bool pin_top = false);
 // flat int64/double serialisation of a program (tests/fused_emulator.py re-executes it on the CPU)
 void serialize_program(const Program& prog, int nl, std::vector<int64_t>& ints, std::vector<double>& dbls);

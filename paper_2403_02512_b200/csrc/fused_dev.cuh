@@ -320,6 +320,10 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
   };
   int cur = 0;
   if (DIRECT) {
+#ifdef FDEV_STAGGER_NS
+    // the two CTAs sharing an SM would otherwise run in lockstep (load together, compute together)
+    if (FDEV_STAGGER_SEL) __nanosleep(FDEV_STAGGER_NS);
+#endif
     for (u64 t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
       const u64 nbase = ((base | ~P.outer) + P.grid_step) & P.outer;
       if (t == blockIdx.x) {

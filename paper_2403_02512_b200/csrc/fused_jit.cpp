@@ -306,6 +306,14 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
   // kernel parameter space: 32764 bytes (sm_70+, CUDA 12.1+); the fixed arguments use < 1 KiB
   if (ncf * sizeof(double2) + sizeof(void*) * 5 + 1024 > 32000) return std::string();
   std::ostringstream k;
+  if (const char* st = getenv("SVB200_JIT_STAGGER")) {   // experiment: "ns,sel" (sel 0: upper half of the grid, 1: odd CTAs)
+    int ns = 0, sel = 0;
+    std::sscanf(st, "%d,%d", &ns, &sel);
+    if (ns > 0) {
+      k << "#define FDEV_STAGGER_NS " << ns << "\n";
+      k << "#define FDEV_STAGGER_SEL " << (sel ? "(blockIdx.x & 1)" : "(blockIdx.x >= gridDim.x / 2)") << "\n";
+    }
+  }
   k << "struct SvCf { double2 v[" << ncf << "]; };\n";
   k << "extern \"C\" __global__ void __launch_bounds__(256, " << (db ? 1 : jit_ctas_per_sm()) << ")\n";
   k << "svb200_pass(double2* __restrict__ state, double2* __restrict__ state_hi, const fdev::DPass P,\n"

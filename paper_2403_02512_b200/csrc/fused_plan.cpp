@@ -17,6 +17,18 @@
 #include "prim_util.h"
 
 namespace fused {
+
+// tile bits of a pass (2^b amplitudes staged per CTA); SVB200_TILE_BITS (9..12) for experiments
+// physical bits every tile contains (2^LB-amplitude contiguous runs); SVB200_LOW_BITS (2..3)
+int low_bits() {
+  static const int lb = getenv("SVB200_LOW_BITS") ? std::max(2, std::min(3, atoi(getenv("SVB200_LOW_BITS")))) : 3;
+  return lb;
+}
+
+int tile_bits() {
+  static const int b = getenv("SVB200_TILE_BITS") ? std::max(9, std::min(kMaxB, atoi(getenv("SVB200_TILE_BITS")))) : kMaxB;
+  return b;
+}
 namespace {
 
 // planner view of a primitive: commutation classes (prim_util.h) + fusability
@@ -504,12 +516,40 @@ std::vector<std::pair<u64, std::vector<int>>> schedule_phases(std::vector<Prim>&
           if ((rq[i].support >> b) & 1) last_on[b] = i;
       }
       if (progress) continue;
-      int pick = -1;
-      for (int i = 0; i < L; ++i)
-        if (!done[i] && npred[i] == 0 && popcount64(R | rq[i].dense) <= kRB) {
+      // stuck: widen the register set by the ready op whose bits unlock the most work in this
+      // phase (simulated: ops that become runnable, transitively), first ready op on ties
+      static const bool greedy = getenv("SVB200_PHASE_GREEDY") && std::string(getenv("SVB200_PHASE_GREEDY")) == "1";
+      int pick = -1, best = -1;
+      std::vector<int> np2;
+      std::vector<char> dn2;
+      for (int i = 0; i < L; ++i) {
+        if (done[i] || npred[i] != 0 || popcount64(R | rq[i].dense) > kRB) continue;
+        if (greedy) {
           pick = i;
           break;
         }
+        const u64 R2 = R | rq[i].dense;
+        np2 = npred;
+        dn2 = done;
+        int gain = 0;
+        for (bool again = true; again;) {
+          again = false;
+          for (int j = 0; j < L; ++j) {
+            if (dn2[j] || np2[j] != 0 || (rq[j].dense & ~R2) != 0) continue;
+            dn2[j] = 1;
+            ++gain;
+            for (int s2 : succ[j]) np2[s2]--;
+            again = true;
+          }
+        }
+        // prefer more unlocked work per new register bit
+        const int cost = popcount64(rq[i].dense & ~R);
+        const int score = cost ? gain * 4 / cost : gain * 16;
+        if (score > best) {
+          best = score;
+          pick = i;
+        }
+      }
       if (pick < 0) break;
       R |= rq[pick].dense;
     }
@@ -524,8 +564,9 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
   Program prog;
   std::vector<Prim> P = prims_in;
   prog.n_prims_in = int64_t(P.size());
-  const int b = std::min(kMaxB, nl);
-  const u64 low = (1ull << std::min(3, nl)) - 1;
+  const int b = std::min(tile_bits(), nl);
+  const int LB = std::min(low_bits(), nl);   // physical bits every tile contains (contiguous runs)
+  const u64 low = (1ull << LB) - 1;
   std::vector<int> perm_total(nl);
   for (int p = 0; p < nl; ++p) perm_total[p] = p;
   std::vector<Req> req(P.size());
@@ -613,7 +654,7 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
     // ---- in-tile relabeling: bring the qubits the next gates target onto physical bits 0..2 ----
     int sigma[64];
     for (int p = 0; p < 64; ++p) sigma[p] = p;
-    if (remap && !rest.empty() && b > 3) {
+    if (remap && !rest.empty() && b > LB) {
       int next_use[64];
       for (int p = 0; p < 64; ++p) next_use[p] = 1 << 30;
       for (size_t k = 0; k < rest.size(); ++k) {
@@ -631,12 +672,12 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
         if (next_use[x] != next_use[y]) return next_use[x] < next_use[y];
         return x < y;
       });
-      std::vector<int> want(cand.begin(), cand.begin() + 3);   // physical positions to move onto 0..2
+      std::vector<int> want(cand.begin(), cand.begin() + LB);   // physical positions to move onto 0..LB-1
       std::vector<int> out_low, in_high;
-      for (int l = 0; l < 3; ++l)
+      for (int l = 0; l < LB; ++l)
         if (std::find(want.begin(), want.end(), l) == want.end()) out_low.push_back(l);
       for (int x : want)
-        if (x >= 3) in_high.push_back(x);
+        if (x >= LB) in_high.push_back(x);
       for (size_t s = 0; s < in_high.size(); ++s) {   // swap(out_low[s], in_high[s])
         sigma[in_high[s]] = out_low[s];
         sigma[out_low[s]] = in_high[s];
@@ -645,7 +686,7 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
     std::vector<int> q_low, q_rest;
     for (int t = 0; t < b; ++t) {
       A.tpos_st[t] = (unsigned char)sigma[A.tpos[t]];
-      if (A.tpos_st[t] < 3) q_low.push_back(t);
+      if (A.tpos_st[t] < LB) q_low.push_back(t);
       else q_rest.push_back(t);
     }
     std::sort(q_low.begin(), q_low.end(), [&](int x, int y) { return A.tpos_st[x] < A.tpos_st[y]; });
@@ -659,7 +700,7 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
     // straight to HBM (no shared-memory round trip) and refills the tile buffer with the next
     // tile while the last phase computes (fused_jit.cpp).
     A.direct = 0;
-    if (A.n_phases > 0 && q_low.size() == 3) {
+    if (A.n_phases > 0 && int(q_low.size()) == LB) {
       FPhase& L = prog.phases[A.phase_begin + A.n_phases - 1];
       bool ok = true;
       u64 lowld = 0;
@@ -813,7 +854,7 @@ PlanStats plan_stats(int nl, const std::vector<Prim>& prims) {
   }
   Program prog = build_program(nl, prims, true);
   s.passes = int64_t(prog.steps.size());
-  s.tile_bits = std::min(kMaxB, nl);
+  s.tile_bits = std::min(tile_bits(), nl);
   s.phases = int64_t(prog.phases.size());
   return s;
 }
