@@ -55,6 +55,21 @@ def main():
         "2 phases, 32 RX": [Op("RX", ((low + mid)[i % 6],), (0.1 * i,)) for i in range(32)],
         "3 phases, 32 RX": [Op("RX", ((low + mid + [n - 7, n - 8, n - 9])[i % 9],), (0.1 * i,)) for i in range(32)],
     }
+    # unmergeable rotation streams: RX on 4 low qubits, then CZs (diagonal) between them, so no two
+    # rotations on a qubit are adjacent (no merging); k rounds -> 4k shears + 4k parity phases, 1 phase
+    def stream(rounds, qs):
+        ops = []
+        for r in range(rounds):
+            for i, q in enumerate(qs):
+                ops.append(Op("RX" if (r + i) % 2 else "RY", (q,), (0.1 + 0.01 * r + 0.001 * i,)))
+            for i in range(len(qs)):
+                ops.append(Op("CZ", (qs[i], qs[(i + 1) % len(qs)])))
+        return ops
+    four = [n - 1, n - 2, n - 3, n - 4]
+    cases["stream 8 rounds (32 shears + 32 CZ), 1 phase"] = stream(8, four)
+    cases["stream 16 rounds (64 shears + 64 CZ), 1 phase"] = stream(16, four)
+    cases["stream 32 rounds (128 shears + 128 CZ), 1 phase"] = stream(32, four)
+    cases["stream 16 rounds on 8 qubits (2+ phases)"] = stream(8, four + [n - 5, n - 6, n - 7, n - 8])
     out = {}
     with Device(n) as d:
         for name, ops in cases.items():

@@ -704,7 +704,7 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
       const JitPass* jp = (!db && s.index < int(prog.jit.size()) && prog.jit[s.index].kernel) ? &prog.jit[s.index] : nullptr;
       if (jp) {
         // generated kernel of this pass: [tile] [phase records] [generator accumulators]
-        const size_t jsmem = (jdb ? 2 : 1) * (size_t(1) << b) * sizeof(double2) + size_t(D.n_phases) * sizeof(DPhase) +
+        const size_t jsmem = (jdb ? 4 : (jp->split ? 3 : 2)) * (size_t(1) << (b - 1)) * sizeof(double2) + size_t(D.n_phases) * sizeof(DPhase) +
                              (A.n_gen ? size_t(threads / 32) * kMaxGens * sizeof(double2) : 0);
         jit_launch(*jp, h->device, g, threads, jsmem, st, state, state_hi, &D, ph, d_jt, d_gen);
       } else if (two) {

@@ -261,7 +261,11 @@ struct DPass {
 //   DIRECT (single buffer, one array): the body's last phase stores its registers straight to HBM
 //   and calls next_load() once it has read the tile, so the next tile streams into the buffer while
 //   the last phase computes; the loop itself then has no store.
-template <bool TWO, bool DB, bool DIRECT, class Body>
+//   SPLIT (with DIRECT): the tile lives in two half buffers (index bit b-1 selects the half) and a
+//   third half buffer rotates with the low one: the next tile's low half streams in during the
+//   whole of this tile's phases, its high half during the last phase (3 half tiles = 96 KiB per
+//   CTA, two CTAs per SM).
+template <bool TWO, bool DB, bool DIRECT, class Body, bool SPLIT = false>
 __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* __restrict__ state_hi, const DPass& P,
                                          const DPhase* __restrict__ phases, double2* __restrict__ gen_partials,
                                          Body body) {
@@ -270,7 +274,7 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
   const int tid = threadIdx.x;
   const int nthreads = blockDim.x;
   const int T = 1 << P.b;
-  DPhase* s_ph = reinterpret_cast<DPhase*>(smem_raw + size_t(DB ? 2 : 1) * T * sizeof(double2));
+  DPhase* s_ph = reinterpret_cast<DPhase*>(smem_raw + size_t(DB ? 4 : (SPLIT ? 3 : 2)) * (T >> 1) * sizeof(double2));
   double2* s_gen = reinterpret_cast<double2*>(s_ph + P.n_phases);
   {
     const int4* src = reinterpret_cast<const int4*>(phases);
@@ -319,7 +323,43 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     asm volatile("cp.async.commit_group;\n" ::);
   };
   int cur = 0;
-  if (DIRECT) {
+  if (SPLIT) {
+    const int HB = T >> 1;
+    auto issue_half = [&](u64 b0, double2* buf, int h) {
+      double2 *p_lo, *p_hi;
+      slot_ptrs(b0 | ld_tid, p_lo, p_hi);
+      const unsigned sb = (unsigned)__cvta_generic_to_shared(buf);
+#pragma unroll
+      for (int i = 8 * h; i < 8 * h + 8; ++i) {   // slot bit 3 is tile index bit b-1
+        const double2* src = (TWO && ((P.ld_hsel >> i) & 1) ? p_hi : p_lo) + P.ld_off[i];
+        const unsigned dst = sb + unsigned((ld_sw ^ P.ld_sm[i]) & (HB - 1)) * 16u;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+      }
+      asm volatile("cp.async.commit_group;\n" ::);
+    };
+    double2* lo_cur = tile;
+    double2* lo_spare = tile + HB;
+    double2* hi_buf = tile + 2 * HB;
+    for (u64 t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+      const u64 nbase = ((base | ~P.outer) + P.grid_step) & P.outer;
+      if (t == blockIdx.x) {
+        __syncthreads();   // phase records staged
+        issue_half(base, lo_cur, 0);
+        issue_half(base, hi_buf, 1);
+      }
+      asm volatile("cp.async.wait_all;\n" ::);
+      __syncthreads();
+      const bool more = t + gridDim.x < P.n_tiles;
+      if (more) issue_half(nbase, lo_spare, 0);   // its last readers passed the barrier above
+      body(lo_cur, hi_buf, s_ph, base, acc_warp, [&]() {
+        if (more) issue_half(nbase, hi_buf, 1);
+      });
+      double2* tmp = lo_cur;
+      lo_cur = lo_spare;
+      lo_spare = tmp;
+      base = nbase;
+    }
+  } else if (DIRECT) {
 #ifdef FDEV_STAGGER_NS
     // the two CTAs sharing an SM would otherwise run in lockstep (load together, compute together)
     if (FDEV_STAGGER_SEL) __nanosleep(FDEV_STAGGER_NS);
@@ -333,7 +373,7 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
       asm volatile("cp.async.wait_all;\n" ::);
       __syncthreads();
       const bool more = t + gridDim.x < P.n_tiles;
-      body(tile, s_ph, base, acc_warp, [&]() {
+      body(tile, tile + (T >> 1), s_ph, base, acc_warp, [&]() {
         if (more) issue_load(nbase, tile);
       });
       base = nbase;
@@ -354,7 +394,7 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     __syncthreads();
     // DB: the other buffer's previous tile was fully read by the store loop before this barrier
     if (DB && t + gridDim.x < P.n_tiles) issue_load(nbase, tile + (cur ^ 1) * T);
-    body(tl, s_ph, base, acc_warp, []() {});   // every phase, each ending with __syncthreads()
+    body(tl, tl + (T >> 1), s_ph, base, acc_warp, []() {});   // every phase, each ending with __syncthreads()
     {
       double2 *p_lo, *p_hi;
       slot_ptrs(base | st_tid, p_lo, p_hi);
@@ -382,12 +422,18 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
 
 // phase entry / exit for generated kernels: registers <- tile (offsets s0 ^ W(r)), and the store
 // honouring the phase's uniform flip and the thread's dynamic flips
+// tile element i (swizzled index): one buffer, or two half buffers selected by index bit b-1
+#ifdef FDEV_SPLIT
+#define FDEV_TILE(i) ((((i) & FDEV_HB) ? tile_hi : tile)[(i) & (FDEV_HB - 1)])
+#else
+#define FDEV_TILE(i) tile[i]
+#endif
 #define FDEV_PHASE_LOAD(F, W0, W1, W2, W3)                                                                       \
   const int s0 = (F).s_lo[threadIdx.x & 15] ^ (F).s_hi[threadIdx.x >> 4];                                      \
   const u64 pb = base | (F).g_lo[threadIdx.x & 15] | (F).g_hi[threadIdx.x >> 4];                                \
   double2 a[fdev::kRegs];                                                                                       \
   _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r) a[r] =                                                \
-      tile[s0 ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)];     \
+      FDEV_TILE(s0 ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)); \
   int fthr = 0;                                                                                                 \
   (void)pb;                                                                                                     \
   (void)fthr;
@@ -396,7 +442,7 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     const int fl = (FLIP) ^ fthr;                                                                               \
     const int sf = s0 ^ ((fl & 1) ? (W0) : 0) ^ ((fl & 2) ? (W1) : 0) ^ ((fl & 4) ? (W2) : 0) ^ ((fl & 8) ? (W3) : 0); \
     _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r)                                                     \
-      tile[sf ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)] = a[r]; \
+      FDEV_TILE(sf ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)) = a[r]; \
   }                                                                                                             \
   __syncthreads();
 

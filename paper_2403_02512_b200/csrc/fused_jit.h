@@ -21,6 +21,7 @@ struct JitPass {
   std::vector<std::pair<int, int>> tab_refs;    // device tables in order: (pass-local op, length)
   std::vector<double2> cf;                      // the parameter block
   int tab_base = 0;                             // first entry in Program::jit_tabs
+  bool split = false;                           // tile in 3 rotating half buffers (1.5 tiles of smem)
 };
 
 // generated source of one pass (empty: not expressible, e.g. parameter block too large)
