@@ -437,6 +437,17 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
   int fthr = 0;                                                                                                 \
   (void)pb;                                                                                                     \
   (void)fthr;
+// ... with the thread's slot offset and physical bits given as expressions (generated kernels
+// compute them from threadIdx.x with literal masks instead of loading the phase's nibble tables)
+#define FDEV_PHASE_LOAD_X(S0, PB, W0, W1, W2, W3)                                                                \
+  const int s0 = (S0);                                                                                          \
+  const u64 pb = base | (PB);                                                                                   \
+  double2 a[fdev::kRegs];                                                                                       \
+  _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r) a[r] =                                                \
+      FDEV_TILE(s0 ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)); \
+  int fthr = 0;                                                                                                 \
+  (void)pb;                                                                                                     \
+  (void)fthr;
 #define FDEV_PHASE_STORE(FLIP, W0, W1, W2, W3)                                                                   \
   {                                                                                                             \
     const int fl = (FLIP) ^ fthr;                                                                               \

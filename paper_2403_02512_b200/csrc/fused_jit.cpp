@@ -293,7 +293,20 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
     int W[4];
     for (int k = 0; k < 4; ++k) W[k] = swz_h(1 << F.reg[k]);
     o << "  {   // phase " << ph << (last_direct ? " (direct store)" : "") << "\n";
-    o << "    FDEV_PHASE_LOAD(s_ph[" << ph << "], " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ")\n";
+    static const bool tab_thr = getenv("SVB200_JIT_THRTAB") && std::string(getenv("SVB200_JIT_THRTAB")) == "1";
+    if (tab_thr) {
+      o << "    FDEV_PHASE_LOAD(s_ph[" << ph << "], " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ")\n";
+    } else {
+      // the thread's slot: swizzled offset and physical bits as literal-mask expressions of tid
+      std::string se = "0", pe = "0ull";
+      for (int j = 0; j < A.nthr; ++j) {
+        const std::string bit = "((threadIdx.x >> " + std::to_string(j) + ") & 1)";
+        se += " ^ (" + bit + " ? " + std::to_string(swz_h(1 << F.thr[j])) + " : 0)";
+        pe += " | (" + bit + " ? " + hex64(1ull << A.tpos[F.thr[j]]) + " : 0ull)";
+      }
+      o << "    FDEV_PHASE_LOAD_X(" << se << ", " << pe << ", " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3]
+        << ")\n";
+    }
     if (last_direct) o << "    __syncthreads();\n    next_load();\n";
     for (int oi = F.op_begin; oi < F.op_end; ++oi)
       if (!emit_op(g, oi - A.op_begin, prog.ops[oi])) return std::string();
