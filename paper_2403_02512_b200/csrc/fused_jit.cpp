@@ -218,11 +218,79 @@ std::map<std::string, std::shared_ptr<JitKernel>> g_jit;
 std::atomic<int64_t> g_jit_compiled{0};
 std::atomic<int64_t> g_jit_compile_us{0};
 
+// On-disk cubin cache shared by the processes of one machine (tests, smoke, bench): the file name
+// is a 64-bit FNV-1a hash of the full source + compiler version + options, and the file stores the
+// full source too, so a hash collision is detected and ignored.  SVB200_JIT_CACHE=<dir> (default
+// $TMPDIR/svb200_jit); "0" disables.
+const char* kOptsKey = "sm_100a|c++17|lineinfo|restrict|default-device";
+
+std::string cache_dir() {
+  const char* e = getenv("SVB200_JIT_CACHE");
+  if (e && std::string(e) == "0") return std::string();
+  if (e && *e) return e;
+  const char* t = getenv("TMPDIR");
+  return std::string(t && *t ? t : "/tmp") + "/svb200_jit";
+}
+
+u64 fnv1a(const std::string& s) {
+  u64 h = 1469598103934665603ull;
+  for (unsigned char c : s) {
+    h ^= c;
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
+bool cache_load(const std::string& path, const std::string& full, std::vector<char>& cubin) {
+  FILE* f = std::fopen(path.c_str(), "rb");
+  if (!f) return false;
+  uint64_t ns = 0, nc = 0;
+  bool ok = std::fread(&ns, 8, 1, f) == 1 && ns == full.size();
+  std::string src;
+  if (ok) {
+    src.resize(ns);
+    ok = std::fread(&src[0], 1, ns, f) == ns && src == full && std::fread(&nc, 8, 1, f) == 1 && nc > 0 &&
+         nc < (uint64_t(1) << 30);
+  }
+  if (ok) {
+    cubin.resize(nc);
+    ok = std::fread(cubin.data(), 1, nc, f) == nc;
+  }
+  std::fclose(f);
+  return ok;
+}
+
+void cache_store(const std::string& dir, const std::string& path, const std::string& full,
+                 const std::vector<char>& cubin) {
+  std::string mk = "mkdir -p '" + dir + "' 2>/dev/null";
+  if (std::system(mk.c_str()) != 0) return;
+  const std::string tmp = path + ".tmp" + std::to_string(uintptr_t(&cubin));
+  FILE* f = std::fopen(tmp.c_str(), "wb");
+  if (!f) return;
+  const uint64_t ns = full.size(), nc = cubin.size();
+  bool ok = std::fwrite(&ns, 8, 1, f) == 1 && std::fwrite(full.data(), 1, ns, f) == ns &&
+            std::fwrite(&nc, 8, 1, f) == 1 && std::fwrite(cubin.data(), 1, nc, f) == nc;
+  ok = (std::fclose(f) == 0) && ok;
+  if (ok) std::rename(tmp.c_str(), path.c_str());   // atomic publish
+  else std::remove(tmp.c_str());
+}
+
 void compile_kernel(JitKernel& k) {
   const auto t0 = std::chrono::steady_clock::now();
   // configuration #defines lead the generated text; they must precede the shared header
   const size_t cut = k.src.find("struct SvCf");
   const std::string full = k.src.substr(0, cut) + std::string(kDevSrc) + "\n" + k.src.substr(cut);
+  int major = 0, minor = 0;
+  nvrtcVersion(&major, &minor);
+  const std::string keyed = full + "\n//" + kOptsKey + "|nvrtc" + std::to_string(major) + "." + std::to_string(minor);
+  const std::string dir = cache_dir();
+  char hb[32];
+  std::snprintf(hb, sizeof(hb), "%016llx", fnv1a(keyed));
+  const std::string path = dir.empty() ? std::string() : dir + "/" + hb + ".svc";
+  if (!path.empty() && cache_load(path, keyed, k.cubin)) {
+    k.ok = true;
+    return;
+  }
   nvrtcProgram prog;
   if (nvrtcCreateProgram(&prog, full.c_str(), "svb200_pass.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
     k.log = "nvrtcCreateProgram failed";
@@ -244,6 +312,7 @@ void compile_kernel(JitKernel& k) {
     k.ok = n > 0;
   }
   nvrtcDestroyProgram(&prog);
+  if (k.ok && !path.empty()) cache_store(dir, path, keyed, k.cubin);
   g_jit_compiled += 1;
   g_jit_compile_us += std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count();
 }
