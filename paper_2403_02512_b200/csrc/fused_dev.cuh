@@ -457,6 +457,11 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
   }                                                                                                             \
   __syncthreads();
 
+#ifdef FDEV_PLAIN_STORE
+#define FDEV_STG(p, v) (*(p) = (v))
+#else
+#define FDEV_STG(p, v) __stcs((p), (v))   // streaming: the state is not re-read before eviction
+#endif
 // last phase of a DIRECT pass: after reading the tile into registers (barrier: every warp has
 // read it), start the next tile's load, compute, then store each register to HBM at
 // gb | WOFF(r ^ fl) (gb = tile base | the thread's store bits, WOFF(r) = register r's store bits)
@@ -467,8 +472,8 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
                    ((fl & 8) ? (O3) : 0ull);                                                                    \
     double2* __restrict__ gp = state + (base | st_thr);                                                         \
     _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r)                                                     \
-      __stcs(gp + ((((r & 1) ? (O0) : 0ull) | ((r & 2) ? (O1) : 0ull) | ((r & 4) ? (O2) : 0ull) |                \
-                   ((r & 8) ? (O3) : 0ull)) ^ wf), a[r]);                                                       \
+      FDEV_STG(gp + ((((r & 1) ? (O0) : 0ull) | ((r & 2) ? (O1) : 0ull) | ((r & 4) ? (O2) : 0ull) |              \
+                     ((r & 8) ? (O3) : 0ull)) ^ wf), a[r]);                                                     \
   }
 
 // ... two-array state (adjoint sweep): indices carrying the selector bit P.hi live in state_hi
@@ -481,7 +486,7 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r) {                                                   \
       const u64 g = gb | ((((r & 1) ? (O0) : 0ull) | ((r & 2) ? (O1) : 0ull) | ((r & 4) ? (O2) : 0ull) |          \
                           ((r & 8) ? (O3) : 0ull)) ^ wf);                                                        \
-      __stcs(((g & P.hi) ? state_hi : state) + (g & ~P.hi), a[r]);                                             \
+      FDEV_STG(((g & P.hi) ? state_hi : state) + (g & ~P.hi), a[r]);                                           \
     }                                                                                                           \
   }
 

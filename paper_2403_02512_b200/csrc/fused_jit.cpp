@@ -401,6 +401,8 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
     }
   }
   if (split) k << "#define FDEV_SPLIT 1\n#define FDEV_HB " << (1 << (A.b - 1)) << "\n";
+  static const bool plain_st = getenv("SVB200_JIT_STCS") && std::string(getenv("SVB200_JIT_STCS")) == "0";
+  if (plain_st) k << "#define FDEV_PLAIN_STORE 1\n";
   k << "struct SvCf { double2 v[" << ncf << "]; };\n";
   k << "extern \"C\" __global__ void __launch_bounds__(256, " << (db ? 1 : jit_ctas_per_sm()) << ")\n";
   k << "svb200_pass(double2* __restrict__ state, double2* __restrict__ state_hi, const fdev::DPass P,\n"

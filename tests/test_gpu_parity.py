@@ -451,3 +451,56 @@ def test_h2_vqe_energy_and_gradient():
     e, g = batched_expval_and_grad(c.ops, h2, n_workers=3, n_qubits=4)
     assert abs(e - evref[0]) < 1e-12 and np.abs(g - jref[0]).max() < 1e-12
     assert abs(e - (-1.1361894540)) < 2e-3
+
+
+def test_generated_kernels_reused_across_parameters():
+    """Pass compiler (csrc/fused_jit.cpp): a circuit re-run with new angles reuses the compiled
+    pass kernels (values travel as kernel parameters) and both runs match the oracle."""
+    from paper_2403_02512_b200.device import plan_compile
+    from paper_2403_02512_b200.ops import Op as _Op
+    n = 14
+    a = workloads.random_circuit(n, 10, seed=11)
+    b = [_Op(op.name, op.wires, tuple(p + 0.37 for p in op.params), op.ctrls, op.ctrl_values) for op in a]
+    probe = [_Op("H", (0,))]
+    with Device(n) as d:
+        d.apply(a)
+        got_a = d.get_state()
+        before = plan_compile(8, probe)["kernels_compiled_total"]
+        d.reset()
+        d.apply(b)
+        got_b = d.get_state()
+        after = plan_compile(8, probe)["kernels_compiled_total"]
+    assert np.abs(got_a - O.run_circuit(n, a)).max() < STATE_TOL
+    assert np.abs(got_b - O.run_circuit(n, b)).max() < STATE_TOL
+    assert after - before <= 1, (before, after)   # at most the probe's own pass
+
+
+def test_interpreter_kernel_matches_oracle_subprocess():
+    """SVB200_JIT=0 keeps the prebuilt op-interpreting tile kernel (k_fused) as the fused engine;
+    it must stay at parity too (run in a child process: the switch is read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np\n"
+        "from oracle import svoracle as O\n"
+        "from paper_2403_02512_b200 import workloads\n"
+        "from paper_2403_02512_b200.device import Device\n"
+        "n = 16\n"
+        "ops = workloads.random_circuit(n, 12, seed=5)\n"
+        "ops2, obs = workloads.sel_config(10, 2, seed=1)\n"
+        "with Device(n) as d:\n"
+        "    d.apply(ops)\n"
+        "    err = float(np.abs(d.get_state() - O.run_circuit(n, ops)).max())\n"
+        "with Device(10) as d:\n"
+        "    jac = d.adjoint_jacobian(ops2, obs)\n"
+        "ref = O.adjoint_jacobian(10, ops2, obs)[0]\n"
+        "errj = float(np.abs(jac - ref).max())\n"
+        "assert err < 1e-12 and errj < 1e-10, (err, errj)\n"
+        "print('ok', err, errj)\n"
+    )
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, SVB200_JIT="0", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert r.stdout.startswith("ok")
