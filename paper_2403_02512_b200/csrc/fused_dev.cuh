@@ -210,6 +210,31 @@ __device__ __forceinline__ void gen_diag_tab(const double2 (&a)[kRegs], const do
   }
 }
 
+// diagonal generator whose table is a parity table (1 on even-parity indices, d on odd: Z, Z..Z):
+// sum_r conj(lambda_r) g psi_r = S_even + d S_odd -- no table loads, no complex product per amplitude.
+// M = register bits carrying table bits, tp = parity of the table's off-register bits and flips.
+template <int T, int M>
+__device__ __forceinline__ void gen_parity(const double2 (&a)[kRegs], const double2 d, int tp, int cm, int cv,
+                                           double& re, double& im) {
+  double er = 0.0, ei = 0.0, orr = 0.0, oi = 0.0;   // register parity 0 / 1 sums
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if ((r >> T) & 1) continue;
+    if ((r & cm) != cv) continue;
+    if (__popc(r & M) & 1) cacc_conj(orr, oi, a[r | (1 << T)], a[r]);
+    else cacc_conj(er, ei, a[r | (1 << T)], a[r]);
+  }
+  if (tp) {   // the thread's off-register parity swaps the roles
+    double t0 = er, t1 = ei;
+    er = orr;
+    ei = oi;
+    orr = t0;
+    oi = t1;
+  }
+  re += er + (d.x * orr - d.y * oi);
+  im += ei + (d.x * oi + d.y * orr);
+}
+
 // warp-reduce one bra-ket and add it to this warp's shared accumulator (every lane calls)
 __device__ __forceinline__ void gen_commit(double re, double im, double2* __restrict__ acc_warp, int slot) {
   for (int s = 16; s > 0; s >>= 1) {

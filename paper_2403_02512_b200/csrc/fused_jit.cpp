@@ -62,6 +62,7 @@ struct Gen {
   std::vector<std::pair<int, int>> tab_refs;  // (pass-local op, table length)
   int tab_len = 0;
 
+  // j = -1: entry 1 of the op's coefficient table (the odd-parity value of a parity table)
   std::string C(int op, int j) {
     cf_refs.push_back({op, j});
     return "cf.v[" + std::to_string(cf_refs.size() - 1) + "]";
@@ -91,7 +92,7 @@ std::string tconst_expr(const FOp& op, int W[4]) {
   return e;
 }
 
-bool emit_op(Gen& g, int i, const FOp& op) {
+bool emit_op(Gen& g, int i, const FOp& op, bool parity_tab) {
   std::ostringstream& o = g.o;
   const int cs = op.cs;
   o << "    {\n";
@@ -116,6 +117,16 @@ bool emit_op(Gen& g, int i, const FOp& op) {
       o << "        const int f = ((fthr >> " << k0 << ") & 1) | (((fthr >> " << k1 << ") & 1) << 1);\n";
       o << "        fdev::gen2<" << k0 << ", " << k1 << ", " << t << ">(a, " << g.T(i, 16) << ", " << cm << ", " << cvd
         << ", f, re, im);\n";
+    } else if (cs < CS_GEND + 4 && parity_tab) {
+      // parity table (Z / Z..Z generators): S_even + d S_odd, d from the parameter block
+      const int t = cs - CS_GEND;
+      int W[4];
+      const std::string tc = tconst_expr(op, W);
+      int M = 0;
+      for (int k = 0; k < 4; ++k)
+        if (W[k]) M |= 1 << k;
+      o << "        fdev::gen_parity<" << t << ", " << M << ">(a, " << g.C(i, -1) << ", __popc(" << tc << ") & 1, " << cm
+        << ", " << cvd << ", re, im);\n";
     } else if (cs < CS_GEND + 4) {
       const int t = cs - CS_GEND;
       int W[4];
@@ -377,8 +388,21 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
         << ")\n";
     }
     if (last_direct) o << "    __syncthreads();\n    next_load();\n";
-    for (int oi = F.op_begin; oi < F.op_end; ++oi)
-      if (!emit_op(g, oi - A.op_begin, prog.ops[oi])) return std::string();
+    for (int oi = F.op_begin; oi < F.op_end; ++oi) {
+      const FOp& op = prog.ops[oi];
+      bool ptab = false;
+      if (op.cs >= CS_GEND && op.cs < CS_GEND + 4 && op.nt >= 1) {
+        // the table's structure (parity form), not its values, decides the code: generators are
+        // fixed per gate kind, so this is stable across parameters
+        const double2* t = prog.coef.data() + op.tab;
+        ptab = t[0].x == 1.0 && t[0].y == 0.0;
+        for (int e = 0; e < (1 << op.nt) && ptab; ++e) {
+          const double2 want = (__builtin_popcount(e) & 1) ? t[1] : make_double2(1.0, 0.0);
+          ptab = t[e].x == want.x && t[e].y == want.y;
+        }
+      }
+      if (!emit_op(g, oi - A.op_begin, op, ptab)) return std::string();
+    }
     if (last_direct) {
       o << "    FDEV_PHASE_STORE_GLOBAL" << (two ? "2(" : "(") << int(F.flip);
       for (int k = 0; k < 4; ++k) o << ", " << hex64(1ull << A.tpos_st[F.reg[k]]);
@@ -480,8 +504,10 @@ void jit_prepare(Program& prog, bool two) {
     if (!jp.kernel) continue;
     const FPassArgs& A = prog.passes[p];
     jp.cf.assign(std::max<size_t>(jp.cf_refs.size(), 1), make_double2(0.0, 0.0));
-    for (size_t r = 0; r < jp.cf_refs.size(); ++r)
-      jp.cf[r] = prog.ops[A.op_begin + jp.cf_refs[r].first].c[jp.cf_refs[r].second];
+    for (size_t r = 0; r < jp.cf_refs.size(); ++r) {
+      const FOp& op = prog.ops[A.op_begin + jp.cf_refs[r].first];
+      jp.cf[r] = jp.cf_refs[r].second < 0 ? prog.coef[op.tab + 1] : op.c[jp.cf_refs[r].second];
+    }
     jp.tab_base = int(prog.jit_tabs.size());
     for (const auto& tr : jp.tab_refs) {
       const FOp& op = prog.ops[A.op_begin + tr.first];
