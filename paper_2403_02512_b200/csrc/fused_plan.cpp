@@ -581,24 +581,45 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
       remaining.erase(remaining.begin());
       continue;
     }
-    // ---- choose the pass: greedy over the dependency order ----
+    // ---- choose the pass: greedy over the dependency order, from several starting points ----
+    // Candidate s: the first s remaining prims may only join if they fit the bits chosen so far
+    // (the register set grows from prim s onward); the candidate taking the most prims wins
+    // (s = 0 is the plain greedy pass).
     u64 B = low;
-    Deferred def;
     std::vector<int> take, rest;
-    int ngen = 0;
-    for (size_t k = 0; k < remaining.size(); ++k) {
-      const int i = remaining[k];
-      const Req& r = req[i];
-      const bool gen = P[i].type == PRIM_GEN || P[i].type == PRIM_GEND;
-      bool ok = r.fusable && int(take.size()) < kMaxSmemOps && !def.blocks(r) && popcount64(B | r.dense) <= b &&
-                (!gen || ngen < kMaxGens);
-      if (ok) {
-        B |= r.dense;
-        take.push_back(i);
-        ngen += gen ? 1 : 0;
-      } else {
-        def.add(r);
-        rest.push_back(i);
+    {
+      static const int n_starts = getenv("SVB200_PASS_STARTS") ? std::max(1, atoi(getenv("SVB200_PASS_STARTS"))) : 48;
+      std::vector<size_t> starts = {0};
+      for (size_t k = 1; k < remaining.size() && int(starts.size()) < n_starts; ++k)
+        if (req[remaining[k]].dense & ~low) starts.push_back(k);
+      size_t best_taken = 0;
+      for (size_t s0 : starts) {
+        u64 Bc = low;
+        Deferred defc;
+        std::vector<int> tk, rs;
+        int ng = 0;
+        for (size_t k = 0; k < remaining.size(); ++k) {
+          const int i = remaining[k];
+          const Req& r = req[i];
+          const bool gen = P[i].type == PRIM_GEN || P[i].type == PRIM_GEND;
+          const bool grow_ok = k >= s0 ? popcount64(Bc | r.dense) <= b : (r.dense & ~Bc) == 0;
+          const bool ok = r.fusable && int(tk.size()) < kMaxSmemOps && !defc.blocks(r) && grow_ok &&
+                          (!gen || ng < kMaxGens);
+          if (ok) {
+            Bc |= r.dense;
+            tk.push_back(i);
+            ng += gen ? 1 : 0;
+          } else {
+            defc.add(r);
+            rs.push_back(i);
+          }
+        }
+        if (tk.size() > best_taken) {
+          best_taken = tk.size();
+          B = Bc;
+          take.swap(tk);
+          rest.swap(rs);
+        }
       }
     }
     for (int p = 0; p < nl && popcount64(B) < b; ++p) B |= 1ull << p;   // fill: longest contiguous runs
