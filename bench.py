@@ -279,6 +279,23 @@ def main():
                         "circuit's effective GB/s (value) is a multiple of the HBM peak"
                 if dom == "fused_tile" else None}
 
+    # the fused kernel also runs the circuit's FP64 arithmetic: its FP64 roofline beside the HBM one
+    # (flops counted from the planned op cases, csrc/fused_plan.cpp program_fp64_flops_per_amp;
+    # peak = 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz, the B200 vector FP64 rate)
+    if dom == "fused_tile" and st["ms"] > 0:
+        from paper_2403_02512_b200.device import plan_fp64_flops_per_amp
+        fpa = plan_fp64_flops_per_amp(n, ops)
+        flops = fpa * float(1 << (n - g)) * args.steps
+        fp_ach = flops / (st["ms"] / 1e3) / 1e12
+        fp_peak = 148 * 64 * 2 * 1.965e9 / 1e12
+        roofline["fp64"] = {"achieved": fp_ach, "peak": fp_peak, "unit": "TFLOP/s", "frac": fp_ach / fp_peak,
+                            "flops_per_amplitude": fpa,
+                            "peak_source": "B200 vector FP64: 148 SMs x 64 FMA/clk x 2 flop x 1.965 GHz (spec-derived)"}
+        roofline["note"] = ("svb200_pass (generated per-pass kernels) makes one HBM read+write per pass and runs many "
+                            "gates per pass; with 34 passes for 2225 gates it is bound by its FP64/shared-memory "
+                            "work, so the HBM frac is the lesser figure -- see roofline.fp64 and "
+                            "profiles/r1_ncu_jit_pass_v6.md")
+
     # global-qubit swaps (rank-0 view): NCCL send/recv of half a shard per swap over NVLink
     comm = None
     if world > 1 and "swap" in stats:

@@ -159,6 +159,9 @@ int sv_plan_summary(int n_qubits, const sv_op* ops, int n_ops, int64_t* out4);
  * sizes2 receives the needed int64 / double counts; buffers are filled when large enough. */
 int sv_plan_program(int n_qubits, const sv_op* ops, int n_ops, int64_t* ints, int64_t ints_cap, double* dbls,
                     int64_t dbls_cap, int64_t* sizes2);
+/* FP64 floating-point operations per state amplitude that the fused program of an op list performs
+ * (DFMA = 2), counted from its planned op cases; host-only (bench.py's FP64 roofline). */
+int sv_plan_fp64(int n_qubits, const sv_op* ops, int n_ops, double* flops_per_amp);
 /* Runtime pass compiler (host-only, no GPU needed): plan the op list and compile every fused pass
  * into its own sm_100a kernel with NVRTC (the kernels the device path launches; cached
  * process-wide by pass structure).  two_array = plan for the adjoint sweep's psi|lambda state.

@@ -1048,6 +1048,12 @@ int sv_plan_summary(int n_qubits, const sv_op* ops, int n_ops, int64_t* out4) {
   API_END
 }
 
+int sv_plan_fp64(int n_qubits, const sv_op* ops, int n_ops, double* flops_per_amp) {
+  API_BEGIN
+  *flops_per_amp = plan_stats(n_qubits, host_prims(n_qubits, ops, n_ops)).fp64_flops_per_amp;
+  API_END
+}
+
 int sv_plan_compile(int n_qubits, const sv_op* ops, int n_ops, int two_array, int64_t* out4) {
   API_BEGIN
   if (n_qubits < 5 || n_qubits > 62) sv_fail(SV_ERR_VALIDATION, "bad qubit count");

@@ -865,6 +865,34 @@ void plan_compile(int nl, const std::vector<Prim>& prims, bool two, int64_t* out
   out4[3] = us;
 }
 
+// FP64 floating-point operations the fused program performs per amplitude of the state (DFMA = 2,
+// DMUL / DADD = 1), counted from the op cases as the device code executes them on a thread's 16
+// amplitudes (register-pattern subsets scale the pair / group counts); for the roofline report.
+double program_fp64_flops_per_amp(const fused::Program& prog) {
+  using namespace fused;
+  double f = 0.0;   // per thread (16 amplitudes)
+  auto subset = [](int cm, int fixed) {   // fraction of register patterns an op's (cm, cv) selects
+    return 1.0 / double(1 << __builtin_popcount(cm & ~fixed & 15));
+  };
+  for (const FOp& o : prog.ops) {
+    const int cs = o.cs;
+    if (cs >= CS_SHEAR && cs < CS_SHEAR + 16) f += 8 * 6 * 2;
+    else if ((cs >= CS_PAIR1 && cs < CS_PAIR1 + 16) || (cs >= CS_PAIR1D && cs < CS_PAIR1D + 16))
+      f += o.mtype == MT_GENERAL ? 8 * 28 : (o.mtype == MT_X ? 0 : 8 * 12);
+    else if ((cs >= CS_PHASE1 && cs < CS_PHASE1 + 8) || (cs >= CS_PHASE1D && cs < CS_PHASE1D + 8)) f += 8 * 6;
+    else if (cs == CS_SCALAR) f += 16 * 6;
+    else if (cs >= CS_PARITY && cs < CS_PARITY + 16) f += 8 * 6;
+    else if (cs >= CS_PAIRGR && cs < CS_PAIRGR + 15) f += 16 * 12 / 2.0 * subset(o.cm, o.xr);
+    else if (cs >= CS_PAIRG && cs < CS_PAIRG + 15) f += 16 * 28 / 2.0 * subset(o.cm, o.xr);
+    else if (cs == CS_DIAGG) f += 16 * 6 * subset(o.cm, 0);
+    else if (cs >= CS_DENSE2 && cs < CS_DENSE2 + 6) f += 4 * 16 * 8 * subset(o.cm, 0);
+    else if (cs >= CS_GEN1 && cs < CS_GEN2) f += 4 * 2 * 24 + 20;
+    else if (cs >= CS_GEN2 && cs < CS_GEND) f += 2 * 4 * (16 * 8 + 8) + 20;
+    else if (cs >= CS_GEND && cs < CS_GEND + 4) f += 8 * 8 + 20;
+  }
+  return f / 16.0;
+}
+
 PlanStats plan_stats(int nl, const std::vector<Prim>& prims) {
   using namespace fused;
   PlanStats s;
@@ -877,5 +905,6 @@ PlanStats plan_stats(int nl, const std::vector<Prim>& prims) {
   s.passes = int64_t(prog.steps.size());
   s.tile_bits = std::min(tile_bits(), nl);
   s.phases = int64_t(prog.phases.size());
+  s.fp64_flops_per_amp = program_fp64_flops_per_amp(prog);
   return s;
 }

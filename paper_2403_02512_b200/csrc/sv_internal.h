@@ -196,6 +196,7 @@ void plan_program_serialized(int n_qubits, const std::vector<Prim>& prims, std::
 void release_fused(sv_handle* h);
 struct PlanStats {
   int64_t passes = 0, ops = 0, tile_bits = 0, phases = 0;
+  double fp64_flops_per_amp = 0.0;
 };
 PlanStats plan_stats(int nl, const std::vector<Prim>& prims);
 void plan_compile(int nl, const std::vector<Prim>& prims, bool two, int64_t* out4);

@@ -235,3 +235,11 @@ def plan_compile(n_qubits, ops, two_array=False):
     _lib.check(_lib.lib().sv_plan_compile(int(n_qubits), packed.ptr, packed.n, int(bool(two_array)), out))
     return {"passes": out[0], "compiled_passes": out[1], "kernels_compiled_total": out[2],
             "compile_s_total": out[3] * 1e-6}
+
+
+def plan_fp64_flops_per_amp(n_qubits, ops):
+    """Host-only: FP64 flops per amplitude the fused program of this op list performs."""
+    packed = _lib.PackedOps(ops)
+    out = ctypes.c_double()
+    _lib.check(_lib.lib().sv_plan_fp64(int(n_qubits), packed.ptr, packed.n, ctypes.byref(out)))
+    return out.value
