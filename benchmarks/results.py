@@ -5,6 +5,7 @@
 row 1: 20q SEL L=4 Jacobian (20 x 240): device s/Jacobian, max |d| vs the reference-backed golden
        (tests/golden/sel20_golden.npz), and the numpy oracle on one observable x 20 (labelled estimate)
 row 2: unfused gate kernels at 30 qubits on every target (RX, H, CNOT(q, q+1)): GB/s min/mean
+row 2f: the same for a complex64 ("f32") state at 31 qubits (also 16 GiB)
 row 3: 33q QAOA p=2 forward + <C> on one GPU (the 33q adjoint needs psi + lambda = 256 GiB: 2 GPUs,
        benchmarks/adjoint_bench.py under torchrun)
 row 5: 28q HEA (1000 trainable, 1000-term H): s per expval + gradient
@@ -53,10 +54,10 @@ def row1(cpu_seconds):
     return rec
 
 
-def row2():
-    n = 30
+def row2(precision="f64"):
+    n = 30 if precision == "f64" else 31
     out = {}
-    with Device(n, fuse=False) as d:
+    with Device(n, precision=precision, fuse=False) as d:
         for name, mk in (("RX", lambda q: Op("RX", (q,), (0.3,))), ("H", lambda q: Op("H", (q,))),
                          ("CNOT", lambda q: Op("CNOT", (q, (q + 1) % n)))):
             gbs = []
@@ -74,6 +75,8 @@ def row2():
                 gbs.append(by / (ms / 1e3) / 1e9)
             out[name] = {"min_GBps": min(gbs), "mean_GBps": float(np.mean(gbs)), "max_GBps": max(gbs),
                          "mean_frac_of_6551": float(np.mean(gbs)) / PEAK, "mean_frac_of_8000": float(np.mean(gbs)) / 8000}
+    if precision == "f32":
+        return {"row": "2f", "workload": "unfused single-gate kernels, complex64 at 31 qubits, every target", **out}
     return {"row": 2, "workload": "unfused single-gate kernels at 30 qubits, every target", **out}
 
 
@@ -119,7 +122,7 @@ def main():
     ap.add_argument("--rows", default="1,2,3,5")
     ap.add_argument("--cpu-seconds", type=float, default=20)
     a = ap.parse_args()
-    fns = {"1": lambda: row1(a.cpu_seconds), "2": row2, "3": row3, "5": row5}
+    fns = {"1": lambda: row1(a.cpu_seconds), "2": row2, "2f": lambda: row2("f32"), "3": row3, "5": row5}
     for r in a.rows.split(","):
         print(json.dumps(fns[r]()), flush=True)
 

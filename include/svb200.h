@@ -25,6 +25,8 @@
  *   sv_sample                      measurements.sample / sample_root
  *   sv_adjoint_jacobian            adjoint_jacobian
  *   sv_create_sharded              ShardedState / shard
+ *   sv_create_ex (precision 32)    StateVector(n, precision="f32")     state.py:20, 34-47
+ *   sv_set_state_c64 / sv_get_state_c64  from_amplitudes(complex64) / .amplitudes  state.py:49-66
  */
 #ifndef SVB200_H
 #define SVB200_H
@@ -103,7 +105,15 @@ int sv_create(int n_qubits, int device, sv_handle** out);
 int sv_nccl_unique_id(void* out128);
 int sv_create_sharded(int n_qubits, int rank, int world, int device, const void* nccl_id, sv_handle** out);
 int sv_destroy(sv_handle* h);
-int sv_info(const sv_handle* h, int64_t* out6); /* n, n_local, rank, world, device, reserved */
+int sv_info(const sv_handle* h, int64_t* out6); /* n, n_local, rank, world, device, precision bits */
+/* Single-GPU state in either precision of the reference's StateVector (state.py:20):
+ * precision_bits 64 = complex128 (as sv_create), 32 = complex64.  A complex64 state runs the
+ * one-kernel-per-op gate kernels in FP32 arithmetic (the reference casts gate matrices to the
+ * state dtype, state.py:264, 273) -- the tile-fusion engine and the fused adjoint sweep are
+ * complex128-only, so `fuse` is ignored -- while expval / var / probs / sample / adjoint
+ * bra-kets accumulate in FP64.  State I/O goes through the _c64 entry points (interleaved
+ * floats == numpy complex64); the double-buffer ones return a validation error. */
+int sv_create_ex(int n_qubits, int device, int precision_bits, sv_handle** out);
 
 /* ---- state I/O (bit-exact round trip) ---- */
 int sv_reset(sv_handle* h);                                  /* |0...0> */
@@ -111,6 +121,8 @@ int sv_set_basis_state(sv_handle* h, uint64_t index);
 int sv_set_state(sv_handle* h, const double* amps, uint64_t n_amps);   /* full 2^n vector */
 int sv_get_state(sv_handle* h, double* out, uint64_t n_amps);         /* full 2^n vector */
 int sv_norm(sv_handle* h, double* out);
+int sv_set_state_c64(sv_handle* h, const float* amps, uint64_t n_amps);  /* complex64 handles */
+int sv_get_state_c64(sv_handle* h, float* out, uint64_t n_amps);
 
 /* ---- gate application ---- */
 int sv_apply_single_qubit(sv_handle* h, int q, const double* m2x2);

@@ -25,6 +25,7 @@ EXPORTS = (
     "sv_expval", "sv_probs", "sv_var", "sv_sample", "sv_adjoint_jacobian", "sv_last_error", "sv_synchronize", "sv_stream",
     "sv_launch_count", "sv_set_profiling", "sv_kernel_stats", "sv_reset_stats", "sv_plan_summary",
     "sv_plan_program", "sv_plan_sharded", "sv_plan_compile", "sv_plan_fp64",
+    "sv_create_ex", "sv_set_state_c64", "sv_get_state_c64",
 )
 
 
@@ -62,6 +63,9 @@ def lib():
         sig = {
             "sv_device_count": [POINTER(c_int)],
             "sv_create": [c_int, c_int, POINTER(H)],
+            "sv_create_ex": [c_int, c_int, c_int, POINTER(H)],
+            "sv_set_state_c64": [H, POINTER(ctypes.c_float), c_uint64],
+            "sv_get_state_c64": [H, POINTER(ctypes.c_float), c_uint64],
             "sv_nccl_unique_id": [c_void_p],
             "sv_create_sharded": [c_int, c_int, c_int, c_int, c_void_p, POINTER(H)],
             "sv_destroy": [H],

@@ -74,8 +74,15 @@ def build(force=False, verbose=False):
               "-I", BUILD]
     gen_dev_inc()
     cmds = []
+    hdrs = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
+        [os.path.join(HERE, "..", "include", "svb200.h")]
+    t_hdr = max(os.path.getmtime(x) for x in hdrs)
     for src in sources():
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+        objs.append(obj)
+        # incremental: an object newer than its source and every header is reused
+        if not force and os.path.exists(obj) and os.path.getmtime(obj) > max(os.path.getmtime(src), t_hdr):
+            continue
         cmd = [nvcc(), *ARCH, "-lineinfo", *common, "-c", src, "-o", obj]
         if src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"] if verbose else []
@@ -83,10 +90,9 @@ def build(force=False, verbose=False):
         else:
             cmd = [nvcc(), *common, "-I", os.path.join(cuda_home(), "include"), "-x", "c++", "-c", src, "-o", obj]
         cmds.append((src, cmd))
-        objs.append(obj)
     # compile the translation units in parallel (fused.cu alone takes ~2 min)
     from concurrent.futures import ThreadPoolExecutor
-    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds), os.cpu_count() or 1))) as ex:
+    with ThreadPoolExecutor(max_workers=max(1, min(len(cmds) or 1, os.cpu_count() or 1))) as ex:
         results = list(ex.map(lambda sc: (sc[0], subprocess.run(sc[1], capture_output=True, text=True)), cmds))
     for src, r in results:
         if r.returncode != 0:

@@ -138,7 +138,7 @@ static void check_handle(const sv_handle* h) {
 static void exec_prims(sv_handle* h, const std::vector<double2*>& states, std::vector<Prim>& prims, int fuse) {
   if (prims.empty()) return;
   fold_diag_phases(prims);
-  if (fuse && !h->recording) {
+  if (fuse && !h->recording && h->prec == 64) {   // the fusion engine is complex128-only
     // fused passes may relabel qubits inside their tiles: the qubit at local position p ends at perm[p]
     const std::vector<int> perm = apply_prims_fused(h, states, prims);
     for (int o = 0; o < h->n; ++o)
@@ -415,7 +415,7 @@ static void apply_observable(sv_handle* h, const sv_obs& o, const double2* psi, 
   }
   auto groups = pauli_groups(h, o, all_states);
   if (groups.empty()) {
-    CUDA_CHECK(cudaMemsetAsync(lam, 0, h->n_local * sizeof(double2), h->stream));
+    CUDA_CHECK(cudaMemsetAsync(lam, 0, h->n_local * amp_bytes(h), h->stream));
     return;
   }
   std::vector<std::pair<u64, std::vector<PauliTerm>>> gl;
@@ -591,13 +591,13 @@ static void create_common(sv_handle* h, int n_qubits, int device) {
   CUDA_CHECK(cudaSetDevice(device));
   size_t free_b = 0, total_b = 0;
   CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-  const double need = double(h->n_local) * sizeof(double2);
+  const double need = double(h->n_local) * amp_bytes(h);
   if (h->nl >= 40 || need > double(free_b))
     sv_fail(SV_ERR_CAPACITY, "cannot allocate 2**" + std::to_string(h->nl) + " amplitudes (" + std::to_string(need / 1e9) +
                                  " GB) on device " + std::to_string(device) + " with " + std::to_string(free_b / 1e9) +
                                  " GB free");
   CUDA_CHECK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
-  CUDA_CHECK(cudaMalloc(&h->state, h->n_local * sizeof(double2)));
+  CUDA_CHECK(cudaMalloc(&h->state, h->n_local * amp_bytes(h)));
   launch_init_zero(h, h->state, 0, h->rank == 0);
   CUDA_CHECK(cudaStreamSynchronize(h->stream));
 }
@@ -638,6 +638,49 @@ int sv_create(int n_qubits, int device, sv_handle** out) {
   create_common(h, n_qubits, device);
   *out = h;
   h = nullptr;
+  API_END
+}
+
+int sv_create_ex(int n_qubits, int device, int precision_bits, sv_handle** out) {
+  sv_handle* h = nullptr;
+  API_BEGIN
+  if (!out) sv_fail(SV_ERR_VALIDATION, "null output handle");
+  *out = nullptr;
+  if (precision_bits != 64 && precision_bits != 32)
+    sv_fail(SV_ERR_VALIDATION, "precision_bits must be 64 (complex128) or 32 (complex64)");
+  h = new sv_handle();
+  h->prec = precision_bits;
+  create_common(h, n_qubits, device);
+  *out = h;
+  h = nullptr;
+  API_END
+}
+
+int sv_set_state_c64(sv_handle* h, const float* amps, uint64_t n_amps) {
+  API_BEGIN
+  check_handle(h);
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->prec != 32) sv_fail(SV_ERR_VALIDATION, "complex128 state: use sv_set_state");
+  if (!amps) sv_fail(SV_ERR_VALIDATION, "null amplitude buffer");
+  if (n_amps != (1ull << h->n))
+    sv_fail(SV_ERR_VALIDATION, "amplitude array length " + std::to_string(n_amps) + " does not match 2**" + std::to_string(h->n));
+  dist_reset_layout(h);
+  CUDA_CHECK(cudaMemcpyAsync(h->state, amps, h->n_local * sizeof(float2), cudaMemcpyHostToDevice, h->stream));
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  API_END
+}
+
+int sv_get_state_c64(sv_handle* h, float* out, uint64_t n_amps) {
+  API_BEGIN
+  check_handle(h);
+  std::lock_guard<std::mutex> lk(h->mu);
+  if (h->prec != 32) sv_fail(SV_ERR_VALIDATION, "complex128 state: use sv_get_state");
+  if (!out) sv_fail(SV_ERR_VALIDATION, "null output buffer");
+  if (n_amps != (1ull << h->n))
+    sv_fail(SV_ERR_VALIDATION, "output length " + std::to_string(n_amps) + " does not match 2**" + std::to_string(h->n));
+  // complex64 handles never run the fusion engine, so the layout is the identity here
+  CUDA_CHECK(cudaMemcpyAsync(out, h->state, h->n_local * sizeof(float2), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
   API_END
 }
 
@@ -690,7 +733,7 @@ int sv_info(const sv_handle* h, int64_t* out6) {
   out6[2] = h->rank;
   out6[3] = h->world;
   out6[4] = h->device;
-  out6[5] = 0;
+  out6[5] = h->prec;
   API_END
 }
 
@@ -723,6 +766,7 @@ int sv_set_state(sv_handle* h, const double* amps, uint64_t n_amps) {
   if (!amps) sv_fail(SV_ERR_VALIDATION, "null amplitude buffer");
   if (n_amps != (1ull << h->n))
     sv_fail(SV_ERR_VALIDATION, "amplitude array length " + std::to_string(n_amps) + " does not match 2**" + std::to_string(h->n));
+  if (h->prec != 64) sv_fail(SV_ERR_VALIDATION, "complex64 state: use sv_set_state_c64");
   dist_reset_layout(h);
   const double* src = amps + 2 * (u64(h->rank) << h->nl);
   CUDA_CHECK(cudaMemcpyAsync(h->state, src, h->n_local * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
@@ -737,6 +781,7 @@ int sv_get_state(sv_handle* h, double* out, uint64_t n_amps) {
   if (!out) sv_fail(SV_ERR_VALIDATION, "null output buffer");
   if (n_amps != (1ull << h->n))
     sv_fail(SV_ERR_VALIDATION, "output length " + std::to_string(n_amps) + " does not match 2**" + std::to_string(h->n));
+  if (h->prec != 64) sv_fail(SV_ERR_VALIDATION, "complex64 state: use sv_get_state_c64");
   dist_canonicalize(h, {h->state});
   if (h->world == 1) {
     CUDA_CHECK(cudaMemcpyAsync(out, h->state, h->n_local * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
@@ -850,7 +895,7 @@ int sv_var(sv_handle* h, const sv_obs* obs, double* out) {
     release_adjoint_buffers(h);
     size_t free_b = 0, total_b = 0;
     CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-    const size_t bytes = h->n_local * sizeof(double2);
+    const size_t bytes = h->n_local * amp_bytes(h);
     double lacking = (bytes + (64ull << 20) > free_b) ? 1.0 : 0.0;
     dist_allreduce_sum(h, &lacking, 1);
     if (lacking > 0) sv_fail(SV_ERR_CAPACITY, "variance needs one extra state buffer");
@@ -942,19 +987,19 @@ int sv_adjoint_jacobian(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs*
   // lower once (logical layout) to learn columns and validate differentiability
   int ncols = 0;
   for (int i = 0; i < n_ops; ++i) lower_op(ops[i], h->n, ncols, true, nullptr);
-  if (fuse && adjoint_fused(h, ops, n_ops, obs, n_obs, ncols, jac, expvals)) return SV_OK;
+  if (fuse && h->prec == 64 && adjoint_fused(h, ops, n_ops, obs, n_obs, ncols, jac, expvals)) return SV_OK;
   // capacity: one lambda per observable; the fused path's kept buffers go first
   release_adjoint_buffers(h);
   size_t free_b = 0, total_b = 0;
   CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-  const double need = double(n_obs) * double(h->n_local) * sizeof(double2);
+  const double need = double(n_obs) * double(h->n_local) * amp_bytes(h);
   if (need > double(free_b))
     sv_fail(SV_ERR_CAPACITY, "adjoint sweep needs " + std::to_string(n_obs) + " extra state copies (" +
                                  std::to_string(need / 1e9) + " GB) but only " + std::to_string(free_b / 1e9) + " GB are free");
   free_aux(h);
   for (int k = 0; k < n_obs; ++k) {
     double2* p = nullptr;
-    CUDA_CHECK(cudaMalloc(&p, h->n_local * sizeof(double2)));
+    CUDA_CHECK(cudaMalloc(&p, h->n_local * amp_bytes(h)));
     h->aux.push_back(p);
   }
   std::vector<double2*> lam_states = h->aux;

@@ -1,7 +1,7 @@
 // sm_100a kernels of libsvb200: one-op-per-pass gate kernels (K1-K6 of SURVEY.md §2.3),
 // observable reductions (K8/K9/K12/K13), observable application (K10) and the generator
-// bra-ket used by the adjoint sweep (K11).  All complex128 (double2), in place, 64-bit
-// indices; every kernel is an HBM streaming pass (~0.44 flop/B).
+// bra-ket used by the adjoint sweep (K11).  Each is instantiated for complex128 (double2) and
+// complex64 (float2, the reference's "f32" precision, state.py:20); in place, 64-bit indices; every kernel is an HBM streaming pass (~0.44 flop/B).
 //
 // Index arithmetic: a PAIR / DIAG / DENSE primitive enumerates a compact counter k over the
 // non-fixed bits and spreads it around the fixed bit positions ("insert a zero bit at each
@@ -31,30 +31,51 @@ __device__ __forceinline__ u64 deposit(u64 k, const Ins& s) {
   return k;
 }
 
+// Complex arithmetic in the state's precision.  complex128 states compute in FP64; complex64
+// states (the reference's "f32" StateVector, state.py:20) compute gate updates in FP32 -- the
+// reference casts the gate matrix to the state dtype before the contraction (state.py:264, 273)
+// -- while every reduction widens to FP64 before accumulating.
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
 __device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {  // a*b + c
   return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
 }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return make_float2(fmaf(a.x, b.x, -a.y * b.y), fmaf(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ float2 cfma(float2 a, float2 b, float2 c) {
+  return make_float2(fmaf(a.x, b.x, fmaf(-a.y, b.y, c.x)), fmaf(a.x, b.y, fmaf(a.y, b.x, c.y)));
+}
 __device__ __forceinline__ double2 conjmul(double2 a, double2 b) {        // conj(a)*b
   return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.x, b.y, -a.y * b.x));
 }
+__device__ __forceinline__ double2 wide(double2 v) { return v; }
+__device__ __forceinline__ double2 wide(float2 v) { return make_double2(v.x, v.y); }
+template <class C> __device__ __forceinline__ C narrow(double2 v);
+template <> __device__ __forceinline__ double2 narrow<double2>(double2 v) { return v; }
+template <> __device__ __forceinline__ float2 narrow<float2>(double2 v) {
+  return make_float2(float(v.x), float(v.y));
+}
+template <class C> __device__ __forceinline__ C czero();
+template <> __device__ __forceinline__ double2 czero<double2>() { return make_double2(0.0, 0.0); }
+template <> __device__ __forceinline__ float2 czero<float2>() { return make_float2(0.f, 0.f); }
 
 // ---------------------------------------------------------------------------
 // K1/K2/K4: PAIR  (Alg. 1 / Alg. 2 generalised; 2x2 on (i0, i0^xmask))
 // ---------------------------------------------------------------------------
+template <class C>
 struct PairParams {
-  double2 m[4];
+  C m[4];
   u64 fval, xmask, count;
   Ins ins;
 };
 
-template <int ITEMS>
-__global__ void __launch_bounds__(kThreads) k_pair(double2* __restrict__ a, const PairParams P) {
+template <int ITEMS, class C>
+__global__ void __launch_bounds__(kThreads) k_pair(C* __restrict__ a, const PairParams<C> P) {
   const u64 base = u64(blockIdx.x) * (ITEMS * kThreads) + threadIdx.x;
   u64 i0[ITEMS];
-  double2 v0[ITEMS], v1[ITEMS];
+  C v0[ITEMS], v1[ITEMS];
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     const u64 k = base + u64(j) * kThreads;
@@ -67,29 +88,61 @@ __global__ void __launch_bounds__(kThreads) k_pair(double2* __restrict__ a, cons
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     if (i0[j] == ~0ull) continue;
-    const double2 o0 = cfma(P.m[0], v0[j], cmul(P.m[1], v1[j]));
-    const double2 o1 = cfma(P.m[2], v0[j], cmul(P.m[3], v1[j]));
+    const C o0 = cfma(P.m[0], v0[j], cmul(P.m[1], v1[j]));
+    const C o1 = cfma(P.m[2], v0[j], cmul(P.m[3], v1[j]));
     a[i0[j]] = o0;
     a[i0[j] ^ P.xmask] = o1;
+  }
+}
+
+// complex64 PAIR with bit 0 free: the two pairs at counters 2m, 2m+1 are adjacent in memory
+// (i0 even), so one 16-byte float4 access moves two amplitudes -- the same access width as
+// the complex128 kernel (a float2 per access only reaches ~90 % of the copy roofline).
+template <int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_pair_v2(float2* __restrict__ a, const PairParams<float2> P) {
+  const u64 base = u64(blockIdx.x) * (ITEMS * kThreads) + threadIdx.x;
+  const u64 count2 = P.count >> 1;
+  float4* a4 = reinterpret_cast<float4*>(a);
+  u64 i0[ITEMS];
+  float4 v0[ITEMS], v1[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const u64 k = base + u64(j) * kThreads;
+    i0[j] = (k < count2) ? (deposit(k << 1, P.ins) | P.fval) : ~0ull;
+    if (i0[j] != ~0ull) {
+      v0[j] = a4[i0[j] >> 1];
+      v1[j] = a4[(i0[j] ^ P.xmask) >> 1];
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    if (i0[j] == ~0ull) continue;
+    const float2 x0 = make_float2(v0[j].x, v0[j].y), y0 = make_float2(v0[j].z, v0[j].w);
+    const float2 x1 = make_float2(v1[j].x, v1[j].y), y1 = make_float2(v1[j].z, v1[j].w);
+    const float2 ox0 = cfma(P.m[0], x0, cmul(P.m[1], x1)), oy0 = cfma(P.m[0], y0, cmul(P.m[1], y1));
+    const float2 ox1 = cfma(P.m[2], x0, cmul(P.m[3], x1)), oy1 = cfma(P.m[2], y0, cmul(P.m[3], y1));
+    a4[i0[j] >> 1] = make_float4(ox0.x, ox0.y, oy0.x, oy0.y);
+    a4[(i0[j] ^ P.xmask) >> 1] = make_float4(ox1.x, ox1.y, oy1.x, oy1.y);
   }
 }
 
 // ---------------------------------------------------------------------------
 // K3: DIAG  (a[i] *= table[bits]; restricted to (i & fmask) == fval)
 // ---------------------------------------------------------------------------
+template <class C>
 struct DiagParams {
-  double2 t[64];
+  C t[64];
   u64 fval, count;
   int nb;
   unsigned char pos[6];
   Ins ins;
 };
 
-template <int ITEMS>
-__global__ void __launch_bounds__(kThreads) k_diag(double2* __restrict__ a, const DiagParams P) {
+template <int ITEMS, class C>
+__global__ void __launch_bounds__(kThreads) k_diag(C* __restrict__ a, const DiagParams<C> P) {
   const u64 base = u64(blockIdx.x) * (ITEMS * kThreads) + threadIdx.x;
   u64 idx[ITEMS];
-  double2 v[ITEMS];
+  C v[ITEMS];
 #pragma unroll
   for (int j = 0; j < ITEMS; ++j) {
     const u64 k = base + u64(j) * kThreads;
@@ -105,28 +158,57 @@ __global__ void __launch_bounds__(kThreads) k_diag(double2* __restrict__ a, cons
   }
 }
 
+// complex64 DIAG with bit 0 free: two adjacent amplitudes per float4 access (see k_pair_v2)
+template <int ITEMS>
+__global__ void __launch_bounds__(kThreads) k_diag_v2(float2* __restrict__ a, const DiagParams<float2> P) {
+  const u64 base = u64(blockIdx.x) * (ITEMS * kThreads) + threadIdx.x;
+  const u64 count2 = P.count >> 1;
+  float4* a4 = reinterpret_cast<float4*>(a);
+  u64 idx[ITEMS];
+  float4 v[ITEMS];
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    const u64 k = base + u64(j) * kThreads;
+    idx[j] = (k < count2) ? (deposit(k << 1, P.ins) | P.fval) : ~0ull;
+    if (idx[j] != ~0ull) v[j] = a4[idx[j] >> 1];
+  }
+#pragma unroll
+  for (int j = 0; j < ITEMS; ++j) {
+    if (idx[j] == ~0ull) continue;
+    int t = 0;
+    for (int b = 0; b < P.nb; ++b) t |= int((idx[j] >> P.pos[b]) & 1ull) << b;
+    int t1 = t;
+    for (int b = 0; b < P.nb; ++b)
+      if (P.pos[b] == 0) t1 |= 1 << b;   // the odd amplitude has bit 0 set
+    const float2 o0 = cmul(P.t[t], make_float2(v[j].x, v[j].y));
+    const float2 o1 = cmul(P.t[t1], make_float2(v[j].z, v[j].w));
+    a4[idx[j] >> 1] = make_float4(o0.x, o0.y, o1.x, o1.y);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K5/K6: DENSE k-qubit (matrix in shared memory; amplitudes in registers for k <= 4)
 // ---------------------------------------------------------------------------
 struct DenseParams {
-  const double2* mat;    // 4^k entries, row-major, index bit j <-> pos[j]
+  const void* mat;       // 4^k entries (state precision; double2 for the bra-ket), row-major, bit j <-> pos[j]
   u64 fval, count;
   int k;
   unsigned char pos[16];
   Ins ins;
 };
 
-template <int K>
-__global__ void __launch_bounds__(kThreads) k_dense(double2* __restrict__ a, const DenseParams P) {
+template <int K, class C>
+__global__ void __launch_bounds__(kThreads) k_dense(C* __restrict__ a, const DenseParams P) {
   constexpr int D = 1 << K;
-  __shared__ double2 M[D * D];
-  for (int i = threadIdx.x; i < D * D; i += kThreads) M[i] = P.mat[i];
+  __shared__ C M[D * D];
+  const C* mat = static_cast<const C*>(P.mat);
+  for (int i = threadIdx.x; i < D * D; i += kThreads) M[i] = mat[i];
   __syncthreads();
   const u64 k = u64(blockIdx.x) * kThreads + threadIdx.x;
   if (k >= P.count) return;
   const u64 base = deposit(k, P.ins) | P.fval;
   u64 off[D];
-  double2 v[D];
+  C v[D];
 #pragma unroll
   for (int r = 0; r < D; ++r) {
     u64 o = 0;
@@ -138,7 +220,7 @@ __global__ void __launch_bounds__(kThreads) k_dense(double2* __restrict__ a, con
   }
 #pragma unroll
   for (int r = 0; r < D; ++r) {
-    double2 acc = make_double2(0.0, 0.0);
+    C acc = czero<C>();
 #pragma unroll
     for (int c = 0; c < D; ++c) acc = cfma(M[r * D + c], v[c], acc);
     a[off[r]] = acc;
@@ -146,11 +228,13 @@ __global__ void __launch_bounds__(kThreads) k_dense(double2* __restrict__ a, con
 }
 
 // k >= 5: one block per group, amplitudes staged in shared memory, one warp per output row.
-__global__ void __launch_bounds__(kThreads) k_dense_big(double2* __restrict__ a, const DenseParams P) {
-  extern __shared__ double2 sm[];
+template <class C>
+__global__ void __launch_bounds__(kThreads) k_dense_big(C* __restrict__ a, const DenseParams P) {
+  extern __shared__ __align__(16) unsigned char dense_smem[];
   const int D = 1 << P.k;
-  double2* in = sm;
-  double2* out = sm + D;
+  C* in = reinterpret_cast<C*>(dense_smem);
+  C* out = in + D;
+  const C* mat = static_cast<const C*>(P.mat);
   for (u64 g = blockIdx.x; g < P.count; g += gridDim.x) {
     const u64 base = deposit(g, P.ins) | P.fval;
     for (int r = threadIdx.x; r < D; r += kThreads) {
@@ -162,8 +246,8 @@ __global__ void __launch_bounds__(kThreads) k_dense_big(double2* __restrict__ a,
     __syncthreads();
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int r = warp; r < D; r += kThreads / 32) {
-      double2 acc = make_double2(0.0, 0.0);
-      const double2* row = P.mat + size_t(r) * D;
+      C acc = czero<C>();
+      const C* row = mat + size_t(r) * D;
       for (int c = lane; c < D; c += 32) acc = cfma(row[c], in[c], acc);
       for (int s = 16; s > 0; s >>= 1) {
         acc.x += __shfl_xor_sync(0xffffffffu, acc.x, s);
@@ -228,21 +312,23 @@ struct PauliApplyTermDev {
   double2 cc;
 };
 
-__global__ void __launch_bounds__(kThreads) k_norm2(const double2* __restrict__ a, u64 n, double* __restrict__ partials) {
+template <class C>
+__global__ void __launch_bounds__(kThreads) k_norm2(const C* __restrict__ a, u64 n, double* __restrict__ partials) {
   double v[1] = {0.0};
   for (u64 i = u64(blockIdx.x) * kThreads + threadIdx.x; i < n; i += u64(gridDim.x) * kThreads) {
-    const double2 x = a[i];
+    const double2 x = wide(a[i]);
     v[0] = fma(x.x, x.x, fma(x.y, x.y, v[0]));
   }
   block_reduce_store<1>(v, partials);
 }
 
 // Re <a|b> partials (K12)
-__global__ void __launch_bounds__(kThreads) k_dot_re(const double2* __restrict__ a, const double2* __restrict__ b, u64 n,
+template <class C>
+__global__ void __launch_bounds__(kThreads) k_dot_re(const C* __restrict__ a, const C* __restrict__ b, u64 n,
                                                      double* __restrict__ partials) {
   double v[1] = {0.0};
   for (u64 i = u64(blockIdx.x) * kThreads + threadIdx.x; i < n; i += u64(gridDim.x) * kThreads) {
-    const double2 x = a[i], y = b[i];
+    const double2 x = wide(a[i]), y = wide(b[i]);
     v[0] = fma(x.x, y.x, fma(x.y, y.y, v[0]));
   }
   block_reduce_store<1>(v, partials);
@@ -266,9 +352,9 @@ __device__ __forceinline__ u64 to_phys(u64 i, const u64* __restrict__ t) {
 }
 
 // one warp per row: acc = sum_k A[i, j_k] psi_j; expval partial += Re(conj(psi_i) acc), or lam_i = acc
-template <bool APPLY>
-__global__ void __launch_bounds__(kThreads) k_csr(const double2* __restrict__ psi, const CsrArgs A,
-                                                  double2* __restrict__ lam, double* __restrict__ partials) {
+template <bool APPLY, class C>
+__global__ void __launch_bounds__(kThreads) k_csr(const C* __restrict__ psi, const CsrArgs A,
+                                                  C* __restrict__ lam, double* __restrict__ partials) {
   const int lane = threadIdx.x & 31;
   const u64 warps = u64(gridDim.x) * (kThreads / 32);
   double v[1] = {0.0};
@@ -276,7 +362,7 @@ __global__ void __launch_bounds__(kThreads) k_csr(const double2* __restrict__ ps
     double ax = 0.0, ay = 0.0;
     for (int64_t k = A.indptr[row] + lane; k < A.indptr[row + 1]; k += 32) {
       const double2 m = A.data[k];
-      const double2 x = psi[to_phys(u64(A.indices[k]), A.perm_tab)];
+      const double2 x = wide(psi[to_phys(u64(A.indices[k]), A.perm_tab)]);
       ax = fma(m.x, x.x, fma(-m.y, x.y, ax));
       ay = fma(m.x, x.y, fma(m.y, x.x, ay));
     }
@@ -287,9 +373,9 @@ __global__ void __launch_bounds__(kThreads) k_csr(const double2* __restrict__ ps
     if (lane == 0) {
       const u64 pr = to_phys(row, A.perm_tab);
       if (APPLY) {
-        lam[pr] = make_double2(ax, ay);
+        lam[pr] = narrow<C>(make_double2(ax, ay));
       } else {
-        const double2 p = psi[pr];
+        const double2 p = wide(psi[pr]);
         v[0] += p.x * ax + p.y * ay;   // Re(conj(p) * acc)
       }
     }
@@ -306,7 +392,8 @@ struct PauliGroupsArgs {
   int ng;
 };
 
-__global__ void __launch_bounds__(kThreads) k_pauli_apply_multi(const double2* __restrict__ psi, double2* __restrict__ lam,
+template <class C>
+__global__ void __launch_bounds__(kThreads) k_pauli_apply_multi(const C* __restrict__ psi, C* __restrict__ lam,
                                                                 u64 n, const PauliGroupsArgs G,
                                                                 const PauliApplyTermDev* __restrict__ terms, int nterms,
                                                                 int accumulate) {
@@ -314,10 +401,10 @@ __global__ void __launch_bounds__(kThreads) k_pauli_apply_multi(const double2* _
   for (int t = threadIdx.x; t < nterms; t += kThreads) sat2[t] = terms[t];
   __syncthreads();
   for (u64 i = u64(blockIdx.x) * kThreads + threadIdx.x; i < n; i += u64(gridDim.x) * kThreads) {
-    double2 o = accumulate ? lam[i] : make_double2(0.0, 0.0);
+    double2 o = accumulate ? wide(lam[i]) : make_double2(0.0, 0.0);
     for (int g = 0; g < G.ng; ++g) {
       const u64 j = i ^ G.x[g];
-      const double2 b = psi[j];
+      const double2 b = wide(psi[j]);
       double2 s = make_double2(0.0, 0.0);
       for (int t = G.t_begin[g]; t < G.t_begin[g + 1]; ++t) {
         const double sg = (__popcll(j & sat2[t].z) & 1) ? -1.0 : 1.0;
@@ -326,7 +413,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_apply_multi(const double2* _
       }
       o = cfma(s, b, o);
     }
-    lam[i] = o;
+    lam[i] = narrow<C>(o);
   }
 }
 
@@ -342,7 +429,8 @@ struct PauliTermDev {
   int use_im;     // 0: Re(w), 1: Im(w)
 };
 
-__global__ void __launch_bounds__(kThreads) k_pauli_expval(const double2* __restrict__ a, u64 xmask, int pivot, u64 count,
+template <class C>
+__global__ void __launch_bounds__(kThreads) k_pauli_expval(const C* __restrict__ a, u64 xmask, int pivot, u64 count,
                                                            const PauliTermDev* __restrict__ terms, int nterms,
                                                            double* __restrict__ partials) {
   extern __shared__ PauliTermDev st[];
@@ -351,7 +439,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_expval(const double2* __rest
   double v[1] = {0.0};
   for (u64 k = u64(blockIdx.x) * kThreads + threadIdx.x; k < count; k += u64(gridDim.x) * kThreads) {
     if (xmask == 0) {
-      const double2 x = a[k];
+      const double2 x = wide(a[k]);
       const double p = fma(x.x, x.x, x.y * x.y);
       double s = 0.0;
       for (int t = 0; t < nterms; ++t) s += (__popcll(k & st[t].z) & 1) ? -st[t].r : st[t].r;
@@ -359,7 +447,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_expval(const double2* __rest
     } else {
       const u64 lo = k & ((1ull << pivot) - 1ull);
       const u64 i = ((k ^ lo) << 1) | lo;
-      const double2 ai = a[i], aj = a[i ^ xmask];
+      const double2 ai = wide(a[i]), aj = wide(a[i ^ xmask]);
       const double2 w = conjmul(aj, ai);
       double s = 0.0;
       for (int t = 0; t < nterms; ++t) {
@@ -374,7 +462,8 @@ __global__ void __launch_bounds__(kThreads) k_pauli_expval(const double2* __rest
 
 // K10: lambda (+)= sum_t cc_t (-1)^{pc((i^x) & z_t)} psi_{i^x}   (PauliApplyTermDev: see above)
 
-__global__ void __launch_bounds__(kThreads) k_pauli_apply(const double2* __restrict__ psi, double2* __restrict__ lam, u64 xmask,
+template <class C>
+__global__ void __launch_bounds__(kThreads) k_pauli_apply(const C* __restrict__ psi, C* __restrict__ lam, u64 xmask,
                                                           u64 n, const PauliApplyTermDev* __restrict__ terms, int nterms,
                                                           int accumulate) {
   extern __shared__ PauliApplyTermDev sat[];
@@ -382,7 +471,7 @@ __global__ void __launch_bounds__(kThreads) k_pauli_apply(const double2* __restr
   __syncthreads();
   for (u64 i = u64(blockIdx.x) * kThreads + threadIdx.x; i < n; i += u64(gridDim.x) * kThreads) {
     const u64 j = i ^ xmask;
-    const double2 b = psi[j];
+    const double2 b = wide(psi[j]);
     double2 s = make_double2(0.0, 0.0);
     for (int t = 0; t < nterms; ++t) {
       const double sg = (__popcll(j & sat[t].z) & 1) ? -1.0 : 1.0;
@@ -391,21 +480,23 @@ __global__ void __launch_bounds__(kThreads) k_pauli_apply(const double2* __restr
     }
     double2 o = cmul(s, b);
     if (accumulate) {
-      const double2 l = lam[i];
+      const double2 l = wide(lam[i]);
       o.x += l.x;
       o.y += l.y;
     }
-    lam[i] = o;
+    lam[i] = narrow<C>(o);
   }
 }
 
-// K11 helper: <bra| P (G (x) I) |ket> over groups (complex partial), G dense 2^K x 2^K in smem.
-template <int K>
-__global__ void __launch_bounds__(kThreads) k_braket(const double2* __restrict__ bra, const double2* __restrict__ ket,
+// K11 helper: <bra| P (G (x) I) |ket> over groups (complex partial), G dense 2^K x 2^K in smem
+// (always FP64: the bra-ket is a reduction, so complex64 states widen on load).
+template <int K, class C>
+__global__ void __launch_bounds__(kThreads) k_braket(const C* __restrict__ bra, const C* __restrict__ ket,
                                                      const DenseParams P, double* __restrict__ partials) {
   constexpr int D = 1 << K;
   __shared__ double2 M[D * D];
-  for (int i = threadIdx.x; i < D * D; i += kThreads) M[i] = P.mat[i];
+  const double2* mat = static_cast<const double2*>(P.mat);
+  for (int i = threadIdx.x; i < D * D; i += kThreads) M[i] = mat[i];
   __syncthreads();
   double v[2] = {0.0, 0.0};
   for (u64 k = u64(blockIdx.x) * kThreads + threadIdx.x; k < P.count; k += u64(gridDim.x) * kThreads) {
@@ -419,14 +510,14 @@ __global__ void __launch_bounds__(kThreads) k_braket(const double2* __restrict__
       for (int j = 0; j < K; ++j)
         if ((r >> j) & 1) o |= 1ull << P.pos[j];
       off[r] = base | o;
-      x[r] = ket[off[r]];
+      x[r] = wide(ket[off[r]]);
     }
 #pragma unroll
     for (int r = 0; r < D; ++r) {
       double2 acc = make_double2(0.0, 0.0);
 #pragma unroll
       for (int c = 0; c < D; ++c) acc = cfma(M[r * D + c], x[c], acc);
-      const double2 b = bra[off[r]];
+      const double2 b = wide(bra[off[r]]);
       const double2 t = conjmul(b, acc);
       v[0] += t.x;
       v[1] += t.y;
@@ -451,7 +542,8 @@ __device__ __forceinline__ u64 bin_pattern(u64 b, const ProbParams& P) {
 }
 
 // one block per (chunk, bin): partials[chunk * bins + bin]
-__global__ void __launch_bounds__(kThreads) k_probs_chunked(const double2* __restrict__ a, const ProbParams P, int chunks,
+template <class C>
+__global__ void __launch_bounds__(kThreads) k_probs_chunked(const C* __restrict__ a, const ProbParams P, int chunks,
                                                             double* __restrict__ partials) {
   const u64 bins = 1ull << P.w;
   const u64 bin = blockIdx.x % bins;
@@ -459,21 +551,22 @@ __global__ void __launch_bounds__(kThreads) k_probs_chunked(const double2* __res
   const u64 pat = bin_pattern(bin, P);
   double v[1] = {0.0};
   for (u64 k = u64(chunk) * kThreads + threadIdx.x; k < P.members; k += u64(chunks) * kThreads) {
-    const double2 x = a[deposit(k, P.ins) | pat];
+    const double2 x = wide(a[deposit(k, P.ins) | pat]);
     v[0] = fma(x.x, x.x, fma(x.y, x.y, v[0]));
   }
   block_reduce_store<1>(v, partials);
 }
 
 // one thread per bin (few members per bin)
-__global__ void __launch_bounds__(kThreads) k_probs_perbin(const double2* __restrict__ a, const ProbParams P, u64 bins,
+template <class C>
+__global__ void __launch_bounds__(kThreads) k_probs_perbin(const C* __restrict__ a, const ProbParams P, u64 bins,
                                                            double* __restrict__ out) {
   const u64 bin = u64(blockIdx.x) * kThreads + threadIdx.x;
   if (bin >= bins) return;
   const u64 pat = bin_pattern(bin, P);
   double s = 0.0;
   for (u64 k = 0; k < P.members; ++k) {
-    const double2 x = a[deposit(k, P.ins) | pat];
+    const double2 x = wide(a[deposit(k, P.ins) | pat]);
     s = fma(x.x, x.x, fma(x.y, x.y, s));
   }
   out[bin] = s;
@@ -498,6 +591,27 @@ inline unsigned red_grid(u64 work) {
 }
 
 double2 d2(cplx c) { return make_double2(c.real(), c.imag()); }
+template <class C> C hc(cplx c);
+template <> double2 hc<double2>(cplx c) { return d2(c); }
+template <> float2 hc<float2>(cplx c) { return make_float2(float(c.real()), float(c.imag())); }
+
+// launch KERNEL<C> on a state buffer in the handle's precision (double2* in the host API)
+#define SV_F32(p) reinterpret_cast<float2*>(const_cast<double2*>(p))
+#define SV_LAUNCH(h, KERNEL, CFG, A0, ...)                        \
+  do {                                                            \
+    if ((h)->prec == 32)                                          \
+      KERNEL<float2><<<CFG>>>(SV_F32(A0), __VA_ARGS__);           \
+    else                                                          \
+      KERNEL<double2><<<CFG>>>(A0, __VA_ARGS__);                  \
+  } while (0)
+#define SV_LAUNCH2(h, KERNEL, CFG, A0, A1, ...)                   \
+  do {                                                            \
+    if ((h)->prec == 32)                                          \
+      KERNEL<float2><<<CFG>>>(SV_F32(A0), SV_F32(A1), __VA_ARGS__); \
+    else                                                          \
+      KERNEL<double2><<<CFG>>>(A0, A1, __VA_ARGS__);              \
+  } while (0)
+#define SV_CFG(...) __VA_ARGS__
 
 // device buffer for small per-launch tables (matrices, term lists); grows, never shrinks
 void* scratch_upload(sv_handle* h, const void* src, size_t bytes);
@@ -562,48 +676,61 @@ void release_scratch(sv_handle* h) {
 // Algorithmic bytes of one unfused primitive: 32 B (16 read + 16 written) per touched amplitude.
 double prim_bytes(const sv_handle* h, const Prim& p) {
   if (p.skip) return 0.0;
-  if (p.type == PRIM_PAIR) return 32.0 * 2.0 * double(h->n_local >> popcount64(p.fmask));
-  if (p.type == PRIM_DIAG) return 32.0 * double(h->n_local >> popcount64(p.fmask));
-  return 32.0 * double(h->n_local >> (popcount64(p.fmask) - p.nb));
+  const double rw = 2.0 * double(amp_bytes(h));   // read + write of one amplitude
+  if (p.type == PRIM_PAIR) return rw * 2.0 * double(h->n_local >> popcount64(p.fmask));
+  if (p.type == PRIM_DIAG) return rw * double(h->n_local >> popcount64(p.fmask));
+  return rw * double(h->n_local >> (popcount64(p.fmask) - p.nb));
 }
 
-void launch_prim(sv_handle* h, double2* a, const Prim& p) {
-  if (p.skip) return;
-  if (h->recording) {   // host-only planning (sv_plan_sharded)
-    h->rec.push_back({REC_PRIM, p, -1});
-    return;
-  }
+template <class C>
+static void launch_prim_t(sv_handle* h, C* a, const Prim& p) {
+  // the same bytes in flight per thread in both precisions (4 x 16 B pairs or 8 x 8 B pairs)
+  constexpr int kItems = sizeof(C) == 8 ? 8 : 4;
   const int nf = popcount64(p.fmask);
   if (nf > h->nl) sv_fail(SV_ERR_DEVICE, "internal: primitive fixes more bits than the shard has");
   const u64 count = h->n_local >> nf;
   cudaEvent_t ev[2];
   if (p.type == PRIM_PAIR) {
-    PairParams P;
-    for (int i = 0; i < 4; ++i) P.m[i] = d2(p.m[i]);
+    PairParams<C> P;
+    for (int i = 0; i < 4; ++i) P.m[i] = hc<C>(p.m[i]);
     P.fval = p.fval;
     P.xmask = p.xmask;
     P.count = count;
     P.ins = make_ins(p.fmask);
     stat_begin(h, KC_PAIR, prim_bytes(h, p), ev);
-    k_pair<4><<<grid_for(count, 4 * kThreads), kThreads, 0, h->stream>>>(a, P);
+    if constexpr (sizeof(C) == 8) {
+      if (!(p.fmask & 1ull) && count >= 2)
+        k_pair_v2<4><<<grid_for(count >> 1, 4 * kThreads), kThreads, 0, h->stream>>>(a, P);
+      else
+        k_pair<kItems, C><<<grid_for(count, kItems * kThreads), kThreads, 0, h->stream>>>(a, P);
+    } else {
+      k_pair<kItems, C><<<grid_for(count, kItems * kThreads), kThreads, 0, h->stream>>>(a, P);
+    }
     stat_end(h, KC_PAIR, prim_bytes(h, p), ev);
   } else if (p.type == PRIM_DIAG) {
-    DiagParams P;
+    DiagParams<C> P;
     if (p.nb > 6) sv_fail(SV_ERR_DEVICE, "internal: diagonal table too large");
-    for (size_t i = 0; i < p.m.size(); ++i) P.t[i] = d2(p.m[i]);
+    for (size_t i = 0; i < p.m.size(); ++i) P.t[i] = hc<C>(p.m[i]);
     P.fval = p.fval;
     P.count = count;
     P.nb = p.nb;
     for (int j = 0; j < p.nb; ++j) P.pos[j] = (unsigned char)p.pos[j];
     P.ins = make_ins(p.fmask);
     stat_begin(h, KC_DIAG, prim_bytes(h, p), ev);
-    k_diag<4><<<grid_for(count, 4 * kThreads), kThreads, 0, h->stream>>>(a, P);
+    if constexpr (sizeof(C) == 8) {
+      if (!(p.fmask & 1ull) && count >= 2)
+        k_diag_v2<4><<<grid_for(count >> 1, 4 * kThreads), kThreads, 0, h->stream>>>(a, P);
+      else
+        k_diag<kItems, C><<<grid_for(count, kItems * kThreads), kThreads, 0, h->stream>>>(a, P);
+    } else {
+      k_diag<kItems, C><<<grid_for(count, kItems * kThreads), kThreads, 0, h->stream>>>(a, P);
+    }
     stat_end(h, KC_DIAG, prim_bytes(h, p), ev);
   } else {
     DenseParams P;
-    std::vector<double2> mat(p.m.size());
-    for (size_t i = 0; i < p.m.size(); ++i) mat[i] = d2(p.m[i]);
-    P.mat = (const double2*)scratch_upload(h, mat.data(), mat.size() * sizeof(double2));
+    std::vector<C> mat(p.m.size());
+    for (size_t i = 0; i < p.m.size(); ++i) mat[i] = hc<C>(p.m[i]);
+    P.mat = scratch_upload(h, mat.data(), mat.size() * sizeof(C));
     P.fval = p.fval;
     P.count = count;
     P.k = p.nb;
@@ -612,16 +739,17 @@ void launch_prim(sv_handle* h, double2* a, const Prim& p) {
     stat_begin(h, KC_DENSE, prim_bytes(h, p), ev);
     const unsigned g = grid_for(count, kThreads);
     switch (p.nb) {
-      case 1: k_dense<1><<<g, kThreads, 0, h->stream>>>(a, P); break;
-      case 2: k_dense<2><<<g, kThreads, 0, h->stream>>>(a, P); break;
-      case 3: k_dense<3><<<g, kThreads, 0, h->stream>>>(a, P); break;
-      case 4: k_dense<4><<<g, kThreads, 0, h->stream>>>(a, P); break;
+      case 1: k_dense<1, C><<<g, kThreads, 0, h->stream>>>(a, P); break;
+      case 2: k_dense<2, C><<<g, kThreads, 0, h->stream>>>(a, P); break;
+      case 3: k_dense<3, C><<<g, kThreads, 0, h->stream>>>(a, P); break;
+      case 4: k_dense<4, C><<<g, kThreads, 0, h->stream>>>(a, P); break;
       default: {
         if (p.nb > 12) sv_fail(SV_ERR_UNSUPPORTED, "dense matrices on more than 12 wires are not supported on the GPU path");
-        const size_t smem = (size_t(2) << p.nb) * sizeof(double2);   // in + out, 2^k each
-        if (smem > 48 * 1024) CUDA_CHECK(cudaFuncSetAttribute(k_dense_big, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        const size_t smem = (size_t(2) << p.nb) * sizeof(C);   // in + out, 2^k each
+        if (smem > 48 * 1024)
+          CUDA_CHECK(cudaFuncSetAttribute(k_dense_big<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
         unsigned gb = unsigned(std::min<u64>(count, 148ull * 16));
-        k_dense_big<<<gb, kThreads, smem, h->stream>>>(a, P);
+        k_dense_big<C><<<gb, kThreads, smem, h->stream>>>(a, P);
       }
     }
     stat_end(h, KC_DENSE, prim_bytes(h, p), ev);
@@ -629,22 +757,38 @@ void launch_prim(sv_handle* h, double2* a, const Prim& p) {
   CUDA_CHECK(cudaGetLastError());
 }
 
+void launch_prim(sv_handle* h, double2* a, const Prim& p) {
+  if (p.skip) return;
+  if (h->recording) {   // host-only planning (sv_plan_sharded)
+    h->rec.push_back({REC_PRIM, p, -1});
+    return;
+  }
+  if (h->prec == 32)
+    launch_prim_t(h, reinterpret_cast<float2*>(a), p);
+  else
+    launch_prim_t(h, a, p);
+}
+
 void launch_init_zero(sv_handle* h, double2* a, u64 basis_local, bool set_one) {
   cudaEvent_t ev[2];
-  stat_begin(h, KC_INIT, 16.0 * double(h->n_local), ev);
-  CUDA_CHECK(cudaMemsetAsync(a, 0, h->n_local * sizeof(double2), h->stream));
+  stat_begin(h, KC_INIT, double(amp_bytes(h)) * double(h->n_local), ev);
+  const size_t eb = amp_bytes(h);
+  CUDA_CHECK(cudaMemsetAsync(a, 0, h->n_local * eb, h->stream));
   if (set_one) {
     static const double2 one = {1.0, 0.0};
-    CUDA_CHECK(cudaMemcpyAsync(a + basis_local, &one, sizeof(double2), cudaMemcpyHostToDevice, h->stream));
+    static const float2 one32 = {1.f, 0.f};
+    const void* src = h->prec == 32 ? static_cast<const void*>(&one32) : static_cast<const void*>(&one);
+    CUDA_CHECK(cudaMemcpyAsync(reinterpret_cast<char*>(a) + basis_local * eb, src, eb, cudaMemcpyHostToDevice, h->stream));
   }
-  stat_end(h, KC_INIT, 16.0 * double(h->n_local), ev);
+  stat_end(h, KC_INIT, double(amp_bytes(h)) * double(h->n_local), ev);
 }
 
 void launch_copy(sv_handle* h, double2* dst, const double2* src, u64 n) {
   cudaEvent_t ev[2];
-  stat_begin(h, KC_INIT, 32.0 * double(n), ev);
-  CUDA_CHECK(cudaMemcpyAsync(dst, src, n * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream));
-  stat_end(h, KC_INIT, 32.0 * double(n), ev);
+  const size_t eb = amp_bytes(h);
+  stat_begin(h, KC_INIT, 2.0 * double(eb) * double(n), ev);
+  CUDA_CHECK(cudaMemcpyAsync(dst, src, n * eb, cudaMemcpyDeviceToDevice, h->stream));
+  stat_end(h, KC_INIT, 2.0 * double(eb) * double(n), ev);
 }
 
 void sum_partials(sv_handle* h, const double* partials, int nblocks, int ncomp, double* d_out) {
@@ -658,9 +802,9 @@ double reduce_norm2(sv_handle* h, const double2* a) {
   ensure_partials(h, g);
   ensure_results(h, 1);
   cudaEvent_t ev[2];
-  stat_begin(h, KC_REDUCE, 16.0 * double(h->n_local), ev);
-  k_norm2<<<g, kThreads, 0, h->stream>>>(a, h->n_local, h->d_partials);
-  stat_end(h, KC_REDUCE, 16.0 * double(h->n_local), ev);
+  stat_begin(h, KC_REDUCE, double(amp_bytes(h)) * double(h->n_local), ev);
+  SV_LAUNCH(h, k_norm2, SV_CFG(g, kThreads, 0, h->stream), a, h->n_local, h->d_partials);
+  stat_end(h, KC_REDUCE, double(amp_bytes(h)) * double(h->n_local), ev);
   CUDA_CHECK(cudaGetLastError());
   sum_partials(h, h->d_partials, g, 1, h->d_results);
   double out = 0;
@@ -690,11 +834,16 @@ void pauli_group_expval_async(sv_handle* h, const double2* a, u64 xmask, const s
   ensure_partials(h, g);
   auto* d_terms = (const PauliTermDev*)scratch_upload(h, dt.data(), dt.size() * sizeof(PauliTermDev));
   size_t smem = dt.size() * sizeof(PauliTermDev);
-  if (smem > 48 * 1024) CUDA_CHECK(cudaFuncSetAttribute(k_pauli_expval, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  if (smem > 48 * 1024) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_pauli_expval<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CUDA_CHECK(cudaFuncSetAttribute(k_pauli_expval<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  }
   cudaEvent_t ev[2];
-  stat_begin(h, KC_REDUCE, 16.0 * double(h->n_local), ev);
-  k_pauli_expval<<<g, kThreads, smem, h->stream>>>(a, xmask, pivot, count, d_terms, int(dt.size()), h->d_partials);
-  stat_end(h, KC_REDUCE, 16.0 * double(h->n_local), ev);
+  const double bytes = double(amp_bytes(h)) * double(h->n_local);
+  stat_begin(h, KC_REDUCE, bytes, ev);
+  SV_LAUNCH(h, k_pauli_expval, SV_CFG(g, kThreads, smem, h->stream), a, xmask, pivot, count, d_terms, int(dt.size()),
+            h->d_partials);
+  stat_end(h, KC_REDUCE, bytes, ev);
   CUDA_CHECK(cudaGetLastError());
   sum_partials(h, h->d_partials, g, 1, d_out);
 }
@@ -708,12 +857,16 @@ void pauli_group_apply(sv_handle* h, const double2* psi, double2* lam, u64 xmask
   }
   auto* d_terms = (const PauliApplyTermDev*)scratch_upload(h, dt.data(), dt.size() * sizeof(PauliApplyTermDev));
   size_t smem = dt.size() * sizeof(PauliApplyTermDev);
-  if (smem > 48 * 1024) CUDA_CHECK(cudaFuncSetAttribute(k_pauli_apply, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  if (smem > 48 * 1024) {
+    CUDA_CHECK(cudaFuncSetAttribute(k_pauli_apply<double2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    CUDA_CHECK(cudaFuncSetAttribute(k_pauli_apply<float2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  }
   const unsigned g = unsigned(std::min<u64>(grid_for(h->n_local, kThreads * 4), 148ull * 64));
-  const double bytes = (accumulate ? 48.0 : 32.0) * double(h->n_local);
+  const double bytes = (accumulate ? 3.0 : 2.0) * double(amp_bytes(h)) * double(h->n_local);
   cudaEvent_t ev[2];
   stat_begin(h, KC_APPLY_OBS, bytes, ev);
-  k_pauli_apply<<<g, kThreads, smem, h->stream>>>(psi, lam, xmask, h->n_local, d_terms, int(dt.size()), accumulate ? 1 : 0);
+  SV_LAUNCH2(h, k_pauli_apply, SV_CFG(g, kThreads, smem, h->stream), psi, lam, xmask, h->n_local, d_terms,
+             int(dt.size()), accumulate ? 1 : 0);
   stat_end(h, KC_APPLY_OBS, bytes, ev);
   CUDA_CHECK(cudaGetLastError());
 }
@@ -734,12 +887,14 @@ void pauli_groups_apply(sv_handle* h, const double2* psi, double2* lam,
     auto* d_terms = (const PauliApplyTermDev*)scratch_upload(h, dt.data(), dt.size() * sizeof(PauliApplyTermDev));
     const size_t smem = dt.size() * sizeof(PauliApplyTermDev);
     if (smem > 48 * 1024)
-      CUDA_CHECK(cudaFuncSetAttribute(k_pauli_apply_multi, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      for (const void* f : {(const void*)k_pauli_apply_multi<double2>, (const void*)k_pauli_apply_multi<float2>})
+        CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const int acc = g0 > 0;
-    const double bytes = (16.0 * G.ng + 16.0 + (acc ? 16.0 : 0.0)) * double(h->n_local);
+    const double bytes = (G.ng + 1.0 + (acc ? 1.0 : 0.0)) * double(amp_bytes(h)) * double(h->n_local);
     cudaEvent_t ev[2];
     stat_begin(h, KC_APPLY_OBS, bytes, ev);
-    k_pauli_apply_multi<<<g, kThreads, smem, h->stream>>>(psi, lam, h->n_local, G, d_terms, int(dt.size()), acc);
+    SV_LAUNCH2(h, k_pauli_apply_multi, SV_CFG(g, kThreads, smem, h->stream), psi, lam, h->n_local, G, d_terms,
+               int(dt.size()), acc);
     stat_end(h, KC_APPLY_OBS, bytes, ev);
     CUDA_CHECK(cudaGetLastError());
   }
@@ -781,18 +936,24 @@ double csr_apply_or_expval(sv_handle* h, const sv_obs& o, const double2* psi, do
   const unsigned g = red_grid(rows * 32);
   double out = 0.0;
   cudaEvent_t ev[2];
-  const double bytes = 16.0 * double(h->n_local) + 24.0 * double(nnz);
+  const double bytes = double(amp_bytes(h)) * double(h->n_local) + 24.0 * double(nnz);
   if (lam) {
-    CUDA_CHECK(cudaMemsetAsync(lam, 0, h->n_local * sizeof(double2), h->stream));
+    CUDA_CHECK(cudaMemsetAsync(lam, 0, h->n_local * amp_bytes(h), h->stream));
     stat_begin(h, KC_APPLY_OBS, bytes, ev);
-    k_csr<true><<<g, kThreads, 0, h->stream>>>(psi, A, lam, nullptr);
+    if (h->prec == 32)
+      k_csr<true, float2><<<g, kThreads, 0, h->stream>>>(SV_F32(psi), A, SV_F32(lam), nullptr);
+    else
+      k_csr<true, double2><<<g, kThreads, 0, h->stream>>>(psi, A, lam, nullptr);
     stat_end(h, KC_APPLY_OBS, bytes, ev);
     CUDA_CHECK(cudaGetLastError());
   } else {
     ensure_partials(h, g);
     ensure_results(h, 1);
     stat_begin(h, KC_REDUCE, bytes, ev);
-    k_csr<false><<<g, kThreads, 0, h->stream>>>(psi, A, nullptr, h->d_partials);
+    if (h->prec == 32)
+      k_csr<false, float2><<<g, kThreads, 0, h->stream>>>(SV_F32(psi), A, nullptr, h->d_partials);
+    else
+      k_csr<false, double2><<<g, kThreads, 0, h->stream>>>(psi, A, nullptr, h->d_partials);
     stat_end(h, KC_REDUCE, bytes, ev);
     CUDA_CHECK(cudaGetLastError());
     sum_partials(h, h->d_partials, g, 1, h->d_results);
@@ -808,9 +969,9 @@ double reduce_dot_re(sv_handle* h, const double2* a, const double2* b) {
   ensure_partials(h, g);
   ensure_results(h, 1);
   cudaEvent_t ev[2];
-  stat_begin(h, KC_REDUCE, 32.0 * double(h->n_local), ev);
-  k_dot_re<<<g, kThreads, 0, h->stream>>>(a, b, h->n_local, h->d_partials);
-  stat_end(h, KC_REDUCE, 32.0 * double(h->n_local), ev);
+  stat_begin(h, KC_REDUCE, 2.0 * double(amp_bytes(h)) * double(h->n_local), ev);
+  SV_LAUNCH2(h, k_dot_re, SV_CFG(g, kThreads, 0, h->stream), a, b, h->n_local, h->d_partials);
+  stat_end(h, KC_REDUCE, 2.0 * double(amp_bytes(h)) * double(h->n_local), ev);
   CUDA_CHECK(cudaGetLastError());
   sum_partials(h, h->d_partials, g, 1, h->d_results);
   double out = 0;
@@ -824,7 +985,7 @@ void braket_prim_async(sv_handle* h, const double2* bra, const double2* ket, con
   DenseParams P;
   std::vector<double2> mat(gp.m.size());
   for (size_t i = 0; i < gp.m.size(); ++i) mat[i] = d2(gp.m[i]);
-  P.mat = (const double2*)scratch_upload(h, mat.data(), mat.size() * sizeof(double2));
+  P.mat = scratch_upload(h, mat.data(), mat.size() * sizeof(double2));   // FP64 in both precisions
   P.fval = gp.fval;
   const int nf = popcount64(gp.fmask);
   P.count = h->n_local >> nf;
@@ -833,14 +994,24 @@ void braket_prim_async(sv_handle* h, const double2* bra, const double2* ket, con
   P.ins = make_ins(gp.fmask);
   const unsigned g = red_grid(P.count);
   ensure_partials(h, size_t(g) * 2);
-  const double bytes = 32.0 * double(P.count << gp.nb);
+  const double bytes = 2.0 * double(amp_bytes(h)) * double(P.count << gp.nb);
   cudaEvent_t ev[2];
   stat_begin(h, KC_BRAKET, bytes, ev);
-  switch (gp.nb) {
-    case 1: k_braket<1><<<g, kThreads, 0, h->stream>>>(bra, ket, P, h->d_partials); break;
-    case 2: k_braket<2><<<g, kThreads, 0, h->stream>>>(bra, ket, P, h->d_partials); break;
-    case 3: k_braket<3><<<g, kThreads, 0, h->stream>>>(bra, ket, P, h->d_partials); break;
-    default: k_braket<4><<<g, kThreads, 0, h->stream>>>(bra, ket, P, h->d_partials); break;
+  if (h->prec == 32) {
+    const float2 *b32 = SV_F32(bra), *k32 = SV_F32(ket);
+    switch (gp.nb) {
+      case 1: k_braket<1, float2><<<g, kThreads, 0, h->stream>>>(b32, k32, P, h->d_partials); break;
+      case 2: k_braket<2, float2><<<g, kThreads, 0, h->stream>>>(b32, k32, P, h->d_partials); break;
+      case 3: k_braket<3, float2><<<g, kThreads, 0, h->stream>>>(b32, k32, P, h->d_partials); break;
+      default: k_braket<4, float2><<<g, kThreads, 0, h->stream>>>(b32, k32, P, h->d_partials); break;
+    }
+  } else {
+    switch (gp.nb) {
+      case 1: k_braket<1, double2><<<g, kThreads, 0, h->stream>>>(bra, ket, P, h->d_partials); break;
+      case 2: k_braket<2, double2><<<g, kThreads, 0, h->stream>>>(bra, ket, P, h->d_partials); break;
+      case 3: k_braket<3, double2><<<g, kThreads, 0, h->stream>>>(bra, ket, P, h->d_partials); break;
+      default: k_braket<4, double2><<<g, kThreads, 0, h->stream>>>(bra, ket, P, h->d_partials); break;
+    }
   }
   stat_end(h, KC_BRAKET, bytes, ev);
   CUDA_CHECK(cudaGetLastError());
@@ -859,18 +1030,19 @@ void probs_async(sv_handle* h, const double2* a, const std::vector<int>& pos_msb
   P.members = h->n_local >> P.w;
   const u64 bins = 1ull << P.w;
   cudaEvent_t ev[2];
-  stat_begin(h, KC_PROBS, 16.0 * double(h->n_local), ev);
+  const double bytes = double(amp_bytes(h)) * double(h->n_local);
+  stat_begin(h, KC_PROBS, bytes, ev);
   if (P.members <= 64) {
-    k_probs_perbin<<<grid_for(bins, kThreads), kThreads, 0, h->stream>>>(a, P, bins, d_out);
-    stat_end(h, KC_PROBS, 16.0 * double(h->n_local), ev);
+    SV_LAUNCH(h, k_probs_perbin, SV_CFG(grid_for(bins, kThreads), kThreads, 0, h->stream), a, P, bins, d_out);
+    stat_end(h, KC_PROBS, bytes, ev);
     CUDA_CHECK(cudaGetLastError());
     return;
   }
   u64 chunks = std::max<u64>(1, std::min<u64>(u64(kRedBlocks) / bins, (P.members + kThreads - 1) / kThreads));
   const u64 nblk = bins * chunks;
   ensure_partials(h, nblk);
-  k_probs_chunked<<<unsigned(nblk), kThreads, 0, h->stream>>>(a, P, int(chunks), h->d_partials);
-  stat_end(h, KC_PROBS, 16.0 * double(h->n_local), ev);
+  SV_LAUNCH(h, k_probs_chunked, SV_CFG(unsigned(nblk), kThreads, 0, h->stream), a, P, int(chunks), h->d_partials);
+  stat_end(h, KC_PROBS, bytes, ev);
   CUDA_CHECK(cudaGetLastError());
   sum_partials(h, h->d_partials, int(chunks), int(bins), d_out);
 }

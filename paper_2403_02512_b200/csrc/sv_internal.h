@@ -101,8 +101,9 @@ struct sv_handle {
   int nl = 0;         // local qubits
   int rank = 0, world = 1, g = 0;
   int device = 0;
+  int prec = 64;                // 64: complex128 (double2); 32: complex64 (float2, state.py:20 "f32")
   cudaStream_t stream = nullptr;
-  double2* state = nullptr;     // 2^nl amplitudes
+  double2* state = nullptr;     // 2^nl amplitudes (float2 storage when prec == 32)
   u64 n_local = 0;
   // logical bit offset o = n-1-q  ->  physical position (>= nl: global/rank bit)
   std::vector<int> phys;
@@ -200,5 +201,8 @@ struct PlanStats {
 };
 PlanStats plan_stats(int nl, const std::vector<Prim>& prims);
 void plan_compile(int nl, const std::vector<Prim>& prims, bool two, int64_t* out4);
+
+// bytes per amplitude in the handle's precision
+inline size_t amp_bytes(const sv_handle* h) { return h->prec == 32 ? sizeof(float2) : sizeof(double2); }
 
 inline int popcount64(u64 x) { return __builtin_popcountll(x); }

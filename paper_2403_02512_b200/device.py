@@ -1,7 +1,7 @@
 """``Device``: the py-bindings device handle of the reference on a B200.
 
-``bind_device(n_qubits, precision, tier)`` returns a handle that owns a complex128 state in
-HBM; ``apply`` / ``expval`` / ``var`` / ``probs`` / ``sample`` / ``adjoint_jacobian`` forward 1:1 to the C-ABI
+``bind_device(n_qubits, precision, tier)`` returns a handle that owns a complex128 ("f64") or
+complex64 ("f32", single GPU, one kernel per op) state in HBM; ``apply`` / ``expval`` / ``var`` / ``probs`` / ``sample`` / ``adjoint_jacobian`` forward 1:1 to the C-ABI
 (include/svb200.h) with copy-out marshalling. One mutator per handle
  is enforced by a per-handle mutex inside the library.
 """
@@ -23,15 +23,16 @@ class Device:
     def __init__(self, n_qubits, precision="f64", device=0, fuse=True, _sharded=None):
         if precision not in ("f64", "f32"):
             raise ValidationError(f"unknown precision {precision!r}; expected 'f64' or 'f32'")
-        if precision != "f64":
-            raise UnsupportedOperationError("the B200 hot path is complex128 only (f32 is a next-round item)")
+        if precision == "f32" and _sharded is not None:
+            raise UnsupportedOperationError("complex64 (f32) states are single-GPU only; shard a complex128 state")
         if not isinstance(n_qubits, (int, np.integer)):
             raise ValidationError(f"n_qubits must be a positive integer, got {n_qubits!r}")
         L = _lib.lib()
         self._h = c_void_p()
         self.fuse = bool(fuse)
         if _sharded is None:
-            _lib.check(L.sv_create(int(n_qubits), int(device), byref(self._h)))
+            bits = 64 if precision == "f64" else 32
+            _lib.check(L.sv_create_ex(int(n_qubits), int(device), bits, byref(self._h)))
         else:
             rank, world, nccl_id = _sharded
             buf = ctypes.create_string_buffer(bytes(nccl_id), 128)
@@ -40,6 +41,7 @@ class Device:
         _lib.check(L.sv_info(self._h, info))
         self.n_qubits, self.n_local, self.rank, self.world, self.device = (int(info[i]) for i in range(5))
         self.precision = precision
+        self.dtype = np.complex128 if precision == "f64" else np.complex64
 
     # ---- lifecycle ---------------------------------------------------------------------
     @classmethod
@@ -84,14 +86,22 @@ class Device:
         _lib.check(_lib.lib().sv_set_basis_state(self.handle, int(index)))
 
     def set_state(self, amplitudes):
-        a = np.ascontiguousarray(amplitudes, dtype=np.complex128)
+        a = np.ascontiguousarray(amplitudes, dtype=self.dtype)
         if a.ndim != 1:
             raise ValidationError("amplitude array must be 1-D")
+        if self.precision == "f32":
+            _lib.check(_lib.lib().sv_set_state_c64(
+                self.handle, a.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float)), a.size))
+            return
         _lib.check(_lib.lib().sv_set_state(self.handle, a.view(np.float64).ctypes.data_as(ctypes.POINTER(c_double)),
                                            a.size))
 
     def get_state(self):
-        out = np.empty(1 << self.n_qubits, dtype=np.complex128)
+        out = np.empty(1 << self.n_qubits, dtype=self.dtype)
+        if self.precision == "f32":
+            _lib.check(_lib.lib().sv_get_state_c64(
+                self.handle, out.view(np.float32).ctypes.data_as(ctypes.POINTER(ctypes.c_float)), out.size))
+            return out
         _lib.check(_lib.lib().sv_get_state(self.handle, out.view(np.float64).ctypes.data_as(ctypes.POINTER(c_double)),
                                            out.size))
         return out

@@ -31,7 +31,11 @@ _NORM_TOL = {"f64": 1e-12, "f32": 1e-5}
 
 
 class StateVector:
-    """2**n_qubits complex128 amplitudes resident on a B200; fresh instances hold |0...0>."""
+    """2**n_qubits amplitudes resident on a B200; fresh instances hold |0...0>.
+
+    ``precision`` selects complex128 ("f64", default) or complex64 ("f32"), as the reference's
+    StateVector (state.py:20, 24-31).
+    """
 
     __slots__ = ("n_qubits", "_dev")
 
@@ -54,10 +58,10 @@ class StateVector:
         n = int(amps.size.bit_length() - 1)
         if n > MAX_QUBITS:
             raise CapacityError(f"{n} qubits exceeds the {MAX_QUBITS}-qubit limit")
-        if amps.dtype == np.complex64:
-            raise UnsupportedOperationError("complex64 state vectors are not supported on the B200 path")
-        sv = cls(n)
-        sv._dev.set_state(amps.astype(np.complex128, copy=False))
+        # complex64 input keeps its precision; anything else becomes complex128 (state.py:56-60)
+        precision = "f32" if amps.dtype == np.complex64 else "f64"
+        sv = cls(n, precision)
+        sv._dev.set_state(amps)
         return sv
 
     @property
@@ -70,11 +74,11 @@ class StateVector:
 
     @property
     def precision(self):
-        return "f64"
+        return self._dev.precision
 
     @property
     def dtype(self):
-        return np.dtype(np.complex128)
+        return np.dtype(self._dev.dtype)
 
     def norm(self):
         return float(self._dev.norm())
@@ -83,7 +87,7 @@ class StateVector:
         return StateVector.from_amplitudes(self.amplitudes)
 
     def __repr__(self):
-        return f"StateVector(n_qubits={self.n_qubits}, precision='f64', device='cuda:{self._dev.device}')"
+        return f"StateVector(n_qubits={self.n_qubits}, precision={self.precision!r}, device='cuda:{self._dev.device}')"
 
 
 def zero_state(n_qubits, precision="f64"):

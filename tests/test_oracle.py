@@ -299,3 +299,28 @@ def test_kat_sparse_expval():
         SparseHermitian([0, 2, 1], [0, 1], [1.0, 1.0])          # non-monotone row pointers
     with pytest.raises(ValidationError):
         SparseHermitian([0, 1, 2], [0, 5], [1.0, 1.0])          # column out of range
+
+
+# ---- complex64 ("f32", state.py:20) goldens from the reference's own complex64 arithmetic ----
+
+F32_TOL = 2e-6   # a few float32 roundings of O(1) amplitudes (reference _NORM_TOL f32 = 1e-5)
+
+
+def test_f32_golden_apply_matrix_vs_oracle():
+    d = load("f32_golden.npz")
+    n = int(d["am_n"])
+    for wires, psi, m, out in zip(d["am_wires"], d["am_in"], d["am_m"], d["am_out"]):
+        w = [int(x) for x in wires if x >= 0]
+        assert psi.dtype == np.complex64 and out.dtype == np.complex64
+        amps = psi.astype(np.complex128)
+        O.apply_matrix(amps, n, w, m[: 1 << len(w), : 1 << len(w)])
+        assert np.abs(amps - out).max() < F32_TOL
+
+
+def test_f32_golden_circuit_vs_oracle():
+    d = load("f32_golden.npz")
+    n = int(d["circ_n"])
+    ops = workloads.random_circuit(n, int(d["circ_depth"]), seed=int(d["circ_seed"]))
+    ref = O.run_circuit(n, ops)
+    assert d["circ_out"].dtype == np.complex64
+    assert np.abs(ref - d["circ_out"]).max() < 1e-5
