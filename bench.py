@@ -25,6 +25,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL's own log lines ("NCCL version ...") default to stdout; keep stdout the one JSON line
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 METRIC = "gate-apply GB/s (effective; random RX/RY/RZ/CNOT circuit depth 50, complex128)"
 UNIT = "GB/s"
