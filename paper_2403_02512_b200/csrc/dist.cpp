@@ -6,6 +6,7 @@
 // the monolithic ones.  The SPEC's block exchange is replaced by
 // index swaps as BASELINE.json's north_star asks, so its message-count law does not apply.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "dist.h"
@@ -40,6 +41,11 @@ void local_bit_swap(sv_handle* h, const std::vector<double2*>& states, int p, in
   h->phys[oq] = p;
 }
 
+// stream-ordered barrier over all ranks (a 1-int allreduce on the handle's stream)
+void device_barrier(sv_handle* h) {
+  NCCL_CHECK(ncclAllReduce(h->d_barrier, h->d_barrier, 1, ncclInt, ncclSum, h->comm, h->stream));
+}
+
 // exchange the top local bit (nl-1) with global position G = nl + j
 void global_swap_top(sv_handle* h, const std::vector<double2*>& states, int G) {
   if (h->recording) {
@@ -63,6 +69,19 @@ void global_swap_top(sv_handle* h, const std::vector<double2*>& states, int G) {
   cudaEvent_t ev[2];
   for (double2* st : states) {
     stat_begin(h, KC_SWAP, 32.0 * double(half), ev);
+    if (h->p2p && st == h->state && h->peer_state[j]) {
+      // Peer-memory swap: our (top = 1-b) half and the partner's (top = b) half exchange
+      // element by element, in place, through the partner's state mapped over NVLink.  The two
+      // ranks split the range (b = 0 the first half, b = 1 the second); barriers before (the
+      // partner's earlier kernels on its state are done) and after (its stores into ours are).
+      const u64 share = half >> 1, lo = b ? share : 0;
+      const u64 peer_off = b ? half : 0;
+      device_barrier(h);
+      launch_exchange(h, st + my_off + lo, h->peer_state[j] + peer_off + lo, b ? half - share : share);
+      device_barrier(h);
+      stat_end(h, KC_SWAP, 32.0 * double(half), ev);
+      continue;
+    }
     int k = 0;
     for (u64 c = 0; c < half; c += chunk, ++k) {
       const u64 len = std::min<u64>(chunk, half - c);
@@ -117,9 +136,68 @@ void dist_init(sv_handle* h, const void* nccl_id) {
     CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_recv[i], cudaEventDisableTiming));
     CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_copy[i], cudaEventDisableTiming));
   }
+  CUDA_CHECK(cudaMalloc(&h->d_barrier, 64 * sizeof(int)));
+  CUDA_CHECK(cudaMemset(h->d_barrier, 0, 64 * sizeof(int)));
+  // Peer-memory swaps: map every partner's state (rank ^ 2^j) through CUDA IPC.  Any rank
+  // failing to map (no P2P path, SVB200_P2P_SWAP=0) turns the feature off on every rank, and
+  // the swaps use NCCL send/recv.
+  const char* env = std::getenv("SVB200_P2P_SWAP");
+  int ok = (env && env[0] == '0') ? 0 : 1;
+  const int gbits = h->g;
+  cudaIpcMemHandle_t mine;
+  std::memset(&mine, 0, sizeof(mine));
+  if (ok && cudaIpcGetMemHandle(&mine, h->state) != cudaSuccess) {
+    cudaGetLastError();
+    ok = 0;
+  }
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  char* d_handles = nullptr;
+  CUDA_CHECK(cudaMalloc(&d_handles, hb * (h->world + 1)));
+  CUDA_CHECK(cudaMemcpy(d_handles + hb * h->world, &mine, hb, cudaMemcpyHostToDevice));
+  NCCL_CHECK(ncclAllGather(d_handles + hb * h->world, d_handles, hb, ncclChar, h->comm, h->stream));
+  std::vector<cudaIpcMemHandle_t> all(h->world);
+  CUDA_CHECK(cudaMemcpyAsync(all.data(), d_handles, hb * h->world, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  CUDA_CHECK(cudaFree(d_handles));
+  for (int j = 0; ok && j < gbits && j < 8; ++j) {
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, all[h->rank ^ (1 << j)], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    h->peer_state[j] = static_cast<double2*>(p);
+  }
+  int* d_ok = h->d_barrier + 1;
+  CUDA_CHECK(cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+  NCCL_CHECK(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, h->comm, h->stream));
+  CUDA_CHECK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  h->p2p = ok != 0;
+  if (!h->p2p)
+    for (int j = 0; j < 8; ++j)
+      if (h->peer_state[j]) {
+        cudaIpcCloseMemHandle(h->peer_state[j]);
+        h->peer_state[j] = nullptr;
+      }
 }
 
 void dist_destroy(sv_handle* h) {
+  if (h->p2p && h->comm) {
+    // no rank unmaps (or frees) a state its partner may still be exchanging with
+    if (ncclAllReduce(h->d_barrier, h->d_barrier, 1, ncclInt, ncclSum, h->comm, h->stream) == ncclSuccess)
+      cudaStreamSynchronize(h->stream);
+  }
+  for (int j = 0; j < 8; ++j)
+    if (h->peer_state[j]) {
+      cudaIpcCloseMemHandle(h->peer_state[j]);
+      h->peer_state[j] = nullptr;
+    }
+  h->p2p = false;
+  if (h->d_barrier) {
+    cudaFree(h->d_barrier);
+    h->d_barrier = nullptr;
+  }
   if (h->comm) {
     ncclCommDestroy(h->comm);
     h->comm = nullptr;

@@ -572,6 +572,33 @@ __global__ void __launch_bounds__(kThreads) k_probs_perbin(const C* __restrict__
   out[bin] = s;
 }
 
+// Global-qubit swap over peer memory: a[i] <-> b[i] with b on the partner GPU (NVLink P2P).
+// Each thread keeps 4 local and 4 remote 16-byte loads in flight (remote latency ~1-2 us).
+__global__ void __launch_bounds__(kThreads) k_exchange(double2* __restrict__ a, double2* __restrict__ b, u64 n) {
+  constexpr int IT = 4;
+  const u64 stride = u64(gridDim.x) * kThreads * IT;
+  for (u64 base = u64(blockIdx.x) * kThreads * IT + threadIdx.x; base < n; base += stride) {
+    double2 x[IT], y[IT];
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+      const u64 i = base + u64(j) * kThreads;
+      if (i < n) {
+        x[j] = a[i];
+        y[j] = b[i];
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < IT; ++j) {
+      const u64 i = base + u64(j) * kThreads;
+      if (i < n) {
+        a[i] = y[j];
+        b[i] = x[j];
+      }
+    }
+  }
+  __threadfence_system();   // remote stores visible before the post-swap barrier
+}
+
 Ins make_ins(u64 fmask) {
   Ins s;
   s.n = 0;
@@ -789,6 +816,14 @@ void launch_copy(sv_handle* h, double2* dst, const double2* src, u64 n) {
   stat_begin(h, KC_INIT, 2.0 * double(eb) * double(n), ev);
   CUDA_CHECK(cudaMemcpyAsync(dst, src, n * eb, cudaMemcpyDeviceToDevice, h->stream));
   stat_end(h, KC_INIT, 2.0 * double(eb) * double(n), ev);
+}
+
+void launch_exchange(sv_handle* h, double2* a, double2* b, u64 n) {
+  if (n == 0) return;
+  const unsigned g = unsigned(std::min<u64>(grid_for(n, kThreads * 4), 148ull * 8));
+  k_exchange<<<g, kThreads, 0, h->stream>>>(a, b, n);
+  h->launches++;
+  CUDA_CHECK(cudaGetLastError());
 }
 
 void sum_partials(sv_handle* h, const double* partials, int nblocks, int ncomp, double* d_out) {

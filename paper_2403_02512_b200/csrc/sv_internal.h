@@ -113,6 +113,10 @@ struct sv_handle {
   cudaStream_t copy_stream = nullptr;          // swap pipeline: staging -> state copies
   cudaEvent_t ev_recv[2] = {nullptr, nullptr};
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
+  // peer-memory swaps (dist.cpp): the partner's state mapped through CUDA IPC, per global bit
+  bool p2p = false;
+  double2* peer_state[8] = {nullptr};
+  int* d_barrier = nullptr;
   // reduction scratch
   double* d_partials = nullptr;
   size_t partials_cap = 0;      // doubles
@@ -158,6 +162,8 @@ void release_scratch(sv_handle* h);
 void launch_prim(sv_handle* h, double2* state, const Prim& p);
 void launch_init_zero(sv_handle* h, double2* state, u64 basis_local, bool set_one);
 void launch_copy(sv_handle* h, double2* dst, const double2* src, u64 n);
+// element-wise exchange a[i] <-> b[i], i < n (b may be a peer GPU's memory mapped over NVLink)
+void launch_exchange(sv_handle* h, double2* a, double2* b, u64 n);
 double reduce_norm2(sv_handle* h, const double2* state);
 // per-term Pauli expectation: terms sharing an x-mask; returns sum_t Re(cc_t * <P_t>) (local part)
 struct PauliTerm {
