@@ -424,6 +424,7 @@ static void apply_observable(sv_handle* h, const sv_obs& o, const double2* psi, 
 }
 
 static void free_aux(sv_handle* h) {
+  for (auto* p : h->aux) dist_forget(h, p);
   for (auto* p : h->aux) cudaFree(p);
   h->aux.clear();
 }
@@ -603,6 +604,8 @@ static void create_common(sv_handle* h, int n_qubits, int device) {
 }
 
 static void release_adjoint_buffers(sv_handle* h) {
+  if (h->adj_lam) dist_forget(h, h->adj_lam);
+  if (h->adj_saved) dist_forget(h, h->adj_saved);
   if (h->adj_lam) cudaFree(h->adj_lam);
   if (h->adj_saved) cudaFree(h->adj_saved);
   h->adj_lam = h->adj_saved = nullptr;

@@ -46,6 +46,61 @@ void device_barrier(sv_handle* h) {
   NCCL_CHECK(ncclAllReduce(h->d_barrier, h->d_barrier, 1, ncclInt, ncclSum, h->comm, h->stream));
 }
 
+// Collective: export `buf` (a cudaMalloc base) with CUDA IPC, all-gather the handles and map the
+// log2 P partners' copies.  Returns 1 when every rank mapped all its partners (else nothing
+// stays mapped on any rank).
+int register_peers(sv_handle* h, double2* buf) {
+  int ok = 1;
+  cudaIpcMemHandle_t mine;
+  std::memset(&mine, 0, sizeof(mine));
+  if (cudaIpcGetMemHandle(&mine, buf) != cudaSuccess) {
+    cudaGetLastError();
+    ok = 0;
+  }
+  const size_t hb = sizeof(cudaIpcMemHandle_t);
+  char* d_handles = nullptr;
+  CUDA_CHECK(cudaMalloc(&d_handles, hb * (h->world + 1)));
+  CUDA_CHECK(cudaMemcpy(d_handles + hb * h->world, &mine, hb, cudaMemcpyHostToDevice));
+  NCCL_CHECK(ncclAllGather(d_handles + hb * h->world, d_handles, hb, ncclChar, h->comm, h->stream));
+  std::vector<cudaIpcMemHandle_t> all(h->world);
+  CUDA_CHECK(cudaMemcpyAsync(all.data(), d_handles, hb * h->world, cudaMemcpyDeviceToHost, h->stream));
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  CUDA_CHECK(cudaFree(d_handles));
+  sv_handle::PeerMap pm;
+  pm.local = buf;
+  for (int j = 0; j < 8; ++j) pm.peer[j] = nullptr;
+  for (int j = 0; ok && j < h->g && j < 8; ++j) {
+    void* p = nullptr;
+    if (cudaIpcOpenMemHandle(&p, all[h->rank ^ (1 << j)], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+      cudaGetLastError();
+      ok = 0;
+      break;
+    }
+    pm.peer[j] = static_cast<double2*>(p);
+  }
+  int* d_ok = h->d_barrier + 1;
+  CUDA_CHECK(cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+  NCCL_CHECK(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, h->comm, h->stream));
+  CUDA_CHECK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  if (ok) {
+    h->peers.push_back(pm);
+  } else {
+    for (int j = 0; j < 8; ++j)
+      if (pm.peer[j]) cudaIpcCloseMemHandle(pm.peer[j]);
+  }
+  return ok;
+}
+
+// partner copy of `buf` for global bit j (registering it on first use), or nullptr
+double2* peer_of(sv_handle* h, double2* buf, int j) {
+  if (!h->p2p || j >= 8) return nullptr;
+  for (const auto& pm : h->peers)
+    if (pm.local == buf) return pm.peer[j];
+  if (!register_peers(h, buf)) return nullptr;
+  return h->peers.back().peer[j];
+}
+
 // exchange the top local bit (nl-1) with global position G = nl + j
 void global_swap_top(sv_handle* h, const std::vector<double2*>& states, int G) {
   if (h->recording) {
@@ -69,7 +124,8 @@ void global_swap_top(sv_handle* h, const std::vector<double2*>& states, int G) {
   cudaEvent_t ev[2];
   for (double2* st : states) {
     stat_begin(h, KC_SWAP, 32.0 * double(half), ev);
-    if (h->p2p && st == h->state && h->peer_state[j]) {
+    double2* peer = peer_of(h, st, j);
+    if (peer) {
       // Peer-memory swap: our (top = 1-b) half and the partner's (top = b) half exchange
       // element by element, in place, through the partner's state mapped over NVLink.  The two
       // ranks split the range (b = 0 the first half, b = 1 the second); barriers before (the
@@ -77,7 +133,7 @@ void global_swap_top(sv_handle* h, const std::vector<double2*>& states, int G) {
       const u64 share = half >> 1, lo = b ? share : 0;
       const u64 peer_off = b ? half : 0;
       device_barrier(h);
-      launch_exchange(h, st + my_off + lo, h->peer_state[j] + peer_off + lo, b ? half - share : share);
+      launch_exchange(h, st + my_off + lo, peer + peer_off + lo, b ? half - share : share);
       device_barrier(h);
       stat_end(h, KC_SWAP, 32.0 * double(half), ev);
       continue;
@@ -138,48 +194,31 @@ void dist_init(sv_handle* h, const void* nccl_id) {
   }
   CUDA_CHECK(cudaMalloc(&h->d_barrier, 64 * sizeof(int)));
   CUDA_CHECK(cudaMemset(h->d_barrier, 0, 64 * sizeof(int)));
-  // Peer-memory swaps: map every partner's state (rank ^ 2^j) through CUDA IPC.  Any rank
-  // failing to map (no P2P path, SVB200_P2P_SWAP=0) turns the feature off on every rank, and
-  // the swaps use NCCL send/recv.
+  // Peer-memory swaps: map every partner's state (rank ^ 2^j) through CUDA IPC now; other
+  // swapped buffers (adjoint lambdas) register on their first swap.  Any rank failing to map
+  // (no P2P path, SVB200_P2P_SWAP=0) turns the feature off on every rank: NCCL send/recv.
   const char* env = std::getenv("SVB200_P2P_SWAP");
-  int ok = (env && env[0] == '0') ? 0 : 1;
-  const int gbits = h->g;
-  cudaIpcMemHandle_t mine;
-  std::memset(&mine, 0, sizeof(mine));
-  if (ok && cudaIpcGetMemHandle(&mine, h->state) != cudaSuccess) {
-    cudaGetLastError();
-    ok = 0;
-  }
-  const size_t hb = sizeof(cudaIpcMemHandle_t);
-  char* d_handles = nullptr;
-  CUDA_CHECK(cudaMalloc(&d_handles, hb * (h->world + 1)));
-  CUDA_CHECK(cudaMemcpy(d_handles + hb * h->world, &mine, hb, cudaMemcpyHostToDevice));
-  NCCL_CHECK(ncclAllGather(d_handles + hb * h->world, d_handles, hb, ncclChar, h->comm, h->stream));
-  std::vector<cudaIpcMemHandle_t> all(h->world);
-  CUDA_CHECK(cudaMemcpyAsync(all.data(), d_handles, hb * h->world, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
-  CUDA_CHECK(cudaFree(d_handles));
-  for (int j = 0; ok && j < gbits && j < 8; ++j) {
-    void* p = nullptr;
-    if (cudaIpcOpenMemHandle(&p, all[h->rank ^ (1 << j)], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
-      cudaGetLastError();
-      ok = 0;
-      break;
-    }
-    h->peer_state[j] = static_cast<double2*>(p);
-  }
+  int want = (env && env[0] == '0') ? 0 : 1;
   int* d_ok = h->d_barrier + 1;
-  CUDA_CHECK(cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_CHECK(cudaMemcpy(d_ok, &want, sizeof(int), cudaMemcpyHostToDevice));
   NCCL_CHECK(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, h->comm, h->stream));
-  CUDA_CHECK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_CHECK(cudaMemcpyAsync(&want, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CUDA_CHECK(cudaStreamSynchronize(h->stream));
-  h->p2p = ok != 0;
-  if (!h->p2p)
-    for (int j = 0; j < 8; ++j)
-      if (h->peer_state[j]) {
-        cudaIpcCloseMemHandle(h->peer_state[j]);
-        h->peer_state[j] = nullptr;
-      }
+  h->p2p = want && register_peers(h, h->state);
+}
+
+void dist_forget(sv_handle* h, double2* buf) {
+  if (!h->p2p || !h->comm) return;
+  for (size_t i = 0; i < h->peers.size(); ++i)
+    if (h->peers[i].local == buf) {
+      // every rank is done with every mapping of this buffer before any rank unmaps or frees it
+      if (ncclAllReduce(h->d_barrier, h->d_barrier, 1, ncclInt, ncclSum, h->comm, h->stream) == ncclSuccess)
+        cudaStreamSynchronize(h->stream);
+      for (int j = 0; j < 8; ++j)
+        if (h->peers[i].peer[j]) cudaIpcCloseMemHandle(h->peers[i].peer[j]);
+      h->peers.erase(h->peers.begin() + long(i));
+      return;
+    }
 }
 
 void dist_destroy(sv_handle* h) {
@@ -188,11 +227,10 @@ void dist_destroy(sv_handle* h) {
     if (ncclAllReduce(h->d_barrier, h->d_barrier, 1, ncclInt, ncclSum, h->comm, h->stream) == ncclSuccess)
       cudaStreamSynchronize(h->stream);
   }
-  for (int j = 0; j < 8; ++j)
-    if (h->peer_state[j]) {
-      cudaIpcCloseMemHandle(h->peer_state[j]);
-      h->peer_state[j] = nullptr;
-    }
+  for (auto& pm : h->peers)
+    for (int j = 0; j < 8; ++j)
+      if (pm.peer[j]) cudaIpcCloseMemHandle(pm.peer[j]);
+  h->peers.clear();
   h->p2p = false;
   if (h->d_barrier) {
     cudaFree(h->d_barrier);

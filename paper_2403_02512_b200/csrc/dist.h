@@ -10,6 +10,8 @@
 
 void dist_init(sv_handle* h, const void* nccl_id);
 void dist_destroy(sv_handle* h);
+// collective: unmap a buffer's peer copies before it is freed (no-op if it was never swapped)
+void dist_forget(sv_handle* h, double2* buf);
 bool prim_needs_swap(const Prim& p, int nl);
 // make the given wires local (dense targets of one op), choosing victims outside `wires`
 void dist_make_local(sv_handle* h, const std::vector<double2*>& states, const std::vector<int>& wires);

@@ -113,9 +113,14 @@ struct sv_handle {
   cudaStream_t copy_stream = nullptr;          // swap pipeline: staging -> state copies
   cudaEvent_t ev_recv[2] = {nullptr, nullptr};
   cudaEvent_t ev_copy[2] = {nullptr, nullptr};
-  // peer-memory swaps (dist.cpp): the partner's state mapped through CUDA IPC, per global bit
+  // peer-memory swaps (dist.cpp): each swapped buffer's partner copies mapped through CUDA
+  // IPC, per global bit j (partner rank ^ 2^j); registered collectively on first swap
+  struct PeerMap {
+    double2* local;
+    double2* peer[8];
+  };
   bool p2p = false;
-  double2* peer_state[8] = {nullptr};
+  std::vector<PeerMap> peers;
   int* d_barrier = nullptr;
   // reduction scratch
   double* d_partials = nullptr;
