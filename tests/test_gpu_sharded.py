@@ -97,3 +97,50 @@ def test_sharded_nccl_matches_oracle(world):
     for k, v in out.items():
         tol = 1e-10 if "j" in k else 1e-12
         assert v < tol, (k, v)
+
+
+def _swap_path_worker(rank, world, nccl_ids, q):
+    try:
+        import os
+        from paper_2403_02512_b200.device import Device
+        n = 14
+        ops = workloads.random_circuit(n, 12, seed=8)
+        qaoa_ops, qaoa_h, _ = workloads.qaoa_maxcut(n, p=2, seed=3)
+        res = []
+        for i, flag in enumerate(("1", "0")):   # peer-memory swaps, then the NCCL send/recv fallback
+            os.environ["SVB200_P2P_SWAP"] = flag
+            d = Device.sharded(n, rank, world, nccl_ids[2 * i], device=rank)
+            d.apply(ops)
+            st = d.get_state()
+            d.release()
+            d = Device.sharded(n, rank, world, nccl_ids[2 * i + 1], device=rank)
+            jac = d.adjoint_jacobian(qaoa_ops, [qaoa_h])
+            d.release()
+            res.append((st, jac))
+        if rank == 0:
+            same_state = bool(np.array_equal(res[0][0].view(np.uint64), res[1][0].view(np.uint64)))
+            same_jac = bool(np.array_equal(res[0][1], res[1][1]))
+            q.put(("ok", {"state": same_state, "jac": same_jac}))
+    except Exception as exc:
+        import traceback
+        q.put(("err", f"rank {rank}: {exc}\n{traceback.format_exc()}"))
+
+
+def test_peer_memory_swap_bit_identical_to_nccl_swap():
+    """The peer-memory exchange kernel and the NCCL send/recv path move the same amplitudes:
+    states and Jacobians must agree bit for bit."""
+    world = 2
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    from paper_2403_02512_b200.device import Device
+    nccl_ids = [Device.nccl_unique_id() for _ in range(4)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_swap_path_worker, args=(r, world, nccl_ids, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    status, out = q.get(timeout=600)
+    for p in procs:
+        p.join(timeout=120)
+    assert status == "ok", out
+    assert out == {"state": True, "jac": True}, out
