@@ -374,7 +374,24 @@ static double expval_impl(sv_handle* h, const sv_obs& o) {
       CUDA_CHECK(cudaMemcpyAsync(z, h->d_results, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
       CUDA_CHECK(cudaStreamSynchronize(h->stream));
     } else {
-      sv_fail(SV_ERR_UNSUPPORTED, "dense observables on more than 4 wires are not supported yet");
+      // 5+ wires: lambda = O psi in one extra buffer (smem DENSE kernel), then Re<psi|lambda>
+      size_t free_b = 0, total_b = 0;
+      CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
+      const size_t bytes = h->n_local * amp_bytes(h);
+      double lacking = (bytes + (64ull << 20) > free_b) ? 1.0 : 0.0;
+      dist_allreduce_sum(h, &lacking, 1);
+      if (lacking > 0) sv_fail(SV_ERR_CAPACITY, "dense observable on more than 4 wires needs one extra state buffer");
+      double2* lam = nullptr;
+      CUDA_CHECK(cudaMalloc(&lam, bytes));
+      try {
+        launch_copy(h, lam, h->state, h->n_local);
+        launch_prim(h, lam, g);
+        z[0] = reduce_dot_re(h, h->state, lam);
+      } catch (...) {
+        cudaFree(lam);
+        throw;
+      }
+      CUDA_CHECK(cudaFree(lam));
     }
     double v = z[0];
     dist_allreduce_sum(h, &v, 1);

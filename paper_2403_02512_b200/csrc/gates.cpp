@@ -335,6 +335,7 @@ void classify_prim(Prim& p) {
       p.m.assign(1, v);
       return;
     }
+    if (k > 6) return;   // DIAG tables hold <= 64 entries; wider diagonals stay DENSE
     std::vector<cplx> t(d);
     for (size_t r = 0; r < d; ++r) t[r] = p.m[r * d + r];
     p.type = PRIM_DIAG;

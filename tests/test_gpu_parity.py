@@ -504,3 +504,58 @@ def test_interpreter_kernel_matches_oracle_subprocess():
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout + r.stderr
     assert r.stdout.startswith("ok")
+
+
+@pytest.mark.parametrize("wires", [(9, 0, 4, 6, 2), (1, 3, 5, 7, 8, 10)])
+def test_dense_observable_many_wires(wires):
+    """DenseHermitian on 5+ wires: lambda = O psi in a scratch buffer through the
+    shared-memory DENSE kernel, then Re<psi|lambda>; expval and variance vs the oracle."""
+    rng = np.random.default_rng(len(wires))
+    n = 11
+    psi = rand_state(rng, n)
+    dim = 1 << len(wires)
+    m = rng.normal(size=(dim, dim)) + 1j * rng.normal(size=(dim, dim))
+    obs = DenseHermitian(wires, m + m.conj().T)
+    with Device(n) as d:
+        d.set_state(psi)
+        assert abs(d.expval(obs) - O.expval(psi, n, obs)) < 1e-10 * max(1.0, np.abs(obs.matrix).sum())
+        got, ref = d.var(obs), O.variance(psi, n, obs)
+        assert abs(got - ref) <= 1e-10 * max(1.0, np.abs(obs.matrix).sum() ** 2)
+        assert np.abs(d.get_state() - psi).max() == 0.0        # expval leaves the state untouched
+
+
+@pytest.mark.parametrize("fuse", [False, True])
+def test_wide_diagonal_matrix(fuse):
+    """A diagonal apply_matrix on 7 wires (state.py:278-303) stays a DENSE primitive (DIAG tables
+    hold <= 64 entries) and matches the oracle."""
+    rng = np.random.default_rng(5)
+    n = 10
+    psi = rand_state(rng, n)
+    wires = (9, 0, 4, 6, 2, 7, 1)
+    m = np.diag(np.exp(1j * rng.uniform(0, 2 * np.pi, 1 << len(wires))))
+    op = Op("Matrix", wires, matrix=m)
+    ref = psi.copy()
+    O.apply_op(ref, n, op)
+    with Device(n) as d:
+        d.set_state(psi)
+        d.apply([op], fuse=fuse)
+        assert np.abs(d.get_state() - ref).max() < STATE_TOL
+
+
+@pytest.mark.parametrize("fuse", [False, True])
+def test_adjoint_dense_observable_many_wires(fuse):
+    """adjoint_jacobian with a 5-wire DenseHermitian observable (lambda = O psi through the
+    shared-memory DENSE kernel) vs the oracle."""
+    rng = np.random.default_rng(77)
+    n = 8
+    ops = workloads.random_circuit(n, 5, seed=3)
+    for op in ops:
+        if ARITY[op.name][1]:
+            op.trainable = (True,) * ARITY[op.name][1]
+    m = rng.normal(size=(32, 32)) + 1j * rng.normal(size=(32, 32))
+    obs = [DenseHermitian((6, 1, 3, 0, 7), m + m.conj().T)]
+    ref, ref_ev = O.adjoint_jacobian(n, ops, obs)
+    with Device(n) as d:
+        jac, ev = d.adjoint_jacobian(ops, obs, return_expvals=True, fuse=fuse)
+    assert_grad_close(jac, ref, obs)
+    assert abs(ev[0] - ref_ev[0]) < 1e-10 * max(1.0, obs_norm1(obs[0]))

@@ -94,3 +94,13 @@ def test_parity_and_shear_cases_are_exercised():
     assert any(106 <= c < 122 for c in cases), "IsingZZ should plan to CS_PARITY"
     assert any(90 <= c < 106 for c in cases), "rotations should plan to CS_SHEAR"
     assert any(106 <= op["cs"] < 122 and op["xm"] for op in prog["ops"]), "some parity bits off the registers"
+
+
+def test_wide_diagonal_matrix_program():
+    """A 7-wire diagonal Matrix stays a DENSE primitive (DIAG tables hold <= 64 entries) and the
+    planned program still reproduces the oracle."""
+    rng = np.random.default_rng(5)
+    n = 13
+    m = np.diag(np.exp(1j * rng.uniform(0, 2 * np.pi, 128)))
+    ops = [Op("H", (q,)) for q in range(n)] + [Op("Matrix", (12, 0, 4, 6, 2, 7, 1), matrix=m), Op("RX", (3,), (0.3,))]
+    check(n, ops)
