@@ -11,7 +11,7 @@ import torch.multiprocessing as mp
 
 from oracle import svoracle as O
 from paper_2403_02512_b200 import workloads
-from paper_2403_02512_b200.observables import Hamiltonian, PauliWord
+from paper_2403_02512_b200.observables import DenseHermitian, Hamiltonian, PauliWord
 from paper_2403_02512_b200.ops import Op
 
 pytestmark = pytest.mark.gpu
@@ -33,6 +33,8 @@ def _worker(rank, world, nccl_ids, q):
         ops += [Op("SWAP", (0, 11)), Op("IsingXX", (1, 0), (0.3,)), Op("CNOT", (0, 1), ctrls=(5,)),
                 Op("DoubleExcitation", (0, 1, 6, 7), (0.4,)), Op("RZ", (1,), (0.7,), ctrls=(0,))]
         res = {}
+        m = rng.normal(size=(32, 32)) + 1j * rng.normal(size=(32, 32))
+        dense = DenseHermitian((0, 9, 1, 4, 6), m + m.conj().T)
         for fuse in (False, True):
             d = Device.sharded(n, rank, world, nccl_ids[int(fuse)], device=rank, fuse=fuse)
             d.set_state(psi)
@@ -45,6 +47,7 @@ def _worker(rank, world, nccl_ids, q):
             res[f"norm{int(fuse)}"] = d.norm()
             res[f"samp{int(fuse)}"] = d.sample_indices(5000, seed=99, wires=[0, 7, 1, 11])
             res[f"var{int(fuse)}"] = d.var(ham)
+            res[f"dense{int(fuse)}"] = d.expval(dense)     # 5 wires incl. global qubit 0
             d.release()
         sel_ops, obs = workloads.sel_config(n, 2, seed=2)
         qaoa_ops, qaoa_h, _ = workloads.qaoa_maxcut(n, p=2, seed=1)
@@ -66,6 +69,7 @@ def _worker(rank, world, nccl_ids, q):
                 out[f"norm{f}"] = abs(res[f"norm{f}"] - 1.0)
                 out[f"samp{f}"] = float((res[f"samp{f}"] != O.sample(ref, n, 5000, seed=99, wires=[0, 7, 1, 11])).sum()) * 5e-13
                 out[f"var{f}"] = abs(res[f"var{f}"] - O.variance(ref, n, ham))
+                out[f"dense{f}"] = abs(res[f"dense{f}"] - O.expval(ref, n, dense)) / max(1.0, np.abs(dense.matrix).sum())
             refs = {"": O.adjoint_jacobian(n, sel_ops, obs[:3]), "q": O.adjoint_jacobian(n, qaoa_ops, [qaoa_h]),
                     "h": O.adjoint_jacobian(n, hea_ops, [hea_h])}
             for key, (jref, evref) in refs.items():
