@@ -190,7 +190,7 @@ def run_reference(args, rank, world):
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "vs_baseline": None,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def main():
@@ -353,12 +353,27 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clocks, "expval_check": ev, "comm": comm,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     dev.release()
     if pg:
         pg.barrier()
         pg.destroy_process_group()
 
 
+_JSON_OUT = None
+
+
+def emit(line):
+    """The one JSON line goes to the original stdout; everything else was moved to stderr."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 if __name__ == "__main__":
+    # NCCL prints "NCCL version ..." straight to fd 1 from C at communicator init whatever
+    # NCCL_DEBUG_FILE says; keep stdout the single JSON line by pointing fd 1 at stderr.
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     main()

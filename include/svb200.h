@@ -133,6 +133,8 @@ int sv_apply_matrix(sv_handle* h, const int32_t* wires, int n_wires, const doubl
 int sv_apply_ops(sv_handle* h, const sv_op* ops, int n_ops, int fuse);
 
 /* ---- measurements ---- */
+/* Dense observables: <= 4 wires as one in-register bra-ket pass; 5..12 wires need one extra
+ * state buffer (lambda = O psi, then Re<psi|lambda>), SV_ERR_CAPACITY when it does not fit. */
 int sv_expval(sv_handle* h, const sv_obs* obs, double* out);
 int sv_probs(sv_handle* h, const int32_t* wires, int n_wires, double* out); /* n_wires=0: all */
 /* <O^2> - <O>^2 (Pauli word: 1 - <P>^2; otherwise |O psi|^2 - <psi|O psi>^2). */

@@ -114,7 +114,9 @@ def test_f32_measurements_vs_oracle():
     psi = c64(rand_state(rng, n))
     ref_psi = psi.astype(np.complex128)
     obs = [PauliWord(((0, "Z"), (3, "X"), (7, "Y"))), workloads.random_pauli_hamiltonian(n, 40, seed=3),
-           DenseHermitian((4, 1), np.diag([1.0, -2.0, 0.5, 3.0]).astype(complex))]
+           DenseHermitian((4, 1), np.diag([1.0, -2.0, 0.5, 3.0]).astype(complex)),
+           DenseHermitian((9, 0, 5, 2, 6), (lambda a: (a + a.conj().T) / 16)(
+               rng.normal(size=(32, 32)) + 1j * rng.normal(size=(32, 32))))]   # 5 wires: scratch-buffer path
     with Device(n, precision="f32") as d:
         d.set_state(psi)
         for o in obs:
