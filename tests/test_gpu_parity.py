@@ -559,3 +559,28 @@ def test_adjoint_dense_observable_many_wires(fuse):
         jac, ev = d.adjoint_jacobian(ops, obs, return_expvals=True, fuse=fuse)
     assert_grad_close(jac, ref, obs)
     assert abs(ev[0] - ref_ev[0]) < 1e-10 * max(1.0, obs_norm1(obs[0]))
+
+
+@pytest.mark.parametrize("n", [12, 15, 17])
+def test_diagonal_hamiltonian_wht_expval(n):
+    """Z-only Hamiltonians with >= 8 terms on states of >= 2^12 amplitudes take the per-tile
+    Walsh-Hadamard kernel (k_pauli_diag_wht): identity, low-only, high-only and mixed masks,
+    repeated masks, and MaxCut's C = sum 1/2 (I - Z_i Z_j), vs the oracle."""
+    rng = np.random.default_rng(n)
+    psi = rand_state(rng, n)
+    words = [PauliWord(())]
+    for _ in range(40):
+        k = int(rng.integers(1, 5))
+        qs = rng.choice(n, size=k, replace=False)
+        words.append(PauliWord(tuple((int(q), "Z") for q in qs)))
+    words += [words[3], PauliWord(((0, "Z"),)), PauliWord(((n - 1, "Z"),)), PauliWord(((0, "Z"), (n - 1, "Z")))]
+    ham = Hamiltonian(list(rng.normal(size=len(words))), words)
+    _, cost, _ = workloads.qaoa_maxcut(n, p=1, seed=1)
+    with Device(n) as d:
+        d.set_state(psi)
+        for h in (ham, cost):
+            assert abs(d.expval(h) - O.expval(psi, n, h)) < 1e-12 * max(1.0, obs_norm1(h))
+    with Device(n, precision="f32") as d:
+        d.set_state(psi.astype(np.complex64))
+        ref = O.expval(psi.astype(np.complex64).astype(np.complex128), n, ham)
+        assert abs(d.expval(ham) - ref) < 1e-9 * max(1.0, obs_norm1(ham))
