@@ -483,7 +483,7 @@ __device__ __forceinline__ int wht_swz(int L) {   // double index -> swizzled do
 }
 
 template <class C>
-__global__ void __launch_bounds__(kThreads) k_pauli_diag_wht(const C* __restrict__ a, u64 ntiles,
+__global__ void __launch_bounds__(kThreads, 2) k_pauli_diag_wht(const C* __restrict__ a, u64 ntiles,
                                                              const DiagGroupDev* __restrict__ groups, int ngroups,
                                                              const DiagTermDev* __restrict__ terms,
                                                              double* __restrict__ partials) {
@@ -492,18 +492,24 @@ __global__ void __launch_bounds__(kThreads) k_pauli_diag_wht(const C* __restrict
   double acc[1] = {0.0};
   for (u64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const u64 H = tile << kWhtBits;
-    // amplitudes of layout B, issued first so the loads overlap the transform
-    double p[16];
+    // amplitudes of layout B, issued first and consumed last so the loads overlap the transform;
+    // the next tile is prefetched into L2 (two 128-byte lines per thread)
+    C x[16];
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const u64 L = (u64(tid) << 1) | (u64(q) << 9);
-      const double2 x0 = wide(a[H + L]), x1 = wide(a[H + L + 1]);
-      p[2 * q] = fma(x0.x, x0.x, x0.y * x0.y);
-      p[2 * q + 1] = fma(x1.x, x1.x, x1.y * x1.y);
+      x[2 * q] = a[H + L];
+      x[2 * q + 1] = a[H + L + 1];
+    }
+    if (tile + gridDim.x < ntiles) {
+      const char* nxt = reinterpret_cast<const char*>(a + ((tile + gridDim.x) << kWhtBits));
+      const size_t per_thread = (size_t(1) << kWhtBits) * sizeof(C) / kThreads;   // 256 B (c128) / 128 B (c64)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(nxt + tid * per_thread));
+      if (per_thread > 128) asm volatile("prefetch.global.L2 [%0];" ::"l"(nxt + tid * per_thread + 128));
     }
     // C_H scattered into the (swizzled) table
 #pragma unroll
-    for (int j = 0; j < 16; ++j) T[(tid << 4) | j] = 0.0;   // zeroing order is irrelevant (all entries)
+    for (int j = 0; j < 16; ++j) T[tid + j * kThreads] = 0.0;   // all entries, conflict-free
     __syncthreads();
     for (int g = tid; g < ngroups; g += kThreads) {
       double c = 0.0;
@@ -515,7 +521,11 @@ __global__ void __launch_bounds__(kThreads) k_pauli_diag_wht(const C* __restrict
     // layout A: L = tid*16 + j
     double v[16];
 #pragma unroll
-    for (int j = 0; j < 16; ++j) v[j] = T[wht_swz((tid << 4) | j)];
+    for (int q = 0; q < 8; ++q) {   // 16-byte accesses: conflict-free per quarter warp with the swizzle
+      const double2 t2 = *reinterpret_cast<const double2*>(&T[wht_swz((tid << 4) | (2 * q))]);
+      v[2 * q] = t2.x;
+      v[2 * q + 1] = t2.y;
+    }
 #pragma unroll
     for (int b = 0; b < 4; ++b)
 #pragma unroll
@@ -535,7 +545,8 @@ __global__ void __launch_bounds__(kThreads) k_pauli_diag_wht(const C* __restrict
       }
     }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) T[wht_swz((tid << 4) | j)] = v[j];   // own entries: no hazard
+    for (int q = 0; q < 8; ++q)   // own entries: no hazard
+      *reinterpret_cast<double2*>(&T[wht_swz((tid << 4) | (2 * q))]) = make_double2(v[2 * q], v[2 * q + 1]);
     __syncthreads();
     // layout B: register j' = b0 | (b9..11 << 1)
 #pragma unroll
@@ -555,7 +566,10 @@ __global__ void __launch_bounds__(kThreads) k_pauli_diag_wht(const C* __restrict
           v[j | (1 << b)] = x - y;
         }
 #pragma unroll
-    for (int j = 0; j < 16; ++j) acc[0] = fma(p[j], v[j], acc[0]);
+    for (int j = 0; j < 16; ++j) {
+      const double2 w = wide(x[j]);
+      acc[0] = fma(fma(w.x, w.x, w.y * w.y), v[j], acc[0]);
+    }
     __syncthreads();   // the next tile rewrites T
   }
   block_reduce_store<1>(acc, partials);
