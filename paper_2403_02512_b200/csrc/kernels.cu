@@ -483,7 +483,7 @@ __device__ __forceinline__ int wht_swz(int L) {   // double index -> swizzled do
 }
 
 template <class C>
-__global__ void __launch_bounds__(kThreads, 2) k_pauli_diag_wht(const C* __restrict__ a, u64 ntiles,
+__global__ void __launch_bounds__(kThreads, 2) k_pauli_diag_wht(const C* __restrict__ a, C* __restrict__ out, u64 ntiles,
                                                              const DiagGroupDev* __restrict__ groups, int ngroups,
                                                              const DiagTermDev* __restrict__ terms,
                                                              double* __restrict__ partials) {
@@ -565,14 +565,24 @@ __global__ void __launch_bounds__(kThreads, 2) k_pauli_diag_wht(const C* __restr
           v[j] = x + y;
           v[j | (1 << b)] = x - y;
         }
+    if (out) {   // lambda = f psi (the adjoint's lambda initialisation, K10 for one diagonal group)
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const double2 w = wide(x[j]);
-      acc[0] = fma(fma(w.x, w.x, w.y * w.y), v[j], acc[0]);
+      for (int q = 0; q < 8; ++q) {
+        const u64 L = (u64(tid) << 1) | (u64(q) << 9);
+        const double2 w0 = wide(x[2 * q]), w1 = wide(x[2 * q + 1]);
+        out[H + L] = narrow<C>(make_double2(v[2 * q] * w0.x, v[2 * q] * w0.y));
+        out[H + L + 1] = narrow<C>(make_double2(v[2 * q + 1] * w1.x, v[2 * q + 1] * w1.y));
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const double2 w = wide(x[j]);
+        acc[0] = fma(fma(w.x, w.x, w.y * w.y), v[j], acc[0]);
+      }
     }
     __syncthreads();   // the next tile rewrites T
   }
-  block_reduce_store<1>(acc, partials);
+  if (!out) block_reduce_store<1>(acc, partials);
 }
 
 // K10: lambda (+)= sum_t cc_t (-1)^{pc((i^x) & z_t)} psi_{i^x}   (PauliApplyTermDev: see above)
@@ -963,6 +973,43 @@ double reduce_norm2(sv_handle* h, const double2* a) {
   return out;
 }
 
+// Diagonal group through k_pauli_diag_wht: out == nullptr -> per-block partials of
+// sum_i |psi_i|^2 f(i) (returns the grid); otherwise out = f psi.  Terms are grouped by their low
+// 12 mask bits on the host (fixed order -> deterministic sums); real coefficients only.
+static unsigned pauli_diag_wht(sv_handle* h, const double2* a, double2* out, const std::vector<PauliTerm>& terms) {
+  const u64 lo = (u64(1) << kWhtBits) - 1;
+  std::vector<size_t> order(terms.size());
+  for (size_t t = 0; t < order.size(); ++t) order[t] = t;
+  std::stable_sort(order.begin(), order.end(),
+                   [&](size_t x, size_t y) { return (terms[x].zmask & lo) < (terms[y].zmask & lo); });
+  std::vector<DiagGroupDev> gr;
+  std::vector<DiagTermDev> tm;
+  for (size_t k = 0; k < order.size(); ++k) {
+    const PauliTerm& t = terms[order[k]];
+    const unsigned zl = unsigned(t.zmask & lo);
+    if (gr.empty() || gr.back().zlo != zl) gr.push_back({zl, int(k), int(k)});
+    tm.push_back({t.zmask & ~lo, t.cc.real()});
+    gr.back().last = int(k) + 1;
+  }
+  // one upload: terms first (8-byte aligned), then the groups
+  const size_t tb = tm.size() * sizeof(DiagTermDev);
+  std::vector<char> blob(tb + gr.size() * sizeof(DiagGroupDev));
+  std::memcpy(blob.data(), tm.data(), tb);
+  std::memcpy(blob.data() + tb, gr.data(), gr.size() * sizeof(DiagGroupDev));
+  auto* d_blob = (const char*)scratch_upload(h, blob.data(), blob.size());
+  const u64 ntiles = h->n_local >> kWhtBits;
+  const unsigned g = unsigned(std::min<u64>(ntiles, 148ull * 6));
+  ensure_partials(h, g);
+  cudaEvent_t ev[2];
+  const double bytes = (out ? 2.0 : 1.0) * double(amp_bytes(h)) * double(h->n_local);
+  stat_begin(h, out ? KC_APPLY_OBS : KC_REDUCE, bytes, ev);
+  SV_LAUNCH2(h, k_pauli_diag_wht, SV_CFG(g, kThreads, 0, h->stream), a, out, ntiles, (const DiagGroupDev*)(d_blob + tb),
+            int(gr.size()), (const DiagTermDev*)d_blob, h->d_partials);
+  stat_end(h, out ? KC_APPLY_OBS : KC_REDUCE, bytes, ev);
+  CUDA_CHECK(cudaGetLastError());
+  return g;
+}
+
 void pauli_group_expval_async(sv_handle* h, const double2* a, u64 xmask, const std::vector<PauliTerm>& terms,
                               double* d_out) {
   std::vector<PauliTermDev> dt(terms.size());
@@ -981,41 +1028,12 @@ void pauli_group_expval_async(sv_handle* h, const double2* a, u64 xmask, const s
   }
   const u64 count = xmask ? (h->n_local >> 1) : h->n_local;
   if (xmask == 0 && terms.size() >= 8 && h->n_local >= (u64(1) << kWhtBits)) {
-    // group the terms by their low 12 mask bits (host, fixed order -> deterministic sums)
-    const u64 lo = (u64(1) << kWhtBits) - 1;
-    std::vector<size_t> order(terms.size());
-    for (size_t t = 0; t < order.size(); ++t) order[t] = t;
-    std::stable_sort(order.begin(), order.end(),
-                     [&](size_t x, size_t y) { return (terms[x].zmask & lo) < (terms[y].zmask & lo); });
-    std::vector<DiagGroupDev> gr;
-    std::vector<DiagTermDev> tm;
-    for (size_t k = 0; k < order.size(); ++k) {
-      const PauliTerm& t = terms[order[k]];
-      const unsigned zl = unsigned(t.zmask & lo);
-      if (gr.empty() || gr.back().zlo != zl) gr.push_back({zl, int(k), int(k)});
-      tm.push_back({t.zmask & ~lo, t.cc.real()});
-      gr.back().last = int(k) + 1;
-    }
-    // one upload: terms first (8-byte aligned), then the groups
-    const size_t tb = tm.size() * sizeof(DiagTermDev);
-    std::vector<char> blob(tb + gr.size() * sizeof(DiagGroupDev));
-    std::memcpy(blob.data(), tm.data(), tb);
-    std::memcpy(blob.data() + tb, gr.data(), gr.size() * sizeof(DiagGroupDev));
-    auto* d_blob = (const char*)scratch_upload(h, blob.data(), blob.size());
-    const u64 ntiles = h->n_local >> kWhtBits;
-    const unsigned g = unsigned(std::min<u64>(ntiles, 148ull * 6));
-    ensure_partials(h, g);
-    cudaEvent_t ev[2];
-    const double bytes = double(amp_bytes(h)) * double(h->n_local);
-    stat_begin(h, KC_REDUCE, bytes, ev);
-    SV_LAUNCH(h, k_pauli_diag_wht, SV_CFG(g, kThreads, 0, h->stream), a, ntiles, (const DiagGroupDev*)(d_blob + tb),
-              int(gr.size()), (const DiagTermDev*)d_blob, h->d_partials);
-    stat_end(h, KC_REDUCE, bytes, ev);
-    CUDA_CHECK(cudaGetLastError());
+    const unsigned g = pauli_diag_wht(h, a, nullptr, terms);
     sum_partials(h, h->d_partials, g, 1, d_out);
     return;
   }
   const unsigned g = red_grid(count);
+
   ensure_partials(h, g);
   auto* d_terms = (const PauliTermDev*)scratch_upload(h, dt.data(), dt.size() * sizeof(PauliTermDev));
   size_t smem = dt.size() * sizeof(PauliTermDev);
@@ -1057,8 +1075,22 @@ void pauli_group_apply(sv_handle* h, const double2* psi, double2* lam, u64 xmask
 }
 
 void pauli_groups_apply(sv_handle* h, const double2* psi, double2* lam,
-                        const std::vector<std::pair<u64, std::vector<PauliTerm>>>& groups) {
+                        const std::vector<std::pair<u64, std::vector<PauliTerm>>>& all_groups) {
   const unsigned g = unsigned(std::min<u64>(grid_for(h->n_local, kThreads * 4), 148ull * 64));
+  // a diagonal group with many real Z terms goes through the per-tile WHT kernel (writes lam),
+  // the other x-groups accumulate on top of it
+  std::vector<std::pair<u64, std::vector<PauliTerm>>> groups;
+  bool written = false;
+  for (const auto& gr : all_groups) {
+    bool diag = !written && gr.first == 0 && gr.second.size() >= 8 && h->n_local >= (u64(1) << kWhtBits);
+    for (const auto& t : gr.second) diag = diag && t.cc.imag() == 0.0;
+    if (diag) {
+      pauli_diag_wht(h, psi, lam, gr.second);
+      written = true;
+    } else {
+      groups.push_back(gr);
+    }
+  }
   for (size_t g0 = 0; g0 < groups.size(); g0 += kMaxXG) {
     PauliGroupsArgs G;
     std::vector<PauliApplyTermDev> dt;
@@ -1074,7 +1106,7 @@ void pauli_groups_apply(sv_handle* h, const double2* psi, double2* lam,
     if (smem > 48 * 1024)
       for (const void* f : {(const void*)k_pauli_apply_multi<double2>, (const void*)k_pauli_apply_multi<float2>})
         CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    const int acc = g0 > 0;
+    const int acc = written || g0 > 0;
     const double bytes = (G.ng + 1.0 + (acc ? 1.0 : 0.0)) * double(amp_bytes(h)) * double(h->n_local);
     cudaEvent_t ev[2];
     stat_begin(h, KC_APPLY_OBS, bytes, ev);

@@ -584,3 +584,36 @@ def test_diagonal_hamiltonian_wht_expval(n):
         d.set_state(psi.astype(np.complex64))
         ref = O.expval(psi.astype(np.complex64).astype(np.complex128), n, ham)
         assert abs(d.expval(ham) - ref) < 1e-9 * max(1.0, obs_norm1(ham))
+
+
+@pytest.mark.parametrize("fuse", [False, True])
+def test_wht_lambda_adjoint_and_variance(fuse):
+    """lambda = H psi through the WHT kernel for the diagonal group (plus ordinary x-groups
+    accumulated on top): adjoint Jacobian and variance vs the oracle at n = 13."""
+    rng = np.random.default_rng(9)
+    n = 13
+    ops = workloads.random_circuit(n, 3, seed=2)
+    for op in ops:
+        if ARITY[op.name][1]:
+            op.trainable = (True,) * ARITY[op.name][1]
+    zw = [PauliWord(tuple((int(q), "Z") for q in rng.choice(n, size=int(rng.integers(1, 4)), replace=False)))
+          for _ in range(20)]
+    h_diag = Hamiltonian(list(rng.normal(size=20)), zw)
+    h_mixed = Hamiltonian(list(rng.normal(size=23)), zw + [PauliWord(((0, "X"), (5, "Z"))), PauliWord(((12, "Y"),)),
+                                                          PauliWord(((3, "X"), (4, "X")))])
+    obs = [h_diag, h_mixed]
+    ref, ref_ev = O.adjoint_jacobian(n, ops, obs)
+    with Device(n) as d:
+        jac, ev = d.adjoint_jacobian(ops, obs, return_expvals=True, fuse=fuse)
+    assert_grad_close(jac, ref, obs)
+    for k in range(2):
+        assert abs(ev[k] - ref_ev[k]) < 1e-10 * max(1.0, obs_norm1(obs[k]))
+    with Device(n) as d:
+        d.apply(ops)
+        psi = d.get_state()
+        for o in obs:
+            assert abs(d.var(o) - O.variance(psi, n, o)) <= 1e-10 * max(1.0, obs_norm1(o) ** 2)
+    _, jq = None, None
+    with Device(n) as d:   # single-observable fused sweep (lambda from the WHT kernel)
+        jac1 = d.adjoint_jacobian(ops, [h_diag], fuse=fuse)
+    assert_grad_close(jac1, ref[:1], [h_diag])
