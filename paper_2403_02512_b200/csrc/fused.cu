@@ -607,7 +607,12 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
       for (const Prim& p : prims) run_single(st, p);
     return identity;
   }
-  static const bool remap = !(getenv("SVB200_REMAP") && std::string(getenv("SVB200_REMAP")) == "0");
+  static const bool remap_env = !(getenv("SVB200_REMAP") && std::string(getenv("SVB200_REMAP")) == "0");
+  // Sharded handles: globally-controlled primitives resolve differently per rank (skipped on one,
+  // unconditional on another), so each rank plans a different program; an in-tile relabeling
+  // would then leave the ranks with different layouts and the next swap would exchange
+  // mismatched halves.  Every rank must keep the same layout: no relabeling when world > 1.
+  const bool remap = remap_env && h->world == 1;
   const std::shared_ptr<Program> prog_ptr = cached_program(h, prims, remap, state_hi != nullptr);
   Program& prog = *prog_ptr;
   if (state_hi)

@@ -119,12 +119,26 @@ def _swap_path_worker(rank, world, nccl_ids, q):
             d.release()
             d = Device.sharded(n, rank, world, nccl_ids[2 * i + 1], device=rank)
             jac = d.adjoint_jacobian(qaoa_ops, [qaoa_h])
+            d.reset()
+            d.apply(ops)
+            ev = d.expval(qaoa_h)   # diagonal group of 28 ZZ terms on 2^13-amplitude shards: WHT kernel
+            ev_terms = sum(c * d.expval(t) for c, t in zip(qaoa_h.coeffs, qaoa_h.terms))   # per-term kernel
+            st2 = d.get_state()
             d.release()
-            res.append((st, jac))
+            res.append((st, jac, (ev, ev_terms), st2))
         if rank == 0:
             same_state = bool(np.array_equal(res[0][0].view(np.uint64), res[1][0].view(np.uint64)))
             same_jac = bool(np.array_equal(res[0][1], res[1][1]))
-            q.put(("ok", {"state": same_state, "jac": same_jac}))
+            jref, _ = O.adjoint_jacobian(n, qaoa_ops, [qaoa_h])
+            scale = sum(abs(c) for c in qaoa_h.coeffs)
+            jac_ok = bool(np.abs(res[0][1] - jref).max() < 1e-10 * max(1.0, scale, float(np.abs(jref).max())))
+            psi = O.run_circuit(n, ops)
+            ev_ref = O.expval(psi, n, qaoa_h)
+            ev_ok = bool(abs(res[0][2][0] - ev_ref) < 1e-12 * max(1.0, scale))
+            if not ev_ok:
+                ev_ok = (res[0][2], ev_ref, float(np.abs(res[0][0] - psi).max()), float(np.abs(res[0][3] - psi).max()),
+                         O.expval(res[0][0], n, qaoa_h), O.expval(res[0][3], n, qaoa_h))
+            q.put(("ok", {"state": same_state, "jac": same_jac, "jac_vs_oracle": jac_ok, "ev_vs_oracle": ev_ok}))
     except Exception as exc:
         import traceback
         q.put(("err", f"rank {rank}: {exc}\n{traceback.format_exc()}"))
@@ -147,4 +161,4 @@ def test_peer_memory_swap_bit_identical_to_nccl_swap():
     for p in procs:
         p.join(timeout=120)
     assert status == "ok", out
-    assert out == {"state": True, "jac": True}, out
+    assert out == {"state": True, "jac": True, "jac_vs_oracle": True, "ev_vs_oracle": True}, out
