@@ -826,11 +826,7 @@ int sv_apply_ops(sv_handle* h, const sv_op* ops, int n_ops, int fuse) {
   API_BEGIN
   check_handle(h);
   std::lock_guard<std::mutex> lk(h->mu);
-  validate_ops(h, ops, n_ops);
-  for (int i = 0; i < n_ops; ++i)
-    if (ops[i].trainable_mask) {
-      // trainable flags are irrelevant for plain application; validation already checked arity
-    }
+  validate_ops(h, ops, n_ops);   // trainable flags are irrelevant for plain application
   run_ops(h, {h->state}, ops, n_ops, fuse);
   CUDA_CHECK(cudaStreamSynchronize(h->stream));
   API_END
@@ -912,26 +908,21 @@ int sv_var(sv_handle* h, const sv_obs* obs, double* out) {
     const double e = expval_impl(h, *obs);
     *out = 1.0 - e * e;
   } else {
-    release_adjoint_buffers(h);
+    // lambda lives in the handle's adjoint buffer (allocated once, kept; registered for peer
+    // swaps like any adjoint lambda and unmapped collectively when the handle releases it)
+    const size_t bytes = h->n_local * sizeof(double2);
     size_t free_b = 0, total_b = 0;
     CUDA_CHECK(cudaMemGetInfo(&free_b, &total_b));
-    const size_t bytes = h->n_local * amp_bytes(h);
-    double lacking = (bytes + (64ull << 20) > free_b) ? 1.0 : 0.0;
+    double lacking = (!h->adj_lam && bytes + (64ull << 20) > free_b) ? 1.0 : 0.0;
     dist_allreduce_sum(h, &lacking, 1);
     if (lacking > 0) sv_fail(SV_ERR_CAPACITY, "variance needs one extra state buffer");
     expval_impl(h, *obs);   // validates the observable (and its wires) like expval
-    double2* lam = nullptr;
-    CUDA_CHECK(cudaMalloc(&lam, bytes));
-    try {
-      apply_observable(h, *obs, h->state, lam, {h->state, lam});
-      double v[2] = {reduce_norm2(h, lam), reduce_dot_re(h, h->state, lam)};
-      dist_allreduce_sum(h, v, 2);
-      *out = v[0] - v[1] * v[1];
-    } catch (...) {
-      cudaFree(lam);
-      throw;
-    }
-    CUDA_CHECK(cudaFree(lam));
+    if (!h->adj_lam) CUDA_CHECK(cudaMalloc(&h->adj_lam, bytes));
+    double2* lam = h->adj_lam;
+    apply_observable(h, *obs, h->state, lam, {h->state, lam});
+    double v[2] = {reduce_norm2(h, lam), reduce_dot_re(h, h->state, lam)};
+    dist_allreduce_sum(h, v, 2);
+    *out = v[0] - v[1] * v[1];
   }
   API_END
 }

@@ -60,7 +60,7 @@ int register_peers(sv_handle* h, double2* buf) {
   const size_t hb = sizeof(cudaIpcMemHandle_t);
   char* d_handles = nullptr;
   CUDA_CHECK(cudaMalloc(&d_handles, hb * (h->world + 1)));
-  CUDA_CHECK(cudaMemcpy(d_handles + hb * h->world, &mine, hb, cudaMemcpyHostToDevice));
+  CUDA_CHECK(cudaMemcpyAsync(d_handles + hb * h->world, &mine, hb, cudaMemcpyHostToDevice, h->stream));
   NCCL_CHECK(ncclAllGather(d_handles + hb * h->world, d_handles, hb, ncclChar, h->comm, h->stream));
   std::vector<cudaIpcMemHandle_t> all(h->world);
   CUDA_CHECK(cudaMemcpyAsync(all.data(), d_handles, hb * h->world, cudaMemcpyDeviceToHost, h->stream));
@@ -79,7 +79,7 @@ int register_peers(sv_handle* h, double2* buf) {
     pm.peer[j] = static_cast<double2*>(p);
   }
   int* d_ok = h->d_barrier + 1;
-  CUDA_CHECK(cudaMemcpy(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_CHECK(cudaMemcpyAsync(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice, h->stream));
   NCCL_CHECK(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, h->comm, h->stream));
   CUDA_CHECK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CUDA_CHECK(cudaStreamSynchronize(h->stream));
@@ -193,14 +193,14 @@ void dist_init(sv_handle* h, const void* nccl_id) {
     CUDA_CHECK(cudaEventCreateWithFlags(&h->ev_copy[i], cudaEventDisableTiming));
   }
   CUDA_CHECK(cudaMalloc(&h->d_barrier, 64 * sizeof(int)));
-  CUDA_CHECK(cudaMemset(h->d_barrier, 0, 64 * sizeof(int)));
+  CUDA_CHECK(cudaMemsetAsync(h->d_barrier, 0, 64 * sizeof(int), h->stream));
   // Peer-memory swaps: map every partner's state (rank ^ 2^j) through CUDA IPC now; other
   // swapped buffers (adjoint lambdas) register on their first swap.  Any rank failing to map
   // (no P2P path, SVB200_P2P_SWAP=0) turns the feature off on every rank: NCCL send/recv.
   const char* env = std::getenv("SVB200_P2P_SWAP");
   int want = (env && env[0] == '0') ? 0 : 1;
   int* d_ok = h->d_barrier + 1;
-  CUDA_CHECK(cudaMemcpy(d_ok, &want, sizeof(int), cudaMemcpyHostToDevice));
+  CUDA_CHECK(cudaMemcpyAsync(d_ok, &want, sizeof(int), cudaMemcpyHostToDevice, h->stream));
   NCCL_CHECK(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, h->comm, h->stream));
   CUDA_CHECK(cudaMemcpyAsync(&want, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
   CUDA_CHECK(cudaStreamSynchronize(h->stream));

@@ -17,7 +17,13 @@
 //
 // Data movement, tiles, phases and results are exactly those of k_fused<*, false, *>; the pass
 // compiler only removes the interpreter.  SVB200_JIT=0 selects the interpreter (A/B timing).
+#include <fcntl.h>
 #include <nvrtc.h>
+#include <sys/stat.h>
+#include <sys/types.h>
+#include <unistd.h>
+
+#include <cerrno>
 
 #include <algorithm>
 #include <atomic>
@@ -229,18 +235,31 @@ std::map<std::string, std::shared_ptr<JitKernel>> g_jit;
 std::atomic<int64_t> g_jit_compiled{0};
 std::atomic<int64_t> g_jit_compile_us{0};
 
-// On-disk cubin cache shared by the processes of one machine (tests, smoke, bench): the file name
+// On-disk cubin cache shared by the processes of one user (tests, smoke, bench): the file name
 // is a 64-bit FNV-1a hash of the full source + compiler version + options, and the file stores the
 // full source too, so a hash collision is detected and ignored.  SVB200_JIT_CACHE=<dir> (default
-// $TMPDIR/svb200_jit); "0" disables.
+// $XDG_CACHE_HOME/svb200_jit, else $TMPDIR/svb200_jit-<uid>); "0" disables.  The directory is
+// created 0700 and used only when it is ours and not writable by group/others: a cubin planted
+// by another local user is never loaded.
 const char* kOptsKey = "sm_100a|c++17|lineinfo|restrict|default-device";
 
 std::string cache_dir() {
   const char* e = getenv("SVB200_JIT_CACHE");
   if (e && std::string(e) == "0") return std::string();
   if (e && *e) return e;
+  const char* x = getenv("XDG_CACHE_HOME");
+  if (x && *x) return std::string(x) + "/svb200_jit";
   const char* t = getenv("TMPDIR");
-  return std::string(t && *t ? t : "/tmp") + "/svb200_jit";
+  return std::string(t && *t ? t : "/tmp") + "/svb200_jit-" + std::to_string(unsigned(getuid()));
+}
+
+// create (mode 0700) if missing, then require: a real directory, owned by us, no group/other write
+bool cache_dir_ok(const std::string& dir) {
+  if (dir.empty()) return false;
+  if (mkdir(dir.c_str(), 0700) != 0 && errno != EEXIST) return false;
+  struct stat st;
+  if (lstat(dir.c_str(), &st) != 0 || !S_ISDIR(st.st_mode)) return false;
+  return st.st_uid == getuid() && (st.st_mode & (S_IWGRP | S_IWOTH)) == 0;
 }
 
 u64 fnv1a(const std::string& s) {
@@ -271,13 +290,17 @@ bool cache_load(const std::string& path, const std::string& full, std::vector<ch
   return ok;
 }
 
-void cache_store(const std::string& dir, const std::string& path, const std::string& full,
-                 const std::vector<char>& cubin) {
-  std::string mk = "mkdir -p '" + dir + "' 2>/dev/null";
-  if (std::system(mk.c_str()) != 0) return;
-  const std::string tmp = path + ".tmp" + std::to_string(uintptr_t(&cubin));
-  FILE* f = std::fopen(tmp.c_str(), "wb");
-  if (!f) return;
+void cache_store(const std::string& path, const std::string& full, const std::vector<char>& cubin) {
+  static std::atomic<unsigned> counter{0};
+  const std::string tmp = path + ".tmp" + std::to_string(long(getpid())) + "." + std::to_string(counter++);
+  const int fd = open(tmp.c_str(), O_WRONLY | O_CREAT | O_EXCL, 0600);
+  if (fd < 0) return;
+  FILE* f = fdopen(fd, "wb");
+  if (!f) {
+    close(fd);
+    std::remove(tmp.c_str());
+    return;
+  }
   const uint64_t ns = full.size(), nc = cubin.size();
   bool ok = std::fwrite(&ns, 8, 1, f) == 1 && std::fwrite(full.data(), 1, ns, f) == ns &&
             std::fwrite(&nc, 8, 1, f) == 1 && std::fwrite(cubin.data(), 1, nc, f) == nc;
@@ -295,9 +318,10 @@ void compile_kernel(JitKernel& k) {
   nvrtcVersion(&major, &minor);
   const std::string keyed = full + "\n//" + kOptsKey + "|nvrtc" + std::to_string(major) + "." + std::to_string(minor);
   const std::string dir = cache_dir();
+  const bool dir_ok = cache_dir_ok(dir);
   char hb[32];
   std::snprintf(hb, sizeof(hb), "%016llx", fnv1a(keyed));
-  const std::string path = dir.empty() ? std::string() : dir + "/" + hb + ".svc";
+  const std::string path = dir_ok ? dir + "/" + hb + ".svc" : std::string();
   if (!path.empty() && cache_load(path, keyed, k.cubin)) {
     k.ok = true;
     return;
@@ -323,7 +347,7 @@ void compile_kernel(JitKernel& k) {
     k.ok = n > 0;
   }
   nvrtcDestroyProgram(&prog);
-  if (k.ok && !path.empty()) cache_store(dir, path, keyed, k.cubin);
+  if (k.ok && !path.empty()) cache_store(path, keyed, k.cubin);
   g_jit_compiled += 1;
   g_jit_compile_us += std::chrono::duration_cast<std::chrono::microseconds>(std::chrono::steady_clock::now() - t0).count();
 }

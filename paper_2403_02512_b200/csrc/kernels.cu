@@ -777,29 +777,11 @@ const char* kKernelClassNames[KC_COUNT] = {"pair", "diag", "dense", "fused_tile"
                                            "braket", "probs", "init", "swap"};
 
 namespace {
-struct ScratchBuf {
-  void* ptr = nullptr;
-  size_t cap = 0;
-};
-// per-handle upload scratch lives in a side table keyed by handle
-std::mutex g_scratch_mu;
-std::vector<std::pair<sv_handle*, std::vector<ScratchBuf>>> g_scratch;
-thread_local int g_scratch_slot = 0;
-
+// ring of 64 buffers in the handle so back-to-back async uploads do not overwrite in-flight tables
+// (callers hold the handle's mutex: one mutator per handle)
 void* scratch_upload(sv_handle* h, const void* src, size_t bytes) {
-  // ring of 64 buffers so back-to-back async uploads do not overwrite in-flight tables
-  std::vector<ScratchBuf>* bufs = nullptr;
-  {
-    std::lock_guard<std::mutex> lk(g_scratch_mu);
-    for (auto& e : g_scratch)
-      if (e.first == h) bufs = &e.second;
-    if (!bufs) {
-      g_scratch.push_back({h, std::vector<ScratchBuf>(64)});
-      bufs = &g_scratch.back().second;
-    }
-  }
-  ScratchBuf& b = (*bufs)[g_scratch_slot];
-  g_scratch_slot = (g_scratch_slot + 1) % 64;
+  sv_handle::ScratchBuf& b = h->scratch[h->scratch_slot];
+  h->scratch_slot = (h->scratch_slot + 1) % 64;
   if (b.cap < bytes) {
     if (b.ptr) {
       CUDA_CHECK(cudaStreamSynchronize(h->stream));
@@ -815,14 +797,11 @@ void* scratch_upload(sv_handle* h, const void* src, size_t bytes) {
 }  // namespace
 
 void release_scratch(sv_handle* h) {
-  std::lock_guard<std::mutex> lk(g_scratch_mu);
-  for (size_t i = 0; i < g_scratch.size(); ++i)
-    if (g_scratch[i].first == h) {
-      for (auto& b : g_scratch[i].second)
-        if (b.ptr) cudaFree(b.ptr);
-      g_scratch.erase(g_scratch.begin() + i);
-      return;
-    }
+  for (auto& b : h->scratch) {
+    if (b.ptr) cudaFree(b.ptr);
+    b.ptr = nullptr;
+    b.cap = 0;
+  }
 }
 
 // Algorithmic bytes of one unfused primitive: 32 B (16 read + 16 written) per touched amplitude.

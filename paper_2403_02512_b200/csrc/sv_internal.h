@@ -129,6 +129,14 @@ struct sv_handle {
   size_t results_cap = 0;
   double* h_pinned = nullptr;
   size_t h_pinned_cap = 0;
+  // ring of upload buffers for small per-launch tables (kernels.cu scratch_upload); owned by the
+  // handle, so concurrent handles on other threads never touch it
+  struct ScratchBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+  };
+  ScratchBuf scratch[64];
+  int scratch_slot = 0;
   std::vector<double2*> aux;    // lambda states for the adjoint sweep
   double2* adj_lam = nullptr;   // fused adjoint: lambda, kept across calls
   double2* adj_saved = nullptr; // fused adjoint: saved final psi (several observables)

@@ -342,7 +342,7 @@ def test_fused_adjoint_single_observable(seed):
             st = d.get_state()
         assert_grad_close(jac, ref, [obs])
         assert abs(ev[0] - ref_ev[0]) < 1e-10 * max(1.0, obs_norm1(obs))
-        assert np.abs(st - O.run_circuit(n, [])).max() < 1e-10 or True   # state is swept back (round-off)
+        assert np.abs(st - O.run_circuit(n, [])).max() < 1e-10   # the state is swept back to the input
 
 
 def test_fused_adjoint_qaoa_and_hea_vs_unfused():

@@ -46,7 +46,7 @@ def check(n, ops, seed=0):
 def test_random_circuit_program(n):
     prog = check(n, workloads.random_circuit(n, 12, seed=n))
     assert any(k == "pass" for k, _ in prog["steps"])
-    assert prog["perm"] != list(range(n)) or True
+    assert prog["perm"] != list(range(n))   # the in-tile relabeling moved qubits
 
 
 @pytest.mark.parametrize("seed", range(6))
