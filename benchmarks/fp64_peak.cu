@@ -98,6 +98,191 @@ __global__ void __launch_bounds__(256) k_dmul(double* out, double a) {
   if (s == 12345.678) out[0] = s;
 }
 
+
+// two register operands per DFMA (the gate-update form: x0 += t * x1, t uniform)
+__global__ void __launch_bounds__(256) k_dfma2r(double* out, double a, double b) {
+  double x[16], y[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    x[i] = threadIdx.x * 1e-3 + i;
+    y[i] = threadIdx.x * 2e-3 - i;
+  }
+  for (int it = 0; it < kIter / 2; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = fma(y[i], a, x[i]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) y[i] = fma(x[i], b, y[i]);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += x[i] + y[i];
+  if (s == 12345.678) out[0] = s;
+}
+
+// three register operands per DFMA
+__global__ void __launch_bounds__(256) k_dfma3r(double* out, double a, double b) {
+  double x[16], y[16];
+  double z = a + threadIdx.x * 1e-12;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    x[i] = threadIdx.x * 1e-3 + i;
+    y[i] = threadIdx.x * 2e-3 - i;
+  }
+  for (int it = 0; it < kIter / 2; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[i] = fma(y[i], z, x[i]);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) y[i] = fma(x[i], z, y[i]);
+    z = z * b;
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += x[i] + y[i];
+  if (s == 12345.678) out[0] = s;
+}
+
+// the pass kernels' RY shear on 16 complex amplitudes in registers (8 pairs on register bit 0..3)
+__global__ void __launch_bounds__(256) k_shear(double* out, double t, double s_) {
+  double2 a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = make_double2(threadIdx.x * 1e-3 + i, i * 0.5);
+  for (int it = 0; it < kIter / 12; ++it) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) {
+        if ((r >> k) & 1) continue;
+        double2& x0 = a[r];
+        double2& x1 = a[r | (1 << k)];
+        x0.x = fma(t, x1.x, x0.x);
+        x0.y = fma(t, x1.y, x0.y);
+        x1.x = fma(s_, x0.x, x1.x);
+        x1.y = fma(s_, x0.y, x1.y);
+        x0.x = fma(t, x1.x, x0.x);
+        x0.y = fma(t, x1.y, x0.y);
+      }
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i].x + a[i].y;
+  if (s == 12345.678) out[0] = s;
+}
+
+// complex phase multiply a *= d on 16 amplitudes (2 DMUL + 2 DFMA each, the RZ / Phase form)
+__global__ void __launch_bounds__(256) k_cmul(double* out, double c, double sn) {
+  double2 a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = make_double2(threadIdx.x * 1e-3 + i, i * 0.5);
+  for (int it = 0; it < kIter / 4; ++it) {
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const double t1 = a[r].y * sn, t2 = a[r].x * sn;
+      a[r].x = fma(a[r].x, c, -t1);
+      a[r].y = fma(a[r].y, c, t2);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i].x + a[i].y;
+  if (s == 12345.678) out[0] = s;
+}
+
+template <int K>
+__device__ __forceinline__ void shear_k(double2 (&a)[16], double t, double s_) {
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    if ((r >> K) & 1) continue;
+    double2& x0 = a[r];
+    double2& x1 = a[r | (1 << K)];
+    x0.x = fma(t, x1.x, x0.x);
+    x0.y = fma(t, x1.y, x0.y);
+    x1.x = fma(s_, x0.x, x1.x);
+    x1.y = fma(s_, x0.y, x1.y);
+    x0.x = fma(t, x1.x, x0.x);
+    x0.y = fma(t, x1.y, x0.y);
+  }
+}
+
+// the same shear stream with a warp-uniform branch around every gate (the *D cases of the pass
+// kernels: a per-thread flip selects the sign of the rotation)
+__global__ void __launch_bounds__(256) k_shear_branch(double* out, double t, double s_, int fl) {
+  double2 a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = make_double2(threadIdx.x * 1e-3 + i, i * 0.5);
+  const int f = fl ^ (threadIdx.x >> 5);   // warp-uniform
+  for (int it = 0; it < kIter / 12; ++it) {
+    if (f & 1) shear_k<0>(a, -t, -s_); else shear_k<0>(a, t, s_);
+    if (f & 2) shear_k<1>(a, -t, -s_); else shear_k<1>(a, t, s_);
+    if (f & 4) shear_k<2>(a, -t, -s_); else shear_k<2>(a, t, s_);
+    if (f & 8) shear_k<3>(a, -t, -s_); else shear_k<3>(a, t, s_);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i].x + a[i].y;
+  if (s == 12345.678) out[0] = s;
+}
+
+// ... with the sign chosen by a select instead (no branch)
+__global__ void __launch_bounds__(256) k_shear_select(double* out, double t, double s_, int fl) {
+  double2 a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = make_double2(threadIdx.x * 1e-3 + i, i * 0.5);
+  const int f = fl ^ (threadIdx.x >> 5);
+  for (int it = 0; it < kIter / 12; ++it) {
+    shear_k<0>(a, (f & 1) ? -t : t, (f & 1) ? -s_ : s_);
+    shear_k<1>(a, (f & 2) ? -t : t, (f & 2) ? -s_ : s_);
+    shear_k<2>(a, (f & 4) ? -t : t, (f & 4) ? -s_ : s_);
+    shear_k<3>(a, (f & 8) ? -t : t, (f & 8) ? -s_ : s_);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i].x + a[i].y;
+  if (s == 12345.678) out[0] = s;
+}
+
+// ... the branch condition made warp-uniform (REDUX into a uniform register: BRA.U, no BSSY)
+__global__ void __launch_bounds__(256) k_shear_ubranch(double* out, double t, double s_, int fl) {
+  double2 a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = make_double2(threadIdx.x * 1e-3 + i, i * 0.5);
+  const int f = __reduce_or_sync(0xffffffffu, fl ^ (threadIdx.x >> 5));
+  for (int it = 0; it < kIter / 12; ++it) {
+    if (f & 1) shear_k<0>(a, -t, -s_); else shear_k<0>(a, t, s_);
+    if (f & 2) shear_k<1>(a, -t, -s_); else shear_k<1>(a, t, s_);
+    if (f & 4) shear_k<2>(a, -t, -s_); else shear_k<2>(a, t, s_);
+    if (f & 8) shear_k<3>(a, -t, -s_); else shear_k<3>(a, t, s_);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i].x + a[i].y;
+  if (s == 12345.678) out[0] = s;
+}
+
+// the pass kernels' form: every gate reads its own coefficients from the by-value parameter block
+// (constant bank 0) -- 64 distinct gates per loop trip
+struct Cf64 {
+  double2 v[64];
+};
+__global__ void __launch_bounds__(256) k_shear_cf(double* out, const Cf64 cf) {
+  double2 a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = make_double2(threadIdx.x * 1e-3 + i, i * 0.5);
+  for (int it = 0; it < kIter / 12 / 16; ++it) {
+#pragma unroll
+    for (int g = 0; g < 64; g += 4) {
+      shear_k<0>(a, cf.v[g].x, cf.v[g].y);
+      shear_k<1>(a, cf.v[g + 1].x, cf.v[g + 1].y);
+      shear_k<2>(a, cf.v[g + 2].x, cf.v[g + 2].y);
+      shear_k<3>(a, cf.v[g + 3].x, cf.v[g + 3].y);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i].x + a[i].y;
+  if (s == 12345.678) out[0] = s;
+}
+
 int main(int argc, char** argv) {
   const double secs = argc > 1 ? atof(argv[1]) : 3.0;
   int sms = 0, clk = 0;
@@ -114,13 +299,31 @@ int main(int argc, char** argv) {
     const char* name;
     int kind, arg;
   } cases[] = {{"dfma", 0, 0}, {"dmul", 3, 0}, {"dmma", 1, 0}, {"mix_dfma16_dmma1", 2, 1},
-               {"mix_dfma16_dmma2", 2, 2}, {"mix_dfma16_dmma4", 2, 4}};
+               {"mix_dfma16_dmma2", 2, 2}, {"mix_dfma16_dmma4", 2, 4},
+               {"dfma_2reg", 4, 0},   {"dfma_3reg", 5, 0},        {"shear16", 6, 0},
+               {"cmul16", 7, 0},      {"shear16_512thr", 8, 0},   {"shear16_branch", 9, 0},
+               {"shear16_select", 10, 0}, {"shear16_branch_8warps", 11, 0}, {"shear16_ubranch", 12, 0},
+               {"shear16_ubranch_8warps", 13, 0}, {"shear16_cf", 14, 0}, {"shear16_cf_8warps", 15, 0}};
+  Cf64 cf;
+  for (int g = 0; g < 64; ++g) cf.v[g] = make_double2(-0.1 + 0.001 * g, 0.19 - 0.002 * g);
   for (const Case& c : cases) {
     auto launch = [&]() {
       if (c.kind == 0) k_dfma<<<blocks, threads>>>(out, 0.999999, 1e-7);
       if (c.kind == 1) k_dmma<<<blocks, threads>>>(out, 0.999999, 1e-7);
       if (c.kind == 2) k_mix<<<blocks, threads>>>(out, 0.999999, 1e-7, c.arg);
       if (c.kind == 3) k_dmul<<<blocks, threads>>>(out, 0.999999);
+      if (c.kind == 4) k_dfma2r<<<blocks, threads>>>(out, 0.999999, 1e-7);
+      if (c.kind == 5) k_dfma3r<<<blocks, threads>>>(out, 0.999999, 1.0000001);
+      if (c.kind == 6) k_shear<<<blocks, threads>>>(out, -0.1, 0.19);
+      if (c.kind == 7) k_cmul<<<blocks, threads>>>(out, 0.8, 0.6);
+      if (c.kind == 8) k_shear<<<sms, 256>>>(out, -0.1, 0.19);   // 8 warps per SM (one PP group)
+      if (c.kind == 9) k_shear_branch<<<blocks, threads>>>(out, -0.1, 0.19, 5);
+      if (c.kind == 10) k_shear_select<<<blocks, threads>>>(out, -0.1, 0.19, 5);
+      if (c.kind == 11) k_shear_branch<<<sms, 256>>>(out, -0.1, 0.19, 5);
+      if (c.kind == 12) k_shear_ubranch<<<blocks, threads>>>(out, -0.1, 0.19, 5);
+      if (c.kind == 13) k_shear_ubranch<<<sms, 256>>>(out, -0.1, 0.19, 5);
+      if (c.kind == 14) k_shear_cf<<<blocks, threads>>>(out, cf);
+      if (c.kind == 15) k_shear_cf<<<sms, 256>>>(out, cf);
     };
     launch();
     CK(cudaDeviceSynchronize());
@@ -142,6 +345,11 @@ int main(int argc, char** argv) {
     if (c.kind == 0) flop_dfma = 2.0 * 16 * kIter * nthr;
     if (c.kind == 3) flop_dfma = 1.0 * 16 * kIter * nthr;
     if (c.kind == 1) flop_dmma = (nthr / 32) * 8 * (kIter / 4) * (8 * 8 * 4 * 2.0);
+    if (c.kind == 4 || c.kind == 5) flop_dfma = 2.0 * 32 * (kIter / 2) * nthr;
+    if (c.kind == 6) flop_dfma = 2.0 * 4 * 8 * 6 * (kIter / 12) * nthr;
+    if (c.kind == 8 || c.kind == 11 || c.kind == 13 || c.kind == 15) flop_dfma = 2.0 * 4 * 8 * 6 * (kIter / 12) * double(sms) * 256;
+    if (c.kind == 9 || c.kind == 10 || c.kind == 12 || c.kind == 14) flop_dfma = 2.0 * 4 * 8 * 6 * (kIter / 12) * nthr;
+    if (c.kind == 7) flop_dfma = 2.0 * 16 * 4 * (kIter / 4) * nthr;   // DMUL counted as 2 like DFMA (pipe ops)
     if (c.kind == 2) {
       flop_dfma = 2.0 * 16 * kIter * nthr;
       flop_dmma = (nthr / 32) * c.arg * kIter * (8 * 8 * 4 * 2.0);

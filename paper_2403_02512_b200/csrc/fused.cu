@@ -421,6 +421,8 @@ DPass make_dpass(const FPassArgs& A, int nl, u64 grid) {
   for (int j = 0; j < A.b; ++j) tilemask |= 1ull << A.tpos[j];
   D.outer = ((nl >= 64) ? ~0ull : ((1ull << nl) - 1)) & ~tilemask;
   D.grid_step = deposit_host(grid, D.outer);
+  D.grid_step2 = deposit_host(2 * grid, D.outer);
+  D.grid_step3 = deposit_host(3 * grid, D.outer);
   D.hi = A.hi_mask;
   const int nthr = A.nthr, nthreads = 1 << nthr;
   for (int j = 0; j < nthr; ++j) {
@@ -650,6 +652,9 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
   const u64 grid = std::min<u64>(prog.passes[0].n_tiles, u64(sms_dev[h->device]) * ((db || jdb) ? 1 : (jit_enabled() ? jit_ctas_per_sm() : 2)) *
                                                     (u64(1) << (kMaxB - std::min(kMaxB, prog.passes[0].b))));   // persistent grid
 
+  // generated ping-pong passes: one CTA per SM (their generator partials use the same [CTA][slot]
+  // layout, so the partial buffer is sized for the larger of the two grids)
+  const u64 pp_grid = std::min<u64>(grid, u64(sms_dev[h->device]));
   // launch records + upload phases | ops | coef in one copy (the buffer is only reused after a sync)
   std::vector<DPhase> dph(prog.phases.size());
   for (const FPassArgs& A : prog.passes)
@@ -707,7 +712,12 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
       const unsigned g = unsigned(grid);
       cudaStream_t st = h->stream;
       const JitPass* jp = (!db && s.index < int(prog.jit.size()) && prog.jit[s.index].kernel) ? &prog.jit[s.index] : nullptr;
-      if (jp) {
+      if (jp && jp->pp) {
+        // ping-pong loop: one 512-thread CTA per SM, three tile buffers (fused_dev.cuh run_pass_pp)
+        DPass Dp = make_dpass(A, h->nl, pp_grid);
+        const size_t psmem = fdev::pp_smem_bytes(A.b, A.n_gen > 0);
+        jit_launch(*jp, h->device, unsigned(pp_grid), fdev::kPPThreads, psmem, st, state, state_hi, &Dp, ph, d_jt, d_gen);
+      } else if (jp) {
         // generated kernel of this pass: [tile] [phase records] [generator accumulators]
         const size_t jsmem = (jdb ? 4 : (jp->split ? 3 : 2)) * (size_t(1) << (b - 1)) * sizeof(double2) + size_t(D.n_phases) * sizeof(DPhase) +
                              (A.n_gen ? size_t(threads / 32) * kMaxGens * sizeof(double2) : 0);

@@ -76,6 +76,32 @@ __device__ __forceinline__ void pairg(double2 (&a)[kRegs], const double2 m0, con
     if ((r & cm) == cv) pair_upd<MT>(a[r], a[r ^ XR], m0, m1, m2, m3);
 }
 
+// register-controlled X (CNOT-type) on register xmask XR: a[r] <-> a[r ^ XR] for the registers
+// whose control bits CC equal CV.  Control bits without a per-thread flip in this phase resolve at
+// compile time -- the swap is a register renaming, no instructions at all; bits that may carry a
+// flip (MD, runtime value fthr) select at run time (SEL on the integer pipe, no FP64).
+// XP = i0's pattern on XR (a multi-bit XR, e.g. SWAP, exchanges only the pairs through XP).
+template <int XR, int CC, int CV, int MD, int XP>
+__device__ __forceinline__ void swap_x(double2 (&a)[kRegs], const int fthr) {
+  constexpr int LOW = XR & -XR;
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if (r & LOW) continue;   // one representative per pair {r, r ^ XR}
+    if ((r & XR) != XP && ((r ^ XR) & XR) != XP) continue;
+    if ((r & CC & ~MD) != (CV & CC & ~MD)) continue;
+    if (MD & CC) {
+      const bool c = (r & MD) == ((CV ^ fthr) & MD);
+      const double2 x0 = a[r], x1 = a[r ^ XR];
+      a[r] = c ? x1 : x0;
+      a[r ^ XR] = c ? x0 : x1;
+    } else {
+      const double2 t = a[r];
+      a[r] = a[r ^ XR];
+      a[r ^ XR] = t;
+    }
+  }
+}
+
 // rotation R(phi) of every (x0, x1) pair on register bit K as shears u += t v; v += s u; u += t v
 // (RY type: on (re0, re1) and (im0, im1); RX type: R(-phi) on (re0, im1), R(phi) on (im0, re1))
 template <int K, bool RX>
@@ -265,6 +291,8 @@ struct DPass {
   u64 n_tiles;
   u64 outer;           // physical bits NOT in the tile (the tile index deposits into these)
   u64 grid_step;       // deposit(gridDim.x): tile t -> t + grid is a masked add
+  u64 grid_step2;      // deposit(2 gridDim.x), deposit(3 gridDim.x) (ping-pong tile loop)
+  u64 grid_step3;
   u64 hi;              // two-array state: indices with this bit live in state_hi
   u64 ld_off[kRegs];   // load slot i: physical offset of its register-slot bits (without hi)
   u64 st_off[kRegs];   // store slot i: the same after the pass's in-tile relabeling
@@ -445,9 +473,196 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
   }
 }
 
+// ---- ping-pong tile loop (generated kernels, PP): two consumer groups, three tile buffers ------
+//
+// One 512-thread CTA per SM = two groups of 8 warps (A = threads 0..255, B = 256..511), each working
+// on its own tile (A: the CTA's even local tiles, B: odd), in three rotating 64 KiB buffers.  A tile
+// is 2P "segments": T_k (phase k's smem round trip: store phase k-1's registers, group barrier, load
+// phase k's registers) and C_k (phase k's gate arithmetic).  Every segment ends with a CTA-wide step
+// barrier, and group B runs an odd number of segments behind A, so the two groups are always in
+// opposite segment kinds: one group's FP64 arithmetic runs while the other group's shared-memory
+// round trip runs (two free-running CTAs per SM instead drift into lockstep -- they contend for the
+// same pipe at the same time -- and the FP64 and shared-memory work of a pass then add up).
+// Loads: a group's last phase, once its registers hold the tile, refills the buffer with the CTA's
+// local tile j+3 by cp.async (16 B per amplitude, through the swizzle) whose completion arrives on
+// the buffer's mbarrier (cp.async.mbarrier.arrive.noinc, 256 arrivals per fill); the consumer --
+// the other group -- waits on the mbarrier's phase parity before its first phase.  The prefetch
+// distance is ~P segments, i.e. the load overlaps both groups' work.
+__device__ __forceinline__ void step_barrier() { asm volatile("barrier.sync 0;\n" ::: "memory"); }
+__device__ __forceinline__ void group_barrier() {
+  asm volatile("barrier.sync %0, 256;\n" ::"r"(1 + (int(threadIdx.x) >> 8)) : "memory");
+}
+__device__ __forceinline__ void mbar_init(unsigned addr, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(addr), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(unsigned addr) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(unsigned addr, unsigned parity) {
+  asm volatile(
+      "{\n"
+      "  .reg .pred p;\n"
+      "SVB200_WAIT_%=:\n"
+      "  mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "  @!p bra SVB200_WAIT_%=;\n"
+      "}\n" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ u64 masked_add(u64 base, u64 outer, u64 step) { return ((base | ~outer) + step) & outer; }
+
+constexpr int kPPThreads = 512;
+// dynamic shared memory of the PP loop: [3 tile buffers][3 mbarriers + pad][generator accumulators]
+__host__ __device__ constexpr unsigned pp_smem_bytes(int b, bool gens) {
+  return 3u * (1u << b) * 16u + 32u + (gens ? unsigned(kPPThreads / 32) * kMaxGens * 16u : 0u);
+}
+
+#ifdef FDEV_SEGPROF
+__shared__ long long fdev_prof[2][64][2];
+__shared__ long long fdev_tl[2];
+#define fdev_t fdev::fdev_tl[threadIdx.x >> 8]
+#endif
+template <bool TWO, class Body>
+__device__ __forceinline__ void run_pass_pp(double2* __restrict__ state, double2* __restrict__ state_hi, const DPass& P,
+                                            double2* __restrict__ gen_partials, Body body) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int T = 1 << P.b;   // 4096 amplitudes: 256 threads x 16 registers per group
+  double2* bufs = reinterpret_cast<double2*>(smem_raw);
+  const unsigned mbar0 = unsigned(__cvta_generic_to_shared(smem_raw + size_t(3) * T * sizeof(double2)));
+  double2* s_gen = reinterpret_cast<double2*>(smem_raw + size_t(3) * T * sizeof(double2) + 32);
+  const int tid = threadIdx.x;
+  const int grp = tid >> 8, gtid = tid & 255;
+  if (P.n_gen)
+    for (int i = tid; i < (kPPThreads >> 5) * kMaxGens; i += kPPThreads) s_gen[i] = make_double2(0.0, 0.0);
+#ifdef FDEV_SEGPROF
+  for (int i = tid; i < 2 * 64 * 2; i += kPPThreads) (&fdev_prof[0][0][0])[i] = 0;
+#endif
+  if (tid == 0) {
+    for (int i = 0; i < 3; ++i) mbar_init(mbar0 + 8u * i, 256u);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+  u64 ld_tid = 0;
+#pragma unroll
+  for (int j = 0; j < kTB; ++j)
+    if (j < P.nthr && ((gtid >> j) & 1)) ld_tid |= P.ld_tb[j];
+  const int ld_sw = swz(gtid);
+  // 16 cp.async per thread (one tile slot per register index), completion -> the buffer's mbarrier
+  auto issue_load = [&](u64 b0, int buf) {
+    u64 g = b0 | ld_tid;
+    const double2* p_lo;
+    const double2* p_hi;
+    if (TWO) {
+      const u64 gl = g & ~P.hi;
+      p_hi = state_hi + gl;
+      p_lo = (g & P.hi) ? p_hi : state + gl;
+    } else {
+      p_lo = p_hi = state + g;
+    }
+    const unsigned sb = unsigned(__cvta_generic_to_shared(bufs + size_t(buf) * T));
+#pragma unroll
+    for (int i = 0; i < kRegs; ++i) {
+      const double2* src = (TWO && ((P.ld_hsel >> i) & 1) ? p_hi : p_lo) + P.ld_off[i];
+      const unsigned dst = sb + unsigned(ld_sw ^ P.ld_sm[i]) * 16u;
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src) : "memory");
+    }
+    mbar_arrive_cp_async(mbar0 + 8u * buf);
+  };
+  const u64 nt = P.n_tiles;
+  const u64 ncta = nt > blockIdx.x ? (nt - 1 - blockIdx.x) / gridDim.x + 1 : 0;   // this CTA's tiles
+  u64 base0 = 0;
+  {
+    u64 m = P.outer;
+    for (u64 v = blockIdx.x; m && v; m &= m - 1, v >>= 1)
+      if (v & 1) base0 |= m & (~m + 1);
+  }
+  if (grp == 0) {
+    if (ncta > 0) issue_load(base0, 0);
+    if (ncta > 2) issue_load(masked_add(base0, P.outer, P.grid_step2), 2);
+  } else if (ncta > 1) {
+    issue_load(masked_add(base0, P.outer, P.grid_step), 1);
+  }
+  u64 base = grp ? masked_add(base0, P.outer, P.grid_step) : base0;
+  const int segs = 2 * P.n_phases;
+  const int offset = P.n_phases | 1;   // odd: B's smem segments line up with A's arithmetic
+  double2* acc_warp = s_gen + (tid >> 5) * kMaxGens;
+  if (grp == 1)
+    for (int i = 0; i < offset; ++i) step_barrier();
+  int buf = grp;              // local tile j lives in buffer j % 3; its fill number is j / 3
+  unsigned fill = 0;
+  const u64 periods = (ncta + 1) >> 1;
+  for (u64 k = 0; k < periods; ++k) {
+    const u64 j = 2 * k + grp;
+    if (j < ncta) {
+      mbar_wait_parity(mbar0 + 8u * buf, fill & 1u);
+      const int cb = buf;
+#ifdef FDEV_SEGPROF
+      if (gtid == 0) fdev_t = clock64();
+#endif
+      body(cb << P.b, base, acc_warp, [&]() {
+        if (j + 3 < ncta) issue_load(masked_add(base, P.outer, P.grid_step3), cb);
+      });
+      base = masked_add(base, P.outer, P.grid_step2);
+    } else {
+      for (int i = 0; i < segs; ++i) step_barrier();
+    }
+    // next local tile of this group: j + 2
+    buf += 2;
+    if (buf >= 3) {
+      buf -= 3;
+      ++fill;
+    }
+  }
+  if (grp == 0)
+    for (int i = 0; i < offset; ++i) step_barrier();
+#ifdef FDEV_SEGPROF
+  __syncthreads();
+  if (blockIdx.x == 0 && tid == 0) {
+    for (int g = 0; g < 2; ++g)
+      for (int k = 0; k < segs; ++k)
+        printf("SEGPROF n_phases=%d grp=%d seg=%d kind=%c work=%lld wait=%lld\n", P.n_phases, g, k, (k & 1) ? 'C' : 'T',
+               fdev_prof[g][k][0], fdev_prof[g][k][1]);
+  }
+#endif
+  if (P.n_gen) {
+    __syncthreads();
+    for (int g = tid; g < P.n_gen; g += kPPThreads) {
+      double2 s = make_double2(0.0, 0.0);
+      for (int w = 0; w < (kPPThreads >> 5); ++w) {
+        s.x += s_gen[w * kMaxGens + g].x;
+        s.y += s_gen[w * kMaxGens + g].y;
+      }
+      gen_partials[size_t(blockIdx.x) * P.n_gen_total + P.gen_base + g] = s;
+    }
+  }
+}
+
 // phase entry / exit for generated kernels: registers <- tile (offsets s0 ^ W(r)), and the store
 // honouring the phase's uniform flip and the thread's dynamic flips
 // tile element i (swizzled index): one buffer, or two half buffers selected by index bit b-1
+// PP (ping-pong loop): a phase's smem round trip syncs only its group; FDEV_STEP ends a segment
+#ifdef FDEV_PP
+#define FDEV_PHASE_SYNC() fdev::group_barrier()
+#ifdef FDEV_SEGPROF
+// diagnostic (SVB200_JIT_SEGPROF=1): thread 0 of each group accumulates, per segment of the tile,
+// the cycles it spent working and the cycles it then waited at the step barrier; CTA 0 prints them
+#define FDEV_STEP_I(K)                                                  \
+  {                                                                     \
+    const long long t1_ = clock64();                                    \
+    if ((threadIdx.x & 255) == 0) fdev::fdev_prof[threadIdx.x >> 8][K][0] += t1_ - fdev_t;  \
+    fdev::step_barrier();                                               \
+    const long long t2_ = clock64();                                    \
+    if ((threadIdx.x & 255) == 0) fdev::fdev_prof[threadIdx.x >> 8][K][1] += t2_ - t1_;     \
+    if ((threadIdx.x & 255) == 0) fdev_t = t2_;                         \
+  }
+#else
+#define FDEV_STEP_I(K) fdev::step_barrier()
+#endif
+#else
+// (non-aligned: versioned phases store from different switch cases in different warps)
+#define FDEV_PHASE_SYNC() asm volatile("barrier.sync 0;\n" ::: "memory")
+#define FDEV_STEP_I(K)
+#endif
 #ifdef FDEV_SPLIT
 #define FDEV_TILE(i) ((((i) & FDEV_HB) ? tile_hi : tile)[(i) & (FDEV_HB - 1)])
 #else
@@ -464,8 +679,13 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
   (void)fthr;
 // ... with the thread's slot offset and physical bits given as expressions (generated kernels
 // compute them from threadIdx.x with literal masks instead of loading the phase's nibble tables)
+#ifdef FDEV_PP
+#define FDEV_TILE_OFF tile_off   // PP: the tile buffer enters the slot index (bits 12-13), base fixed
+#else
+#define FDEV_TILE_OFF 0
+#endif
 #define FDEV_PHASE_LOAD_X(S0, PB, W0, W1, W2, W3)                                                                \
-  const int s0 = (S0);                                                                                          \
+  const int s0 = (S0) ^ FDEV_TILE_OFF;                                                                         \
   const u64 pb = base | (PB);                                                                                   \
   double2 a[fdev::kRegs];                                                                                       \
   _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r) a[r] =                                                \
@@ -480,7 +700,7 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r)                                                     \
       FDEV_TILE(sf ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)) = a[r]; \
   }                                                                                                             \
-  __syncthreads();
+  FDEV_PHASE_SYNC();
 
 #ifdef FDEV_PLAIN_STORE
 #define FDEV_STG(p, v) (*(p) = (v))

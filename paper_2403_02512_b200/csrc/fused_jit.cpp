@@ -68,16 +68,24 @@ struct Gen {
   std::vector<std::pair<int, int>> tab_refs;  // (pass-local op, table length)
   int tab_len = 0;
 
+  std::map<std::pair<int, int>, int> cf_slot, tab_off;   // one slot per (op, entry) even when emitted twice
   // j = -1: entry 1 of the op's coefficient table (the odd-parity value of a parity table)
   std::string C(int op, int j) {
-    cf_refs.push_back({op, j});
-    return "cf.v[" + std::to_string(cf_refs.size() - 1) + "]";
+    auto it = cf_slot.find({op, j});
+    if (it == cf_slot.end()) {
+      cf_refs.push_back({op, j});
+      it = cf_slot.emplace(std::make_pair(op, j), int(cf_refs.size()) - 1).first;
+    }
+    return "cf.v[" + std::to_string(it->second) + "]";
   }
   std::string T(int op, int len) {
-    tab_refs.push_back({op, len});
-    const int off = tab_len;
-    tab_len += len;
-    return "(tabs + " + std::to_string(off) + ")";
+    auto it = tab_off.find({op, len});
+    if (it == tab_off.end()) {
+      tab_refs.push_back({op, len});
+      it = tab_off.emplace(std::make_pair(op, len), tab_len).first;
+      tab_len += len;
+    }
+    return "(tabs + " + std::to_string(it->second) + ")";
   }
 };
 
@@ -98,13 +106,68 @@ std::string tconst_expr(const FOp& op, int W[4]) {
   return e;
 }
 
-bool emit_op(Gen& g, int i, const FOp& op, bool parity_tab) {
+// Versioned phases: the thread-dependent predicates of a phase (the patterns of thread-predicated X
+// gates and of thread-controlled ops, the parities of parity phases) are evaluated once at the
+// phase start and the phase's op sequence is emitted once per outcome, so inside a version every
+// per-thread flip is a compile-time constant -- no branch between gates (a warp-uniform branch
+// between two gates costs ~20 % of the FP64 rate, benchmarks/fp64_peak.cu shear16_branch).
+struct VPred {
+  int kind;   // 0: (pb & m) == v; 1: parity(pb & m)
+  u64 m, v;
+};
+struct VCtx {
+  std::vector<VPred> preds;
+  int ver = 0;    // outcome bits, one per predicate
+  int fthr = 0;   // the per-thread flip mask so far (compile-time in this version)
+  bool eval(int kind, u64 m, u64 v) const {
+    for (size_t i = 0; i < preds.size(); ++i)
+      if (preds[i].kind == kind && preds[i].m == m && preds[i].v == v) return (ver >> i) & 1;
+    return false;
+  }
+};
+
+// Warp-uniform predicates: when no predicate of a phase involves a lane bit, every predicate is the
+// same across a warp; the phase evaluates them once into a uniform register (one REDUX.OR), so the
+// flips, the thread-controlled ops and the *D cases branch on uniform values (BRA.U, no
+// divergence bookkeeping: a uniform branch between two gates costs ~4 % of the FP64 rate instead
+// of ~22 %, benchmarks/fp64_peak.cu shear16_ubranch vs shear16_branch).
+struct UPreds {
+  std::vector<VPred> preds;
+  std::string of(int kind, u64 m, u64 v) const {
+    for (size_t i = 0; i < preds.size(); ++i)
+      if (preds[i].kind == kind && preds[i].m == m && preds[i].v == v) return "((vp_ >> " + std::to_string(i) + ") & 1)";
+    return std::string();
+  }
+};
+
+// dyn: register bits that may carry a per-thread flip at this op (fthr starts at 0 every phase)
+// vc: versioned phase (predicates and flips are compile-time), or nullptr
+// up: the phase's predicates in the uniform register vp_, or nullptr
+bool emit_op(Gen& g, int i, const FOp& op, bool parity_tab, int& dyn, VCtx* vc = nullptr, const UPreds* up = nullptr) {
   std::ostringstream& o = g.o;
   const int cs = op.cs;
-  o << "    {\n";
-  if (op.fk) o << "      if ((pb & " << hex64(op.fpm) << ") == " << hex64(op.fpv) << ") fthr ^= " << op.fk << ";\n";
-  const bool has_pred = op.pm != 0 || op.pv != 0;
-  const std::string pred = "((pb & " + hex64(op.pm) + ") == " + hex64(op.pv) + ")";
+  bool has_pred = op.pm != 0 || op.pv != 0;
+  if (vc) {
+    if (op.fk && vc->eval(0, op.fpm, op.fpv)) vc->fthr ^= op.fk;
+    const bool active = !has_pred || vc->eval(0, op.pm, op.pv);
+    if (cs >= CS_XFLIP && cs < CS_XFLIP + 4) {
+      if (active) vc->fthr ^= 1 << (cs - CS_XFLIP);
+      return true;
+    }
+    if (!active) return true;   // thread-controlled op off for this version (a GEN op adds 0)
+    has_pred = false;
+    dyn = 0;
+    o << "    {\n      const int fthr = " << vc->fthr << ";\n";
+  } else {
+    o << "    {\n";
+    if (op.fk) {
+      if (up) o << "      if " << up->of(0, op.fpm, op.fpv) << " fthr ^= " << op.fk << ";\n";
+      else o << "      if ((pb & " << hex64(op.fpm) << ") == " << hex64(op.fpv) << ") fthr ^= " << op.fk << ";\n";
+      dyn |= op.fk;
+    }
+    if (cs >= CS_XFLIP && cs < CS_XFLIP + 4) dyn |= 1 << (cs - CS_XFLIP);
+  }
+  const std::string pred = up && has_pred ? up->of(0, op.pm, op.pv) : "((pb & " + hex64(op.pm) + ") == " + hex64(op.pv) + ")";
   const std::string cm = std::to_string(int(op.cm));
   const std::string cvd = "(" + std::to_string(int(op.cv)) + " ^ (fthr & " + cm + "))";
   if (cs >= CS_GEN1) {
@@ -186,9 +249,19 @@ bool emit_op(Gen& g, int i, const FOp& op, bool parity_tab) {
   } else if (cs >= CS_PARITY && cs < CS_PARITY + 16) {
     const int M = cs - CS_PARITY;
     std::string tp = "(__popc(fthr & " + std::to_string(M) + ") + " + std::to_string(int(op.v));
-    if (op.xm) tp += " + __popcll(pb & " + hex64(op.xm) + ")";
+    if (op.xm && vc) tp += std::string(" + ") + (vc->eval(1, op.xm, 0) ? "1" : "0");
+    else if (op.xm && up) tp += " + " + up->of(1, op.xm, 0);
+    else if (op.xm) tp += " + __popcll(pb & " + hex64(op.xm) + ")";
     tp += ") & 1";
     o << "      fdev::parity_phase<" << M << ">(a, " << g.C(i, 0) << ", " << tp << ");\n";
+  } else if (cs >= CS_PAIRGR && cs < CS_PAIRGR + 15 && op.mtype == MT_X &&
+             (vc || __builtin_popcount(cs - CS_PAIRGR + 1) == 1 || (dyn & (cs - CS_PAIRGR + 1)) == 0)) {
+    // register-controlled X: register renaming (static control bits) or selects (flipped ones);
+    // a multi-bit xmask needs its i0 pattern static
+    const int xr = cs - CS_PAIRGR + 1, cc = op.cm & ~xr & 15;
+    const int fs = vc ? vc->fthr : 0;   // versioned: the flips are folded into the pattern
+    o << "      fdev::swap_x<" << xr << ", " << cc << ", " << ((op.cv ^ fs) & cc) << ", " << (dyn & cc) << ", "
+      << ((op.cv ^ fs) & xr) << ">(a, fthr);\n";
   } else if (cs >= CS_PAIRGR && cs < CS_PAIRGR + 15) {
     o << "      fdev::pairg<" << (cs - CS_PAIRGR + 1) << ", fdev::kMtReal>(a, " << g.C(i, 0) << ", " << g.C(i, 1) << ", "
       << g.C(i, 2) << ", " << g.C(i, 3) << ", " << cm << ", " << cvd << ");\n";
@@ -366,6 +439,27 @@ bool jit_db() {
   return db;
 }
 
+// SVB200_JIT_VMAX: most thread predicates a phase may have and still be emitted once per outcome
+// (2^VMAX copies of its ops); 0 turns versioning off
+int jit_vmax() {
+  static const int v = getenv("SVB200_JIT_VMAX") ? std::max(0, std::min(4, atoi(getenv("SVB200_JIT_VMAX")))) : 0;
+  return v;
+}
+
+// SVB200_JIT_UNIFORM=0: per-thread predicate evaluation instead of one warp-uniform REDUX per phase
+bool jit_uniform_preds() {
+  static const bool on = !(getenv("SVB200_JIT_UNIFORM") && std::string(getenv("SVB200_JIT_UNIFORM")) == "0");
+  return on;
+}
+
+// SVB200_JIT_PP=1: direct passes use the ping-pong loop instead of two free-running CTAs per SM.
+// Measured on the 30-qubit bench circuit: 0.410 s (PP) vs 0.401 s (two CTAs) -- the lockstep hides
+// the shared-memory round trips, but its arithmetic segments then run on 8 warps; off by default.
+bool jit_pp() {
+  static const bool on = getenv("SVB200_JIT_PP") && std::string(getenv("SVB200_JIT_PP")) == "1";
+  return on;
+}
+
 // resident CTAs per SM of the single-buffer form (SVB200_JIT_CTAS, default 2)
 int jit_ctas_per_sm() {
   static const int n = getenv("SVB200_JIT_CTAS") ? std::max(1, std::min(3, atoi(getenv("SVB200_JIT_CTAS")))) : 2;
@@ -383,7 +477,9 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
   // measured: hiding the rest of the next tile's load this way does not pay (0.539 vs 0.529 s on
   // the bench circuit) -- the passes are bound by their compute phases, not the load -- so off
   static const bool split_on = getenv("SVB200_JIT_SPLIT") && std::string(getenv("SVB200_JIT_SPLIT")) == "1";
-  const bool split = split_on && direct && jit_ctas_per_sm() <= 2;
+  const bool split = split_on && direct && jit_ctas_per_sm() <= 2 && !jit_pp();
+  // ping-pong tile loop (fused_dev.cuh run_pass_pp): direct passes on full 12-bit tiles
+  const bool pp = jit_pp() && direct && A.b == kMaxB && A.nthr == kMaxB - kRB;
   if (direct) {
     // the thread's physical store bits in the last phase (its lane bits land on physical 0..2)
     const FPhase& L = prog.phases[A.phase_begin + A.n_phases - 1];
@@ -398,7 +494,7 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
     for (int k = 0; k < 4; ++k) W[k] = swz_h(1 << F.reg[k]);
     o << "  {   // phase " << ph << (last_direct ? " (direct store)" : "") << "\n";
     static const bool tab_thr = getenv("SVB200_JIT_THRTAB") && std::string(getenv("SVB200_JIT_THRTAB")) == "1";
-    if (tab_thr) {
+    if (tab_thr && !pp) {
       o << "    FDEV_PHASE_LOAD(s_ph[" << ph << "], " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ")\n";
     } else {
       // the thread's slot: swizzled offset and physical bits as literal-mask expressions of tid
@@ -411,9 +507,9 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
       o << "    FDEV_PHASE_LOAD_X(" << se << ", " << pe << ", " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3]
         << ")\n";
     }
-    if (last_direct) o << "    __syncthreads();\n    next_load();\n";
-    for (int oi = F.op_begin; oi < F.op_end; ++oi) {
-      const FOp& op = prog.ops[oi];
+    if (pp) o << "    FDEV_STEP_I(" << 2 * ph << ");\n";   // end of segment T_ph
+    if (last_direct) o << (pp ? "    next_load();\n" : "    __syncthreads();\n    next_load();\n");
+    auto parity_tab_of = [&](const FOp& op) {
       bool ptab = false;
       if (op.cs >= CS_GEND && op.cs < CS_GEND + 4 && op.nt >= 1) {
         // the table's structure (parity form), not its values, decides the code: generators are
@@ -425,14 +521,84 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
           ptab = t[e].x == want.x && t[e].y == want.y;
         }
       }
-      if (!emit_op(g, oi - A.op_begin, op, ptab)) return std::string();
+      return ptab;
+    };
+    auto emit_store = [&]() {
+      if (last_direct) {
+        o << "    FDEV_PHASE_STORE_GLOBAL" << (two ? "2(" : "(") << int(F.flip);
+        for (int k = 0; k < 4; ++k) o << ", " << hex64(1ull << A.tpos_st[F.reg[k]]);
+        o << ")\n";
+        if (pp) o << "    FDEV_STEP_I(" << 2 * ph + 1 << ");\n";   // end of segment C_ph
+      } else {
+        if (pp) o << "    FDEV_STEP_I(" << 2 * ph + 1 << ");\n";   // end of segment C_ph; the store opens T_ph+1
+        o << "    FDEV_PHASE_STORE(" << int(F.flip) << ", " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ")\n";
+      }
+    };
+    // the phase's thread-dependent predicates; versioned when few and warp-uniform (no lane bits)
+    VCtx vc;
+    bool versioned = jit_vmax() > 0;
+    {
+      u64 lanes = 0;
+      for (int j = 0; j < 5 && j < A.nthr; ++j) lanes |= 1ull << A.tpos[F.thr[j]];
+      auto add = [&](int kind, u64 m, u64 v) {
+        if (m & lanes) versioned = false;
+        for (const VPred& q : vc.preds)
+          if (q.kind == kind && q.m == m && q.v == v) return;
+        vc.preds.push_back({kind, m, v});
+      };
+      for (int oi = F.op_begin; oi < F.op_end; ++oi) {
+        const FOp& op = prog.ops[oi];
+        if (op.fk) add(0, op.fpm, op.fpv);
+        if (op.pm != 0 || op.pv != 0) add(0, op.pm, op.pv);
+        if (op.cs >= CS_PARITY && op.cs < CS_PARITY + 16 && op.xm) add(1, op.xm, 0);
+      }
+      if (vc.preds.empty() || int(vc.preds.size()) > jit_vmax()) versioned = false;
     }
-    if (last_direct) {
-      o << "    FDEV_PHASE_STORE_GLOBAL" << (two ? "2(" : "(") << int(F.flip);
-      for (int k = 0; k < 4; ++k) o << ", " << hex64(1ull << A.tpos_st[F.reg[k]]);
-      o << ")\n";
+    if (!versioned) {
+      // lane-free predicates (at most 32): evaluated once per phase into a warp-uniform register
+      UPreds up;
+      bool uni = jit_uniform_preds() && !vc.preds.empty() && vc.preds.size() <= 32;
+      {
+        u64 lanes = 0;
+        for (int j = 0; j < 5 && j < A.nthr; ++j) lanes |= 1ull << A.tpos[F.thr[j]];
+        for (const VPred& q : vc.preds)
+          if (q.m & lanes) uni = false;
+      }
+      if (uni) {
+        up.preds = vc.preds;
+        o << "    const unsigned vp_ = __reduce_or_sync(0xffffffffu, 0u";
+        for (size_t q = 0; q < up.preds.size(); ++q) {
+          const VPred& P = up.preds[q];
+          if (P.kind == 0) o << " | (((pb & " << hex64(P.m) << ") == " << hex64(P.v) << ") ? " << (1u << q) << "u : 0u)";
+          else o << " | (unsigned(__popcll(pb & " << hex64(P.m) << ") & 1) << " << q << ")";
+        }
+        o << ");\n";
+      }
+      int dyn = 0;
+      for (int oi = F.op_begin; oi < F.op_end; ++oi)
+        if (!emit_op(g, oi - A.op_begin, prog.ops[oi], parity_tab_of(prog.ops[oi]), dyn, nullptr, uni ? &up : nullptr))
+          return std::string();
+      emit_store();
     } else {
-      o << "    FDEV_PHASE_STORE(" << int(F.flip) << ", " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ")\n";
+      o << "    const int ver_ = 0";
+      for (size_t q = 0; q < vc.preds.size(); ++q) {
+        const VPred& P = vc.preds[q];
+        if (P.kind == 0) o << " | (((pb & " << hex64(P.m) << ") == " << hex64(P.v) << ") ? " << (1 << q) << " : 0)";
+        else o << " | ((__popcll(pb & " << hex64(P.m) << ") & 1) << " << q << ")";
+      }
+      o << ";\n    switch (ver_) {\n";
+      for (int v = 0; v < (1 << vc.preds.size()); ++v) {
+        vc.ver = v;
+        vc.fthr = 0;
+        o << "    " << (v + 1 < (1 << int(vc.preds.size())) ? "case " + std::to_string(v) : std::string("default")) << ": {\n";
+        int dyn = 0;
+        for (int oi = F.op_begin; oi < F.op_end; ++oi)
+          if (!emit_op(g, oi - A.op_begin, prog.ops[oi], parity_tab_of(prog.ops[oi]), dyn, &vc)) return std::string();
+        o << "    {\n    const int fthr = " << vc.fthr << ";\n";
+        emit_store();
+        o << "    }\n    break;\n    }\n";
+      }
+      o << "    }\n";
     }
     o << "  }\n";
   }
@@ -449,22 +615,37 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
     }
   }
   if (split) k << "#define FDEV_SPLIT 1\n#define FDEV_HB " << (1 << (A.b - 1)) << "\n";
+  if (pp) k << "#define FDEV_PP 1\n";
+  static const bool segprof = getenv("SVB200_JIT_SEGPROF") && std::string(getenv("SVB200_JIT_SEGPROF")) == "1";
+  if (pp && segprof) k << "#define FDEV_SEGPROF 1\n";
   static const bool plain_st = getenv("SVB200_JIT_STCS") && std::string(getenv("SVB200_JIT_STCS")) == "0";
   if (plain_st) k << "#define FDEV_PLAIN_STORE 1\n";
   k << "struct SvCf { double2 v[" << ncf << "]; };\n";
-  k << "extern \"C\" __global__ void __launch_bounds__(256, " << (db ? 1 : jit_ctas_per_sm()) << ")\n";
+  if (pp) k << "extern \"C\" __global__ void __launch_bounds__(512, 1)\n";
+  else k << "extern \"C\" __global__ void __launch_bounds__(256, " << (db ? 1 : jit_ctas_per_sm()) << ")\n";
   k << "svb200_pass(double2* __restrict__ state, double2* __restrict__ state_hi, const fdev::DPass P,\n"
        "            const fdev::DPhase* __restrict__ phases, const double2* __restrict__ tabs,\n"
        "            double2* __restrict__ gen_partials, const SvCf cf) {\n";
-  k << "  auto body = [&](double2* __restrict__ tile, double2* __restrict__ tile_hi,\n"
-       "                  const fdev::DPhase* __restrict__ s_ph, const u64 base, double2* __restrict__ acc_warp,\n"
-       "                  auto next_load) {\n";
-  k << "  (void)acc_warp; (void)tabs; (void)next_load; (void)tile_hi;\n";
-  k << o.str();
-  k << "  };\n";
-  k << "  fdev::run_pass<" << (two ? "true" : "false") << ", " << (db ? "true" : "false") << ", "
-    << (direct ? "true" : "false") << ", decltype(body), " << (split ? "true" : "false")
-    << ">(state, state_hi, P, phases, gen_partials, body);\n}\n";
+  if (pp) {
+    k << "  (void)phases;\n";
+    k << "  extern __shared__ __align__(16) unsigned char smem_raw[];\n";
+    k << "  double2* __restrict__ tile = reinterpret_cast<double2*>(smem_raw);   // 3 buffers; tile_off picks one\n";
+    k << "  auto body = [&](const int tile_off, const u64 base, double2* __restrict__ acc_warp, auto next_load) {\n";
+    k << "  (void)acc_warp; (void)tabs; (void)next_load;\n";
+    k << o.str();
+    k << "  };\n";
+    k << "  fdev::run_pass_pp<" << (two ? "true" : "false") << ">(state, state_hi, P, gen_partials, body);\n}\n";
+  } else {
+    k << "  auto body = [&](double2* __restrict__ tile, double2* __restrict__ tile_hi,\n"
+         "                  const fdev::DPhase* __restrict__ s_ph, const u64 base, double2* __restrict__ acc_warp,\n"
+         "                  auto next_load) {\n";
+    k << "  (void)acc_warp; (void)tabs; (void)next_load; (void)tile_hi;\n";
+    k << o.str();
+    k << "  };\n";
+    k << "  fdev::run_pass<" << (two ? "true" : "false") << ", " << (db ? "true" : "false") << ", "
+      << (direct ? "true" : "false") << ", decltype(body), " << (split ? "true" : "false")
+      << ">(state, state_hi, P, phases, gen_partials, body);\n}\n";
+  }
 
   if (cf_refs) *cf_refs = g.cf_refs;
   if (tab_refs) *tab_refs = g.tab_refs;
@@ -494,6 +675,7 @@ void jit_prepare(Program& prog, bool two) {
     }
     jp.kernel = it->second;
     jp.split = src.find("#define FDEV_SPLIT") != std::string::npos;
+    jp.pp = src.find("#define FDEV_PP") != std::string::npos;
   }
   if (const char* dump = getenv("SVB200_JIT_DUMP")) {   // debugging: write the generated sources
     for (size_t i = 0; i < todo.size(); ++i) {

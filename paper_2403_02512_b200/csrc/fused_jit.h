@@ -22,11 +22,13 @@ struct JitPass {
   std::vector<double2> cf;                      // the parameter block
   int tab_base = 0;                             // first entry in Program::jit_tabs
   bool split = false;                           // tile in 3 rotating half buffers (1.5 tiles of smem)
+  bool pp = false;                              // ping-pong loop: 512 threads, 1 CTA/SM, 3 tile buffers
 };
 
 // generated source of one pass (empty: not expressible, e.g. parameter block too large)
 bool jit_enabled();   // SVB200_JIT != 0: passes run as generated kernels (planner keeps structure value-free)
 bool jit_db();
+bool jit_pp();   // direct full-tile passes use the ping-pong tile loop (fused_dev.cuh run_pass_pp)
 int jit_ctas_per_sm();   // generated kernels use the double-buffered 1-CTA-per-SM tile loop
 std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, std::vector<std::pair<int, int>>* cf_refs,
                             std::vector<std::pair<int, int>>* tab_refs);

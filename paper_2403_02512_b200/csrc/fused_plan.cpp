@@ -272,7 +272,9 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
         op.mtype = uint8_t(mtype_of(m));
       } else {
         op.kind = FK_PAIRG;
-        op.mtype = uint8_t((mt == MT_X || mt == MT_REAL) ? MT_REAL : MT_GENERAL);
+        // MT_X stays visible (register-controlled X): the pass compiler turns it into register
+        // renaming instead of FP64 arithmetic; the interpreter runs it as the real 2x2 it is
+        op.mtype = uint8_t(mt == MT_X ? MT_X : (mt == MT_REAL ? MT_REAL : MT_GENERAL));
       }
       for (int j = 0; j < 4; ++j) prog.coef.push_back(make_double2(m[j].real(), m[j].imag()));
     } else if (p.type == PRIM_DIAG && p.nb == 0 && popcount64(op.cm) <= 1) {
@@ -367,7 +369,7 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
       case FK_PAIR1: op.cs = (dyn ? CS_PAIR1D : CS_PAIR1) + op.k * 4 + op.mtype; break;
       case FK_PHASE1: op.cs = (dyn ? CS_PHASE1D : CS_PHASE1) + op.k * 2 + op.v; break;
       case FK_SCALAR: op.cs = CS_SCALAR; break;
-      case FK_PAIRG: op.cs = (op.mtype == MT_REAL ? CS_PAIRGR : CS_PAIRG) + op.xr - 1; break;
+      case FK_PAIRG: op.cs = (op.mtype == MT_REAL || op.mtype == MT_X ? CS_PAIRGR : CS_PAIRG) + op.xr - 1; break;
       case FK_DIAGG: op.cs = CS_DIAGG; break;
       default: {
         static const uint8_t pairs[6] = {0x10, 0x20, 0x30, 0x21, 0x31, 0x32};
@@ -453,6 +455,18 @@ bool mergeable(const Prim& j, const Prim& i) {
   return false;
 }
 
+// Merging two rotations about different axes yields a general 2x2 (16 FP64 ops per amplitude
+// pair) where the two rotations cost 12 (two 3-shear rotations): only merge a PAIR into a PAIR
+// when the product is no more general than the more general of the two.
+bool merge_pays(const Prim& j, const Prim& i) {
+  if (i.type != PRIM_PAIR) return true;
+  const std::vector<cplx> a = i.m, b = j.m;
+  const std::vector<cplx> m = {a[0] * b[0] + a[1] * b[2], a[0] * b[1] + a[1] * b[3], a[2] * b[0] + a[3] * b[2],
+                               a[2] * b[1] + a[3] * b[3]};
+  auto general = [](const std::vector<cplx>& x) { return mtype_of(x) == MT_GENERAL; };
+  return !general(m) || general(a) || general(b);
+}
+
 void merge_into(Prim& j, const Prim& i) {
   if (i.type == PRIM_PAIR) {   // apply j then i: M = Mi * Mj
     const std::vector<cplx> a = i.m, b = j.m;
@@ -506,7 +520,7 @@ std::vector<std::pair<u64, std::vector<int>>> schedule_phases(std::vector<Prim>&
           }
         static const bool merge_on = !(getenv("SVB200_MERGE") && std::string(getenv("SVB200_MERGE")) == "0");
         if (merge_on && cand >= 0 && rq[cand].support == rq[i].support &&
-            mergeable(prims[list[cand]], prims[list[i]])) {
+            mergeable(prims[list[cand]], prims[list[i]]) && merge_pays(prims[list[cand]], prims[list[i]])) {
           merge_into(prims[list[cand]], prims[list[i]]);
           ++merged;
           continue;
@@ -882,7 +896,7 @@ double program_fp64_flops_per_amp(const fused::Program& prog) {
     else if ((cs >= CS_PHASE1 && cs < CS_PHASE1 + 8) || (cs >= CS_PHASE1D && cs < CS_PHASE1D + 8)) f += 8 * 6;
     else if (cs == CS_SCALAR) f += 16 * 6;
     else if (cs >= CS_PARITY && cs < CS_PARITY + 16) f += 8 * 6;
-    else if (cs >= CS_PAIRGR && cs < CS_PAIRGR + 15) f += 16 * 12 / 2.0 * subset(o.cm, o.xr);
+    else if (cs >= CS_PAIRGR && cs < CS_PAIRGR + 15) f += o.mtype == MT_X ? 0.0 : 16 * 12 / 2.0 * subset(o.cm, o.xr);
     else if (cs >= CS_PAIRG && cs < CS_PAIRG + 15) f += 16 * 28 / 2.0 * subset(o.cm, o.xr);
     else if (cs == CS_DIAGG) f += 16 * 6 * subset(o.cm, 0);
     else if (cs >= CS_DENSE2 && cs < CS_DENSE2 + 6) f += 4 * 16 * 8 * subset(o.cm, 0);
