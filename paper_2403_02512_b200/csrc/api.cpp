@@ -1,7 +1,9 @@
 // C-ABI of libsvb200 (include/svb200.h): handle lifecycle, validation with the reference's
 // error taxonomy, op-list execution, measurements and the adjoint-Jacobian driver.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
+#include <thread>
 #include <cstring>
 #include <functional>
 #include <map>
@@ -54,7 +56,7 @@ void sv_nccl_check(ncclResult_t r, const char* what) {
 void ensure_partials(sv_handle* h, size_t doubles) {
   if (h->partials_cap >= doubles) return;
   if (h->d_partials) {
-    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    stream_sync(h);
     CUDA_CHECK(cudaFree(h->d_partials));
   }
   size_t cap = std::max<size_t>(doubles, 4096);
@@ -65,12 +67,42 @@ void ensure_partials(sv_handle* h, size_t doubles) {
 void ensure_results(sv_handle* h, size_t doubles) {
   if (h->results_cap >= doubles) return;
   if (h->d_results) {
-    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    stream_sync(h);
     CUDA_CHECK(cudaFree(h->d_results));
   }
   size_t cap = std::max<size_t>(doubles, 1024);
   CUDA_CHECK(cudaMalloc(&h->d_results, cap * sizeof(double)));
   h->results_cap = cap;
+}
+
+// Wait for the handle's stream.  Sharded handles poll instead of blocking: a peer that failed (or
+// died) leaves this rank's NCCL kernels waiting forever, so after SVB200_NCCL_TIMEOUT seconds
+// (default 600) -- or as soon as NCCL reports an asynchronous error -- the communicator is
+// aborted (ncclCommAbort, which also tears down the waiting kernels) and the call fails with a
+// device error instead of hanging every rank.
+void stream_sync(sv_handle* h) {
+  if (!h->comm) {
+    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    return;
+  }
+  static const double timeout_s = getenv("SVB200_NCCL_TIMEOUT") ? atof(getenv("SVB200_NCCL_TIMEOUT")) : 600.0;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (int spin = 0;; ++spin) {
+    const cudaError_t e = cudaStreamQuery(h->stream);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) CUDA_CHECK(e);
+    ncclResult_t ae = ncclSuccess;
+    ncclCommGetAsyncError(h->comm, &ae);
+    const double waited = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if ((ae != ncclSuccess && ae != ncclInProgress) || waited > timeout_s) {
+      dist_abort(h);
+      sv_fail(SV_ERR_DEVICE, ae != ncclSuccess && ae != ncclInProgress
+                                 ? std::string("NCCL asynchronous error: ") + ncclGetErrorString(ae) + "; communicator aborted"
+                                 : "no progress for " + std::to_string(int(waited)) +
+                                       " s (a peer rank failed?); communicator aborted");
+    }
+    if (spin > 64) std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
 }
 
 static double* ensure_pinned(sv_handle* h, size_t doubles) {
@@ -114,7 +146,7 @@ void stat_end(sv_handle* h, int cls, double bytes, cudaEvent_t* ev) {
 
 static void drain_timings(sv_handle* h) {
   if (h->pending.empty()) return;
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   for (auto& p : h->pending) {
     float ms = 0;
     CUDA_CHECK(cudaEventElapsedTime(&ms, p.start, p.stop));
@@ -199,8 +231,7 @@ static void schedule_sharded(sv_handle* h, const std::vector<double2*>& states, 
     std::vector<int> keep;
     for (int o = 0; o < h->n; ++o)
       if ((req[rem[0]].dense >> o) & 1) keep.push_back(o);
-    for (int o : keep)
-      if (h->phys[o] >= h->nl) dist_swap_in(h, states, o, keep, next_use);
+    dist_bring_local(h, states, keep, next_use);
   }
 }
 
@@ -372,7 +403,7 @@ static double expval_impl(sv_handle* h, const sv_obs& o) {
     if (g.nb <= 4) {
       braket_prim_async(h, h->state, h->state, g, h->d_results);
       CUDA_CHECK(cudaMemcpyAsync(z, h->d_results, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-      CUDA_CHECK(cudaStreamSynchronize(h->stream));
+      stream_sync(h);
     } else {
       // 5+ wires: lambda = O psi in one extra buffer (smem DENSE kernel), then Re<psi|lambda>
       size_t free_b = 0, total_b = 0;
@@ -404,7 +435,7 @@ static double expval_impl(sv_handle* h, const sv_obs& o) {
   std::vector<double> vals(groups.size());
   if (!groups.empty()) {
     CUDA_CHECK(cudaMemcpyAsync(vals.data(), h->d_results, groups.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    stream_sync(h);
   }
   dist_allreduce_sum(h, vals.data(), vals.size());
   double s = 0.0;
@@ -528,7 +559,7 @@ static double adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const
     for (auto& g : gens) im[g.first] += g.second.imag();
     batch.clear();
   });
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   dist_allreduce_sum(h, im.data(), im.size());
   for (int c = 0; c < ncols; ++c) jac_row[c] = -2.0 * prefactor[c] * im[c];
   return im[ncols];
@@ -617,7 +648,7 @@ static void create_common(sv_handle* h, int n_qubits, int device) {
   CUDA_CHECK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
   CUDA_CHECK(cudaMalloc(&h->state, h->n_local * amp_bytes(h)));
   launch_init_zero(h, h->state, 0, h->rank == 0);
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
 }
 
 static void release_adjoint_buffers(sv_handle* h) {
@@ -686,7 +717,7 @@ int sv_set_state_c64(sv_handle* h, const float* amps, uint64_t n_amps) {
     sv_fail(SV_ERR_VALIDATION, "amplitude array length " + std::to_string(n_amps) + " does not match 2**" + std::to_string(h->n));
   dist_reset_layout(h);
   CUDA_CHECK(cudaMemcpyAsync(h->state, amps, h->n_local * sizeof(float2), cudaMemcpyHostToDevice, h->stream));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   API_END
 }
 
@@ -700,7 +731,7 @@ int sv_get_state_c64(sv_handle* h, float* out, uint64_t n_amps) {
     sv_fail(SV_ERR_VALIDATION, "output length " + std::to_string(n_amps) + " does not match 2**" + std::to_string(h->n));
   // complex64 handles never run the fusion engine, so the layout is the identity here
   CUDA_CHECK(cudaMemcpyAsync(out, h->state, h->n_local * sizeof(float2), cudaMemcpyDeviceToHost, h->stream));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   API_END
 }
 
@@ -763,7 +794,7 @@ int sv_reset(sv_handle* h) {
   std::lock_guard<std::mutex> lk(h->mu);
   dist_reset_layout(h);
   launch_init_zero(h, h->state, 0, h->rank == 0);
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   API_END
 }
 
@@ -775,7 +806,7 @@ int sv_set_basis_state(sv_handle* h, uint64_t index) {
   dist_reset_layout(h);
   const u64 owner = index >> h->nl;
   launch_init_zero(h, h->state, index & (h->n_local - 1), owner == u64(h->rank));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   API_END
 }
 
@@ -790,7 +821,7 @@ int sv_set_state(sv_handle* h, const double* amps, uint64_t n_amps) {
   dist_reset_layout(h);
   const double* src = amps + 2 * (u64(h->rank) << h->nl);
   CUDA_CHECK(cudaMemcpyAsync(h->state, src, h->n_local * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   API_END
 }
 
@@ -805,7 +836,7 @@ int sv_get_state(sv_handle* h, double* out, uint64_t n_amps) {
   dist_canonicalize(h, {h->state});
   if (h->world == 1) {
     CUDA_CHECK(cudaMemcpyAsync(out, h->state, h->n_local * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
-    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    stream_sync(h);
   } else {
     dist_gather_state(h, out);
   }
@@ -828,7 +859,7 @@ int sv_apply_ops(sv_handle* h, const sv_op* ops, int n_ops, int fuse) {
   std::lock_guard<std::mutex> lk(h->mu);
   validate_ops(h, ops, n_ops);   // trainable flags are irrelevant for plain application
   run_ops(h, {h->state}, ops, n_ops, fuse);
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   API_END
 }
 
@@ -845,7 +876,7 @@ int sv_apply_single_qubit(sv_handle* h, int q, const double* m2x2) {
   op.matrix = m2x2;
   std::lock_guard<std::mutex> lk(h->mu);
   run_ops(h, {h->state}, &op, 1, 0);
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   API_END
 }
 
@@ -867,7 +898,7 @@ int sv_apply_controlled_single_qubit(sv_handle* h, const int32_t* ctrls, int n_c
   validate_op(op, h->n);
   std::lock_guard<std::mutex> lk(h->mu);
   run_ops(h, {h->state}, &op, 1, 0);
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   API_END
 }
 
@@ -883,7 +914,7 @@ int sv_apply_matrix(sv_handle* h, const int32_t* wires, int n_wires, const doubl
   validate_op(op, h->n);
   std::lock_guard<std::mutex> lk(h->mu);
   run_ops(h, {h->state}, &op, 1, 0);
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   API_END
 }
 
@@ -1035,7 +1066,7 @@ int sv_adjoint_jacobian(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs*
 int sv_synchronize(sv_handle* h) {
   API_BEGIN
   check_handle(h);
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   API_END
 }
 
@@ -1148,6 +1179,14 @@ int sv_plan_sharded(int n_qubits, int rank, int world, const sv_op* ops, int n_o
       I.push_back(s.G);
       continue;
     }
+    if (s.kind == REC_XSWAP) {
+      I.push_back(int64_t(s.Gs.size()));
+      for (size_t i = 0; i < s.Gs.size(); ++i) {
+        I.push_back(s.Gs[i]);
+        I.push_back(s.ps[i]);
+      }
+      continue;
+    }
     const Prim& p = s.p;
     I.push_back(p.type);
     I.push_back(int64_t(p.fmask));
@@ -1245,7 +1284,7 @@ void adjoint_sweep(sv_handle* h, const sv_op* ops, int n_ops, const std::vector<
   std::vector<double> z(size_t(ncols) * n_obs * 2, 0.0);
   if (!z.empty()) {
     CUDA_CHECK(cudaMemcpyAsync(z.data(), h->d_results, z.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    stream_sync(h);
   }
   dist_allreduce_sum(h, z.data(), z.size());
   for (int k = 0; k < n_obs; ++k)

@@ -46,14 +46,14 @@ void device_barrier(sv_handle* h) {
   NCCL_CHECK(ncclAllReduce(h->d_barrier, h->d_barrier, 1, ncclInt, ncclSum, h->comm, h->stream));
 }
 
-// Collective: export `buf` (a cudaMalloc base) with CUDA IPC, all-gather the handles and map the
-// log2 P partners' copies.  Returns 1 when every rank mapped all its partners (else nothing
-// stays mapped on any rank).
+// Collective: export `buf` (a cudaMalloc base) with CUDA IPC, all-gather the handles and map
+// every other rank's copy (world <= 8: a multi-bit exchange talks to any rank of its group).
+// Returns 1 when every rank mapped all its peers (else nothing stays mapped on any rank).
 int register_peers(sv_handle* h, double2* buf) {
-  int ok = 1;
+  int ok = h->world <= 8 ? 1 : 0;
   cudaIpcMemHandle_t mine;
   std::memset(&mine, 0, sizeof(mine));
-  if (cudaIpcGetMemHandle(&mine, buf) != cudaSuccess) {
+  if (ok && cudaIpcGetMemHandle(&mine, buf) != cudaSuccess) {
     cudaGetLastError();
     ok = 0;
   }
@@ -64,101 +64,145 @@ int register_peers(sv_handle* h, double2* buf) {
   NCCL_CHECK(ncclAllGather(d_handles + hb * h->world, d_handles, hb, ncclChar, h->comm, h->stream));
   std::vector<cudaIpcMemHandle_t> all(h->world);
   CUDA_CHECK(cudaMemcpyAsync(all.data(), d_handles, hb * h->world, cudaMemcpyDeviceToHost, h->stream));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   CUDA_CHECK(cudaFree(d_handles));
   sv_handle::PeerMap pm;
   pm.local = buf;
-  for (int j = 0; j < 8; ++j) pm.peer[j] = nullptr;
-  for (int j = 0; ok && j < h->g && j < 8; ++j) {
+  for (int r = 0; r < 8; ++r) pm.by_rank[r] = nullptr;
+  for (int r = 0; ok && r < h->world; ++r) {
+    if (r == h->rank) continue;
     void* p = nullptr;
-    if (cudaIpcOpenMemHandle(&p, all[h->rank ^ (1 << j)], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+    if (cudaIpcOpenMemHandle(&p, all[r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
       cudaGetLastError();
       ok = 0;
       break;
     }
-    pm.peer[j] = static_cast<double2*>(p);
+    pm.by_rank[r] = static_cast<double2*>(p);
   }
   int* d_ok = h->d_barrier + 1;
   CUDA_CHECK(cudaMemcpyAsync(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice, h->stream));
   NCCL_CHECK(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, h->comm, h->stream));
   CUDA_CHECK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   if (ok) {
     h->peers.push_back(pm);
   } else {
-    for (int j = 0; j < 8; ++j)
-      if (pm.peer[j]) cudaIpcCloseMemHandle(pm.peer[j]);
+    for (int r = 0; r < 8; ++r)
+      if (pm.by_rank[r]) cudaIpcCloseMemHandle(pm.by_rank[r]);
   }
   return ok;
 }
 
-// partner copy of `buf` for global bit j (registering it on first use), or nullptr
-double2* peer_of(sv_handle* h, double2* buf, int j) {
-  if (!h->p2p || j >= 8) return nullptr;
+// the peer map of `buf` (registering it on first use, collectively); false when unavailable.
+// Returned by value: registering another buffer may reallocate h->peers.
+bool peers_of(sv_handle* h, double2* buf, sv_handle::PeerMap* out) {
+  if (!h->p2p) return false;
   for (const auto& pm : h->peers)
-    if (pm.local == buf) return pm.peer[j];
-  if (!register_peers(h, buf)) return nullptr;
-  return h->peers.back().peer[j];
+    if (pm.local == buf) {
+      *out = pm;
+      return true;
+    }
+  if (!register_peers(h, buf)) return false;
+  *out = h->peers.back();
+  return true;
+}
+
+// Exchange global positions Gs[i] with local positions ps[i] (i < k <= 3), all at once: an amplitude
+// whose bits at ps spell c (bit i <-> ps[i]) moves to the rank whose bits at Gs spell c, at the same
+// local index with the ps bits set to this rank's bits at Gs.  k = 1 is a qubit-index swap with
+// one partner (half the shard crosses NVLink); k = log2 P is one all-to-all over all ranks
+// ((1 - 2^-k) of the shard) -- cheaper than k sequential single-bit swaps (k / 2 of the shard) and
+// with no local bit-permutation pass: the victims stay where they are.
+//   peer memory (default): one kernel reads and writes the partners' states mapped over NVLink,
+//     each rank pair splitting its pairs on a free local bit; two stream-ordered barriers;
+//   fallback (NCCL): per partner (XOR schedule, deadlock-free), gather the elements through the
+//     staging buffer, ncclSend/ncclRecv, scatter -- the same element placement, so both paths
+//     give bit-identical states.
+void exchange_bits(sv_handle* h, const std::vector<double2*>& states, const std::vector<int>& Gs,
+                   const std::vector<int>& ps) {
+  const int k = int(Gs.size());
+  if (k == 0) return;
+  if (k > 3 || int(ps.size()) != k) sv_fail(SV_ERR_DEVICE, "internal: bad exchange");
+  auto relayout = [&]() {
+    std::vector<int> og(k), op(k);
+    for (int i = 0; i < k; ++i) {
+      og[i] = logical_at(h, Gs[i]);
+      op[i] = logical_at(h, ps[i]);
+    }
+    for (int i = 0; i < k; ++i) {
+      h->phys[og[i]] = ps[i];
+      h->phys[op[i]] = Gs[i];
+    }
+  };
+  if (h->recording) {
+    RecStep st;
+    st.kind = REC_XSWAP;
+    st.Gs = Gs;
+    st.ps = ps;
+    h->rec.push_back(st);
+    relayout();
+    return;
+  }
+  const int nc = 1 << k;
+  u64 vmask = 0, vdep[8] = {0};
+  for (int c = 0; c < nc; ++c)
+    for (int i = 0; i < k; ++i)
+      if ((c >> i) & 1) vdep[c] |= 1ull << ps[i];
+  for (int i = 0; i < k; ++i) vmask |= 1ull << ps[i];
+  int g = 0, rank_of[8];
+  for (int i = 0; i < k; ++i) g |= ((h->rank >> (Gs[i] - h->nl)) & 1) << i;
+  for (int c = 0; c < nc; ++c) {
+    int r = h->rank;
+    for (int i = 0; i < k; ++i) r = (r & ~(1 << (Gs[i] - h->nl))) | (((c >> i) & 1) << (Gs[i] - h->nl));
+    rank_of[c] = r;
+  }
+  const u64 moved = (h->n_local >> k) * u64(nc - 1);   // amplitudes leaving this rank
+  cudaEvent_t ev[2];
+  bool p2p = h->p2p;
+  std::vector<sv_handle::PeerMap> maps(states.size());
+  for (size_t si = 0; si < states.size() && p2p; ++si) p2p = peers_of(h, states[si], &maps[si]);
+  for (size_t si = 0; si < states.size(); ++si) {
+    double2* st = states[si];
+    stat_begin(h, KC_SWAP, 32.0 * double(moved), ev);
+    if (p2p) {
+      // pairs with partner c split on the highest local bit that is not a victim
+      int q = h->nl - 1;
+      while ((vmask >> q) & 1) --q;
+      double2* peer[8];
+      u64 own[8];
+      for (int c = 0; c < nc; ++c) {
+        peer[c] = c == g ? nullptr : maps[si].by_rank[rank_of[c]];
+        own[c] = h->rank < rank_of[c] ? 0ull : (1ull << q);
+      }
+      device_barrier(h);   // the partners' earlier kernels on their states are done
+      launch_exchange_multi(h, st, peer, vdep, own, vdep[g], nc, vmask | (1ull << q), h->n_local >> (k + 1));
+      device_barrier(h);   // their stores into ours are visible
+    } else {
+      const u64 per = h->n_local >> k;   // amplitudes exchanged with each partner
+      const u64 chunk = h->staging_amps / 2;
+      double2* sbuf = h->staging;
+      double2* rbuf = h->staging + chunk;
+      for (int step = 1; step < nc; ++step) {
+        const int c = g ^ step;
+        for (u64 t = 0; t < per; t += chunk) {
+          const u64 len = std::min<u64>(chunk, per - t);
+          launch_pack_sel(h, st, sbuf, vmask, vdep[c], t, len, false);
+          NCCL_CHECK(ncclGroupStart());
+          NCCL_CHECK(ncclSend(sbuf, len * 2, ncclDouble, rank_of[c], h->comm, h->stream));
+          NCCL_CHECK(ncclRecv(rbuf, len * 2, ncclDouble, rank_of[c], h->comm, h->stream));
+          NCCL_CHECK(ncclGroupEnd());
+          launch_pack_sel(h, st, rbuf, vmask, vdep[c], t, len, true);
+        }
+      }
+    }
+    stat_end(h, KC_SWAP, 32.0 * double(moved), ev);
+  }
+  relayout();
 }
 
 // exchange the top local bit (nl-1) with global position G = nl + j
 void global_swap_top(sv_handle* h, const std::vector<double2*>& states, int G) {
-  if (h->recording) {
-    h->rec.push_back({REC_GSWAP, Prim(), G});
-    int ot = logical_at(h, h->nl - 1), og = logical_at(h, G);
-    h->phys[ot] = G;
-    h->phys[og] = h->nl - 1;
-    return;
-  }
-  const int j = G - h->nl;
-  const int partner = h->rank ^ (1 << j);
-  const int b = (h->rank >> j) & 1;
-  const u64 half = h->n_local >> 1;
-  // we send our (top bit = 1-b) half and receive the partner's (top bit = b) half into it
-  const u64 my_off = (1 - b) ? half : 0;
-  // Chunk k: send our chunk k and receive the partner's into staging slot k&1 (main stream), then
-  // copy the slot over our chunk k on the copy stream -- so the copy of chunk k overlaps the
-  // transfer of chunk k+1.  A slot is reused only after its previous copy finished; chunk k+1's
-  // send reads a region no copy has touched yet.
-  const u64 chunk = h->staging_amps / 2;
-  cudaEvent_t ev[2];
-  for (double2* st : states) {
-    stat_begin(h, KC_SWAP, 32.0 * double(half), ev);
-    double2* peer = peer_of(h, st, j);
-    if (peer) {
-      // Peer-memory swap: our (top = 1-b) half and the partner's (top = b) half exchange
-      // element by element, in place, through the partner's state mapped over NVLink.  The two
-      // ranks split the range (b = 0 the first half, b = 1 the second); barriers before (the
-      // partner's earlier kernels on its state are done) and after (its stores into ours are).
-      const u64 share = half >> 1, lo = b ? share : 0;
-      const u64 peer_off = b ? half : 0;
-      device_barrier(h);
-      launch_exchange(h, st + my_off + lo, peer + peer_off + lo, b ? half - share : share);
-      device_barrier(h);
-      stat_end(h, KC_SWAP, 32.0 * double(half), ev);
-      continue;
-    }
-    int k = 0;
-    for (u64 c = 0; c < half; c += chunk, ++k) {
-      const u64 len = std::min<u64>(chunk, half - c);
-      double2* slot = h->staging + (k & 1) * chunk;
-      if (k >= 2) CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_copy[k & 1], 0));
-      NCCL_CHECK(ncclGroupStart());
-      NCCL_CHECK(ncclSend(st + my_off + c, len * 2, ncclDouble, partner, h->comm, h->stream));
-      NCCL_CHECK(ncclRecv(slot, len * 2, ncclDouble, partner, h->comm, h->stream));
-      NCCL_CHECK(ncclGroupEnd());
-      CUDA_CHECK(cudaEventRecord(h->ev_recv[k & 1], h->stream));
-      CUDA_CHECK(cudaStreamWaitEvent(h->copy_stream, h->ev_recv[k & 1], 0));
-      CUDA_CHECK(cudaMemcpyAsync(st + my_off + c, slot, len * sizeof(double2), cudaMemcpyDeviceToDevice,
-                                 h->copy_stream));
-      CUDA_CHECK(cudaEventRecord(h->ev_copy[k & 1], h->copy_stream));
-    }
-    for (int s = 0; s < std::min(k, 2); ++s) CUDA_CHECK(cudaStreamWaitEvent(h->stream, h->ev_copy[s], 0));
-    stat_end(h, KC_SWAP, 32.0 * double(half), ev);
-  }
-  int ot = logical_at(h, h->nl - 1), og = logical_at(h, G);
-  h->phys[ot] = G;
-  h->phys[og] = h->nl - 1;
+  exchange_bits(h, states, {G}, {h->nl - 1});
 }
 
 // bring logical offset o (currently global) local, evicting a local qubit not in `keep`
@@ -176,8 +220,7 @@ void make_one_local(sv_handle* h, const std::vector<double2*>& states, int o, co
       break;
     }
   if (victim < 0) sv_fail(SV_ERR_CAPACITY, "gate acts on more qubits than one shard holds locally");
-  local_bit_swap(h, states, victim, h->nl - 1);
-  global_swap_top(h, states, G);
+  exchange_bits(h, states, {G}, {victim});
 }
 }  // namespace
 
@@ -203,7 +246,7 @@ void dist_init(sv_handle* h, const void* nccl_id) {
   CUDA_CHECK(cudaMemcpyAsync(d_ok, &want, sizeof(int), cudaMemcpyHostToDevice, h->stream));
   NCCL_CHECK(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, h->comm, h->stream));
   CUDA_CHECK(cudaMemcpyAsync(&want, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   h->p2p = want && register_peers(h, h->state);
 }
 
@@ -213,23 +256,41 @@ void dist_forget(sv_handle* h, double2* buf) {
     if (h->peers[i].local == buf) {
       // every rank is done with every mapping of this buffer before any rank unmaps or frees it
       if (ncclAllReduce(h->d_barrier, h->d_barrier, 1, ncclInt, ncclSum, h->comm, h->stream) == ncclSuccess)
-        cudaStreamSynchronize(h->stream);
-      for (int j = 0; j < 8; ++j)
-        if (h->peers[i].peer[j]) cudaIpcCloseMemHandle(h->peers[i].peer[j]);
+        try {
+          stream_sync(h);   // bounded wait: a dead peer aborts the communicator instead of hanging
+        } catch (const SvError&) {
+        }
+      for (int r = 0; r < 8; ++r)
+        if (h->peers[i].by_rank[r]) cudaIpcCloseMemHandle(h->peers[i].by_rank[r]);
       h->peers.erase(h->peers.begin() + long(i));
       return;
     }
 }
 
+void dist_abort(sv_handle* h) {
+  if (!h->comm) return;
+  ncclCommAbort(h->comm);
+  h->comm = nullptr;
+  h->p2p = false;   // peer mappings stay until destroy; no further exchanges
+}
+
 void dist_destroy(sv_handle* h) {
+  const cudaError_t q = h->comm ? cudaStreamQuery(h->stream) : cudaSuccess;
+  if (q != cudaSuccess && q != cudaErrorNotReady) {
+    cudaGetLastError();
+    dist_abort(h);   // a failed device context: destroying would wait on peers forever
+  }
   if (h->p2p && h->comm) {
     // no rank unmaps (or frees) a state its partner may still be exchanging with
     if (ncclAllReduce(h->d_barrier, h->d_barrier, 1, ncclInt, ncclSum, h->comm, h->stream) == ncclSuccess)
-      cudaStreamSynchronize(h->stream);
+      try {
+        stream_sync(h);
+      } catch (const SvError&) {
+      }
   }
   for (auto& pm : h->peers)
-    for (int j = 0; j < 8; ++j)
-      if (pm.peer[j]) cudaIpcCloseMemHandle(pm.peer[j]);
+    for (int r = 0; r < 8; ++r)
+      if (pm.by_rank[r]) cudaIpcCloseMemHandle(pm.by_rank[r]);
   h->peers.clear();
   h->p2p = false;
   if (h->d_barrier) {
@@ -264,6 +325,50 @@ bool prim_needs_swap(const Prim& p, int nl) {
   return false;
 }
 
+// Bring every global qubit in `keep` local with ONE exchange (exchange_bits), plus -- while an
+// exchange is happening anyway -- the other global qubits needed again before some local qubit
+// would be (Belady: victims are the local qubits not in `keep` whose next use is furthest; ties
+// prefer positions >= 3 (whole 128-byte runs stay together) and then the highest position).
+void dist_bring_local(sv_handle* h, const std::vector<double2*>& states, const std::vector<int>& keep,
+                      const std::vector<int>& next_use) {
+  std::vector<int> in;
+  for (int o : keep)
+    if (h->phys[o] >= h->nl) in.push_back(o);
+  if (in.empty()) return;
+  std::vector<std::pair<int, int>> cand;   // (next use, local position)
+  for (int p = 0; p < h->nl; ++p) {
+    const int lo = logical_at(h, p);
+    if (std::find(keep.begin(), keep.end(), lo) != keep.end()) continue;
+    cand.push_back({next_use[lo], p});
+  }
+  std::sort(cand.begin(), cand.end(), [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+    if (a.first != b.first) return a.first > b.first;
+    if ((a.second >= 3) != (b.second >= 3)) return a.second >= 3;
+    return a.second > b.second;
+  });
+  if (cand.size() < in.size()) sv_fail(SV_ERR_CAPACITY, "operation spans more qubits than a shard holds locally");
+  std::vector<std::pair<int, int>> extra;   // (next use, logical offset) of the other global qubits
+  for (int G = h->nl; G < h->n; ++G) {
+    const int o = logical_at(h, G);
+    if (std::find(in.begin(), in.end(), o) == in.end() && next_use[o] < (1 << 30)) extra.push_back({next_use[o], o});
+  }
+  std::sort(extra.begin(), extra.end());
+  size_t vi = in.size();
+  for (const auto& e : extra)
+    if (vi < cand.size() && cand[vi].first > e.first) {
+      in.push_back(e.second);
+      ++vi;
+    }
+  for (size_t b = 0; b < in.size(); b += 3) {   // at most 3 bits per exchange (P <= 8 in one go)
+    std::vector<int> Gs, ps;
+    for (size_t i = b; i < std::min(in.size(), b + 3); ++i) {
+      Gs.push_back(h->phys[in[i]]);
+      ps.push_back(cand[i].second);
+    }
+    exchange_bits(h, states, Gs, ps);
+  }
+}
+
 void dist_swap_in(sv_handle* h, const std::vector<double2*>& states, int o, const std::vector<int>& keep,
                   const std::vector<int>& next_use) {
   const int G = h->phys[o];
@@ -279,8 +384,7 @@ void dist_swap_in(sv_handle* h, const std::vector<double2*>& states, int o, cons
     }
   }
   if (victim < 0) sv_fail(SV_ERR_CAPACITY, "operation spans more qubits than a shard holds locally");
-  local_bit_swap(h, states, victim, h->nl - 1);
-  global_swap_top(h, states, G);
+  exchange_bits(h, states, {G}, {victim});
 }
 
 void dist_make_local(sv_handle* h, const std::vector<double2*>& states, const std::vector<int>& wires) {
@@ -325,7 +429,7 @@ void dist_gather_state(sv_handle* h, double* out) {
       const double2* src = (r == h->rank) ? h->state + c : h->staging;
       NCCL_CHECK(ncclBroadcast(h->state + c, h->staging, len * 2, ncclDouble, r, h->comm, h->stream));
       CUDA_CHECK(cudaMemcpyAsync(out + 2 * (u64(r) * nl + c), src, len * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
-      CUDA_CHECK(cudaStreamSynchronize(h->stream));
+      stream_sync(h);
     }
   }
 }
@@ -336,7 +440,7 @@ void dist_allreduce_sum(sv_handle* h, double* host, size_t n) {
   CUDA_CHECK(cudaMemcpyAsync(h->d_results, host, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
   NCCL_CHECK(ncclAllReduce(h->d_results, h->d_results, n, ncclDouble, ncclSum, h->comm, h->stream));
   CUDA_CHECK(cudaMemcpyAsync(host, h->d_results, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
 }
 
 void dist_probs(sv_handle* h, const std::vector<int>& wires, double* out) {
@@ -360,7 +464,7 @@ void dist_probs(sv_handle* h, const std::vector<int>& wires, double* out) {
   probs_async(h, h->state, lpos, h->d_results);
   std::vector<double> local(lbins);
   CUDA_CHECK(cudaMemcpyAsync(local.data(), h->d_results, lbins * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   const u64 bins = 1ull << w;
   if (h->world == 1) {
     std::memcpy(out, local.data(), bins * sizeof(double));

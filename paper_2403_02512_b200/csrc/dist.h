@@ -19,6 +19,10 @@ void dist_make_local_set(sv_handle* h, const std::vector<double2*>& states, cons
 // bring logical offset o local; victim = local qubit (offset not in keep) with the furthest next_use[offset]
 void dist_swap_in(sv_handle* h, const std::vector<double2*>& states, int o, const std::vector<int>& keep,
                   const std::vector<int>& next_use);
+// bring every global offset in keep local in one multi-bit exchange (plus Belady prefetch of the
+// other global qubits needed before the victims are)
+void dist_bring_local(sv_handle* h, const std::vector<double2*>& states, const std::vector<int>& keep,
+                      const std::vector<int>& next_use);
 void dist_canonicalize(sv_handle* h, const std::vector<double2*>& states);
 void dist_reset_layout(sv_handle* h);
 void dist_gather_state(sv_handle* h, double* out);

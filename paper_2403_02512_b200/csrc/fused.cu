@@ -539,7 +539,7 @@ void* program_buffer(sv_handle* h, size_t bytes) {
   for (auto& e : g_progs)
     if (e.first == h) {
       if (e.second.cap < bytes) {
-        CUDA_CHECK(cudaStreamSynchronize(h->stream));
+        stream_sync(h);
         CUDA_CHECK(cudaFree(e.second.buf));
         e.second.cap = std::max(bytes, size_t(1) << 20);
         CUDA_CHECK(cudaMalloc(&e.second.buf, e.second.cap));
@@ -676,7 +676,7 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
   }
   std::memcpy(host.data() + align(b_ph) + align(b_op), prog.coef.data(), b_cf);
   if (b_jt) std::memcpy(host.data() + align(b_ph) + align(b_op) + align(b_cf), prog.jit_tabs.data(), b_jt);
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));   // previous program may still be in use
+  stream_sync(h);   // previous program may still be in use
   char* dbuf = (char*)program_buffer(h, total);
   CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), total, cudaMemcpyHostToDevice, h->stream));
   const DPhase* d_ph = (const DPhase*)dbuf;
@@ -744,7 +744,7 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
     std::vector<double> z(size_t(2) * n_gen);
     CUDA_CHECK(cudaMemcpyAsync(z.data(), h->d_results, z.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     CUDA_CHECK(cudaFreeAsync(d_gen, h->stream));
-    CUDA_CHECK(cudaStreamSynchronize(h->stream));
+    stream_sync(h);
     gen_out->clear();
     for (int s = 0; s < n_gen; ++s) gen_out->push_back({prog.gen_slot_of[s], cplx(z[2 * s], z[2 * s + 1])});
   }

@@ -724,6 +724,65 @@ __global__ void __launch_bounds__(kThreads) k_exchange(double2* __restrict__ a, 
   __threadfence_system();   // remote stores visible before the post-swap barrier
 }
 
+// Multi-bit qubit-index exchange over peer memory (dist.cpp exchange_bits): the victim local bits
+// (vdep) of element i spell the partner c; element i swaps with element (i's base | gdep) of
+// partner c's state.  Each pair of ranks splits its pairs on one free local bit (own[c]).  The
+// counter t enumerates the local bits that are neither victims nor the split bit; consecutive t
+// are consecutive amplitudes when those bits are the low ones, so every access is a full sector.
+struct XchgParams {
+  double2* peer[8];
+  u64 vdep[8];
+  u64 own[8];
+  u64 gdep;
+  u64 count;
+  Ins ins;
+  int nc;
+};
+
+__global__ void __launch_bounds__(kThreads) k_exchange_multi(double2* __restrict__ a, const XchgParams P) {
+  constexpr int IT = 2;
+  const u64 stride = u64(gridDim.x) * kThreads * IT;
+  for (u64 t0 = u64(blockIdx.x) * kThreads * IT + threadIdx.x; t0 < P.count; t0 += stride) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      if (c >= P.nc || !P.peer[c]) continue;
+      double2 x[IT], y[IT];
+      u64 il[IT], ir[IT];
+#pragma unroll
+      for (int j = 0; j < IT; ++j) {
+        const u64 t = t0 + u64(j) * kThreads;
+        if (t < P.count) {
+          const u64 b = deposit(t, P.ins) | P.own[c];
+          il[j] = b | P.vdep[c];
+          ir[j] = b | P.gdep;
+          x[j] = a[il[j]];
+          y[j] = P.peer[c][ir[j]];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < IT; ++j) {
+        const u64 t = t0 + u64(j) * kThreads;
+        if (t < P.count) {
+          a[il[j]] = y[j];
+          P.peer[c][ir[j]] = x[j];
+        }
+      }
+    }
+  }
+  __threadfence_system();   // remote stores visible before the post-exchange barrier
+}
+
+// NCCL fallback of the same exchange: gather / scatter the elements whose victim bits spell one
+// partner (counter t over the non-victim bits, the same order on both ranks) through staging.
+__global__ void __launch_bounds__(kThreads) k_pack_sel(const double2* __restrict__ a, double2* __restrict__ out,
+                                                      const Ins ins, u64 vdep, u64 t_begin, u64 n, int unpack) {
+  for (u64 t = u64(blockIdx.x) * kThreads + threadIdx.x; t < n; t += u64(gridDim.x) * kThreads) {
+    const u64 i = deposit(t_begin + t, ins) | vdep;
+    if (unpack) const_cast<double2*>(a)[i] = out[t];
+    else out[t] = a[i];
+  }
+}
+
 Ins make_ins(u64 fmask) {
   Ins s;
   s.n = 0;
@@ -784,7 +843,7 @@ void* scratch_upload(sv_handle* h, const void* src, size_t bytes) {
   h->scratch_slot = (h->scratch_slot + 1) % 64;
   if (b.cap < bytes) {
     if (b.ptr) {
-      CUDA_CHECK(cudaStreamSynchronize(h->stream));
+      stream_sync(h);
       CUDA_CHECK(cudaFree(b.ptr));
     }
     size_t cap = std::max<size_t>(bytes, 4096);
@@ -930,6 +989,34 @@ void launch_exchange(sv_handle* h, double2* a, double2* b, u64 n) {
   CUDA_CHECK(cudaGetLastError());
 }
 
+void launch_exchange_multi(sv_handle* h, double2* a, double2* const* peer_by_c, const u64* vdep, const u64* own, u64 gdep,
+                           int nc, u64 split_fmask, u64 count) {
+  if (count == 0) return;
+  XchgParams P;
+  std::memset(&P, 0, sizeof(P));
+  for (int c = 0; c < nc; ++c) {
+    P.peer[c] = peer_by_c[c];
+    P.vdep[c] = vdep[c];
+    P.own[c] = own[c];
+  }
+  P.gdep = gdep;
+  P.count = count;
+  P.nc = nc;
+  P.ins = make_ins(split_fmask);
+  const unsigned g = unsigned(std::min<u64>(grid_for(count, kThreads * 2), 148ull * 8));
+  k_exchange_multi<<<g, kThreads, 0, h->stream>>>(a, P);
+  h->launches++;
+  CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_pack_sel(sv_handle* h, double2* a, double2* buf, u64 victim_mask, u64 vdep, u64 t_begin, u64 n, bool unpack) {
+  if (n == 0) return;
+  const unsigned g = unsigned(std::min<u64>(grid_for(n, kThreads), 148ull * 16));
+  k_pack_sel<<<g, kThreads, 0, h->stream>>>(a, buf, make_ins(victim_mask), vdep, t_begin, n, unpack ? 1 : 0);
+  h->launches++;
+  CUDA_CHECK(cudaGetLastError());
+}
+
 void sum_partials(sv_handle* h, const double* partials, int nblocks, int ncomp, double* d_out) {
   k_sum_partials<<<ncomp, kThreads, 0, h->stream>>>(partials, nblocks, ncomp, d_out);
   h->launches++;
@@ -948,7 +1035,7 @@ double reduce_norm2(sv_handle* h, const double2* a) {
   sum_partials(h, h->d_partials, g, 1, h->d_results);
   double out = 0;
   CUDA_CHECK(cudaMemcpyAsync(&out, h->d_results, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   return out;
 }
 
@@ -1156,7 +1243,7 @@ double csr_apply_or_expval(sv_handle* h, const sv_obs& o, const double2* psi, do
     CUDA_CHECK(cudaMemcpyAsync(&out, h->d_results, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
   }
   CUDA_CHECK(cudaFreeAsync(buf, h->stream));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   return out;
 }
 
@@ -1172,7 +1259,7 @@ double reduce_dot_re(sv_handle* h, const double2* a, const double2* b) {
   sum_partials(h, h->d_partials, g, 1, h->d_results);
   double out = 0;
   CUDA_CHECK(cudaMemcpyAsync(&out, h->d_results, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  CUDA_CHECK(cudaStreamSynchronize(h->stream));
+  stream_sync(h);
   return out;
 }
 

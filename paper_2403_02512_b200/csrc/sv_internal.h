@@ -83,11 +83,12 @@ extern const char* kKernelClassNames[KC_COUNT];
 
 // Recording mode (host-only planning of a sharded run, used by sv_plan_sharded): instead of
 // launching, the executors append what they would do.
-enum RecKind { REC_PRIM = 0, REC_GSWAP = 1 };
+enum RecKind { REC_PRIM = 0, REC_GSWAP = 1, REC_XSWAP = 2 };
 struct RecStep {
   int kind;
   Prim p;      // REC_PRIM
   int G = -1;  // REC_GSWAP: global physical position exchanged with the top local bit
+  std::vector<int> Gs, ps;   // REC_XSWAP: global positions Gs[i] exchanged with local positions ps[i]
 };
 
 struct PendingTiming {
@@ -117,7 +118,7 @@ struct sv_handle {
   // IPC, per global bit j (partner rank ^ 2^j); registered collectively on first swap
   struct PeerMap {
     double2* local;
-    double2* peer[8];
+    double2* by_rank[8];   // every other rank's copy (world <= 8), nullptr for this rank
   };
   bool p2p = false;
   std::vector<PeerMap> peers;
@@ -169,6 +170,11 @@ void classify_prim(Prim& p);   // DENSE -> DIAG / PAIR specialisations when exac
 Prim adjoint_prim(const Prim& p);
 
 
+// api.cpp: wait for the handle's stream (sharded handles: NCCL watchdog + ncclCommAbort)
+void stream_sync(sv_handle* h);
+// dist.cpp: abort the communicator after a failure (peers then fail their own waits, not hang)
+void dist_abort(sv_handle* h);
+
 // kernels.cu
 double prim_bytes(const sv_handle* h, const Prim& p);
 void release_scratch(sv_handle* h);
@@ -177,6 +183,13 @@ void launch_init_zero(sv_handle* h, double2* state, u64 basis_local, bool set_on
 void launch_copy(sv_handle* h, double2* dst, const double2* src, u64 n);
 // element-wise exchange a[i] <-> b[i], i < n (b may be a peer GPU's memory mapped over NVLink)
 void launch_exchange(sv_handle* h, double2* a, double2* b, u64 n);
+// multi-bit exchange over peer memory (dist.cpp exchange_bits): for every partner c < nc with
+// peer_by_c[c] != nullptr, swap a[base | own[c] | vdep[c]] with peer_by_c[c][base | own[c] | gdep];
+// base = deposit(t, zero bits at split_fmask) for t < count
+void launch_exchange_multi(sv_handle* h, double2* a, double2* const* peer_by_c, const u64* vdep, const u64* own, u64 gdep,
+                           int nc, u64 split_fmask, u64 count);
+// buf[t] = a[deposit(t_begin + t, zeros at victim_mask) | vdep] for t < n (unpack: the reverse)
+void launch_pack_sel(sv_handle* h, double2* a, double2* buf, u64 victim_mask, u64 vdep, u64 t_begin, u64 n, bool unpack);
 double reduce_norm2(sv_handle* h, const double2* state);
 // per-term Pauli expectation: terms sharing an x-mask; returns sum_t Re(cc_t * <P_t>) (local part)
 struct PauliTerm {

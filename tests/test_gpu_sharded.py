@@ -1,4 +1,4 @@
-"""GPU, world_size 2 (and 4 when available): sharded state over NCCL vs the oracle.
+"""GPU, world_size 2, 4 and 8 (each skipped without enough GPUs): sharded state over NCCL vs the oracle.
 
 One process per GPU (SPEC.md:429-486 semantics; global qubits = top log2 P): state after
 random circuits (global-qubit swaps), expvals with X/Y/Z on global qubits, probabilities over
@@ -22,21 +22,67 @@ def n_gpus():
     return _lib.device_count()
 
 
+def run_world(target, world, n_ids, timeout=900):
+    """Spawn one process per GPU, return rank 0's (status, result).  A rank that fails makes its
+    peers' NCCL waits time out (SVB200_NCCL_TIMEOUT, communicator aborted) instead of hanging; any
+    process still alive at the end is killed."""
+    import os
+    from paper_2403_02512_b200.device import Device
+    os.environ.setdefault("SVB200_NCCL_TIMEOUT", "180")
+    nccl_ids = [Device.nccl_unique_id() for _ in range(n_ids)]   # one id per communicator
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=target, args=(r, world, nccl_ids, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    try:
+        status, out = q.get(timeout=timeout)
+    finally:
+        for p in procs:
+            p.join(timeout=60 if p is procs[0] else 30)
+            if p.is_alive():
+                p.kill()
+    return status, out
+
+
+# Shards span several 2^12-amplitude tiles (n_local = 14): the sharded fused passes run their
+# multi-tile tile loops on every rank (the bug class of round 1 lived exactly there).
+N_LOCAL = 14
+
+
+def sharded_ops(n, world, seed=3):
+    """Random circuit plus gates whose targets, controls and partners sit on the global qubits
+    0 .. log2(world)-1: globally-controlled gates (no exchange), dense gates across two global bits
+    (multi-bit exchange), SWAP / DoubleExcitation spanning global and local bits."""
+    g = world.bit_length() - 1
+    ops = workloads.random_circuit(n, 10, seed=seed)
+    ops += [Op("SWAP", (0, n - 1)), Op("IsingXX", (1 % n, 0), (0.3,)), Op("CNOT", (0, 1), ctrls=(5,)),
+            Op("DoubleExcitation", (0, 1, 6, 7), (0.4,)), Op("RZ", (1,), (0.7,), ctrls=(0,)),
+            Op("RY", (n - 2,), (0.9,), ctrls=(0,), ctrl_values=(0,)),
+            Op("CNOT", (n - 3, n - 4), ctrls=(g - 1,)),
+            Op("Rot", (g - 1,), (0.1, 0.2, 0.3)),
+            Op("IsingXY", (0, g - 1) if g > 1 else (0, 2), (0.6,)),
+            Op("SWAP", (0, g - 1) if g > 1 else (0, 3)),
+            Op("RX", (n - 1,), (1.1,), ctrls=(g - 1,)),
+            Op("H", (g - 1,)), Op("CZ", (0, g - 1) if g > 1 else (0, 4))]
+    ops += workloads.random_circuit(n, 4, seed=seed + 1)
+    return ops
+
+
 def _worker(rank, world, nccl_ids, q):
     try:
         from paper_2403_02512_b200.device import Device
-        n = 12
+        n = N_LOCAL + world.bit_length() - 1
         rng = np.random.default_rng(5)
         psi = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
         psi /= np.linalg.norm(psi)
-        ops = workloads.random_circuit(n, 10, seed=3)
-        ops += [Op("SWAP", (0, 11)), Op("IsingXX", (1, 0), (0.3,)), Op("CNOT", (0, 1), ctrls=(5,)),
-                Op("DoubleExcitation", (0, 1, 6, 7), (0.4,)), Op("RZ", (1,), (0.7,), ctrls=(0,))]
+        ops = sharded_ops(n, world)
         res = {}
         m = rng.normal(size=(32, 32)) + 1j * rng.normal(size=(32, 32))
         dense = DenseHermitian((0, 9, 1, 4, 6), m + m.conj().T)
         for fuse in (False, True):
             d = Device.sharded(n, rank, world, nccl_ids[int(fuse)], device=rank, fuse=fuse)
+            assert d.n_local >= 13, "shards must span several fused tiles"
             d.set_state(psi)
             d.apply(ops)
             res[f"state{int(fuse)}"] = d.get_state()
@@ -83,20 +129,11 @@ def _worker(rank, world, nccl_ids, q):
         q.put(("err", f"rank {rank}: {exc}\n{traceback.format_exc()}"))
 
 
-@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("world", [2, 4, 8])
 def test_sharded_nccl_matches_oracle(world):
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    from paper_2403_02512_b200.device import Device
-    nccl_ids = [Device.nccl_unique_id() for _ in range(4)]   # one id per communicator
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=_worker, args=(r, world, nccl_ids, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    status, out = q.get(timeout=600)
-    for p in procs:
-        p.join(timeout=120)
+    status, out = run_world(_worker, world, 4)
     assert status == "ok", out
     for k, v in out.items():
         tol = 1e-10 if "j" in k else 1e-12
@@ -107,8 +144,8 @@ def _swap_path_worker(rank, world, nccl_ids, q):
     try:
         import os
         from paper_2403_02512_b200.device import Device
-        n = 14
-        ops = workloads.random_circuit(n, 12, seed=8)
+        n = N_LOCAL + world.bit_length() - 1
+        ops = sharded_ops(n, world, seed=8)
         qaoa_ops, qaoa_h, _ = workloads.qaoa_maxcut(n, p=2, seed=3)
         res = []
         for i, flag in enumerate(("1", "0")):   # peer-memory swaps, then the NCCL send/recv fallback
@@ -134,7 +171,8 @@ def _swap_path_worker(rank, world, nccl_ids, q):
             jac_ok = bool(np.abs(res[0][1] - jref).max() < 1e-10 * max(1.0, scale, float(np.abs(jref).max())))
             psi = O.run_circuit(n, ops)
             ev_ref = O.expval(psi, n, qaoa_h)
-            ev_ok = bool(abs(res[0][2][0] - ev_ref) < 1e-12 * max(1.0, scale))
+            ev_ok = bool(abs(res[0][2][0] - ev_ref) < 1e-12 * max(1.0, scale)
+                         and abs(res[0][2][1] - ev_ref) < 1e-12 * max(1.0, scale))
             if not ev_ok:
                 ev_ok = (res[0][2], ev_ref, float(np.abs(res[0][0] - psi).max()), float(np.abs(res[0][3] - psi).max()),
                          O.expval(res[0][0], n, qaoa_h), O.expval(res[0][3], n, qaoa_h))
@@ -144,21 +182,40 @@ def _swap_path_worker(rank, world, nccl_ids, q):
         q.put(("err", f"rank {rank}: {exc}\n{traceback.format_exc()}"))
 
 
-def test_peer_memory_swap_bit_identical_to_nccl_swap():
-    """The peer-memory exchange kernel and the NCCL send/recv path move the same amplitudes:
-    states and Jacobians must agree bit for bit."""
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_memory_swap_bit_identical_to_nccl_swap(world):
+    """The peer-memory exchange kernels (single- and multi-bit) and the NCCL send/recv path move
+    the same amplitudes: states and Jacobians must agree bit for bit."""
+    if n_gpus() < world:
+        pytest.skip(f"needs {world} GPUs")
+    status, out = run_world(_swap_path_worker, world, 4)
+    assert status == "ok", out
+    assert out == {"state": True, "jac": True, "jac_vs_oracle": True, "ev_vs_oracle": True}, out
+
+
+def _dead_peer_worker(rank, world, nccl_ids, q):
+    import os
+    import time
+    os.environ["SVB200_NCCL_TIMEOUT"] = "20"
+    from paper_2403_02512_b200.device import Device
+    from paper_2403_02512_b200.errors import DeviceError
+    d = Device.sharded(16, rank, world, nccl_ids[0], device=rank)
+    if rank == 1:
+        os._exit(0)   # the peer disappears without a word
+    t0 = time.time()
+    try:
+        d.expval(PauliWord(((0, "Z"),)))   # an allreduce no peer will ever join
+        q.put(("ok", "collective returned without its peer"))
+    except DeviceError as e:
+        q.put(("ok", ("aborted", str(e), time.time() - t0)))
+
+
+def test_dead_peer_aborts_instead_of_hanging():
+    """A rank whose peer died does not hang in NCCL: the stream watchdog aborts the communicator
+    (ncclCommAbort) after SVB200_NCCL_TIMEOUT seconds and the call raises DeviceError."""
     world = 2
     if n_gpus() < world:
         pytest.skip(f"needs {world} GPUs")
-    from paper_2403_02512_b200.device import Device
-    nccl_ids = [Device.nccl_unique_id() for _ in range(4)]
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    procs = [ctx.Process(target=_swap_path_worker, args=(r, world, nccl_ids, q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    status, out = q.get(timeout=600)
-    for p in procs:
-        p.join(timeout=120)
-    assert status == "ok", out
-    assert out == {"state": True, "jac": True, "jac_vs_oracle": True, "ev_vs_oracle": True}, out
+    status, out = run_world(_dead_peer_worker, world, 1, timeout=300)
+    assert status == "ok" and out[0] == "aborted", out
+    assert "aborted" in out[1] and out[2] < 120, out

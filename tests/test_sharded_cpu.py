@@ -1,4 +1,4 @@
-"""CPU, world_size 2 and 4 over gloo: the sharded driver's own decisions (sv_plan_sharded:
+"""CPU, world_size 2, 4 and 8 over gloo: the sharded driver's own decisions (sv_plan_sharded:
 per-rank local primitives, global-qubit swaps, final canonicalisation) replayed on CPU ranks
 reproduce the monolithic oracle ("sharded equivalence").
 
@@ -68,6 +68,31 @@ def replay(rank, world, ints, dbls, shard):
                 dist.recv(recv, partner)
                 dist.send(send, partner)
             shard[off:off + half] = recv.numpy().view(np.complex128)
+            swaps += 1
+            continue
+        if kind == 2:   # multi-bit exchange (dist.cpp exchange_bits): global Gs[i] <-> local ps[i]
+            k = nxt()
+            Gs, ps = [], []
+            for _ in range(k):
+                Gs.append(nxt())
+                ps.append(nxt())
+            g = sum(((rank >> (G - nl)) & 1) << i for i, G in enumerate(Gs))
+            vbits = sum(((idx >> p) & 1) << i for i, p in enumerate(ps))
+            for step in range(1, 1 << k):   # XOR schedule, as the NCCL fallback runs it
+                c = g ^ step
+                partner = rank
+                for i, G in enumerate(Gs):
+                    partner = (partner & ~(1 << (G - nl))) | (((c >> i) & 1) << (G - nl))
+                sel = idx[vbits == c]   # ascending = ordered by the non-victim bits on both ranks
+                send = torch.from_numpy(np.ascontiguousarray(shard[sel]).view(np.float64).copy())
+                recv = torch.empty_like(send)
+                if rank < partner:
+                    dist.send(send, partner)
+                    dist.recv(recv, partner)
+                else:
+                    dist.recv(recv, partner)
+                    dist.send(send, partner)
+                shard[sel] = recv.numpy().view(np.complex128)
             swaps += 1
             continue
         t, fmask, fval, xmask, nb = nxt(), nxt() & 0xFFFFFFFFFFFFFFFF, nxt() & 0xFFFFFFFFFFFFFFFF, \
@@ -150,7 +175,8 @@ def free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("world,kind", [(2, "random"), (2, "mixed"), (4, "sel"), (4, "mixed")])
+@pytest.mark.parametrize("world,kind", [(2, "random"), (2, "mixed"), (4, "sel"), (4, "mixed"), (8, "random"),
+                                        (8, "mixed")])
 def test_sharded_replay_matches_monolithic(world, kind):
     n = 9
     ctx = mp.get_context("spawn")
@@ -167,6 +193,26 @@ def test_sharded_replay_matches_monolithic(world, kind):
     assert swaps > 0
 
 
+def test_multi_bit_exchange_is_one_all_to_all():
+    """At P = 8 a layer that needs all three global qubits brings them in with one exchange
+    (multi-bit swaps via all-to-all), not three sequential pairwise swaps."""
+    n = 10
+    ops = [Op("RX", (q,), (0.1 * (q + 1),)) for q in range(n)]   # every qubit, globals first
+    ints, _ = plan_sharded(n, 0, 8, ops)
+    nsteps, pos, xs = int(ints[5]), 6, []
+    for _ in range(nsteps):
+        k = int(ints[pos])
+        if k == 2:
+            xs.append(int(ints[pos + 1]))
+            pos += 2 + 2 * int(ints[pos + 1])
+        elif k == 1:
+            pos += 2
+        else:
+            nb = int(ints[pos + 5])
+            pos += 6 + nb + 2
+    assert xs and xs[0] == 3, xs
+
+
 def test_plan_sharded_no_comm_for_diagonal_and_controls_on_global():
     """Diagonal gates and controls on global qubits need no exchange (SURVEY §8(e) no-comm cases)."""
     n = 8
@@ -181,6 +227,8 @@ def test_plan_sharded_no_comm_for_diagonal_and_controls_on_global():
             kinds.append(k)
             if k == 1:
                 pos += 2
+            elif k == 2:
+                pos += 2 + 2 * int(ints[pos + 1])
             else:
                 nb = int(ints[pos + 5])
                 pos += 6 + nb + 2
