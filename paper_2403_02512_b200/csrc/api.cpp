@@ -105,6 +105,17 @@ void stream_sync(sv_handle* h) {
   }
 }
 
+static double* ensure_pinned(sv_handle* h, size_t doubles);
+
+// Small device->host result copy through the handle's pinned buffer + stream_sync: a copy into
+// pageable memory would block inside cudaMemcpyAsync, out of the watchdog's reach.
+void d2h(sv_handle* h, void* host, const void* dev, size_t bytes) {
+  double* pin = ensure_pinned(h, (bytes + sizeof(double) - 1) / sizeof(double));
+  CUDA_CHECK(cudaMemcpyAsync(pin, dev, bytes, cudaMemcpyDeviceToHost, h->stream));
+  stream_sync(h);
+  std::memcpy(host, pin, bytes);
+}
+
 static double* ensure_pinned(sv_handle* h, size_t doubles) {
   if (h->h_pinned_cap < doubles) {
     if (h->h_pinned) cudaFreeHost(h->h_pinned);
@@ -402,8 +413,7 @@ static double expval_impl(sv_handle* h, const sv_obs& o) {
     double z[2];
     if (g.nb <= 4) {
       braket_prim_async(h, h->state, h->state, g, h->d_results);
-      CUDA_CHECK(cudaMemcpyAsync(z, h->d_results, 2 * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-      stream_sync(h);
+      d2h(h, z, h->d_results, 2 * sizeof(double));
     } else {
       // 5+ wires: lambda = O psi in one extra buffer (smem DENSE kernel), then Re<psi|lambda>
       size_t free_b = 0, total_b = 0;
@@ -434,8 +444,7 @@ static double expval_impl(sv_handle* h, const sv_obs& o) {
     pauli_group_expval_async(h, h->state, groups[gi].x, groups[gi].terms, h->d_results + gi);
   std::vector<double> vals(groups.size());
   if (!groups.empty()) {
-    CUDA_CHECK(cudaMemcpyAsync(vals.data(), h->d_results, groups.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    stream_sync(h);
+    d2h(h, vals.data(), h->d_results, groups.size() * sizeof(double));
   }
   dist_allreduce_sum(h, vals.data(), vals.size());
   double s = 0.0;
@@ -1283,8 +1292,7 @@ void adjoint_sweep(sv_handle* h, const sv_op* ops, int n_ops, const std::vector<
   }
   std::vector<double> z(size_t(ncols) * n_obs * 2, 0.0);
   if (!z.empty()) {
-    CUDA_CHECK(cudaMemcpyAsync(z.data(), h->d_results, z.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-    stream_sync(h);
+    d2h(h, z.data(), h->d_results, z.size() * sizeof(double));
   }
   dist_allreduce_sum(h, z.data(), z.size());
   for (int k = 0; k < n_obs; ++k)

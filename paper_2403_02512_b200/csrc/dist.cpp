@@ -63,8 +63,7 @@ int register_peers(sv_handle* h, double2* buf) {
   CUDA_CHECK(cudaMemcpyAsync(d_handles + hb * h->world, &mine, hb, cudaMemcpyHostToDevice, h->stream));
   NCCL_CHECK(ncclAllGather(d_handles + hb * h->world, d_handles, hb, ncclChar, h->comm, h->stream));
   std::vector<cudaIpcMemHandle_t> all(h->world);
-  CUDA_CHECK(cudaMemcpyAsync(all.data(), d_handles, hb * h->world, cudaMemcpyDeviceToHost, h->stream));
-  stream_sync(h);
+  d2h(h, all.data(), d_handles, hb * h->world);
   CUDA_CHECK(cudaFree(d_handles));
   sv_handle::PeerMap pm;
   pm.local = buf;
@@ -82,8 +81,7 @@ int register_peers(sv_handle* h, double2* buf) {
   int* d_ok = h->d_barrier + 1;
   CUDA_CHECK(cudaMemcpyAsync(d_ok, &ok, sizeof(int), cudaMemcpyHostToDevice, h->stream));
   NCCL_CHECK(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, h->comm, h->stream));
-  CUDA_CHECK(cudaMemcpyAsync(&ok, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  stream_sync(h);
+  d2h(h, &ok, d_ok, sizeof(int));
   if (ok) {
     h->peers.push_back(pm);
   } else {
@@ -245,8 +243,7 @@ void dist_init(sv_handle* h, const void* nccl_id) {
   int* d_ok = h->d_barrier + 1;
   CUDA_CHECK(cudaMemcpyAsync(d_ok, &want, sizeof(int), cudaMemcpyHostToDevice, h->stream));
   NCCL_CHECK(ncclAllReduce(d_ok, d_ok, 1, ncclInt, ncclMin, h->comm, h->stream));
-  CUDA_CHECK(cudaMemcpyAsync(&want, d_ok, sizeof(int), cudaMemcpyDeviceToHost, h->stream));
-  stream_sync(h);
+  d2h(h, &want, d_ok, sizeof(int));
   h->p2p = want && register_peers(h, h->state);
 }
 
@@ -439,8 +436,7 @@ void dist_allreduce_sum(sv_handle* h, double* host, size_t n) {
   ensure_results(h, n);
   CUDA_CHECK(cudaMemcpyAsync(h->d_results, host, n * sizeof(double), cudaMemcpyHostToDevice, h->stream));
   NCCL_CHECK(ncclAllReduce(h->d_results, h->d_results, n, ncclDouble, ncclSum, h->comm, h->stream));
-  CUDA_CHECK(cudaMemcpyAsync(host, h->d_results, n * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  stream_sync(h);
+  d2h(h, host, h->d_results, n * sizeof(double));
 }
 
 void dist_probs(sv_handle* h, const std::vector<int>& wires, double* out) {
@@ -463,8 +459,7 @@ void dist_probs(sv_handle* h, const std::vector<int>& wires, double* out) {
   ensure_results(h, lbins);
   probs_async(h, h->state, lpos, h->d_results);
   std::vector<double> local(lbins);
-  CUDA_CHECK(cudaMemcpyAsync(local.data(), h->d_results, lbins * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  stream_sync(h);
+  d2h(h, local.data(), h->d_results, lbins * sizeof(double));
   const u64 bins = 1ull << w;
   if (h->world == 1) {
     std::memcpy(out, local.data(), bins * sizeof(double));

@@ -742,9 +742,8 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
     ensure_results(h, size_t(2) * n_gen);
     sum_partials(h, reinterpret_cast<const double*>(d_gen), int(grid), 2 * n_gen, h->d_results);
     std::vector<double> z(size_t(2) * n_gen);
-    CUDA_CHECK(cudaMemcpyAsync(z.data(), h->d_results, z.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
     CUDA_CHECK(cudaFreeAsync(d_gen, h->stream));
-    stream_sync(h);
+    d2h(h, z.data(), h->d_results, z.size() * sizeof(double));
     gen_out->clear();
     for (int s = 0; s < n_gen; ++s) gen_out->push_back({prog.gen_slot_of[s], cplx(z[2 * s], z[2 * s + 1])});
   }

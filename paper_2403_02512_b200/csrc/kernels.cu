@@ -1034,8 +1034,7 @@ double reduce_norm2(sv_handle* h, const double2* a) {
   CUDA_CHECK(cudaGetLastError());
   sum_partials(h, h->d_partials, g, 1, h->d_results);
   double out = 0;
-  CUDA_CHECK(cudaMemcpyAsync(&out, h->d_results, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  stream_sync(h);
+  d2h(h, &out, h->d_results, sizeof(double));
   return out;
 }
 
@@ -1258,8 +1257,7 @@ double reduce_dot_re(sv_handle* h, const double2* a, const double2* b) {
   CUDA_CHECK(cudaGetLastError());
   sum_partials(h, h->d_partials, g, 1, h->d_results);
   double out = 0;
-  CUDA_CHECK(cudaMemcpyAsync(&out, h->d_results, sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-  stream_sync(h);
+  d2h(h, &out, h->d_results, sizeof(double));
   return out;
 }
 

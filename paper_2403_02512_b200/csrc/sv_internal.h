@@ -172,6 +172,8 @@ Prim adjoint_prim(const Prim& p);
 
 // api.cpp: wait for the handle's stream (sharded handles: NCCL watchdog + ncclCommAbort)
 void stream_sync(sv_handle* h);
+// small device->host copy (pinned bounce buffer, then stream_sync)
+void d2h(sv_handle* h, void* host, const void* dev, size_t bytes);
 // dist.cpp: abort the communicator after a failure (peers then fail their own waits, not hang)
 void dist_abort(sv_handle* h);
 

@@ -203,11 +203,22 @@ def _dead_peer_worker(rank, world, nccl_ids, q):
     if rank == 1:
         os._exit(0)   # the peer disappears without a word
     t0 = time.time()
+    log = os.environ.get("SVB200_TEST_LOG")
     try:
         d.expval(PauliWord(((0, "Z"),)))   # an allreduce no peer will ever join
         q.put(("ok", "collective returned without its peer"))
     except DeviceError as e:
+        if log:
+            with open(log, "a") as f:
+                f.write(f"rank 0 raised after {time.time() - t0:.1f} s: {e}\n")
         q.put(("ok", ("aborted", str(e), time.time() - t0)))
+    if log:
+        with open(log, "a") as f:
+            f.write("rank 0 releasing\n")
+    d.release()
+    if log:
+        with open(log, "a") as f:
+            f.write("rank 0 released\n")
 
 
 def test_dead_peer_aborts_instead_of_hanging():
