@@ -740,7 +740,7 @@ struct XchgParams {
 };
 
 __global__ void __launch_bounds__(kThreads) k_exchange_multi(double2* __restrict__ a, const XchgParams P) {
-  constexpr int IT = 2;
+  constexpr int IT = 4;   // 4 local + 4 remote 16-byte loads in flight per thread and partner
   const u64 stride = u64(gridDim.x) * kThreads * IT;
   for (u64 t0 = u64(blockIdx.x) * kThreads * IT + threadIdx.x; t0 < P.count; t0 += stride) {
 #pragma unroll
@@ -1003,7 +1003,7 @@ void launch_exchange_multi(sv_handle* h, double2* a, double2* const* peer_by_c, 
   P.count = count;
   P.nc = nc;
   P.ins = make_ins(split_fmask);
-  const unsigned g = unsigned(std::min<u64>(grid_for(count, kThreads * 2), 148ull * 8));
+  const unsigned g = unsigned(std::min<u64>(grid_for(count, kThreads * 4), 148ull * 8));
   k_exchange_multi<<<g, kThreads, 0, h->stream>>>(a, P);
   h->launches++;
   CUDA_CHECK(cudaGetLastError());

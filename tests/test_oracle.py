@@ -324,3 +324,14 @@ def test_f32_golden_circuit_vs_oracle():
     ref = O.run_circuit(n, ops)
     assert d["circ_out"].dtype == np.complex64
     assert np.abs(ref - d["circ_out"]).max() < 1e-5
+
+
+def test_qaoa_p1_closed_form_matches_oracle():
+    """The closed-form p=1 MaxCut expectation (the 33-qubit parity check, where no CPU state fits)
+    equals the oracle's <C> on small graphs, 3- and 4-regular, with triangles."""
+    from oracle.qaoa_closed_form import maxcut_p1_expectation
+    for n, seed, deg in [(10, 0, 3), (12, 3, 3), (11, 5, 4), (12, 7, 4)]:
+        ops, ham, edges = workloads.qaoa_maxcut(n, p=1, seed=seed, degree=deg)
+        ev = O.expval(O.run_circuit(n, ops), n, ham)
+        g, b = ops[n].params[0] / 2, ops[-1].params[0] / 2
+        assert abs(ev - maxcut_p1_expectation(n, edges, g, b)) < 1e-12
