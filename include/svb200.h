@@ -182,6 +182,9 @@ int sv_plan_fp64(int n_qubits, const sv_op* ops, int n_ops, double* flops_per_am
  * out[0]=passes, out[1]=passes with a generated kernel, out[2]=kernels compiled so far in this
  * process, out[3]=their total compile time in microseconds. */
 int sv_plan_compile(int n_qubits, const sv_op* ops, int n_ops, int two_array, int64_t* out4);
+/* Process-wide pass-compiler counters: out3[0] = kernels compiled (NVRTC runs, disk-cache hits
+ * excluded), out3[1] = microseconds spent compiling, out3[2] = distinct kernels held. */
+int sv_jit_stats(int64_t* out3);
 /* The sharded driver's decisions for one rank (local primitives, global-qubit swaps, final
  * canonicalisation), recorded without a GPU; same sizing convention. */
 int sv_plan_sharded(int n_qubits, int rank, int world, const sv_op* ops, int n_ops, int64_t* ints, int64_t ints_cap,

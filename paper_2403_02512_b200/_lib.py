@@ -24,7 +24,7 @@ EXPORTS = (
     "sv_apply_single_qubit", "sv_apply_controlled_single_qubit", "sv_apply_matrix", "sv_apply_ops",
     "sv_expval", "sv_probs", "sv_var", "sv_sample", "sv_adjoint_jacobian", "sv_last_error", "sv_synchronize", "sv_stream",
     "sv_launch_count", "sv_set_profiling", "sv_kernel_stats", "sv_reset_stats", "sv_plan_summary",
-    "sv_plan_program", "sv_plan_sharded", "sv_plan_compile", "sv_plan_fp64",
+    "sv_plan_program", "sv_plan_sharded", "sv_plan_compile", "sv_plan_fp64", "sv_jit_stats",
     "sv_create_ex", "sv_set_state_c64", "sv_get_state_c64",
 )
 
@@ -95,6 +95,7 @@ def lib():
             "sv_plan_sharded": [c_int, c_int, c_int, POINTER(SvOp), c_int, POINTER(c_int64), c_int64,
                                 POINTER(c_double), c_int64, POINTER(c_int64)],
             "sv_plan_compile": [c_int, POINTER(SvOp), c_int, c_int, POINTER(c_int64)],
+            "sv_jit_stats": [POINTER(c_int64)],
             "sv_plan_fp64": [c_int, POINTER(SvOp), c_int, POINTER(c_double)],
         }
         for name, args in sig.items():

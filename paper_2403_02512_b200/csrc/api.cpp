@@ -10,6 +10,7 @@
 #include <new>
 
 #include "dist.h"
+#include "fused_jit.h"
 #include "prim_util.h"
 #include "sv_internal.h"
 
@@ -257,7 +258,46 @@ static void run_ops_sharded(sv_handle* h, const std::vector<double2*>& states, c
   schedule_sharded(h, states, L, [&](std::vector<Prim>& batch) { exec_prims(h, states, batch, fuse); });
 }
 
+// Single GPU: undo the qubit relabeling that fused passes leave behind (qubit at logical offset o
+// back to physical position o) with ONE fused program of bit-SWAP primitives and no relabeling of
+// its own -- SWAPs inside a tile are free register renamings, so this is a few pure-bandwidth
+// passes (3 for the 30-qubit bench circuit's final layout) instead of one kernel per transposition.
+static bool identity_layout(const sv_handle* h) {
+  for (int o = 0; o < h->n; ++o)
+    if (h->phys[o] != o) return false;
+  return true;
+}
+
+static void canonicalize_single(sv_handle* h, const std::vector<double2*>& states) {
+  if (identity_layout(h)) return;
+  std::vector<int> at(h->nl);   // physical position -> logical offset
+  for (int o = 0; o < h->n; ++o) at[h->phys[o]] = o;
+  std::vector<Prim> swaps;
+  for (int p = 0; p < h->nl; ++p)
+    while (at[p] != p) {
+      const int q = at[p];   // the qubit that belongs at q sits at p: exchange positions p and q
+      Prim s;
+      s.type = PRIM_PAIR;
+      s.fmask = (1ull << p) | (1ull << q);
+      s.fval = 1ull << p;
+      s.xmask = s.fmask;
+      s.m = {cplx(0), cplx(1), cplx(1), cplx(0)};
+      swaps.push_back(s);
+      std::swap(at[p], at[q]);
+    }
+  if (h->prec == 64) {
+    apply_prims_fused(h, states, swaps, nullptr, nullptr, false);
+  } else {
+    for (double2* st : states)
+      for (const Prim& p : swaps) launch_prim(h, st, p);
+  }
+  for (int o = 0; o < h->n; ++o) h->phys[o] = o;
+}
+
 static void run_ops(sv_handle* h, const std::vector<double2*>& states, const sv_op* ops, int n_ops, int fuse) {
+  // plans and generated kernels are keyed by the physical layout: an apply on a relabeled state
+  // first restores the canonical layout, so repeated applies reuse the same program
+  if (h->world == 1 && fuse && !h->recording && n_ops > 0) canonicalize_single(h, states);
   if (h->world > 1) {
     run_ops_sharded(h, states, ops, n_ops, fuse);
     return;
@@ -842,7 +882,8 @@ int sv_get_state(sv_handle* h, double* out, uint64_t n_amps) {
   if (n_amps != (1ull << h->n))
     sv_fail(SV_ERR_VALIDATION, "output length " + std::to_string(n_amps) + " does not match 2**" + std::to_string(h->n));
   if (h->prec != 64) sv_fail(SV_ERR_VALIDATION, "complex64 state: use sv_get_state_c64");
-  dist_canonicalize(h, {h->state});
+  if (h->world == 1) canonicalize_single(h, {h->state});
+  else dist_canonicalize(h, {h->state});
   if (h->world == 1) {
     CUDA_CHECK(cudaMemcpyAsync(out, h->state, h->n_local * sizeof(double2), cudaMemcpyDeviceToHost, h->stream));
     stream_sync(h);
@@ -1147,6 +1188,13 @@ int sv_plan_summary(int n_qubits, const sv_op* ops, int n_ops, int64_t* out4) {
 int sv_plan_fp64(int n_qubits, const sv_op* ops, int n_ops, double* flops_per_amp) {
   API_BEGIN
   *flops_per_amp = plan_stats(n_qubits, host_prims(n_qubits, ops, n_ops)).fp64_flops_per_amp;
+  API_END
+}
+
+int sv_jit_stats(int64_t* out3) {
+  API_BEGIN
+  if (!out3) sv_fail(SV_ERR_VALIDATION, "null output");
+  fused::jit_stats(&out3[0], &out3[1], &out3[2]);
   API_END
 }
 

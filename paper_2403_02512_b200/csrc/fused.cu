@@ -587,7 +587,7 @@ void release_fused(sv_handle* h) {
 }
 
 std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& states, const std::vector<Prim>& prims,
-                                   std::vector<std::pair<int, cplx>>* gen_out, double2* state_hi) {
+                                   std::vector<std::pair<int, cplx>>* gen_out, double2* state_hi, bool allow_remap) {
   using namespace fused;
   std::vector<int> identity(h->nl);
   for (int p = 0; p < h->nl; ++p) identity[p] = p;
@@ -614,7 +614,7 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
   // unconditional on another), so each rank plans a different program; an in-tile relabeling
   // would then leave the ranks with different layouts and the next swap would exchange
   // mismatched halves.  Every rank must keep the same layout: no relabeling when world > 1.
-  const bool remap = remap_env && h->world == 1;
+  const bool remap = remap_env && h->world == 1 && allow_remap;
   const std::shared_ptr<Program> prog_ptr = cached_program(h, prims, remap, state_hi != nullptr);
   Program& prog = *prog_ptr;
   if (state_hi)

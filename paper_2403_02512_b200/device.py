@@ -247,6 +247,14 @@ def plan_compile(n_qubits, ops, two_array=False):
             "compile_s_total": out[3] * 1e-6}
 
 
+def jit_stats():
+    """Process-wide pass-compiler counters: {compiled, compile_s, kernels} (NVRTC runs; disk-cache
+    hits are not compiles)."""
+    out = (c_int64 * 3)()
+    _lib.check(_lib.lib().sv_jit_stats(out))
+    return {"compiled": int(out[0]), "compile_s": out[1] * 1e-6, "kernels": int(out[2])}
+
+
 def plan_fp64_flops_per_amp(n_qubits, ops):
     """Host-only: FP64 flops per amplitude the fused program of this op list performs."""
     packed = _lib.PackedOps(ops)

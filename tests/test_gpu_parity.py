@@ -617,3 +617,51 @@ def test_wht_lambda_adjoint_and_variance(fuse):
     with Device(n) as d:   # single-observable fused sweep (lambda from the WHT kernel)
         jac1 = d.adjoint_jacobian(ops, [h_diag], fuse=fuse)
     assert_grad_close(jac1, ref[:1], [h_diag])
+
+
+def test_alg1_alg2_goldens_through_the_c_abi_entry_points(sg):
+    """sv_apply_single_qubit / sv_apply_controlled_single_qubit (include/svb200.h; state.py:154-171
+    and :192-226) called directly through ctypes on the reference's Alg. 1 / Alg. 2 goldens."""
+    import ctypes
+    from paper_2403_02512_b200 import _lib
+    L = _lib.lib()
+    dbl = ctypes.POINTER(ctypes.c_double)
+    i32 = ctypes.POINTER(ctypes.c_int32)
+    for n, q, psi, m, out in zip(sg["alg1_n"], sg["alg1_q"], sg["alg1_in"], sg["alg1_m"], sg["alg1_out"]):
+        with Device(int(n)) as d:
+            d.set_state(psi[: 1 << int(n)])
+            mm = np.ascontiguousarray(np.asarray(m, dtype=np.complex128).reshape(4))
+            _lib.check(L.sv_apply_single_qubit(d.handle, int(q), mm.view(np.float64).ctypes.data_as(dbl)))
+            assert np.abs(d.get_state() - out[: 1 << int(n)]).max() < STATE_TOL
+    for i in range(len(sg["alg2_n"])):
+        n, q = int(sg["alg2_n"][i]), int(sg["alg2_q"][i])
+        ctrls = np.array([c for c in sg["alg2_ctrls"][i] if c >= 0], dtype=np.int32)
+        vals = np.array([v for v in sg["alg2_vals"][i] if v >= 0], dtype=np.int32)
+        mm = np.ascontiguousarray(np.asarray(sg["alg2_m"][i], dtype=np.complex128).reshape(4))
+        with Device(n) as d:
+            d.set_state(sg["alg2_in"][i][: 1 << n])
+            _lib.check(L.sv_apply_controlled_single_qubit(d.handle, ctrls.ctypes.data_as(i32), len(ctrls), q,
+                                                           mm.view(np.float64).ctypes.data_as(dbl),
+                                                           vals.ctypes.data_as(i32) if len(vals) else None))
+            assert np.abs(d.get_state() - sg["alg2_out"][i][: 1 << n]).max() < STATE_TOL
+
+
+def test_repeated_apply_restores_layout_and_reuses_kernels():
+    """apply() on a relabeled state first restores the canonical layout (one fused SWAP program),
+    so repeated applies without reset stay correct and plan/compile nothing new after the first."""
+    from paper_2403_02512_b200.device import jit_stats
+    n = 16
+    ops = workloads.random_circuit(n, 12, seed=21)
+    ref = O.run_circuit(n, [])
+    with Device(n) as d:
+        d.apply(ops)
+        d.apply(ops)   # first apply from a drifted layout: compiles the canonicalising program
+        before = jit_stats()["compiled"]
+        for _ in range(2):
+            d.apply(ops)
+        after = jit_stats()["compiled"]
+        st = d.get_state()
+    for _ in range(4):
+        ref = O.run_circuit(n, ops, ref)
+    assert np.abs(st - ref).max() < 1e-12
+    assert after == before, (before, after)

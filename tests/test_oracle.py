@@ -335,3 +335,14 @@ def test_qaoa_p1_closed_form_matches_oracle():
         ev = O.expval(O.run_circuit(n, ops), n, ham)
         g, b = ops[n].params[0] / 2, ops[-1].params[0] / 2
         assert abs(ev - maxcut_p1_expectation(n, edges, g, b)) < 1e-12
+
+
+def test_product_get_masks_matches_reference(sg):
+    """The package's own get_masks (paper_2403_02512_b200/state.py) against the reference's
+    recorded get_masks outputs (masks_repr golden, state.py:128-151)."""
+    from paper_2403_02512_b200 import state as S
+    for n, excl, masks, strides in ast.literal_eval(str(sg["masks_repr"])):
+        ms = S.get_masks(excl, n)
+        got_m = list(ms.masks) if hasattr(ms, "masks") else list(ms[0])
+        got_s = list(ms.strides) if hasattr(ms, "strides") else list(ms[1])
+        assert got_m == masks and got_s == strides
