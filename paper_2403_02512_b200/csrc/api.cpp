@@ -294,7 +294,80 @@ static void canonicalize_single(sv_handle* h, const std::vector<double2*>& state
   for (int o = 0; o < h->n; ++o) h->phys[o] = o;
 }
 
+// K14: from |0...0>, an op list that starts with H on every qubit followed by
+// diagonal gates is ONE write-only pass: psi = 2^(-n/2) exp(i f), f = the Walsh expansion of the
+// diagonal gates' phases (the reference's uniform start, state.py:41-45, plus e.g. QAOA's first
+// cost layer), evaluated per 4096-amplitude tile by the WHT kernel.  Returns how many leading ops
+// it consumed (0: not applicable -- the ops then run as usual).
+static int try_uniform_prefix(sv_handle* h, const sv_op* ops, int n_ops) {
+  static const bool off = getenv("SVB200_K14") && std::string(getenv("SVB200_K14")) == "0";
+  if (off || !h->zero_state || h->recording || h->prec != 64 || h->nl < 12 || n_ops < h->n || !identity_layout(h))
+    return 0;
+  std::vector<char> seen(h->n, 0);
+  for (int k = 0; k < h->n; ++k) {
+    const sv_op& op = ops[k];
+    if (op.kind != SV_GATE_H || op.n_wires != 1 || op.n_ctrls != 0) return 0;
+    if (seen[op.wires[0]]) return 0;
+    seen[op.wires[0]] = 1;
+  }
+  std::map<u64, double> walsh;   // physical bit mask -> coefficient of (-1)^pc(i & mask) in the phase
+  int end = h->n;
+  for (; end < n_ops; ++end) {
+    int col = 0;
+    const auto pieces = lower_op(ops[end], h->n, col, false, h->phys.data());
+    bool diag = !pieces.empty();
+    for (const auto& pc : pieces) {
+      if (pc.fwd.type != PRIM_DIAG || pc.fwd.nb > 6 || popcount64(pc.fwd.fmask) > 4) diag = false;
+      for (const cplx& t : pc.fwd.m)
+        if (std::abs(std::abs(t) - 1.0) > 1e-12) diag = false;   // unit-modulus phases only
+    }
+    if (!diag) break;
+    for (const auto& pc : pieces) {
+      const Prim& p = pc.fwd;
+      std::vector<int> bits(p.pos, p.pos + p.nb);   // S = table bits + control bits
+      for (int b = 0; b < 64; ++b)
+        if (((p.fmask >> b) & 1) && std::find(bits.begin(), bits.end(), b) == bits.end()) bits.push_back(b);
+      const int k = int(bits.size());
+      std::vector<double> theta(size_t(1) << k, 0.0);
+      for (size_t x = 0; x < theta.size(); ++x) {
+        u64 z = 0;
+        for (int j = 0; j < k; ++j)
+          if ((x >> j) & 1) z |= 1ull << bits[j];
+        if ((z & p.fmask) != p.fval) continue;
+        size_t t = 0;
+        for (int j = 0; j < p.nb; ++j)
+          if ((z >> p.pos[j]) & 1) t |= size_t(1) << j;
+        theta[x] = std::arg(p.m[t]);
+      }
+      for (size_t sidx = 0; sidx < theta.size(); ++sidx) {   // Walsh coefficients over S
+        double c = 0.0;
+        for (size_t x = 0; x < theta.size(); ++x) c += (popcount64(x & sidx) & 1) ? -theta[x] : theta[x];
+        c /= double(theta.size());
+        if (c == 0.0) continue;
+        u64 mask = 0;
+        for (int j = 0; j < k; ++j)
+          if ((sidx >> j) & 1) mask |= 1ull << bits[j];
+        walsh[mask] += c;
+      }
+    }
+  }
+  std::vector<PauliTerm> terms;
+  const u64 lmask = (h->nl >= 64) ? ~0ull : ((1ull << h->nl) - 1);
+  for (const auto& e : walsh) {
+    const bool neg = popcount64(u64(h->rank) & (e.first >> h->nl)) & 1;   // global bits: this rank's values
+    terms.push_back({e.first & lmask, cplx(neg ? -e.second : e.second, 0.0)});
+  }
+  init_uniform_phase(h, h->state, terms, std::pow(2.0, -0.5 * double(h->n)));
+  return end;
+}
+
 static void run_ops(sv_handle* h, const std::vector<double2*>& states, const sv_op* ops, int n_ops, int fuse) {
+  if (fuse && states.size() == 1 && states[0] == h->state) {
+    const int done = try_uniform_prefix(h, ops, n_ops);
+    ops += done;
+    n_ops -= done;
+  }
+  h->zero_state = false;
   // plans and generated kernels are keyed by the physical layout: an apply on a relabeled state
   // first restores the canonical layout, so repeated applies reuse the same program
   if (h->world == 1 && fuse && !h->recording && n_ops > 0) canonicalize_single(h, states);
@@ -698,6 +771,7 @@ static void create_common(sv_handle* h, int n_qubits, int device) {
   CUDA_CHECK(cudaMalloc(&h->state, h->n_local * amp_bytes(h)));
   launch_init_zero(h, h->state, 0, h->rank == 0);
   stream_sync(h);
+  h->zero_state = true;
 }
 
 static void release_adjoint_buffers(sv_handle* h) {
@@ -765,6 +839,7 @@ int sv_set_state_c64(sv_handle* h, const float* amps, uint64_t n_amps) {
   if (n_amps != (1ull << h->n))
     sv_fail(SV_ERR_VALIDATION, "amplitude array length " + std::to_string(n_amps) + " does not match 2**" + std::to_string(h->n));
   dist_reset_layout(h);
+  h->zero_state = false;
   CUDA_CHECK(cudaMemcpyAsync(h->state, amps, h->n_local * sizeof(float2), cudaMemcpyHostToDevice, h->stream));
   stream_sync(h);
   API_END
@@ -844,6 +919,7 @@ int sv_reset(sv_handle* h) {
   dist_reset_layout(h);
   launch_init_zero(h, h->state, 0, h->rank == 0);
   stream_sync(h);
+  h->zero_state = true;
   API_END
 }
 
@@ -853,6 +929,7 @@ int sv_set_basis_state(sv_handle* h, uint64_t index) {
   std::lock_guard<std::mutex> lk(h->mu);
   if (h->n < 64 && index >= (1ull << h->n)) sv_fail(SV_ERR_VALIDATION, "basis index out of range");
   dist_reset_layout(h);
+  h->zero_state = false;
   const u64 owner = index >> h->nl;
   launch_init_zero(h, h->state, index & (h->n_local - 1), owner == u64(h->rank));
   stream_sync(h);
@@ -868,6 +945,7 @@ int sv_set_state(sv_handle* h, const double* amps, uint64_t n_amps) {
     sv_fail(SV_ERR_VALIDATION, "amplitude array length " + std::to_string(n_amps) + " does not match 2**" + std::to_string(h->n));
   if (h->prec != 64) sv_fail(SV_ERR_VALIDATION, "complex64 state: use sv_set_state_c64");
   dist_reset_layout(h);
+  h->zero_state = false;
   const double* src = amps + 2 * (u64(h->rank) << h->nl);
   CUDA_CHECK(cudaMemcpyAsync(h->state, src, h->n_local * sizeof(double2), cudaMemcpyHostToDevice, h->stream));
   stream_sync(h);

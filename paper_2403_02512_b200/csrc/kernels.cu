@@ -486,7 +486,10 @@ template <class C>
 __global__ void __launch_bounds__(kThreads, 2) k_pauli_diag_wht(const C* __restrict__ a, C* __restrict__ out, u64 ntiles,
                                                              const DiagGroupDev* __restrict__ groups, int ngroups,
                                                              const DiagTermDev* __restrict__ terms,
-                                                             double* __restrict__ partials) {
+                                                             double* __restrict__ partials, double init_scale = 0.0) {
+  // init_scale != 0 (K14): out = init_scale * exp(i f), write-only -- H on every qubit of |0...0>
+  // followed by a run of diagonal gates, f = the Walsh expansion of the gates' phases
+  const bool init = init_scale != 0.0;
   __shared__ __align__(16) double T[1 << kWhtBits];
   const int tid = threadIdx.x, lane = tid & 31;
   double acc[1] = {0.0};
@@ -495,13 +498,15 @@ __global__ void __launch_bounds__(kThreads, 2) k_pauli_diag_wht(const C* __restr
     // amplitudes of layout B, issued first and consumed last so the loads overlap the transform;
     // the next tile is prefetched into L2 (two 128-byte lines per thread)
     C x[16];
+    if (!init) {
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      const u64 L = (u64(tid) << 1) | (u64(q) << 9);
-      x[2 * q] = a[H + L];
-      x[2 * q + 1] = a[H + L + 1];
+      for (int q = 0; q < 8; ++q) {
+        const u64 L = (u64(tid) << 1) | (u64(q) << 9);
+        x[2 * q] = a[H + L];
+        x[2 * q + 1] = a[H + L + 1];
+      }
     }
-    if (tile + gridDim.x < ntiles) {
+    if (!init && tile + gridDim.x < ntiles) {
       const char* nxt = reinterpret_cast<const char*>(a + ((tile + gridDim.x) << kWhtBits));
       const size_t per_thread = (size_t(1) << kWhtBits) * sizeof(C) / kThreads;   // 256 B (c128) / 128 B (c64)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(nxt + tid * per_thread));
@@ -565,7 +570,17 @@ __global__ void __launch_bounds__(kThreads, 2) k_pauli_diag_wht(const C* __restr
           v[j] = x + y;
           v[j | (1 << b)] = x - y;
         }
-    if (out) {   // lambda = f psi (the adjoint's lambda initialisation, K10 for one diagonal group)
+    if (init) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const u64 L = (u64(tid) << 1) | (u64(q) << 9);
+        double s0, c0, s1, c1;
+        sincos(v[2 * q], &s0, &c0);
+        sincos(v[2 * q + 1], &s1, &c1);
+        __stcs(reinterpret_cast<double2*>(out) + H + L, make_double2(init_scale * c0, init_scale * s0));
+        __stcs(reinterpret_cast<double2*>(out) + H + L + 1, make_double2(init_scale * c1, init_scale * s1));
+      }
+    } else if (out) {   // lambda = f psi (the adjoint's lambda initialisation, K10 for one diagonal group)
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const u64 L = (u64(tid) << 1) | (u64(q) << 9);
@@ -1041,7 +1056,8 @@ double reduce_norm2(sv_handle* h, const double2* a) {
 // Diagonal group through k_pauli_diag_wht: out == nullptr -> per-block partials of
 // sum_i |psi_i|^2 f(i) (returns the grid); otherwise out = f psi.  Terms are grouped by their low
 // 12 mask bits on the host (fixed order -> deterministic sums); real coefficients only.
-static unsigned pauli_diag_wht(sv_handle* h, const double2* a, double2* out, const std::vector<PauliTerm>& terms) {
+static unsigned pauli_diag_wht(sv_handle* h, const double2* a, double2* out, const std::vector<PauliTerm>& terms,
+                               double init_scale = 0.0) {
   const u64 lo = (u64(1) << kWhtBits) - 1;
   std::vector<size_t> order(terms.size());
   for (size_t t = 0; t < order.size(); ++t) order[t] = t;
@@ -1068,11 +1084,25 @@ static unsigned pauli_diag_wht(sv_handle* h, const double2* a, double2* out, con
   cudaEvent_t ev[2];
   const double bytes = (out ? 2.0 : 1.0) * double(amp_bytes(h)) * double(h->n_local);
   stat_begin(h, out ? KC_APPLY_OBS : KC_REDUCE, bytes, ev);
-  SV_LAUNCH2(h, k_pauli_diag_wht, SV_CFG(g, kThreads, 0, h->stream), a, out, ntiles, (const DiagGroupDev*)(d_blob + tb),
-            int(gr.size()), (const DiagTermDev*)d_blob, h->d_partials);
+  if (init_scale != 0.0) {
+    k_pauli_diag_wht<double2><<<g, kThreads, 0, h->stream>>>(a, out, ntiles, (const DiagGroupDev*)(d_blob + tb),
+                                                            int(gr.size()), (const DiagTermDev*)d_blob, h->d_partials,
+                                                            init_scale);
+  } else {
+    SV_LAUNCH2(h, k_pauli_diag_wht, SV_CFG(g, kThreads, 0, h->stream), a, out, ntiles, (const DiagGroupDev*)(d_blob + tb),
+              int(gr.size()), (const DiagTermDev*)d_blob, h->d_partials);
+  }
   stat_end(h, out ? KC_APPLY_OBS : KC_REDUCE, bytes, ev);
   CUDA_CHECK(cudaGetLastError());
   return g;
+}
+
+// K14: the state H^n |0...0> followed by diagonal gates with total phase f(i) = sum_t r_t
+// (-1)^{pc(i & z_t)} (terms in local physical bits; global bits already folded into r_t), written
+// in one write-only pass: psi_i = 2^{-n/2} exp(i f(i)).  Needs n_local >= 12 (one WHT tile).
+void init_uniform_phase(sv_handle* h, double2* state, const std::vector<PauliTerm>& terms, double scale) {
+  if (h->nl < kWhtBits) sv_fail(SV_ERR_DEVICE, "internal: K14 init needs a full 4096-amplitude tile");
+  pauli_diag_wht(h, nullptr, state, terms.empty() ? std::vector<PauliTerm>{{0, cplx(0.0)}} : terms, scale);
 }
 
 void pauli_group_expval_async(sv_handle* h, const double2* a, u64 xmask, const std::vector<PauliTerm>& terms,

@@ -143,6 +143,7 @@ struct sv_handle {
   double2* adj_saved = nullptr; // fused adjoint: saved final psi (several observables)
   std::mutex mu;
   bool recording = false;       // host-only planning handle (no device memory)
+  bool zero_state = false;      // the state is exactly |0...0> in the canonical layout (create / reset)
   std::vector<RecStep> rec;
   // stats
   int64_t launches = 0;
@@ -198,6 +199,8 @@ struct PauliTerm {
   u64 zmask;
   cplx cc;   // coefficient * i^{nY} * global-sign
 };
+// K14: state = scale * exp(i f), f(i) = sum_t Re(cc_t) (-1)^{pc(i & zmask_t)} (one write-only pass)
+void init_uniform_phase(sv_handle* h, double2* state, const std::vector<PauliTerm>& terms, double scale);
 void pauli_group_expval_async(sv_handle* h, const double2* state, u64 xmask, const std::vector<PauliTerm>& terms,
                               double* d_out);
 void pauli_group_apply(sv_handle* h, const double2* psi, double2* lam, u64 xmask,

@@ -665,3 +665,33 @@ def test_repeated_apply_restores_layout_and_reuses_kernels():
         ref = O.run_circuit(n, ops, ref)
     assert np.abs(st - ref).max() < 1e-12
     assert after == before, (before, after)
+
+
+@pytest.mark.parametrize("kind", ["qaoa", "mixed_diag"])
+def test_k14_uniform_prefix_write_only_init(kind):
+    """K14: from |0...0>, H on every qubit followed by diagonal gates (any controls, any phases) is
+    one write-only pass (WHT of the Walsh-expanded phases + sincos); the state equals the oracle's
+    gate-by-gate result.  The same list from a non-zero state runs gate by gate."""
+    n = 15
+    rng = np.random.default_rng(7)
+    if kind == "qaoa":
+        ops, _, _ = workloads.qaoa_maxcut(n, p=2, seed=4)
+    else:
+        ops = [Op("H", (q,)) for q in rng.permutation(n)]
+        for _ in range(40):
+            a, b, c = (int(x) for x in rng.choice(n, size=3, replace=False))
+            pick = int(rng.integers(7))
+            th = float(rng.uniform(-7, 7))
+            ops.append([Op("RZ", (a,), (th,)), Op("IsingZZ", (a, b), (th,)), Op("CZ", (a, b)), Op("T", (a,)),
+                        Op("Phase", (a,), (th,), ctrls=(b,)), Op("RZ", (a,), (th,), ctrls=(b, c), ctrl_values=(1, 0)),
+                        Op("S", (a,), inverse=True)][pick])
+        ops += workloads.random_circuit(n, 3, seed=9)
+    ref = O.run_circuit(n, ops)
+    with Device(n) as d:
+        d.apply(ops)
+        st = d.get_state()
+        d.set_state(ref)                      # not |0...0>: the prefix must run gate by gate
+        d.apply(ops)
+        st2 = d.get_state()
+    assert np.abs(st - ref).max() < 1e-12
+    assert np.abs(st2 - O.run_circuit(n, ops, ref)).max() < 1e-12
