@@ -283,6 +283,109 @@ __global__ void __launch_bounds__(256) k_shear_cf(double* out, const Cf64 cf) {
   if (s == 12345.678) out[0] = s;
 }
 
+// Do the FP64 pipe and the shared-memory pipe overlap?  Warps [0, nfp) run the shear stream,
+// warps [nfp, 16) stream 16-byte LDS/STS round trips through a 64 KiB tile (the pass kernels'
+// phase transitions).  mode 0: both kinds, 1: FP64 warps only, 2: smem warps only.
+__global__ void __launch_bounds__(512, 1) k_overlap(double* out, double t, double s_, int nfp, int mode, int smem_iters) {
+  extern __shared__ __align__(16) double2 tile[];
+  const int warp = threadIdx.x >> 5;
+  double2 a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = make_double2(threadIdx.x * 1e-3 + i, i * 0.5);
+  if (warp < nfp) {
+    if (mode == 2) return;
+    for (int it = 0; it < kIter / 12; ++it) {
+      shear_k<0>(a, t, s_);
+      shear_k<1>(a, t, s_);
+      shear_k<2>(a, t, s_);
+      shear_k<3>(a, t, s_);
+    }
+  } else {
+    if (mode == 1) return;
+    const int lt = threadIdx.x - nfp * 32;
+    const int nt = (16 - nfp) * 32;
+    for (int it = 0; it < smem_iters; ++it) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r) tile[(lt + r * nt) & 4095] = a[r];
+      asm volatile("bar.sync 1, %0;" ::"r"(nt));
+#pragma unroll
+      for (int r = 0; r < 16; ++r) a[r] = tile[((lt ^ 37) + r * nt) & 4095];
+      asm volatile("bar.sync 1, %0;" ::"r"(nt));
+    }
+  }
+  double sum = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) sum += a[i].x + a[i].y;
+  if (sum == 12345.678) out[0] = sum;
+}
+
+// 8 distinct per-gate coefficient pairs, loaded once before the loop (loop-invariant, 32 URs)
+__global__ void __launch_bounds__(256) k_shear_cf8(double* out, const Cf64 cf) {
+  double2 a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = make_double2(threadIdx.x * 1e-3 + i, i * 0.5);
+  const double2 c0 = cf.v[0], c1 = cf.v[1], c2 = cf.v[2], c3 = cf.v[3], c4 = cf.v[4], c5 = cf.v[5], c6 = cf.v[6],
+                c7 = cf.v[7];
+  for (int it = 0; it < kIter / 24; ++it) {
+    shear_k<0>(a, c0.x, c0.y);
+    shear_k<1>(a, c1.x, c1.y);
+    shear_k<2>(a, c2.x, c2.y);
+    shear_k<3>(a, c3.x, c3.y);
+    shear_k<0>(a, c4.x, c4.y);
+    shear_k<1>(a, c5.x, c5.y);
+    shear_k<2>(a, c6.x, c6.y);
+    shear_k<3>(a, c7.x, c7.y);
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i].x + a[i].y;
+  if (s == 12345.678) out[0] = s;
+}
+
+// per-gate coefficients staged in shared memory (LDS.128 per gate, uniform address -> broadcast)
+__global__ void __launch_bounds__(256) k_shear_smemcf(double* out, const Cf64 cf) {
+  __shared__ double2 sc[64];
+  if (threadIdx.x < 64) sc[threadIdx.x] = cf.v[threadIdx.x];
+  __syncthreads();
+  double2 a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = make_double2(threadIdx.x * 1e-3 + i, i * 0.5);
+  for (int it = 0; it < kIter / 12 / 16; ++it) {
+#pragma unroll
+    for (int g = 0; g < 64; g += 4) {
+      shear_k<0>(a, sc[g].x, sc[g].y);
+      shear_k<1>(a, sc[g + 1].x, sc[g + 1].y);
+      shear_k<2>(a, sc[g + 2].x, sc[g + 2].y);
+      shear_k<3>(a, sc[g + 3].x, sc[g + 3].y);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i].x + a[i].y;
+  if (s == 12345.678) out[0] = s;
+}
+
+// per-gate coefficients, warps desynchronised: warp w starts the 64-gate sequence at gate 4 w
+__global__ void __launch_bounds__(256) k_shear_cf_desync(double* out, const Cf64 cf) {
+  double2 a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = make_double2(threadIdx.x * 1e-3 + i, i * 0.5);
+  const int w = (threadIdx.x >> 5) & 7;
+  for (int it = 0; it < kIter / 12 / 16; ++it) {
+    for (int gg = 0; gg < 64; gg += 4) {
+      const int g = (gg + 8 * w) & 63;
+      shear_k<0>(a, cf.v[g].x, cf.v[g].y);
+      shear_k<1>(a, cf.v[g + 1].x, cf.v[g + 1].y);
+      shear_k<2>(a, cf.v[g + 2].x, cf.v[g + 2].y);
+      shear_k<3>(a, cf.v[g + 3].x, cf.v[g + 3].y);
+    }
+  }
+  double s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s += a[i].x + a[i].y;
+  if (s == 12345.678) out[0] = s;
+}
+
 int main(int argc, char** argv) {
   const double secs = argc > 1 ? atof(argv[1]) : 3.0;
   int sms = 0, clk = 0;
@@ -303,9 +406,28 @@ int main(int argc, char** argv) {
                {"dfma_2reg", 4, 0},   {"dfma_3reg", 5, 0},        {"shear16", 6, 0},
                {"cmul16", 7, 0},      {"shear16_512thr", 8, 0},   {"shear16_branch", 9, 0},
                {"shear16_select", 10, 0}, {"shear16_branch_8warps", 11, 0}, {"shear16_ubranch", 12, 0},
-               {"shear16_ubranch_8warps", 13, 0}, {"shear16_cf", 14, 0}, {"shear16_cf_8warps", 15, 0}};
+               {"shear16_ubranch_8warps", 13, 0}, {"shear16_cf", 14, 0}, {"shear16_cf_8warps", 15, 0},
+               {"shear16_cf8_invariant", 16, 0}, {"shear16_smem_cf", 17, 0}, {"shear16_smem_cf_8warps", 18, 0},
+               {"shear16_cf_desync", 19, 0}};
   Cf64 cf;
   for (int g = 0; g < 64; ++g) cf.v[g] = make_double2(-0.1 + 0.001 * g, 0.19 - 0.002 * g);
+  {
+    // overlap test: 8 FP64 warps + 8 smem warps per SM, each kind alone, then together
+    CK(cudaFuncSetAttribute(k_overlap, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536));
+    const int smem_iters = 280;
+    float ms[3];
+    for (int mode = 0; mode < 3; ++mode) {
+      k_overlap<<<sms, 512, 65536>>>(out, -0.1, 0.19, 8, mode, smem_iters);
+      CK(cudaDeviceSynchronize());
+      CK(cudaEventRecord(e0));
+      for (int r = 0; r < 20; ++r) k_overlap<<<sms, 512, 65536>>>(out, -0.1, 0.19, 8, mode, smem_iters);
+      CK(cudaEventRecord(e1));
+      CK(cudaEventSynchronize(e1));
+      CK(cudaEventElapsedTime(&ms[mode], e0, e1));
+    }
+    std::printf("{\"case\": \"overlap_fp64_smem\", \"ms_both\": %.3f, \"ms_fp64_only\": %.3f, \"ms_smem_only\": %.3f}\n",
+                ms[0] / 20, ms[1] / 20, ms[2] / 20);
+  }
   for (const Case& c : cases) {
     auto launch = [&]() {
       if (c.kind == 0) k_dfma<<<blocks, threads>>>(out, 0.999999, 1e-7);
@@ -324,6 +446,10 @@ int main(int argc, char** argv) {
       if (c.kind == 13) k_shear_ubranch<<<sms, 256>>>(out, -0.1, 0.19, 5);
       if (c.kind == 14) k_shear_cf<<<blocks, threads>>>(out, cf);
       if (c.kind == 15) k_shear_cf<<<sms, 256>>>(out, cf);
+      if (c.kind == 16) k_shear_cf8<<<blocks, threads>>>(out, cf);
+      if (c.kind == 17) k_shear_smemcf<<<blocks, threads>>>(out, cf);
+      if (c.kind == 18) k_shear_smemcf<<<sms, 256>>>(out, cf);
+      if (c.kind == 19) k_shear_cf_desync<<<blocks, threads>>>(out, cf);
     };
     launch();
     CK(cudaDeviceSynchronize());
@@ -347,8 +473,9 @@ int main(int argc, char** argv) {
     if (c.kind == 1) flop_dmma = (nthr / 32) * 8 * (kIter / 4) * (8 * 8 * 4 * 2.0);
     if (c.kind == 4 || c.kind == 5) flop_dfma = 2.0 * 32 * (kIter / 2) * nthr;
     if (c.kind == 6) flop_dfma = 2.0 * 4 * 8 * 6 * (kIter / 12) * nthr;
-    if (c.kind == 8 || c.kind == 11 || c.kind == 13 || c.kind == 15) flop_dfma = 2.0 * 4 * 8 * 6 * (kIter / 12) * double(sms) * 256;
-    if (c.kind == 9 || c.kind == 10 || c.kind == 12 || c.kind == 14) flop_dfma = 2.0 * 4 * 8 * 6 * (kIter / 12) * nthr;
+    if (c.kind == 8 || c.kind == 11 || c.kind == 13 || c.kind == 15 || c.kind == 18) flop_dfma = 2.0 * 4 * 8 * 6 * (kIter / 12) * double(sms) * 256;
+    if (c.kind == 9 || c.kind == 10 || c.kind == 12 || c.kind == 14 || c.kind == 17 || c.kind == 19) flop_dfma = 2.0 * 4 * 8 * 6 * (kIter / 12) * nthr;
+    if (c.kind == 16) flop_dfma = 2.0 * 8 * 8 * 6 * (kIter / 24) * nthr;
     if (c.kind == 7) flop_dfma = 2.0 * 16 * 4 * (kIter / 4) * nthr;   // DMUL counted as 2 like DFMA (pipe ops)
     if (c.kind == 2) {
       flop_dfma = 2.0 * 16 * kIter * nthr;

@@ -371,7 +371,12 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     for (int i = 0; i < kRegs; ++i) {
       const double2* src = (TWO && ((P.ld_hsel >> i) & 1) ? p_hi : p_lo) + P.ld_off[i];
       const unsigned dst = sb + unsigned(ld_sw ^ P.ld_sm[i]) * 16u;
+#ifndef FDEV_EXP_NOMEM
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+#else
+      (void)dst;
+      (void)src;
+#endif
     }
     asm volatile("cp.async.commit_group;\n" ::);
   };
@@ -586,8 +591,15 @@ __device__ __forceinline__ void run_pass_pp(double2* __restrict__ state, double2
   const int segs = 2 * P.n_phases;
   const int offset = P.n_phases | 1;   // odd: B's smem segments line up with A's arithmetic
   double2* acc_warp = s_gen + (tid >> 5) * kMaxGens;
+#ifdef FDEV_PP_FREE
+  // free-running groups (no step barriers): each group is an independent consumer of the shared
+  // three-buffer ring; only the mbarriers order loads and uses
+  (void)offset;
+  (void)segs;
+#else
   if (grp == 1)
     for (int i = 0; i < offset; ++i) step_barrier();
+#endif
   int buf = grp;              // local tile j lives in buffer j % 3; its fill number is j / 3
   unsigned fill = 0;
   const u64 periods = (ncta + 1) >> 1;
@@ -600,11 +612,16 @@ __device__ __forceinline__ void run_pass_pp(double2* __restrict__ state, double2
       if (gtid == 0) fdev_t = clock64();
 #endif
       body(cb << P.b, base, acc_warp, [&]() {
+#ifdef FDEV_PP_FREE
+        group_barrier();   // every thread of the group has read the buffer (no step barrier did it)
+#endif
         if (j + 3 < ncta) issue_load(masked_add(base, P.outer, P.grid_step3), cb);
       });
       base = masked_add(base, P.outer, P.grid_step2);
     } else {
+#ifndef FDEV_PP_FREE
       for (int i = 0; i < segs; ++i) step_barrier();
+#endif
     }
     // next local tile of this group: j + 2
     buf += 2;
@@ -613,8 +630,10 @@ __device__ __forceinline__ void run_pass_pp(double2* __restrict__ state, double2
       ++fill;
     }
   }
+#ifndef FDEV_PP_FREE
   if (grp == 0)
     for (int i = 0; i < offset; ++i) step_barrier();
+#endif
 #ifdef FDEV_SEGPROF
   __syncthreads();
   if (blockIdx.x == 0 && tid == 0) {
@@ -655,6 +674,8 @@ __device__ __forceinline__ void run_pass_pp(double2* __restrict__ state, double2
     if ((threadIdx.x & 255) == 0) fdev::fdev_prof[threadIdx.x >> 8][K][1] += t2_ - t1_;     \
     if ((threadIdx.x & 255) == 0) fdev_t = t2_;                         \
   }
+#elif defined(FDEV_PP_FREE)
+#define FDEV_STEP_I(K)
 #else
 #define FDEV_STEP_I(K) fdev::step_barrier()
 #endif
@@ -701,9 +722,24 @@ __device__ __forceinline__ void run_pass_pp(double2* __restrict__ state, double2
       FDEV_TILE(sf ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)) = a[r]; \
   }                                                                                                             \
   FDEV_PHASE_SYNC();
+// ... when the next phase keeps this phase's warp-bit positions: the exchange stays inside each
+// warp (fused_plan.cpp choose_warp_bits), so only the warp synchronises
+#define FDEV_PHASE_STORE_WARP(FLIP, W0, W1, W2, W3)                                                                   \
+  {                                                                                                             \
+    const int fl = (FLIP) ^ fthr;                                                                               \
+    const int sf = s0 ^ ((fl & 1) ? (W0) : 0) ^ ((fl & 2) ? (W1) : 0) ^ ((fl & 4) ? (W2) : 0) ^ ((fl & 8) ? (W3) : 0); \
+    _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r)                                                     \
+      FDEV_TILE(sf ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)) = a[r]; \
+  }                                                                                                             \
+  __syncwarp();
 
 #ifdef FDEV_PLAIN_STORE
 #define FDEV_STG(p, v) (*(p) = (v))
+#elif defined(FDEV_EXP_NOMEM)
+// timing experiment only (wrong results): no HBM traffic -- the store is kept alive behind a
+// condition that is never true at run time
+#define FDEV_STG(p, v) \
+  if (P.n_tiles == 0) *(p) = (v)
 #else
 #define FDEV_STG(p, v) __stcs((p), (v))   // streaming: the state is not re-read before eviction
 #endif

@@ -71,6 +71,11 @@ struct Gen {
   std::map<std::pair<int, int>, int> cf_slot, tab_off;   // one slot per (op, entry) even when emitted twice
   // j = -1: entry 1 of the op's coefficient table (the odd-parity value of a parity table)
   std::string C(int op, int j) {
+    static const bool one = getenv("SVB200_JIT_EXP_ONECF") && std::string(getenv("SVB200_JIT_EXP_ONECF")) == "1";
+    if (one) {   // timing experiment only (wrong results): every op reads the same coefficient slot
+      if (cf_refs.empty()) cf_refs.push_back({op, j});
+      return "cf.v[0]";
+    }
     auto it = cf_slot.find({op, j});
     if (it == cf_slot.end()) {
       cf_refs.push_back({op, j});
@@ -480,6 +485,7 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
   const bool split = split_on && direct && jit_ctas_per_sm() <= 2 && !jit_pp();
   // ping-pong tile loop (fused_dev.cuh run_pass_pp): direct passes on full 12-bit tiles
   const bool pp = jit_pp() && direct && A.b == kMaxB && A.nthr == kMaxB - kRB;
+  if (getenv("SVB200_JIT_EXP_NOSMEM") && std::string(getenv("SVB200_JIT_EXP_NOSMEM")) == "1") o << "  double2 ap_[16];\n";
   if (direct) {
     // the thread's physical store bits in the last phase (its lane bits land on physical 0..2)
     const FPhase& L = prog.phases[A.phase_begin + A.n_phases - 1];
@@ -504,8 +510,14 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
         se += " ^ (" + bit + " ? " + std::to_string(swz_h(1 << F.thr[j])) + " : 0)";
         pe += " | (" + bit + " ? " + hex64(1ull << A.tpos[F.thr[j]]) + " : 0ull)";
       }
-      o << "    FDEV_PHASE_LOAD_X(" << se << ", " << pe << ", " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3]
-        << ")\n";
+      static const bool exp_nosmem = getenv("SVB200_JIT_EXP_NOSMEM") && std::string(getenv("SVB200_JIT_EXP_NOSMEM")) == "1";
+      if (exp_nosmem && ph > 0) {   // timing experiment only (wrong results): no smem round trip between phases
+        o << "    const int s0 = (" << se << "); const u64 pb = base | (" << pe << "); double2 a[16];\n";
+        o << "    _Pragma(\"unroll\") for (int r = 0; r < 16; ++r) a[r] = ap_[r];\n    int fthr = 0; (void)pb; (void)s0; (void)fthr;\n";
+      } else {
+        o << "    FDEV_PHASE_LOAD_X(" << se << ", " << pe << ", " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3]
+          << ")\n";
+      }
     }
     if (pp) o << "    FDEV_STEP_I(" << 2 * ph << ");\n";   // end of segment T_ph
     if (last_direct) o << (pp ? "    next_load();\n" : "    __syncthreads();\n    next_load();\n");
@@ -531,7 +543,16 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
         if (pp) o << "    FDEV_STEP_I(" << 2 * ph + 1 << ");\n";   // end of segment C_ph
       } else {
         if (pp) o << "    FDEV_STEP_I(" << 2 * ph + 1 << ");\n";   // end of segment C_ph; the store opens T_ph+1
-        o << "    FDEV_PHASE_STORE(" << int(F.flip) << ", " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3] << ")\n";
+        static const bool exp_nosmem = getenv("SVB200_JIT_EXP_NOSMEM") && std::string(getenv("SVB200_JIT_EXP_NOSMEM")) == "1";
+        // the next phase keeps the warp-bit positions: warp-local exchange (fused_plan.cpp)
+        bool warp_local = ph + 1 < A.n_phases && A.nthr == kMaxB - kRB;
+        if (warp_local) {
+          const FPhase& N = prog.phases[A.phase_begin + ph + 1];
+          for (int j = 5; j < A.nthr; ++j) warp_local = warp_local && N.thr[j] == F.thr[j];
+        }
+        if (exp_nosmem) o << "    _Pragma(\"unroll\") for (int r = 0; r < 16; ++r) ap_[r] = a[r];\n";
+        else o << "    FDEV_PHASE_STORE" << (warp_local ? "_WARP(" : "(") << int(F.flip) << ", " << W[0] << ", " << W[1] << ", "
+               << W[2] << ", " << W[3] << ")\n";
       }
     };
     // the phase's thread-dependent predicates; versioned when few and warp-uniform (no lane bits)
@@ -575,7 +596,8 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
         o << ");\n";
       }
       int dyn = 0;
-      for (int oi = F.op_begin; oi < F.op_end; ++oi)
+      static const bool exp_noops = getenv("SVB200_JIT_EXP_NOOPS") && std::string(getenv("SVB200_JIT_EXP_NOOPS")) == "1";
+      for (int oi = F.op_begin; oi < F.op_end && !exp_noops; ++oi)   // (NOOPS: timing experiment, wrong results)
         if (!emit_op(g, oi - A.op_begin, prog.ops[oi], parity_tab_of(prog.ops[oi]), dyn, nullptr, uni ? &up : nullptr))
           return std::string();
       emit_store();
@@ -616,6 +638,9 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
   }
   if (split) k << "#define FDEV_SPLIT 1\n#define FDEV_HB " << (1 << (A.b - 1)) << "\n";
   if (pp) k << "#define FDEV_PP 1\n";
+  if (getenv("SVB200_JIT_EXP_NOMEM") && std::string(getenv("SVB200_JIT_EXP_NOMEM")) == "1") k << "#define FDEV_EXP_NOMEM 1\n";
+  static const bool pp_free = getenv("SVB200_JIT_PP_FREE") && std::string(getenv("SVB200_JIT_PP_FREE")) == "1";
+  if (pp && pp_free) k << "#define FDEV_PP_FREE 1\n";
   static const bool segprof = getenv("SVB200_JIT_SEGPROF") && std::string(getenv("SVB200_JIT_SEGPROF")) == "1";
   if (pp && segprof) k << "#define FDEV_SEGPROF 1\n";
   static const bool plain_st = getenv("SVB200_JIT_STCS") && std::string(getenv("SVB200_JIT_STCS")) == "0";

@@ -7,6 +7,7 @@
 // e.g. RX or the X of a CNOT) or generally.  Two primitives commute when every shared bit is
 // Z-like in both or X-like in both -- so RZ slides past CNOT controls and RX past CNOT targets.
 #include <algorithm>
+#include <functional>
 #include <array>
 #include <cstdio>
 #include <cstdlib>
@@ -22,6 +23,16 @@ namespace fused {
 // physical bits every tile contains (2^LB-amplitude contiguous runs); SVB200_LOW_BITS (2..3)
 int low_bits() {
   static const int lb = getenv("SVB200_LOW_BITS") ? std::max(2, std::min(3, atoi(getenv("SVB200_LOW_BITS")))) : 3;
+  return lb;
+}
+
+// Low physical bits every tile contains (SVB200_TILE_LOW, 3..9): a tile is then 2^LBT-amplitude
+// contiguous runs, which is what keeps HBM efficient -- one fused pass streams at 97 % of the copy
+// peak when its tile holds bits 3..11 but at 66-71 % when the tile's other bits are all high
+// (benchmarks/tile_locality.py: scattered 128-byte lines from many tiles hit DRAM pages out of
+// order).  The in-tile relabeling then moves the next gates' qubits onto these low positions.
+int tile_low_bits() {
+  static const int lb = getenv("SVB200_TILE_LOW") ? std::max(3, std::min(9, atoi(getenv("SVB200_TILE_LOW")))) : 3;
   return lb;
 }
 
@@ -62,14 +73,17 @@ int mtype_of(const std::vector<cplx>& m) {
 }
 
 // choose extra register positions so each bank class {p mod 3} keeps a free thread position
-void fill_regs(std::vector<int>& reg, int b) {
+// (avoid: positions to keep off the registers when possible -- the epoch's warp bits)
+void fill_regs(std::vector<int>& reg, int b, const std::vector<int>& avoid = {}) {
   auto cls_free = [&](int c, const std::vector<int>& R) {
     for (int p = c; p < b; p += 3)
-      if (std::find(R.begin(), R.end(), p) == R.end()) return true;
+      if (std::find(R.begin(), R.end(), p) == R.end() && std::find(avoid.begin(), avoid.end(), p) == avoid.end())
+        return true;
     return false;
   };
   for (int p = b - 1; p >= 0 && int(reg.size()) < kRB; --p) {
     if (std::find(reg.begin(), reg.end(), p) != reg.end()) continue;
+    if (std::find(avoid.begin(), avoid.end(), p) != avoid.end()) continue;
     std::vector<int> trial = reg;
     trial.push_back(p);
     if (cls_free(0, trial) && cls_free(1, trial) && cls_free(2, trial)) reg = trial;
@@ -83,22 +97,92 @@ void fill_regs(std::vector<int>& reg, int b) {
 // for the remaining bits, positions the phase's ops test as predicates (controls, diagonal
 // patterns: `use`) go to the high, warp-uniform thread bits, so those predicates -- and the
 // per-thread X flips they drive -- do not split warps.
-void make_phase_thr(FPhase& F, const std::vector<int>& reg, int b, const int* use) {
+// warp: when non-empty (b = 12), the tile positions of the warp-index bits thr[5..7], in order --
+// kept from the previous phase so that the phase change stays inside each warp (see build_program).
+void make_phase_thr(FPhase& F, const std::vector<int>& reg, int b, const int* use, const std::vector<int>& warp = {}) {
   for (int k = 0; k < kRB; ++k) F.reg[k] = (uint8_t)reg[k];
   auto is_reg = [&](int p) { return std::find(reg.begin(), reg.end(), p) != reg.end(); };
+  auto is_warp = [&](int p) { return std::find(warp.begin(), warp.end(), p) != warp.end(); };
   std::vector<int> thr;
   for (int c = 0; c < 3; ++c) {
     int best = -1;
     for (int p = c; p < b; p += 3)
-      if (!is_reg(p) && (best < 0 || use[p] < use[best])) best = p;
+      if (!is_reg(p) && !is_warp(p) && (best < 0 || use[p] < use[best])) best = p;
     if (best >= 0) thr.push_back(best);
   }
   std::vector<int> rest;
   for (int p = 0; p < b; ++p)
-    if (!is_reg(p) && std::find(thr.begin(), thr.end(), p) == thr.end()) rest.push_back(p);
+    if (!is_reg(p) && !is_warp(p) && std::find(thr.begin(), thr.end(), p) == thr.end()) rest.push_back(p);
   std::stable_sort(rest.begin(), rest.end(), [&](int x, int y) { return use[x] < use[y]; });
   thr.insert(thr.end(), rest.begin(), rest.end());
+  thr.insert(thr.end(), warp.begin(), warp.end());
   for (int j = 0; j < b - kRB; ++j) F.thr[j] = (uint8_t)thr[j];
+}
+
+// Warp-local phase changes.  A 12-bit tile is 4 register bits x 5 lane bits x 3 warp bits; when two
+// consecutive phases put the SAME tile positions on the warp bits, every amplitude stays inside its
+// warp across the change, so the shared-memory round trip needs only __syncwarp, not a CTA barrier:
+// the warps of a CTA then drift apart and one warp's round trip overlaps other warps' FP64 work
+// (a CTA-wide barrier per phase serialises the two).  An epoch's warp positions must hold every
+// predicate position of its phases that is not a register (thread predicates on lanes would split
+// warps); among such choices the one that lasts for the most following phases wins.  Returns {}
+// when the phase's predicates do not fit three warp bits or no choice leaves a lane of each
+// residue class mod 3.
+bool lanes_ok(const std::vector<int>& reg, const std::vector<int>& warp, int b) {
+  for (int c = 0; c < 3; ++c) {
+    bool free = false;
+    for (int p = c; p < b; p += 3)
+      if (std::find(reg.begin(), reg.end(), p) == reg.end() && std::find(warp.begin(), warp.end(), p) == warp.end())
+        free = true;
+    if (!free) return false;
+  }
+  return true;
+}
+
+std::vector<int> choose_warp_bits(const std::vector<int>& reg_now, const std::vector<u64>& future_dense,
+                                  const std::vector<u64>& future_pred, int b) {
+  u64 rmask = 0;
+  for (int p : reg_now) rmask |= 1ull << p;
+  const u64 need = future_pred.empty() ? 0 : (future_pred[0] & ~rmask);
+  if (popcount64(need) > 3) return {};
+  std::vector<int> base, cand;
+  for (int p = 0; p < b; ++p) {
+    if ((need >> p) & 1) base.push_back(p);
+    else if (!((rmask >> p) & 1)) cand.push_back(p);
+  }
+  auto run = [&](const std::vector<int>& w) {
+    u64 wm = 0;
+    for (int p : w) wm |= 1ull << p;
+    int r = 0;
+    for (size_t j = 0; j < future_dense.size(); ++j) {
+      if ((future_dense[j] & wm) || (future_pred[j] & ~future_dense[j] & ~wm)) break;
+      ++r;
+    }
+    return r;
+  };
+  std::vector<int> best;
+  int best_run = -1;
+  const size_t m = 3 - base.size();
+  std::vector<size_t> idx(m);
+  std::function<void(size_t, size_t)> rec = [&](size_t start, size_t depth) {
+    if (depth == m) {
+      std::vector<int> w = base;
+      for (size_t i : idx) w.push_back(cand[i]);
+      if (!lanes_ok(reg_now, w, b)) return;
+      const int r = run(w);
+      if (r > best_run) {
+        best_run = r;
+        best = w;
+      }
+      return;
+    }
+    for (size_t i = start; i < cand.size(); ++i) {
+      idx[depth] = i;
+      rec(i + 1, depth + 1);
+    }
+  };
+  rec(0, 0);
+  return best;
 }
 
 // A diagonal table that is 1 on even-parity indices and one constant d on odd ones (IsingZZ
@@ -579,8 +663,9 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
   std::vector<Prim> P = prims_in;
   prog.n_prims_in = int64_t(P.size());
   const int b = std::min(tile_bits(), nl);
-  const int LB = std::min(low_bits(), nl);   // physical bits every tile contains (contiguous runs)
-  const u64 low = (1ull << LB) - 1;
+  const int LB = std::min(low_bits(), nl);   // physical bits the direct store's 8-lane groups cover
+  const int LBT = std::max(LB, std::min(tile_low_bits(), b - 3));   // physical bits every tile contains
+  const u64 low = (1ull << LBT) - 1;
   std::vector<int> perm_total(nl);
   for (int p = 0; p < nl; ++p) perm_total[p] = p;
   std::vector<Req> req(P.size());
@@ -653,11 +738,29 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
     A.n_tiles = 1ull << (nl - b);
     A.phase_begin = int(prog.phases.size());
     A.gen_base = int(prog.gen_slot_of.size());
-    for (auto& ph : schedule_phases(P, take, prog.n_prims_merged)) {
+    const auto sched = schedule_phases(P, take, prog.n_prims_merged);
+    std::vector<u64> dense_tile(sched.size(), 0);   // register (dense) tile positions per phase
+    std::vector<u64> pred_tile(sched.size(), 0);    // tile positions its ops test per thread
+    for (size_t k = 0; k < sched.size(); ++k) {
+      for (int p = 0; p < 64; ++p)
+        if ((sched[k].first >> p) & 1) dense_tile[k] |= 1ull << tile_pos_of[p];
+      for (int i : sched[k].second) {
+        for (int p = 0; p < 64; ++p)
+          if (((P[i].fmask >> p) & 1) && tile_pos_of[p] >= 0) pred_tile[k] |= 1ull << tile_pos_of[p];
+        if (P[i].type == PRIM_DIAG)
+          for (int j = 0; j < P[i].nb; ++j)
+            if (tile_pos_of[P[i].pos[j]] >= 0) pred_tile[k] |= 1ull << tile_pos_of[P[i].pos[j]];
+      }
+    }
+    // SVB200_WARP_LOCAL=1 (off by default): on the 30-qubit bench circuit only 15 of 141 phase
+    // changes qualify once predicates must stay off the lanes, and the run measured 0.43 s vs 0.41 s
+    static const bool warp_local = getenv("SVB200_WARP_LOCAL") && std::string(getenv("SVB200_WARP_LOCAL")) == "1";
+    std::vector<int> W;   // warp-bit positions of the current epoch
+    for (size_t k = 0; k < sched.size(); ++k) {
+      const auto& ph = sched[k];
       std::vector<int> R;
       for (int p = 0; p < 64; ++p)
         if ((ph.first >> p) & 1) R.push_back(tile_pos_of[p]);
-      fill_regs(R, b);
       int use[kMaxB] = {0};   // predicate tests per tile position in this phase
       for (int i : ph.second) {
         for (int p = 0; p < 64; ++p)
@@ -666,9 +769,31 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
           for (int j = 0; j < P[i].nb; ++j)
             if (tile_pos_of[P[i].pos[j]] >= 0) ++use[tile_pos_of[P[i].pos[j]]];
       }
+      if (warp_local && b == kMaxB) {
+        u64 wm = 0;
+        for (int p : W) wm |= 1ull << p;
+        // the epoch continues if its warp positions stay off this phase's registers and hold all of
+        // its off-register predicates, and the register filler can avoid them
+        bool keep = !W.empty() && !(dense_tile[k] & wm) && !(pred_tile[k] & ~dense_tile[k] & ~wm);
+        if (keep) {
+          std::vector<int> Rf = R;
+          fill_regs(Rf, b, W);
+          for (int p : W) keep = keep && std::find(Rf.begin(), Rf.end(), p) == Rf.end();
+          keep = keep && lanes_ok(Rf, W, b);
+        }
+        if (!keep)
+          W = choose_warp_bits(R, std::vector<u64>(dense_tile.begin() + long(k), dense_tile.end()),
+                               std::vector<u64>(pred_tile.begin() + long(k), pred_tile.end()), b);
+        fill_regs(R, b, W);
+        for (int p : W)
+          if (std::find(R.begin(), R.end(), p) != R.end()) W.clear();
+        if (!W.empty() && !lanes_ok(R, W, b)) W.clear();
+      } else {
+        fill_regs(R, b);
+      }
       FPhase F;
       std::memset(&F, 0, sizeof(F));
-      make_phase_thr(F, R, b, use);
+      make_phase_thr(F, R, b, use, W);
       F.op_begin = int(prog.ops.size());
       F.flip = uint8_t(emit_ops(prog, P, ph.second, tile_pos_of, R));
       F.op_end = int(prog.ops.size());
@@ -689,7 +814,7 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
     // ---- in-tile relabeling: bring the qubits the next gates target onto physical bits 0..2 ----
     int sigma[64];
     for (int p = 0; p < 64; ++p) sigma[p] = p;
-    if (remap && !rest.empty() && b > LB) {
+    if (remap && !rest.empty() && b > LBT) {
       int next_use[64];
       for (int p = 0; p < 64; ++p) next_use[p] = 1 << 30;
       for (size_t k = 0; k < rest.size(); ++k) {
@@ -707,12 +832,12 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
         if (next_use[x] != next_use[y]) return next_use[x] < next_use[y];
         return x < y;
       });
-      std::vector<int> want(cand.begin(), cand.begin() + LB);   // physical positions to move onto 0..LB-1
+      std::vector<int> want(cand.begin(), cand.begin() + LBT);   // physical positions to move onto 0..LBT-1
       std::vector<int> out_low, in_high;
-      for (int l = 0; l < LB; ++l)
+      for (int l = 0; l < LBT; ++l)
         if (std::find(want.begin(), want.end(), l) == want.end()) out_low.push_back(l);
       for (int x : want)
-        if (x >= LB) in_high.push_back(x);
+        if (x >= LBT) in_high.push_back(x);
       for (size_t s = 0; s < in_high.size(); ++s) {   // swap(out_low[s], in_high[s])
         sigma[in_high[s]] = out_low[s];
         sigma[out_low[s]] = in_high[s];
