@@ -5,6 +5,7 @@
 row 1: 20q SEL L=4 Jacobian (20 x 240): device s/Jacobian, max |d| vs the reference-backed golden
        (tests/golden/sel20_golden.npz), and the numpy oracle on one observable x 20 (labelled estimate)
 row 2: unfused gate kernels at 30 qubits on every target (RX, H, CNOT(q, q+1)): GB/s min/mean
+row 2c: CNOT on every ordered (control, target) pair at 30 qubits
 row 2f: the same for a complex64 ("f32") state at 31 qubits (also 16 GiB)
 row 3: 33q QAOA p=2 forward + <C> on one GPU (the 33q adjoint needs psi + lambda = 256 GiB: 2 GPUs,
        benchmarks/adjoint_bench.py under torchrun)
@@ -80,6 +81,42 @@ def row2(precision="f64"):
     return {"row": 2, "workload": "unfused single-gate kernels at 30 qubits, every target", **out}
 
 
+def row2c():
+    """CNOT on every ordered (control, target) pair at 30 qubits (PAPER.md:128 'every gate index
+    pairing'): GB/s of algorithmic bytes (the half of the state a CNOT changes).
+    A control on physical bit 0 (qubit n-1) changes one amplitude of every 32-byte sector, so
+    DRAM moves twice the algorithmic bytes there: those pairs are reported separately."""
+    n = 30
+    rows = {}
+    with Device(n, fuse=False) as d:
+        for c in range(n):
+            for t in range(n):
+                if c == t:
+                    continue
+                op = [Op("CNOT", (c, t))]
+                d.apply(op)
+                d.reset_stats()
+                d.set_profiling(True)
+                for _ in range(2):
+                    d.apply(op)
+                st = d.kernel_stats()
+                d.set_profiling(False)
+                ms = sum(v["ms"] for v in st.values())
+                by = sum(v["bytes"] for v in st.values())
+                rows[(c, t)] = by / (ms / 1e3) / 1e9
+    g = np.array(list(rows.values()))
+    ctrl0 = np.array([v for (c, t), v in rows.items() if c == n - 1])
+    rest = np.array([v for (c, t), v in rows.items() if c != n - 1])
+    worst = sorted(rows.items(), key=lambda kv: kv[1])[:5]
+    return {"row": "2c", "workload": "unfused CNOT, 30 qubits, all 870 ordered (control, target) pairs",
+            "min_GBps": float(g.min()), "mean_GBps": float(g.mean()), "max_GBps": float(g.max()),
+            "mean_frac_of_6551": float(g.mean()) / PEAK,
+            "control_not_on_bit0": {"min_GBps": float(rest.min()), "mean_GBps": float(rest.mean())},
+            "control_on_bit0": {"mean_GBps": float(ctrl0.mean()),
+                                "note": "half of every 32 B sector changes: DRAM traffic = 2x algorithmic"},
+            "worst5": [[c, t, v] for (c, t), v in worst]}
+
+
 def row3():
     n = 33
     ops, ham, edges = workloads.qaoa_maxcut(n, p=2, seed=0)
@@ -122,7 +159,7 @@ def main():
     ap.add_argument("--rows", default="1,2,3,5")
     ap.add_argument("--cpu-seconds", type=float, default=20)
     a = ap.parse_args()
-    fns = {"1": lambda: row1(a.cpu_seconds), "2": row2, "2f": lambda: row2("f32"), "3": row3, "5": row5}
+    fns = {"1": lambda: row1(a.cpu_seconds), "2": row2, "2c": row2c, "2f": lambda: row2("f32"), "3": row3, "5": row5}
     for r in a.rows.split(","):
         print(json.dumps(fns[r]()), flush=True)
 

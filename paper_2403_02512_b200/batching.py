@@ -12,9 +12,14 @@ Partition rule: without ``batch_size`` the n terms go to g chu
 ceil/floor(n/g) (9 terms, g=4 -> 3,2,2,2); with ``batch_size`` b, chunks of b terms are dealt to
 the workers round-robin (b trades memory -- one lambda per chunk in flight -- for recompute).
 
-Determinism: for fixed (g, b) the result is bit-identical run to run (chunk partials summed in
-chunk order). Different g or b regroup the terms, so energies agree to ~1e-15 relative, well
-inside the SPEC's 1e-12.
+Determinism ("bit-identical for g in {1,2,4,8} and b in {1,3,n}"): the unit of
+arithmetic is a CANONICAL chunk that depends on the Hamiltonian alone -- the terms split by the
+ceil(n/8) rule into at most 8 chunks -- never on g or b.  Each canonical chunk's energy and
+gradient come from one reverse sweep with that chunk as the observable; the workers (the SPEC
+partition above decides which worker owns which canonical chunk: the owner of its first term)
+only change where a chunk is computed, and b only how many canonical chunks share one adjoint
+call (one forward pass).  The merge sums canonical chunks in chunk order, so energy and gradient
+are bit-identical for every g and b; they equal the unbatched adjoint within 1e-12.
 
 Environment overrides (the paper's PL_FWD_BATCH / PL_BWD_BATCH analogue):
 ``SVB200_BATCH_WORKERS`` (default: number of visible GPUs), ``SVB200_BATCH_SIZE``.
@@ -73,22 +78,33 @@ def batched_expval_and_grad(ops, hamiltonian, n_workers=None, batch_size=None, d
     if batch_size is None and os.environ.get("SVB200_BATCH_SIZE"):
         batch_size = int(os.environ["SVB200_BATCH_SIZE"])
     plan = plan_chunks(len(h.terms), n_workers, batch_size)
+    canon = canonical_chunks(len(h.terms))
+    owner_of_term = {}
+    for w, idx in plan:
+        for i in idx:
+            owner_of_term[i] = w
+    owner = [owner_of_term[idx[0]] for idx in canon]
+    per_call = max(1, (batch_size or len(h.terms)) // max(1, len(canon[0]))) if canon else 1
     ncols = sum(op.n_trainable for op in ops)
-    energy_c = [0.0] * len(plan)
-    grad_c = [np.zeros(ncols) for _ in plan]
+    energy_c = [0.0] * len(canon)
+    grad_c = [np.zeros(ncols) for _ in canon]
     errors = []
 
     def worker(w):
-        mine = [(k, idx) for k, (ww, idx) in enumerate(plan) if ww == w and idx]
+        mine = [k for k in range(len(canon)) if owner[k] == w]
         if not mine:
             return
         try:
             with Device(n_qubits, device=devices[w % len(devices)], fuse=fuse) as dev:
-                obs = [Hamiltonian(tuple(h.coeffs[i] for i in idx), tuple(h.terms[i] for i in idx)) for _, idx in mine]
-                jac, ev = dev.adjoint_jacobian(ops, obs, return_expvals=True)
-            for r, (k, _) in enumerate(mine):
-                energy_c[k] = float(ev[r])
-                grad_c[k] = jac[r]
+                for s in range(0, len(mine), per_call):   # b: canonical chunks per adjoint call
+                    ks = mine[s:s + per_call]
+                    obs = [Hamiltonian(tuple(h.coeffs[i] for i in canon[k]), tuple(h.terms[i] for i in canon[k]))
+                           for k in ks]
+                    dev.reset()
+                    jac, ev = dev.adjoint_jacobian(ops, obs, return_expvals=True)
+                    for r, k in enumerate(ks):
+                        energy_c[k] = float(ev[r])
+                        grad_c[k] = jac[r]
         except Exception as exc:  # surfaced on the calling thread
             errors.append(exc)
 
@@ -101,7 +117,15 @@ def batched_expval_and_grad(ops, hamiltonian, n_workers=None, batch_size=None, d
         raise errors[0]
     energy = 0.0
     grad = np.zeros(ncols)
-    for k in range(len(plan)):          # fixed reduction order: chunk index
+    for k in range(len(canon)):         # fixed reduction order: canonical chunk index
         energy += energy_c[k]
         grad = grad + grad_c[k]
     return energy, grad
+
+
+def canonical_chunks(n_terms, max_chunks=8):
+    """The arithmetic unit of batching: the ceil(n/8) partition of the terms (at most 8 chunks),
+    a function of the Hamiltonian alone (g and b never regroup terms)."""
+    if n_terms == 0:
+        return []
+    return [idx for _, idx in plan_chunks(n_terms, min(max_chunks, n_terms)) if idx]

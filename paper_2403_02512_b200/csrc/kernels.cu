@@ -69,7 +69,16 @@ struct PairParams {
   C m[4];
   u64 fval, xmask, count;
   Ins ins;
+  int stream;   // state larger than L2: streaming (evict-first) stores, the state is not re-read soon
 };
+
+// store one amplitude (vector) -- streaming when the state does not fit L2 (K1-K4
+// write the state once per gate; keeping it in L2 only evicts lines the next reads need)
+template <class T>
+__device__ __forceinline__ void st_amp(T* p, const T v, int stream) {
+  if (stream) __stcs(p, v);
+  else *p = v;
+}
 
 template <int ITEMS, class C>
 __global__ void __launch_bounds__(kThreads) k_pair(C* __restrict__ a, const PairParams<C> P) {
@@ -90,8 +99,8 @@ __global__ void __launch_bounds__(kThreads) k_pair(C* __restrict__ a, const Pair
     if (i0[j] == ~0ull) continue;
     const C o0 = cfma(P.m[0], v0[j], cmul(P.m[1], v1[j]));
     const C o1 = cfma(P.m[2], v0[j], cmul(P.m[3], v1[j]));
-    a[i0[j]] = o0;
-    a[i0[j] ^ P.xmask] = o1;
+    st_amp(&a[i0[j]], o0, P.stream);
+    st_amp(&a[i0[j] ^ P.xmask], o1, P.stream);
   }
 }
 
@@ -121,8 +130,8 @@ __global__ void __launch_bounds__(kThreads) k_pair_v2(float2* __restrict__ a, co
     const float2 x1 = make_float2(v1[j].x, v1[j].y), y1 = make_float2(v1[j].z, v1[j].w);
     const float2 ox0 = cfma(P.m[0], x0, cmul(P.m[1], x1)), oy0 = cfma(P.m[0], y0, cmul(P.m[1], y1));
     const float2 ox1 = cfma(P.m[2], x0, cmul(P.m[3], x1)), oy1 = cfma(P.m[2], y0, cmul(P.m[3], y1));
-    a4[i0[j] >> 1] = make_float4(ox0.x, ox0.y, oy0.x, oy0.y);
-    a4[(i0[j] ^ P.xmask) >> 1] = make_float4(ox1.x, ox1.y, oy1.x, oy1.y);
+    st_amp(&a4[i0[j] >> 1], make_float4(ox0.x, ox0.y, oy0.x, oy0.y), P.stream);
+    st_amp(&a4[(i0[j] ^ P.xmask) >> 1], make_float4(ox1.x, ox1.y, oy1.x, oy1.y), P.stream);
   }
 }
 
@@ -134,6 +143,7 @@ struct DiagParams {
   C t[64];
   u64 fval, count;
   int nb;
+  int stream;
   unsigned char pos[6];
   Ins ins;
 };
@@ -154,7 +164,7 @@ __global__ void __launch_bounds__(kThreads) k_diag(C* __restrict__ a, const Diag
     if (idx[j] == ~0ull) continue;
     int t = 0;
     for (int b = 0; b < P.nb; ++b) t |= int((idx[j] >> P.pos[b]) & 1ull) << b;
-    a[idx[j]] = cmul(P.t[t], v[j]);
+    st_amp(&a[idx[j]], cmul(P.t[t], v[j]), P.stream);
   }
 }
 
@@ -182,7 +192,7 @@ __global__ void __launch_bounds__(kThreads) k_diag_v2(float2* __restrict__ a, co
       if (P.pos[b] == 0) t1 |= 1 << b;   // the odd amplitude has bit 0 set
     const float2 o0 = cmul(P.t[t], make_float2(v[j].x, v[j].y));
     const float2 o1 = cmul(P.t[t1], make_float2(v[j].z, v[j].w));
-    a4[idx[j] >> 1] = make_float4(o0.x, o0.y, o1.x, o1.y);
+    st_amp(&a4[idx[j] >> 1], make_float4(o0.x, o0.y, o1.x, o1.y), P.stream);
   }
 }
 
@@ -894,9 +904,11 @@ static void launch_prim_t(sv_handle* h, C* a, const Prim& p) {
   const int nf = popcount64(p.fmask);
   if (nf > h->nl) sv_fail(SV_ERR_DEVICE, "internal: primitive fixes more bits than the shard has");
   const u64 count = h->n_local >> nf;
+  const int stream = double(h->n_local) * sizeof(C) > 256.0 * (1 << 20) ? 1 : 0;   // state >> 126 MB L2
   cudaEvent_t ev[2];
   if (p.type == PRIM_PAIR) {
     PairParams<C> P;
+    P.stream = stream;
     for (int i = 0; i < 4; ++i) P.m[i] = hc<C>(p.m[i]);
     P.fval = p.fval;
     P.xmask = p.xmask;
@@ -914,6 +926,7 @@ static void launch_prim_t(sv_handle* h, C* a, const Prim& p) {
     stat_end(h, KC_PAIR, prim_bytes(h, p), ev);
   } else if (p.type == PRIM_DIAG) {
     DiagParams<C> P;
+    P.stream = stream;
     if (p.nb > 6) sv_fail(SV_ERR_DEVICE, "internal: diagonal table too large");
     for (size_t i = 0; i < p.m.size(); ++i) P.t[i] = hc<C>(p.m[i]);
     P.fval = p.fval;

@@ -21,6 +21,29 @@ def test_plan_partition_rules():
         plan_chunks(3, 0)                                          # g == 0 -> validation error
 
 
+def test_canonical_chunks_depend_on_the_hamiltonian_only():
+    from paper_2403_02512_b200.batching import canonical_chunks
+    assert [len(c) for c in canonical_chunks(9)] == [2, 1, 1, 1, 1, 1, 1, 1]
+    assert [len(c) for c in canonical_chunks(40)] == [5] * 8
+    assert canonical_chunks(3) == [[0], [1], [2]]
+    assert sorted(i for c in canonical_chunks(1000) for i in c) == list(range(1000))
+
+
+@pytest.mark.gpu
+def test_batching_bit_identical_across_workers_and_batch_sizes():
+    """energy/gradient bit-identical for g in {1,2,4,8} and b in {1,3,n}."""
+    n = 12
+    ops = workloads.hardware_efficient_ansatz(n, layers=3, n_trainable=60, seed=11)
+    ham = workloads.random_pauli_hamiltonian(n, 40, seed=11)
+    ref = None
+    for g in (1, 2, 4, 8):
+        for b in (None, 1, 3, 40):
+            e, grad = batched_expval_and_grad(ops, ham, n_workers=g, batch_size=b, n_qubits=n)
+            if ref is None:
+                ref = (e, grad)
+            assert e == ref[0] and (grad == ref[1]).all(), (g, b)
+
+
 @pytest.mark.gpu
 def test_batched_matches_unbatched():
     from paper_2403_02512_b200.device import Device
