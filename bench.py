@@ -115,6 +115,21 @@ def measured_peak():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
+def measured_fp64_peak():
+    """Sustained DFMA rate measured on this pool's B200s (benchmarks/fp64_peak.cu, 3 s back to back at
+    full clock: profiles/r2_fp64_peak.jsonl), else the spec-derived 148 SMs x 64 FMA/clk x 2 x 1.965 GHz."""
+    p = os.path.join(ROOT, "profiles", "r2_fp64_peak.jsonl")
+    try:
+        with open(p) as f:
+            for line in f:
+                d = json.loads(line)
+                if d.get("case") == "dfma":
+                    return float(d["dfma_tflops"]), "measured (profiles/r2_fp64_peak.jsonl: DFMA, 3 s sustained, 1965 MHz)"
+    except Exception:
+        pass
+    return 148 * 64 * 2 * 1.965e9 / 1e12, "spec-derived: 148 SMs x 64 FMA/clk x 2 flop x 1.965 GHz"
+
+
 def ncu_traffic(kernel_class):
     """dram bytes per launch from the committed ncu capture summary, if any."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
@@ -368,14 +383,15 @@ def main():
         fpa = plan_fp64_flops_per_amp(n, ops)
         flops = fpa * float(1 << (n - g)) * args.steps
         fp_ach = flops / (st["ms"] / 1e3) / 1e12
-        fp_peak = 148 * 64 * 2 * 1.965e9 / 1e12
+        fp_peak, fp_src = measured_fp64_peak()
         roofline["fp64"] = {"achieved": fp_ach, "peak": fp_peak, "unit": "TFLOP/s", "frac": fp_ach / fp_peak,
                             "flops_per_amplitude": fpa,
-                            "peak_source": "B200 vector FP64: 148 SMs x 64 FMA/clk x 2 flop x 1.965 GHz (spec-derived)"}
+                            "peak_source": fp_src}
         roofline["note"] = ("svb200_pass (generated per-pass kernels) makes one HBM read+write per pass and runs many "
-                            "gates per pass; with 34 passes for 2225 gates it is bound by its FP64/shared-memory "
-                            "work, so the HBM frac is the lesser figure -- see roofline.fp64 and "
-                            "profiles/r1_ncu_jit_pass_v6.md")
+                            "gates per pass (34 passes for 2225 gates): its time is FP64 arithmetic (89 % of the pipe "
+                            "alone), the tile stream (75 % of HBM alone) and shared-memory phase round trips, which "
+                            "only partly overlap -- profiles/r2_pass_time_decomposition.md; the HBM frac is the "
+                            "lesser figure, see roofline.fp64 (DMUL counted as 1 flop, so the pipe is busier than it)")
 
     # global-qubit swaps (rank-0 view): NCCL send/recv of half a shard per swap over NVLink
     comm = None

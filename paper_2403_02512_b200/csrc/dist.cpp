@@ -161,8 +161,19 @@ void exchange_bits(sv_handle* h, const std::vector<double2*>& states, const std:
   for (size_t si = 0; si < states.size() && p2p; ++si) p2p = peers_of(h, states[si], &maps[si]);
   for (size_t si = 0; si < states.size(); ++si) {
     double2* st = states[si];
+    // peer memory: the partners' earlier kernels on their states are done -- the wait absorbs any
+    // skew between the ranks' programs, so it stays outside the swap's timed region
+    if (p2p) device_barrier(h);
     stat_begin(h, KC_SWAP, 32.0 * double(moved), ev);
-    if (p2p) {
+    static const bool old_top = getenv("SVB200_XCHG_TOP") && std::string(getenv("SVB200_XCHG_TOP")) == "1";
+    if (p2p && old_top && k == 1 && ps[0] == h->nl - 1) {
+      // A/B reference: the round-1 contiguous half-shard exchange (victim on the top local bit)
+      const int b = g;
+      const u64 half = h->n_local >> 1, share = half >> 1, lo = b ? share : 0;
+      double2* peer = maps[si].by_rank[rank_of[1 - g]];
+      launch_exchange(h, st + ((1 - b) ? half : 0) + lo, peer + (b ? half : 0) + lo, b ? half - share : share);
+      device_barrier(h);
+    } else if (p2p) {
       // pairs with partner c split on the highest local bit that is not a victim
       int q = h->nl - 1;
       while ((vmask >> q) & 1) --q;
@@ -172,7 +183,6 @@ void exchange_bits(sv_handle* h, const std::vector<double2*>& states, const std:
         peer[c] = c == g ? nullptr : maps[si].by_rank[rank_of[c]];
         own[c] = h->rank < rank_of[c] ? 0ull : (1ull << q);
       }
-      device_barrier(h);   // the partners' earlier kernels on their states are done
       launch_exchange_multi(h, st, peer, vdep, own, vdep[g], nc, vmask | (1ull << q), h->n_local >> (k + 1));
       device_barrier(h);   // their stores into ours are visible
     } else {
