@@ -261,3 +261,28 @@ def plan_fp64_flops_per_amp(n_qubits, ops):
     out = ctypes.c_double()
     _lib.check(_lib.lib().sv_plan_fp64(int(n_qubits), packed.ptr, packed.n, ctypes.byref(out)))
     return out.value
+
+
+B200_HBM_BYTES = 179 * 10**9   # usable HBM3e per B200 (cudaMemGetInfo total on this pool's boxes, ~179 GB)
+
+
+def memory_plan(n_qubits, world=1, n_observables=1, fused=True, precision="f64"):
+    """Per-GPU device memory of a state-vector job (the buffers libsvb200 allocates): the shard, the
+    adjoint sweep's lambda (one kept buffer for the fused sweep, plus one saved final state when
+    several observables share the forward pass; the per-gate sweep keeps one lambda per
+    observable), and the sharded swap staging (two slots of up to 1 GiB each).  Returns a dict of
+    byte counts and whether it fits one B200 (SPEC.md:643 capacity errors surface as
+    CapacityError at run time; this is the plan the north star's 35-qubit / 8-GPU adjoint rests on)."""
+    amp = 16 if precision == "f64" else 8
+    g = world.bit_length() - 1
+    if world < 1 or (world & (world - 1)):
+        raise ValidationError("n_shards must be a power of two")
+    shard = amp * (1 << (n_qubits - g))
+    if fused:
+        lam = shard * (1 + (1 if n_observables > 1 else 0))
+    else:
+        lam = shard * n_observables
+    staging = 0 if world == 1 else min(2 * 2**30, 16 * (1 << (n_qubits - g - 1)))
+    total = shard + lam + staging
+    return {"n_qubits": n_qubits, "world": world, "state_bytes": shard, "adjoint_bytes": lam,
+            "staging_bytes": staging, "total_bytes": total, "fits_b200": total < B200_HBM_BYTES}

@@ -97,3 +97,16 @@ def test_ctypes_signatures_cover_exports(lib):
     for s in _lib.EXPORTS:
         f = getattr(lib, s)
         assert isinstance(f, ctypes._CFuncPtr)
+
+
+def test_memory_plan_of_the_north_star_configs():
+    """33q adjoint needs 2 GPUs (psi + lambda = 275 GB); 34q fits 4, 35q fits 8 with
+    psi + lambda = 137.4 GB per GPU (document and assert the 35q / P=8 plan)."""
+    from paper_2403_02512_b200.device import memory_plan
+    assert memory_plan(30)["state_bytes"] == 16 * 2**30
+    assert not memory_plan(33, 1)["fits_b200"] and memory_plan(33, 2)["fits_b200"]
+    p35 = memory_plan(35, 8)
+    assert p35["state_bytes"] + p35["adjoint_bytes"] == 2 * 16 * 2**32   # 137.4 GB
+    assert p35["fits_b200"] and memory_plan(34, 4)["fits_b200"]
+    assert not memory_plan(35, 4)["fits_b200"]                          # 35q adjoint needs 8 GPUs
+    assert memory_plan(35, 4, n_observables=0)["state_bytes"] < 179e9   # the 35q forward fits 4
