@@ -20,8 +20,12 @@ def main():
     a = ap.parse_args()
     n = a.n
     sets = {"bits 3-11 (contiguous tile)": list(range(3, 12)), "bits 12-20": list(range(12, 21)),
-            "bits 21-29 (top)": list(range(n - 9, n)), "spread 3,6,..,27": list(range(3, 30, 3)),
-            "bits 3-6 + 26-29": [3, 4, 5, 6, 26, 27, 28, 29, 15]}
+            f"bits {n - 9}-{n - 1} (top)": list(range(n - 9, n)), "spread 3,6,..,27": list(range(3, 30, 3)),
+            "bits 3-6 + 26-29": [3, 4, 5, 6, 26, 27, 28, 29, 15],
+            "bits 17-25": list(range(17, 26)), "bits 3-7 + top 4": [3, 4, 5, 6, 7] + list(range(n - 4, n)),
+            "bits 21-26 + top 3": list(range(21, 27)) + list(range(n - 3, n)),
+            "bits 18-23 + top 3": list(range(18, 24)) + list(range(n - 3, n)),
+            "bits 3-8 + top 3": list(range(3, 9)) + list(range(n - 3, n))}
     out = {}
     with Device(n) as d:
         for name, bits in sets.items():
