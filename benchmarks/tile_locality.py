@@ -24,6 +24,10 @@ def main():
             "bits 3-6 + 26-29": [3, 4, 5, 6, 26, 27, 28, 29, 15],
             "bits 17-25": list(range(17, 26)), "bits 3-7 + top 4": [3, 4, 5, 6, 7] + list(range(n - 4, n)),
             "bits 21-26 + top 3": list(range(21, 27)) + list(range(n - 3, n)),
+            "bits 21-26 + 27-29": list(range(21, 30)),
+            "bits 15-20 + top 3": list(range(15, 21)) + list(range(n - 3, n)),
+            "bits 21-23 + 27-29 + top 3": [21, 22, 23, 27, 28, 29] + list(range(n - 3, n)),
+            "bits 24-26 + top 3 + 3-5": [3, 4, 5, 24, 25, 26] + list(range(n - 3, n)),
             "bits 18-23 + top 3": list(range(18, 24)) + list(range(n - 3, n)),
             "bits 3-8 + top 3": list(range(3, 9)) + list(range(n - 3, n))}
     out = {}

@@ -888,7 +888,8 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
         for (int j = 0; j < o.nt; ++j)
           if (o.treg[j] == 0xFF && ((lowld >> o.tphys[j]) & 1)) ok = false;
       }
-      if (ok) {
+      static const bool store_phase = !(getenv("SVB200_STORE_PHASE") && std::string(getenv("SVB200_STORE_PHASE")) == "0");
+      if (ok && lanes.size() >= 2) {
         // a low store bit held in a register splits the thread's 128-byte run over two stores of
         // full 32-byte sectors (still merged in L2); lanes carry the others
         std::vector<int> thr(lanes.begin(), lanes.end());
@@ -896,6 +897,33 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
           if (std::find(lanes.begin(), lanes.end(), int(L.thr[j])) == lanes.end()) thr.push_back(L.thr[j]);
         for (int j = 0; j < b - kRB; ++j) L.thr[j] = uint8_t(thr[j]);
         A.direct = 1;
+      } else if (store_phase && b == kMaxB) {
+        // The last phase holds two or more of the store's low bits in registers (or tests them
+        // as predicates): its stores would write 16-32 bytes per 128-byte line per instruction,
+        // which streams several times slower (a 33-qubit QAOA pass: 296 ms vs ~50).  Append an
+        // op-free phase whose lanes ARE those bits: one more shared-memory round trip, and the pass
+        // keeps its coalesced direct store and its overlapped next-tile load.
+        FPhase E;
+        std::memset(&E, 0, sizeof(E));
+        std::vector<int> R;
+        for (int k = 0; k < kRB; ++k)
+          if (std::find(q_low.begin(), q_low.end(), int(L.reg[k])) == q_low.end()) R.push_back(L.reg[k]);
+        fill_regs(R, b, q_low);
+        bool clash = false;
+        for (int t : q_low) clash |= std::find(R.begin(), R.end(), t) != R.end();
+        if (!clash) {
+          int use0[kMaxB] = {0};
+          make_phase_thr(E, R, b, use0);
+          std::vector<int> thr(q_low.begin(), q_low.end());
+          for (int j = 0; j < b - kRB; ++j)
+            if (std::find(q_low.begin(), q_low.end(), int(E.thr[j])) == q_low.end()) thr.push_back(E.thr[j]);
+          for (int j = 0; j < b - kRB; ++j) E.thr[j] = uint8_t(thr[j]);
+          E.op_begin = E.op_end = int(prog.ops.size());
+          E.flip = 0;
+          prog.phases.push_back(E);
+          A.n_phases += 1;
+          A.direct = 1;
+        }
       }
     }
     bool moved = false;
