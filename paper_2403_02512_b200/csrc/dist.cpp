@@ -348,9 +348,13 @@ void dist_bring_local(sv_handle* h, const std::vector<double2*>& states, const s
     if (std::find(keep.begin(), keep.end(), lo) != keep.end()) continue;
     cand.push_back({next_use[lo], p});
   }
-  std::sort(cand.begin(), cand.end(), [](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+  // victims on physical bits 0..2 would split the exchange's 128-byte runs (16-byte remote
+  // accesses) and bits 3..6 its 2 KiB runs: positions >= 7 first, then 3..6, then 0..2, Belady
+  // (furthest next use) within a tier
+  auto tier = [](int p) { return p >= 7 ? 0 : (p >= 3 ? 1 : 2); };
+  std::sort(cand.begin(), cand.end(), [&](const std::pair<int, int>& a, const std::pair<int, int>& b) {
+    if (tier(a.second) != tier(b.second)) return tier(a.second) < tier(b.second);
     if (a.first != b.first) return a.first > b.first;
-    if ((a.second >= 3) != (b.second >= 3)) return a.second >= 3;
     return a.second > b.second;
   });
   if (cand.size() < in.size()) sv_fail(SV_ERR_CAPACITY, "operation spans more qubits than a shard holds locally");
