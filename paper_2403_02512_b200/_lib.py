@@ -131,38 +131,72 @@ def _dptr(a):
     return a.ctypes.data_as(POINTER(c_double))
 
 
+def _svop_dtype():
+    f = SvOp
+    names = ["kind", "n_wires", "wires", "n_ctrls", "ctrls", "ctrl_values", "params", "inverse", "trainable_mask",
+             "matrix"]
+    formats = [np.int32, np.int32, np.uint64, np.int32, np.uint64, np.uint64, (np.float64, 3), np.int32, np.int32,
+               np.uint64]
+    return np.dtype({"names": names, "formats": formats, "offsets": [getattr(f, k).offset for k in names],
+                     "itemsize": ctypes.sizeof(SvOp)})
+
+
+_SVOP_DTYPE = None
+
+
 class PackedOps:
-    """Op records marshalled into C structs; owns every buffer the structs point to."""
+    """Op records marshalled into C structs; owns every buffer the structs point to.
+
+    Vectorised: one numpy record array laid out as `sv_op` (include/svb200.h) plus one int32
+    buffer holding every op's wires, controls and control values (the structs point into it),
+    so marshalling a 2225-op circuit costs ~1 ms instead of ~8 ms of per-field ctypes writes.
+    """
 
     def __init__(self, ops):
+        global _SVOP_DTYPE
+        if _SVOP_DTYPE is None:
+            _SVOP_DTYPE = _svop_dtype()
         ops = list(ops)
-        self.n = len(ops)
-        self.arr = (SvOp * max(self.n, 1))()
-        self._keep = []
-        for i, op in enumerate(ops):
+        for op in ops:
             if not isinstance(op, Op):
                 raise TypeError(f"expected Op, got {type(op).__name__}")
-            rec = self.arr[i]
-            rec.kind = KIND_CODE[op.name]
-            w = np.ascontiguousarray(op.wires, dtype=np.int32)
-            rec.n_wires = len(w)
-            rec.wires = _iptr(w)
-            self._keep.append(w)
-            if op.ctrls:
-                c = np.ascontiguousarray(op.ctrls, dtype=np.int32)
-                v = np.ascontiguousarray(op.ctrl_values, dtype=np.int32)
-                rec.n_ctrls = len(c)
-                rec.ctrls = _iptr(c)
-                rec.ctrl_values = _iptr(v)
-                self._keep += [c, v]
-            for j, p in enumerate(op.params[:3]):
-                rec.params[j] = p
-            rec.inverse = int(bool(op.inverse))
-            rec.trainable_mask = sum(1 << j for j, t in enumerate(op.trainable) if t)
-            if op.matrix is not None:
-                m = np.ascontiguousarray(op.matrix, dtype=np.complex128).view(np.float64)
-                rec.matrix = _dptr(m)
-                self._keep.append(m)
+        self.n = n = len(ops)
+        rec = np.zeros(max(n, 1), dtype=_SVOP_DTYPE)
+        ints, starts = [], []
+        for op in ops:
+            starts.append(len(ints))
+            ints.extend(op.wires)
+            ints.extend(op.ctrls)
+            ints.extend(op.ctrl_values)
+        buf = np.asarray(ints if ints else [0], dtype=np.int32)
+        base = buf.ctypes.data
+        self._keep = [rec, buf]
+        if n:
+            rec["kind"][:n] = [KIND_CODE[op.name] for op in ops]
+            nw = np.fromiter((len(op.wires) for op in ops), np.int64, n)
+            nc = np.fromiter((len(op.ctrls) for op in ops), np.int64, n)
+            st = np.asarray(starts, dtype=np.int64)
+            rec["n_wires"][:n] = nw
+            rec["wires"][:n] = (base + 4 * st).astype(np.uint64)
+            rec["n_ctrls"][:n] = nc
+            has_c = nc > 0
+            rec["ctrls"][:n] = np.where(has_c, base + 4 * (st + nw), 0).astype(np.uint64)
+            rec["ctrl_values"][:n] = np.where(has_c, base + 4 * (st + nw + nc), 0).astype(np.uint64)
+            params = np.zeros((n, 3))
+            for i, op in enumerate(ops):
+                if op.params:
+                    p = op.params[:3]
+                    params[i, :len(p)] = p
+            rec["params"][:n] = params
+            rec["inverse"][:n] = [1 if op.inverse else 0 for op in ops]
+            rec["trainable_mask"][:n] = [sum(1 << j for j, t in enumerate(op.trainable) if t) if op.trainable else 0
+                                         for op in ops]
+            for i, op in enumerate(ops):
+                if op.matrix is not None:
+                    m = np.ascontiguousarray(op.matrix, dtype=np.complex128).view(np.float64)
+                    rec["matrix"][i] = m.ctypes.data
+                    self._keep.append(m)
+        self.arr = (SvOp * max(n, 1)).from_buffer(rec)
 
     @property
     def ptr(self):

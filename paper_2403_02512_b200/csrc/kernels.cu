@@ -1199,6 +1199,14 @@ void pauli_groups_apply(sv_handle* h, const double2* psi, double2* lam,
       groups.push_back(gr);
     }
   }
+  // Groups in x-mask order: the up-to-16 groups of one launch then share their high x bits, so the
+  // gathers psi[i ^ x_g] of a launch fall in the same L2-resident window of psi (the grid streams
+  // a ~38 MB window of i at a time) and DRAM reads psi about once per launch instead of once per
+  // group (config 5, 1000 random terms: 450 x-masks but 37 distinct x >> 20).
+  std::stable_sort(groups.begin(), groups.end(),
+                   [](const std::pair<u64, std::vector<PauliTerm>>& a, const std::pair<u64, std::vector<PauliTerm>>& b) {
+                     return a.first < b.first;
+                   });
   for (size_t g0 = 0; g0 < groups.size(); g0 += kMaxXG) {
     PauliGroupsArgs G;
     std::vector<PauliApplyTermDev> dt;
