@@ -10,6 +10,7 @@ row 2f: the same for a complex64 ("f32") state at 31 qubits (also 16 GiB)
 row 3: 33q QAOA p=2 forward + <C> on one GPU (the 33q adjoint needs psi + lambda = 256 GiB: 2 GPUs,
        benchmarks/adjoint_bench.py under torchrun)
 row 5: 28q HEA (1000 trainable, 1000-term H): s per expval + gradient
+row 5s: the same with a 9000-term H (SURVEY §8(d) stress variant)
 """
 import argparse
 import json
@@ -154,12 +155,33 @@ def row5():
             "s": min(ts), "expval": float(ev[0])}
 
 
+def row5s():
+    """Config 5's stress variant (T ~ 9000 terms, C2H4 scale)."""
+    n = 28
+    ops = workloads.hardware_efficient_ansatz(n, layers=18, n_trainable=1000, seed=0)
+    ham = workloads.random_pauli_hamiltonian(n, 9000, seed=1)
+    with Device(n) as d:
+        d.adjoint_jacobian(ops, [ham])
+        d.reset()
+        d.synchronize()
+        d.reset_stats()
+        d.set_profiling(True)
+        t0 = time.perf_counter()
+        jac, ev = d.adjoint_jacobian(ops, [ham], return_expvals=True)
+        d.synchronize()
+        t = time.perf_counter() - t0
+        st = {k: {"launches": v["launches"], "ms": v["ms"]} for k, v in d.kernel_stats().items() if v["launches"]}
+        d.set_profiling(False)
+    return {"row": "5s", "workload": "28q HEA 18 layers, 1000 trainable, 9000-term random Pauli H: expval + gradient",
+            "s": t, "expval": float(ev[0]), "kernel_classes": st}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rows", default="1,2,3,5")
     ap.add_argument("--cpu-seconds", type=float, default=20)
     a = ap.parse_args()
-    fns = {"1": lambda: row1(a.cpu_seconds), "2": row2, "2c": row2c, "2f": lambda: row2("f32"), "3": row3, "5": row5}
+    fns = {"1": lambda: row1(a.cpu_seconds), "2": row2, "2c": row2c, "2f": lambda: row2("f32"), "3": row3, "5": row5, "5s": row5s}
     for r in a.rows.split(","):
         print(json.dumps(fns[r]()), flush=True)
 
