@@ -107,7 +107,20 @@ __device__ __forceinline__ void diagg(double2 (&a)[kRegs], const FOp& op, const 
     pair_shear<K, false>(a, sw ? -op.c[0].x : op.c[0].x, sw ? -op.c[0].y : op.c[0].y);       \
     break;                                                                                    \
   }
-#define DENSE2_CASE(PI, K0, K1)                                                              \
+#define TAN_CASE(K)                                                                   \
+  case CS_TAN + K * 4 + 0: fdev::pair_tan<K, false, false>(a, op.c[0].x); break;      \
+  case CS_TAN + K * 4 + 1: fdev::pair_tan<K, true, false>(a, op.c[0].x); break;       \
+  case CS_TAN + K * 4 + 2: fdev::pair_tan<K, false, true>(a, op.c[0].x); break;       \
+  case CS_TAN + K * 4 + 3: fdev::pair_tan<K, true, true>(a, op.c[0].x); break;       \
+  case CS_TAND + K * 2 + 0:                                                            \
+    if ((fthr >> K) & 1) fdev::pair_tan<K, false, false, true>(a, op.c[0].x);          \
+    else fdev::pair_tan<K, false, false>(a, op.c[0].x);                                \
+    break;                                                                             \
+  case CS_TAND + K * 2 + 1:                                                            \
+    if ((fthr >> K) & 1) fdev::pair_tan<K, false, true, true>(a, op.c[0].x);           \
+    else fdev::pair_tan<K, false, true>(a, op.c[0].x);                                 \
+    break;
+#define DENSE2_CASE(PI, K0, K1)                                                         \
   case CS_DENSE2 + PI:                                                                        \
     if (FULL) {                                                                               \
       const int f = ((fthr >> K0) & 1) | (((fthr >> K1) & 1) << 1);                          \
@@ -209,6 +222,7 @@ __device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const int cs, cons
     PHASE1_CASE(0) PHASE1_CASE(1) PHASE1_CASE(2) PHASE1_CASE(3)
     SHEAR_CASE(0) SHEAR_CASE(1) SHEAR_CASE(2) SHEAR_CASE(3)
     case CS_SHEAR + 3: case CS_SHEAR + 7: case CS_SHEAR + 11: case CS_SHEAR + 15: break;
+    TAN_CASE(0) TAN_CASE(1) TAN_CASE(2) TAN_CASE(3)
     PARITY_CASE(0) PARITY_CASE(1) PARITY_CASE(2) PARITY_CASE(3) PARITY_CASE(4) PARITY_CASE(5)
     PARITY_CASE(6) PARITY_CASE(7) PARITY_CASE(8) PARITY_CASE(9) PARITY_CASE(10) PARITY_CASE(11)
     PARITY_CASE(12) PARITY_CASE(13) PARITY_CASE(14) PARITY_CASE(15)
@@ -222,6 +236,14 @@ __device__ __forceinline__ void apply_op(double2 (&a)[kRegs], const int cs, cons
     case CS_XFLIP + 1: fthr ^= 2; break;
     case CS_XFLIP + 2: fthr ^= 4; break;
     case CS_XFLIP + 3: fthr ^= 8; break;
+    case CS_RDIAG: {
+      const unsigned aff = unsigned(op.xm);
+#pragma unroll
+      for (int r = 0; r < kRegs; ++r)
+        if ((aff >> r) & 1) cmul_ip(a[r], coef[op.tab + r]);
+      break;
+    }
+    case CS_RDIAG + 1: break;
     PAIRG_CASE(1) PAIRG_CASE(2) PAIRG_CASE(3) PAIRG_CASE(4) PAIRG_CASE(5) PAIRG_CASE(6) PAIRG_CASE(7)
     PAIRG_CASE(8) PAIRG_CASE(9) PAIRG_CASE(10) PAIRG_CASE(11) PAIRG_CASE(12) PAIRG_CASE(13)
     PAIRG_CASE(14) PAIRG_CASE(15)
@@ -745,7 +767,8 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
     CUDA_CHECK(cudaFreeAsync(d_gen, h->stream));
     d2h(h, z.data(), h->d_results, z.size() * sizeof(double));
     gen_out->clear();
-    for (int s = 0; s < n_gen; ++s) gen_out->push_back({prog.gen_slot_of[s], cplx(z[2 * s], z[2 * s + 1])});
+    for (int s = 0; s < n_gen; ++s)   // gen_scale: scaled rotations ahead of the bra-ket in its pass
+      gen_out->push_back({prog.gen_slot_of[s], prog.gen_scale[s] * cplx(z[2 * s], z[2 * s + 1])});
   }
   return prog.perm;
 }

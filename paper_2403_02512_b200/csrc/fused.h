@@ -64,10 +64,21 @@ constexpr int SH_RY = 0, SH_RX = 1, SH_RYD = 2;
 // parity phase (IsingZZ / ZZ..Z-string phases): a *= d where parity(register bits M of r) ^
 // parity(physical base & xm) ^ parity(fthr & M) ^ v == 1
 constexpr int CS_PARITY = 106;   // + M (register mask, 0..15)                        (106..121)
+// unconditioned rotations in scaled form, 2 FMAs per real pair (runtime pass compiler only): the op
+// applies R(phi)/c (TAN: tau = tan(phi), |phi| <= pi/4) or R(phi)/s (COT: kappa = cot(phi)); the
+// pass's product of the dropped factors is absorbed once per pass (fused_plan.cpp absorb_pass_scale).
+// c[0] = (tau or kappa, dropped factor), c[1].x = cos(phi), c[2] = (sin(phi), RX-type ? 1 : 0)
+constexpr double kTanBand = 2.5;  // hysteresis: a remembered form is kept while |tau| or |kappa| <= 2.5
+constexpr int CS_TAN = 122;      // + k*4 + {0: RY-type TAN, 1: RX-type TAN, 2: RY-type COT, 3: RX-type COT} (122..137)
+// ... RY type on a register bit that may carry a per-thread flip (the flipped threads apply R(-phi))
+constexpr int CS_TAND = 138;     // + k*2 + {0: TAN, 1: COT}                                 (138..145)
+// register diagonal: a[r] *= coef[tab + r] for the registers r in the 16-bit mask xm -- a group of
+// PHASE1 ops of one phase multiplied together (fused_plan.cpp group_phase_diagonals)
+constexpr int CS_RDIAG = 146;    // (147 unused)
 // adjoint bra-kets (psi and lambda share the tile; t = register bit selecting lambda)
-constexpr int CS_GEN1 = 122;     // + k*4 + t: 2x2 generator on register bit k        (122..137)
-constexpr int CS_GEN2 = 138;     // + pair*4 + t: 4x4 generator on register bits pair (138..161)
-constexpr int CS_GEND = 162;     // + t: diagonal generator (table on any bits; only t in registers) (162..165)
+constexpr int CS_GEN1 = 148;     // + k*4 + t: 2x2 generator on register bit k        (148..163)
+constexpr int CS_GEN2 = 164;     // + pair*4 + t: 4x4 generator on register bits pair (164..187)
+constexpr int CS_GEND = 188;     // + t: diagonal generator (table on any bits; only t in registers) (188..191)
 constexpr int kMaxGens = 64;     // generator slots per pass (per-warp shared-memory accumulators)
 static_assert(sizeof(FOp) == 144, "FOp layout");
 
@@ -113,8 +124,12 @@ struct Program {
   std::vector<int> perm;           // final layout: physical position p now holds what was at p before...
                                    // ... i.e. the qubit at p moved to perm[p]
   std::vector<int> gen_slot_of;    // program result slot -> Prim::slot (the caller's Jacobian slot)
+  std::vector<double> gen_scale;   // ... and the factor its bra-ket is multiplied by (scaled rotations
+                                   // before it in its pass leave psi and lambda scaled: 1 / f^2)
   int64_t n_prims_in = 0, n_prims_merged = 0;
   int owed_neg = 0;                // global -1 owed by rotations emitted as -R(phi') (planner only)
+  std::vector<uint8_t> tan_forms;  // planner only: COT (1) / TAN (0) of each scaled rotation, in order
+  std::vector<uint8_t> tan_hint;   // ... as the previous plan of the same structure chose them
   // runtime pass compiler (fused_jit.cpp): per-pass kernels and their parameter blocks
   bool jit_ready = false, jit_two = false;
   std::vector<JitPass> jit;

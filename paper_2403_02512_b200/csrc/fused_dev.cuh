@@ -129,6 +129,54 @@ __device__ __forceinline__ void pair_shear(double2 (&a)[kRegs], const double t, 
   }
 }
 
+// rotation R(phi) of every (x0, x1) pair on register bit K, scaled: R/cos(phi) (TAN, t = tan phi)
+// or R/sin(phi) (COT, t = cot phi) -- 2 FMAs per real pair instead of the shears' 3; the pass owes
+// the state the dropped factor, absorbed once per pass by the planner (fused_plan.cpp).
+//   RY type R = [[c, -s], [s, c]]:     TAN x0 - t x1, x1 + t x0          COT t x0 - x1, t x1 + x0
+//   RX type R = [[c, -is], [-is, c]]:  TAN x0 - i t x1, x1 - i t x0      COT t x0 - i x1, t x1 - i x0
+// NEG: the flipped roles of a per-thread flip, R(-phi) (RY type; TAN negates t, COT the +-1 terms)
+template <int K, bool RX, bool COT, bool NEG = false>
+__device__ __forceinline__ void pair_tan(double2 (&a)[kRegs], double t) {
+  if (NEG && !COT) t = -t;
+#pragma unroll
+  for (int r = 0; r < kRegs; ++r) {
+    if ((r >> K) & 1) continue;
+    double2& x0 = a[r];
+    double2& x1 = a[r | (1 << K)];
+    const double2 y0 = x0, y1 = x1;
+    if (RX) {   // -i t x = t x.y - i t x.x
+      if (COT) {
+        x0.x = fma(t, y0.x, y1.y);
+        x0.y = fma(t, y0.y, -y1.x);
+        x1.x = fma(t, y1.x, y0.y);
+        x1.y = fma(t, y1.y, -y0.x);
+      } else {
+        x0.x = fma(t, y1.y, y0.x);
+        x0.y = fma(-t, y1.x, y0.y);
+        x1.x = fma(t, y0.y, y1.x);
+        x1.y = fma(-t, y0.x, y1.y);
+      }
+    } else {
+      if (COT && NEG) {
+        x0.x = fma(t, y0.x, y1.x);
+        x0.y = fma(t, y0.y, y1.y);
+        x1.x = fma(t, y1.x, -y0.x);
+        x1.y = fma(t, y1.y, -y0.y);
+      } else if (COT) {
+        x0.x = fma(t, y0.x, -y1.x);
+        x0.y = fma(t, y0.y, -y1.y);
+        x1.x = fma(t, y1.x, y0.x);
+        x1.y = fma(t, y1.y, y0.y);
+      } else {
+        x0.x = fma(-t, y1.x, y0.x);
+        x0.y = fma(-t, y1.y, y0.y);
+        x1.x = fma(t, y0.x, y1.x);
+        x1.y = fma(t, y0.y, y1.y);
+      }
+    }
+  }
+}
+
 // a[r] *= d for registers r with parity(r & M) == 1 ^ tp (tp: the thread's parity part)
 template <int M>
 __device__ __forceinline__ void parity_phase(double2 (&a)[kRegs], const double2 d, const int tp) {

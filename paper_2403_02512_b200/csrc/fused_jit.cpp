@@ -251,6 +251,20 @@ bool emit_op(Gen& g, int i, const FOp& op, bool parity_tab, int& dyn, VCtx* vc =
         << ".y);\n";
       o << "      else fdev::pair_shear<" << k << ", false>(a, " << c0 << ".x, " << c0 << ".y);\n";
     }
+  } else if (cs >= CS_TAN && cs < CS_TAN + 16) {
+    const int k = (cs - CS_TAN) / 4, sub = (cs - CS_TAN) % 4;
+    o << "      fdev::pair_tan<" << k << ", " << ((sub & 1) ? "true" : "false") << ", " << ((sub & 2) ? "true" : "false")
+      << ">(a, " << g.C(i, 0) << ".x);\n";
+  } else if (cs == CS_RDIAG) {
+    for (int r = 0; r < 16; ++r)
+      if ((op.xm >> r) & 1) o << "      fdev::cmul_ip(a[" << r << "], " << g.C(i, 16 + r) << ");\n";
+  } else if (cs >= CS_TAND && cs < CS_TAND + 8) {
+    const int k = (cs - CS_TAND) / 2;
+    const char* cot = (cs - CS_TAND) % 2 ? "true" : "false";
+    const std::string c0 = g.C(i, 0);
+    o << "      if ((fthr >> " << k << ") & 1) fdev::pair_tan<" << k << ", false, " << cot << ", true>(a, " << c0
+      << ".x);\n";
+    o << "      else fdev::pair_tan<" << k << ", false, " << cot << ">(a, " << c0 << ".x);\n";
   } else if (cs >= CS_PARITY && cs < CS_PARITY + 16) {
     const int M = cs - CS_PARITY;
     std::string tp = "(__popc(fthr & " + std::to_string(M) + ") + " + std::to_string(int(op.v));
@@ -737,7 +751,8 @@ void jit_prepare(Program& prog, bool two) {
     jp.cf.assign(std::max<size_t>(jp.cf_refs.size(), 1), make_double2(0.0, 0.0));
     for (size_t r = 0; r < jp.cf_refs.size(); ++r) {
       const FOp& op = prog.ops[A.op_begin + jp.cf_refs[r].first];
-      jp.cf[r] = jp.cf_refs[r].second < 0 ? prog.coef[op.tab + 1] : op.c[jp.cf_refs[r].second];
+      const int j = jp.cf_refs[r].second;   // -1: coef[tab + 1]; 16 + r: coef[tab + r]; else inline c[j]
+      jp.cf[r] = j < 0 ? prog.coef[op.tab + 1] : (j >= 16 ? prog.coef[op.tab + j - 16] : op.c[j]);
     }
     jp.tab_base = int(prog.jit_tabs.size());
     for (const auto& tr : jp.tab_refs) {

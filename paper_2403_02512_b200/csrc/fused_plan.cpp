@@ -11,7 +11,10 @@
 #include <array>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 
 #include "fused.h"
@@ -195,6 +198,99 @@ bool parity_table(const Prim& p) {
   return true;
 }
 
+// Register bits an op mixes (acts on non-diagonally), flips, or reads as a whole (bra-kets): a
+// diagonal op on any other register bit commutes with it.
+int nondiag_regs(const FOp& o) {
+  const int cs = o.cs;
+  int m = o.fk;   // an attached thread-predicated X flips its bit before the op
+  if ((cs >= CS_PAIR1 && cs < CS_PAIR1 + 16) || (cs >= CS_PAIR1D && cs < CS_PAIR1D + 16)) m |= 1 << o.k;
+  else if (cs >= CS_SHEAR && cs < CS_SHEAR + 16) m |= 1 << ((cs - CS_SHEAR) / 4);
+  else if (cs >= CS_TAN && cs < CS_TAN + 16) m |= 1 << ((cs - CS_TAN) / 4);
+  else if (cs >= CS_TAND && cs < CS_TAND + 8) m |= 1 << ((cs - CS_TAND) / 2);
+  else if (cs >= CS_XFLIP && cs < CS_XFLIP + 4) m |= 1 << (cs - CS_XFLIP);
+  else if (cs >= CS_PAIRGR && cs < CS_PAIRG + 15) m |= cs < CS_PAIRG ? cs - CS_PAIRGR + 1 : cs - CS_PAIRG + 1;
+  else if (cs >= CS_DENSE2 && cs < CS_DENSE2 + 6) m |= (1 << (o.xr & 15)) | (1 << (o.xr >> 4));
+  else if (cs >= CS_GEN1) m |= 15;
+  return m & 15;
+}
+
+// Diagonal grouping (pass compiler only): the unpredicated PHASE1 ops of a phase commute with every
+// op that touches their bit only diagonally, so each may float inside its window (between the ops
+// before and after it that act on its bit non-diagonally).  Windows are covered greedily by as few
+// points as possible (sorted by window end); the ops sharing a point become one register diagonal
+// (CS_RDIAG: a[r] *= t[r], one complex product per affected register).  m ops on distinct bits then
+// cost 4 FP64 ops on (1 - 2^-m) of the amplitudes instead of 2m per amplitude.  The affected-register
+// mask is structure (kernel text), the table values (kernel parameters).
+void group_phase_diagonals(Program& prog, int first) {
+  const int n = int(prog.ops.size()) - first;
+  std::vector<int> cand, lo, hi;
+  std::vector<int> nd(static_cast<size_t>(n));
+  for (int i = 0; i < n; ++i) {
+    const FOp& o = prog.ops[size_t(first + i)];
+    const bool c = o.cs >= CS_PHASE1 && o.cs < CS_PHASE1 + 8 && o.pm == 0 && o.fk == 0;
+    nd[size_t(i)] = c ? 0 : nondiag_regs(o);
+    if (c) cand.push_back(i);
+  }
+  if (cand.size() < 2) return;
+  for (int i : cand) {
+    const int k = (prog.ops[size_t(first + i)].cs - CS_PHASE1) / 2;
+    int l = i - 1, h = i + 1;
+    while (l >= 0 && !((nd[size_t(l)] >> k) & 1)) --l;
+    while (h < n && !((nd[size_t(h)] >> k) & 1)) ++h;
+    lo.push_back(l);   // may be placed right before any op index p with l < p <= h (p = n: the end)
+    hi.push_back(h);
+  }
+  std::vector<int> order(cand.size()), point(cand.size(), -1);
+  for (size_t j = 0; j < cand.size(); ++j) order[j] = int(j);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return hi[size_t(x)] < hi[size_t(y)]; });
+  for (int j : order) {
+    if (point[size_t(j)] >= 0) continue;
+    const int p = hi[size_t(j)];
+    for (int q : order)
+      if (point[size_t(q)] < 0 && lo[size_t(q)] < p && p <= hi[size_t(q)]) point[size_t(q)] = p;
+  }
+  // rebuild the phase: every non-candidate op in order, each point's group inserted before op p
+  std::vector<FOp> out;
+  out.reserve(size_t(n));
+  std::vector<char> is_cand(size_t(n), 0);
+  for (int i : cand) is_cand[size_t(i)] = 1;
+  auto emit_group = [&](int p) {
+    std::vector<int> mem;
+    for (size_t j = 0; j < cand.size(); ++j)
+      if (point[j] == p) mem.push_back(cand[j]);
+    if (mem.empty()) return;
+    if (mem.size() == 1) {
+      out.push_back(prog.ops[size_t(first + mem[0])]);
+      return;
+    }
+    FOp g = prog.ops[size_t(first + mem[0])];
+    cplx tab[16];
+    for (int r = 0; r < 16; ++r) tab[r] = cplx(1.0, 0.0);
+    u64 aff = 0;   // structure only: a product that happens to be 1 still counts
+    for (int i : mem) {
+      const FOp& o = prog.ops[size_t(first + i)];
+      const int k = (o.cs - CS_PHASE1) / 2, v = (o.cs - CS_PHASE1) % 2;
+      for (int r = 0; r < 16; ++r)
+        if (((r >> k) & 1) == v) {
+          tab[r] *= cplx(o.c[0].x, o.c[0].y);
+          aff |= 1ull << r;
+        }
+    }
+    g.kind = FK_DIAGG;
+    g.cs = CS_RDIAG;
+    g.xm = aff;
+    g.tab = int(prog.coef.size());
+    for (int r = 0; r < 16; ++r) prog.coef.push_back(make_double2(tab[r].real(), tab[r].imag()));
+    out.push_back(g);
+  };
+  for (int i = 0; i <= n; ++i) {
+    emit_group(i);
+    if (i < n && !is_cand[size_t(i)]) out.push_back(prog.ops[size_t(first + i)]);
+  }
+  prog.ops.resize(size_t(first));
+  prog.ops.insert(prog.ops.end(), out.begin(), out.end());
+}
+
 // Emit the device ops of one phase.  Unconditional X on a register bit is not executed: it is
 // absorbed into a flip mask F (logical register index j lives in register j ^ F); later ops of
 // the phase are rewritten for F and the phase's store offsets apply it.  Thread-predicated X
@@ -212,6 +308,7 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
   int F = 0;   // uniform flips (applied here, on the host)
   int D = 0;   // register bits that may carry a per-thread flip (handled by the kernel)
   static const bool shear_on = !(getenv("SVB200_SHEAR") && std::string(getenv("SVB200_SHEAR")) == "0");
+  static const bool tan_on = !(getenv("SVB200_TAN") && std::string(getenv("SVB200_TAN")) == "0");
   const bool stable = jit_enabled();
   const int op_first = int(prog.ops.size());
   // A thread-predicated X is not an op of its own: it rides on the next op of the phase (the
@@ -441,6 +538,28 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
           sn = -sn;
           neg ^= 1;
         }
+        if (stable && tan_on) {
+          // scaled form (2 FMAs per real pair): R/c for |phi| <= pi/4, else R/s; the factor is
+          // owed to the state until absorb_pass_scale folds the pass's product into one op
+          bool cot = std::fabs(sn) > c;
+          // hysteresis: the form is structure (part of the generated kernel), so a re-plan of the
+          // same circuit with new angles keeps the previous plan's form while its coefficient stays
+          // within kTanBand (|phi| <= 68 deg as TAN, >= 22 deg as COT) -- no recompilation for
+          // small parameter updates; beyond the band the pass is recompiled once for the new form
+          const size_t idx = prog.tan_forms.size();
+          if (idx < prog.tan_hint.size()) {
+            const bool hc = prog.tan_hint[idx] != 0;
+            if (hc != cot && std::fabs(hc ? c / sn : sn / c) <= kTanBand) cot = hc;
+          }
+          prog.tan_forms.push_back(cot ? 1 : 0);
+          // RX type is symmetric under a per-thread flip; RY type on a flippable bit: CS_TAND
+          op.cs = (!rx && dyn) ? CS_TAND + op.k * 2 + (cot ? 1 : 0) : CS_TAN + op.k * 4 + (rx ? 1 : 0) + (cot ? 2 : 0);
+          op.c[0] = make_double2(cot ? c / sn : sn / c, cot ? sn : c);
+          op.c[1] = make_double2(c, 0.0);
+          op.c[2] = make_double2(sn, rx ? 1.0 : 0.0);
+          push_op(op);
+          continue;
+        }
         op.cs = CS_SHEAR + op.k * 4 + (rx ? SH_RX : (dyn ? SH_RYD : SH_RY));   // RX is symmetric under flips
         op.c[0] = make_double2(-sn / (1.0 + c), sn);
         op.c[1] = make_double2(c, 0.0);   // (c, s) kept for a later conversion back to the 2x2 form
@@ -468,6 +587,7 @@ int emit_ops(Program& prog, const std::vector<Prim>& prims, const std::vector<in
   }
   if (pend) prog.ops.push_back(pend_op);
   prog.owed_neg ^= neg;   // resolved once per program (absorb_rotation_signs)
+  if (stable) group_phase_diagonals(prog, op_first);
   return F;
 }
 
@@ -524,6 +644,94 @@ void absorb_rotation_signs(Program& prog, bool stable) {
     return;
   }
   if (sg < 0) sv_fail(SV_ERR_DEVICE, "internal: unabsorbed rotation sign");
+}
+
+// Form memory of the scaled rotations, per circuit structure (see emit_ops): the last plan's
+// TAN/COT choice of every scaled rotation, in emission order.
+std::mutex g_tan_mu;
+std::map<u64, std::vector<uint8_t>> g_tan_forms;
+
+u64 structure_key(int nl, const std::vector<Prim>& prims, bool remap, bool pin_top) {
+  u64 h = 1469598103934665603ull;
+  auto mix = [&](u64 v) {
+    h ^= v;
+    h *= 1099511628211ull;
+  };
+  mix(u64(nl) | (u64(remap) << 8) | (u64(pin_top) << 9));
+  for (const Prim& p : prims) {
+    mix(u64(p.type) | (u64(p.nb) << 8) | (u64(p.m.size()) << 16));
+    mix(p.fmask);
+    mix(p.fval);
+    mix(p.xmask);
+    for (int t = 0; t < p.nb; ++t) mix(u64(p.pos[t]));
+  }
+  return h;
+}
+
+// Scaled rotations (CS_TAN) apply R/f with f = cos(phi) or sin(phi): after them the stored state
+// is the true one divided by the product of their factors.  The pass restores it before its store:
+// the product S is multiplied into one unconditioned op of the pass that takes any coefficient
+// (a SCALAR or a non-X PAIR1 on every amplitude), or else the pass's last scaled rotation goes back
+// to the full 2x2 form carrying S.  The choice depends only on op kinds (structure), never on
+// values, so generated kernels stay keyed on structure.  A bra-ket op in between sees psi and
+// lambda both scaled by the running factor r: its result is corrected by 1 / r^2 on the host
+// (Program::gen_scale).  Factors are >= 1/sqrt(2) each, so S stays far from underflow within a
+// pass.
+void absorb_pass_scale(Program& prog, const FPassArgs& A) {
+  auto is_tan = [](const FOp& o) { return o.cs >= CS_TAN && o.cs < CS_TAND + 8; };
+  double S = 1.0;
+  int last = -1, absorber = -1;
+  for (int oi = A.op_begin; oi < A.op_end; ++oi) {
+    const FOp& o = prog.ops[oi];
+    if (is_tan(o)) {
+      S *= o.c[0].y;
+      last = oi;
+    } else if (absorber < 0 && o.pm == 0 && o.cs < CS_GEN1) {
+      const bool p1 = (o.cs >= CS_PAIR1 && o.cs < CS_PAIR1 + 16) || (o.cs >= CS_PAIR1D && o.cs < CS_PAIR1D + 16);
+      if (o.cs == CS_SCALAR || (p1 && o.mtype != MT_X && (o.cs % 4) != 3)) absorber = oi;
+    }
+  }
+  if (last < 0) return;
+  double Sx = 1.0;   // product of the factors of every scaled rotation but the last (no division)
+  for (int oi = A.op_begin; oi < A.op_end; ++oi)
+    if (oi != last && is_tan(prog.ops[oi])) Sx *= prog.ops[oi].c[0].y;
+  const bool convert = absorber < 0;
+  if (convert) {
+    // the last scaled rotation becomes the full rotation times the other rotations' factors
+    FOp& o = prog.ops[last];
+    const double c = o.c[1].x, sn = o.c[2].x;
+    const bool rx = o.c[2].y != 0.0;
+    const bool dyn = o.cs >= CS_TAND;
+    const int k = dyn ? (o.cs - CS_TAND) / 2 : (o.cs - CS_TAN) / 4;
+    std::array<cplx, 4> mm;
+    if (rx) mm = {cplx(c, 0), cplx(0, -sn), cplx(0, -sn), cplx(c, 0)};
+    else mm = {cplx(c, 0), cplx(-sn, 0), cplx(sn, 0), cplx(c, 0)};
+    o.tab = int(prog.coef.size());
+    for (int j = 0; j < 4; ++j) {
+      prog.coef.push_back(make_double2(Sx * mm[j].real(), Sx * mm[j].imag()));
+      o.c[j] = prog.coef.back();
+    }
+    o.mtype = uint8_t(rx ? MT_RXLIKE : MT_REAL);
+    o.kind = FK_PAIR1;
+    o.cs = (dyn ? CS_PAIR1D : CS_PAIR1) + k * 4 + o.mtype;
+    absorber = last;
+  } else {
+    FOp& o = prog.ops[absorber];
+    const int nc = o.cs == CS_SCALAR ? 1 : 4;
+    for (int j = 0; j < nc; ++j) {
+      o.c[j] = make_double2(S * o.c[j].x, S * o.c[j].y);
+      prog.coef[o.tab + j] = o.c[j];
+    }
+  }
+  // running factor of the stored state at each bra-ket
+  if (prog.gen_scale.size() < prog.gen_slot_of.size()) prog.gen_scale.resize(prog.gen_slot_of.size(), 1.0);
+  double r = 1.0;
+  for (int oi = A.op_begin; oi < A.op_end; ++oi) {
+    const FOp& o = prog.ops[oi];
+    if (is_tan(o)) r /= o.c[0].y;
+    else if (oi == absorber) r *= convert ? Sx : S;
+    else if (o.cs >= CS_GEN1) prog.gen_scale[size_t(A.gen_base + o.slot)] = 1.0 / (r * r);
+  }
 }
 
 // Can prim i be folded into prim j (j runs right before i on every bit i touches)?
@@ -662,6 +870,12 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
   Program prog;
   std::vector<Prim> P = prims_in;
   prog.n_prims_in = int64_t(P.size());
+  const u64 skey = structure_key(nl, prims_in, remap, pin_top);
+  {
+    std::lock_guard<std::mutex> lk(g_tan_mu);
+    auto it = g_tan_forms.find(skey);
+    if (it != g_tan_forms.end()) prog.tan_hint = it->second;
+  }
   const int b = std::min(tile_bits(), nl);
   const int LB = std::min(low_bits(), nl);   // physical bits the direct store's 8-lane groups cover
   const int LBT = std::max(LB, std::min(tile_low_bits(), b - 3));   // physical bits every tile contains
@@ -811,6 +1025,7 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
                                   (o.kind == FK_PAIRG && o.mtype == MT_GENERAL))) ||
               (o.cs >= CS_GEN2 && o.cs < CS_GEND);
     }
+    absorb_pass_scale(prog, A);
     // ---- in-tile relabeling: bring the qubits the next gates target onto physical bits 0..2 ----
     int sigma[64];
     for (int p = 0; p < 64; ++p) sigma[p] = p;
@@ -942,7 +1157,13 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
   }
   prog.perm = perm_total;
   for (auto& A : prog.passes) A.n_gen_total = int(prog.gen_slot_of.size());
+  prog.gen_scale.resize(prog.gen_slot_of.size(), 1.0);
   absorb_rotation_signs(prog, jit_enabled());
+  if (!prog.tan_forms.empty()) {
+    std::lock_guard<std::mutex> lk(g_tan_mu);
+    if (g_tan_forms.size() > 4096) g_tan_forms.clear();
+    g_tan_forms[skey] = prog.tan_forms;
+  }
   return prog;
 }
 
@@ -1055,6 +1276,8 @@ double program_fp64_flops_per_amp(const fused::Program& prog) {
   for (const FOp& o : prog.ops) {
     const int cs = o.cs;
     if (cs >= CS_SHEAR && cs < CS_SHEAR + 16) f += 8 * 6 * 2;
+    else if (cs >= CS_TAN && cs < CS_TAND + 8) f += 8 * 4 * 2;
+    else if (cs == CS_RDIAG) f += 6.0 * __builtin_popcountll(o.xm);
     else if ((cs >= CS_PAIR1 && cs < CS_PAIR1 + 16) || (cs >= CS_PAIR1D && cs < CS_PAIR1D + 16))
       f += o.mtype == MT_GENERAL ? 8 * 28 : (o.mtype == MT_X ? 0 : 8 * 12);
     else if ((cs >= CS_PHASE1 && cs < CS_PHASE1 + 8) || (cs >= CS_PHASE1D && cs < CS_PHASE1D + 8)) f += 8 * 6;

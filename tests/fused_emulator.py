@@ -19,6 +19,9 @@ CS_PAIR1, CS_PHASE1, CS_SCALAR, CS_PAIRGR, CS_PAIRG = 0, 16, 24, 25, 40
 CS_DIAGG, CS_DENSE2, CS_XFLIP, CS_PAIR1D, CS_PHASE1D = 55, 56, 62, 66, 82
 CS_SHEAR = 90   # + k*4 + {0: RY-type, 1: RX-type, 2: RY-type on a flipped bit}
 CS_PARITY = 106  # + register mask M
+CS_TAN = 122     # + k*4 + {0: RY TAN, 1: RX TAN, 2: RY COT, 3: RX COT}: R/cos or R/sin, 2 FMAs per real pair
+CS_TAND = 138    # + k*2 + {0: TAN, 1: COT}: RY type on a per-thread flippable bit (flipped: R(-phi))
+CS_RDIAG = 146   # a[r] *= coef[tab + r] for the registers r in the mask xm (grouped PHASE1 ops)
 KRB = 4
 KMAXB = 12
 
@@ -208,6 +211,31 @@ def _apply(a, op, pred, fthr, phys_base, coef):
                 n0, n1 = r0 + 1j * i0, r1 + 1j * i1
             a[..., r] = np.where(pred, n0, x0)
             a[..., r | (1 << k)] = np.where(pred, n1, x1)
+    elif CS_TAN <= cs < CS_TAND + 8:
+        if cs >= CS_TAND:
+            k, kind = (cs - CS_TAND) // 2, 2 * ((cs - CS_TAND) % 2)
+            neg = ((fthr >> k) & 1).astype(bool)
+        else:
+            k, kind = (cs - CS_TAN) // 4, (cs - CS_TAN) % 4
+            neg = np.zeros_like(pred, dtype=bool)
+        t = c[0].real
+        # flipped roles = R(-phi): TAN negates t; COT negates the +-1 terms (R(-phi) = s[[k, 1], [-1, k]])
+        tt = np.where(neg, -t, t) if kind == 0 else t
+        one = np.where(neg, -1.0, 1.0)
+        for r in range(16):
+            if (r >> k) & 1:
+                continue
+            x0, x1 = a[..., r].copy(), a[..., r | (1 << k)].copy()
+            if kind == 0:     # x0 - t x1, x1 + t x0
+                n0, n1 = x0 - tt * x1, x1 + tt * x0
+            elif kind == 1:   # x0 - i t x1, x1 - i t x0
+                n0, n1 = x0 - 1j * t * x1, x1 - 1j * t * x0
+            elif kind == 2:   # t x0 - x1, t x1 + x0
+                n0, n1 = t * x0 - one * x1, t * x1 + one * x0
+            else:             # t x0 - i x1, t x1 - i x0
+                n0, n1 = t * x0 - 1j * x1, t * x1 - 1j * x0
+            a[..., r] = np.where(pred, n0, x0)
+            a[..., r | (1 << k)] = np.where(pred, n1, x1)
     elif CS_PARITY <= cs < CS_PARITY + 16:
         M = cs - CS_PARITY
         popc = np.vectorize(lambda x: bin(int(x)).count("1"))
@@ -221,6 +249,10 @@ def _apply(a, op, pred, fthr, phys_base, coef):
         for r in range(16):
             hit = pred & (((r >> k) & 1) == v)
             a[..., r] = np.where(hit, c[0] * a[..., r], a[..., r])
+    elif cs == CS_RDIAG:
+        for r in range(16):
+            if (op["xm"] >> r) & 1:
+                a[..., r] = np.where(pred, coef[op["tab"] + r] * a[..., r], a[..., r])
     elif cs == CS_SCALAR:
         for r in range(16):
             a[..., r] = np.where(pred, c[0] * a[..., r], a[..., r])

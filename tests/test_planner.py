@@ -79,7 +79,7 @@ def test_structured_workloads_program():
 
 def test_parity_and_shear_cases_are_exercised():
     """IsingZZ becomes a parity phase (register mask + per-thread parity), unconditioned
-    rotations become shears -- both re-executed against the oracle."""
+    rotations become scaled 2-FMA rotations -- both re-executed against the oracle."""
     rng = np.random.default_rng(11)
     n = 14
     ops = [Op("H", (q,)) for q in range(n)]
@@ -92,7 +92,7 @@ def test_parity_and_shear_cases_are_exercised():
     prog = check(n, ops)
     cases = [op["cs"] for op in prog["ops"]]
     assert any(106 <= c < 122 for c in cases), "IsingZZ should plan to CS_PARITY"
-    assert any(90 <= c < 106 for c in cases), "rotations should plan to CS_SHEAR"
+    assert any(122 <= c < 146 for c in cases), "rotations should plan to the scaled CS_TAN / CS_TAND forms"
     assert any(106 <= op["cs"] < 122 and op["xm"] for op in prog["ops"]), "some parity bits off the registers"
 
 
@@ -104,3 +104,21 @@ def test_wide_diagonal_matrix_program():
     m = np.diag(np.exp(1j * rng.uniform(0, 2 * np.pi, 128)))
     ops = [Op("H", (q,)) for q in range(n)] + [Op("Matrix", (12, 0, 4, 6, 2, 7, 1), matrix=m), Op("RX", (3,), (0.3,))]
     check(n, ops)
+
+
+def test_scaled_rotations_tan_and_cot():
+    """Unconditioned rotations plan to the scaled 2-FMA form (CS_TAN: R/cos for |phi| <= pi/4, R/sin
+    beyond), the pass's product of dropped factors is absorbed into one op of the pass, and the
+    program still reproduces the oracle (fused_plan.cpp absorb_pass_scale)."""
+    n = 13
+    prog = check(n, workloads.random_circuit(n, 20, seed=5))
+    tans = [op["cs"] for op in prog["ops"] if 122 <= op["cs"] < 138]
+    assert any((c - 122) % 4 < 2 for c in tans), "TAN form"
+    assert any((c - 122) % 4 >= 2 for c in tans), "COT form"
+    # RY on a bit a thread-predicated X may flip: CS_TAND (flipped threads apply R(-phi))
+    prog = check(n, workloads.random_circuit(n, 30, seed=0), seed=1)
+    assert any(138 <= op["cs"] < 146 for op in prog["ops"]), "TAND form"
+    # near-pi rotations (RX(pi) = -iX-like): COT with kappa ~ 0, and exact multiples of pi/2
+    ops = [Op("RX", (q,), (np.pi - 1e-9 * q,)) for q in range(n)] + \
+          [Op("RY", (q,), (np.pi / 2,)) for q in range(n)] + workloads.random_circuit(n, 4, seed=1)
+    check(n, ops, seed=2)
