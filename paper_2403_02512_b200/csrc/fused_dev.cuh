@@ -366,7 +366,11 @@ struct DPass {
 //   third half buffer rotates with the low one: the next tile's low half streams in during the
 //   whole of this tile's phases, its high half during the last phase (3 half tiles = 96 KiB per
 //   CTA, two CTAs per SM).
-template <bool TWO, bool DB, bool DIRECT, class Body, bool SPLIT = false>
+//   DFL (with DIRECT): no staged load at all -- the first phase reads its registers straight from
+//   global memory (L2 hits: every tile's 128-byte lines were prefetched into L2 with
+//   cp.async.bulk.prefetch while the CTA's previous tile was computed), saving the tile's
+//   shared-memory write and first read; next_load() then issues the following tile's L2 prefetch.
+template <bool TWO, bool DB, bool DIRECT, class Body, bool SPLIT = false, bool DFL = false>
 __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* __restrict__ state_hi, const DPass& P,
                                          const DPhase* __restrict__ phases, double2* __restrict__ gen_partials,
                                          Body body) {
@@ -429,7 +433,32 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     asm volatile("cp.async.commit_group;\n" ::);
   };
   int cur = 0;
-  if (SPLIT) {
+  if (DFL) {
+    // L2 prefetch of a tile: its 2^(b-3) 128-byte lines, two per thread (thread group tid >> 3
+    // covers the lines of load slots tid & 7 and (tid & 7) + 8, as issue_load would read them)
+    auto prefetch_tile = [&](u64 b0) {
+      double2 *p_lo, *p_hi;
+      slot_ptrs(b0 | (ld_tid & ~7ull), p_lo, p_hi);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int i = (tid & 7) + 8 * h;
+        const double2* src = (TWO && ((P.ld_hsel >> i) & 1) ? p_hi : p_lo) + P.ld_off[i];
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], 128;\n" ::"l"(src) : "memory");
+      }
+    };
+    for (u64 t = blockIdx.x; t < P.n_tiles; t += gridDim.x) {
+      const u64 nbase = ((base | ~P.outer) + P.grid_step) & P.outer;
+      if (t == blockIdx.x) {
+        __syncthreads();   // phase records and generator accumulators staged
+        prefetch_tile(base);
+      }
+      const bool more = t + gridDim.x < P.n_tiles;
+      body(tile, tile + (T >> 1), s_ph, base, acc_warp, [&]() {
+        if (more) prefetch_tile(nbase);
+      });
+      base = nbase;
+    }
+  } else if (SPLIT) {
     const int HB = T >> 1;
     auto issue_half = [&](u64 b0, double2* buf, int h) {
       double2 *p_lo, *p_hi;
@@ -804,6 +833,20 @@ __device__ __forceinline__ void run_pass_pp(double2* __restrict__ state, double2
       FDEV_STG(gp + ((((r & 1) ? (O0) : 0ull) | ((r & 2) ? (O1) : 0ull) | ((r & 4) ? (O2) : 0ull) |              \
                      ((r & 8) ? (O3) : 0ull)) ^ wf), a[r]);                                                     \
   }
+
+// first phase of a DFL pass: registers straight from global memory (L2-resident after the
+// prefetch), a[r] = state[pb | OFF(r)]; s0 is still the thread's shared-memory slot for the store
+#define FDEV_PHASE_LOAD_G(S0, PB, O0, O1, O2, O3)                                                                \
+  const int s0 = (S0);                                                                                         \
+  const u64 pb = base | (PB);                                                                                   \
+  double2 a[fdev::kRegs];                                                                                       \
+  _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r) {                                                     \
+    const u64 g_ = pb | (((r & 1) ? (O0) : 0ull) | ((r & 2) ? (O1) : 0ull) | ((r & 4) ? (O2) : 0ull) |         \
+                         ((r & 8) ? (O3) : 0ull));                                                              \
+    a[r] = __ldcg(((g_ & P.hi) ? state_hi : state) + (g_ & ~P.hi));                                             \
+  }                                                                                                             \
+  int fthr = 0;                                                                                                 \
+  (void)fthr;
 
 // ... two-array state (adjoint sweep): indices carrying the selector bit P.hi live in state_hi
 #define FDEV_PHASE_STORE_GLOBAL2(FLIP, O0, O1, O2, O3)                                                           \

@@ -499,6 +499,9 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
   const bool split = split_on && direct && jit_ctas_per_sm() <= 2 && !jit_pp();
   // ping-pong tile loop (fused_dev.cuh run_pass_pp): direct passes on full 12-bit tiles
   const bool pp = jit_pp() && direct && A.b == kMaxB && A.nthr == kMaxB - kRB;
+  // first phase straight from global memory after an L2 prefetch (fused_dev.cuh run_pass DFL)
+  static const bool dfl_on = getenv("SVB200_JIT_DFL") && std::string(getenv("SVB200_JIT_DFL")) == "1";
+  const bool dfl = dfl_on && direct && !pp && !split;
   if (getenv("SVB200_JIT_EXP_NOSMEM") && std::string(getenv("SVB200_JIT_EXP_NOSMEM")) == "1") o << "  double2 ap_[16];\n";
   if (direct) {
     // the thread's physical store bits in the last phase (its lane bits land on physical 0..2)
@@ -525,7 +528,11 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
         pe += " | (" + bit + " ? " + hex64(1ull << A.tpos[F.thr[j]]) + " : 0ull)";
       }
       static const bool exp_nosmem = getenv("SVB200_JIT_EXP_NOSMEM") && std::string(getenv("SVB200_JIT_EXP_NOSMEM")) == "1";
-      if (exp_nosmem && ph > 0) {   // timing experiment only (wrong results): no smem round trip between phases
+      if (dfl && ph == 0) {
+        o << "    FDEV_PHASE_LOAD_G(" << se << ", " << pe;
+        for (int k = 0; k < 4; ++k) o << ", " << hex64(1ull << A.tpos[F.reg[k]]);
+        o << ")\n    next_load();\n";
+      } else if (exp_nosmem && ph > 0) {   // timing experiment only (wrong results): no smem round trip between phases
         o << "    const int s0 = (" << se << "); const u64 pb = base | (" << pe << "); double2 a[16];\n";
         o << "    _Pragma(\"unroll\") for (int r = 0; r < 16; ++r) a[r] = ap_[r];\n    int fthr = 0; (void)pb; (void)s0; (void)fthr;\n";
       } else {
@@ -534,7 +541,8 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
       }
     }
     if (pp) o << "    FDEV_STEP_I(" << 2 * ph << ");\n";   // end of segment T_ph
-    if (last_direct) o << (pp ? "    next_load();\n" : "    __syncthreads();\n    next_load();\n");
+    // DFL: the barrier still separates this phase's reads from the next tile's first store
+    if (last_direct) o << (pp ? "    next_load();\n" : (dfl ? "    __syncthreads();\n" : "    __syncthreads();\n    next_load();\n"));
     auto parity_tab_of = [&](const FOp& op) {
       bool ptab = false;
       if (op.cs >= CS_GEND && op.cs < CS_GEND + 4 && op.nt >= 1) {
@@ -682,8 +690,8 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
     k << o.str();
     k << "  };\n";
     k << "  fdev::run_pass<" << (two ? "true" : "false") << ", " << (db ? "true" : "false") << ", "
-      << (direct ? "true" : "false") << ", decltype(body), " << (split ? "true" : "false")
-      << ">(state, state_hi, P, phases, gen_partials, body);\n}\n";
+      << (direct ? "true" : "false") << ", decltype(body), " << (split ? "true" : "false") << ", "
+      << (dfl ? "true" : "false") << ">(state, state_hi, P, phases, gen_partials, body);\n}\n";
   }
 
   if (cf_refs) *cf_refs = g.cf_refs;
