@@ -388,10 +388,11 @@ def main():
                             "flops_per_amplitude": fpa,
                             "peak_source": fp_src}
         roofline["note"] = ("svb200_pass (generated per-pass kernels) makes one HBM read+write per pass and runs many "
-                            "gates per pass (34 passes for 2225 gates): its time is FP64 arithmetic (89 % of the pipe "
-                            "alone), the tile stream (75 % of HBM alone) and shared-memory phase round trips, which "
-                            "only partly overlap -- profiles/r2_pass_time_decomposition.md; the HBM frac is the "
-                            "lesser figure, see roofline.fp64 (DMUL counted as 1 flop, so the pipe is busier than it)")
+                            "gates per pass (34 passes for 2225 gates).  With 2-FMA scaled rotations its FP64 floor "
+                            "(flops_per_amplitude at the measured DFMA rate) is below the HBM floor of its passes; "
+                            "what bounds it is the shared-memory phase round trips (~52 % of the LSU data pipe) and "
+                            "their barriers overlapping the arithmetic and the tile stream, at sw_power_cap clocks "
+                            "-- profiles/r2_ncu_jit_pass_tan.md, DESIGN.md 5.3")
 
     # global-qubit swaps (rank-0 view): NCCL send/recv of half a shard per swap over NVLink
     comm = None

@@ -810,6 +810,18 @@ __device__ __forceinline__ void run_pass_pp(double2* __restrict__ state, double2
   }                                                                                                             \
   __syncwarp();
 
+// ... when the next phase keeps the top one / two thread bits: each 128-thread half / 64-thread
+// quarter of the CTA holds the same amplitudes in both phases, so only that group synchronises
+// (named barriers 1-2 for halves, 3-6 for quarters; fused_plan.cpp build_program `fixed`)
+#define FDEV_PHASE_STORE_GROUP(FLIP, W0, W1, W2, W3, BAR_ID, BAR_N)                                                   \
+  {                                                                                                             \
+    const int fl = (FLIP) ^ fthr;                                                                               \
+    const int sf = s0 ^ ((fl & 1) ? (W0) : 0) ^ ((fl & 2) ? (W1) : 0) ^ ((fl & 4) ? (W2) : 0) ^ ((fl & 8) ? (W3) : 0); \
+    _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r)                                                     \
+      FDEV_TILE(sf ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)) = a[r]; \
+  }                                                                                                             \
+  asm volatile("barrier.sync %0, %1;\n" ::"r"(BAR_ID), "r"(BAR_N) : "memory");
+
 #ifdef FDEV_PLAIN_STORE
 #define FDEV_STG(p, v) (*(p) = (v))
 #elif defined(FDEV_EXP_NOMEM)

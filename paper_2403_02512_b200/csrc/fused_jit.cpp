@@ -572,7 +572,17 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
           const FPhase& N = prog.phases[A.phase_begin + ph + 1];
           for (int j = 5; j < A.nthr; ++j) warp_local = warp_local && N.thr[j] == F.thr[j];
         }
+        // top thread bits kept by the next phase: 1 -> each 128-thread half, 2 -> each 64-thread
+        // quarter of the CTA exchanges only within itself (named barrier over the group)
+        int kept = 0;
+        if (!warp_local && !pp && ph + 1 < A.n_phases && A.nthr == kMaxB - kRB) {
+          const FPhase& N = prog.phases[A.phase_begin + ph + 1];
+          while (kept < 2 && N.thr[A.nthr - 1 - kept] == F.thr[A.nthr - 1 - kept]) ++kept;
+        }
         if (exp_nosmem) o << "    _Pragma(\"unroll\") for (int r = 0; r < 16; ++r) ap_[r] = a[r];\n";
+        else if (kept > 0)
+          o << "    FDEV_PHASE_STORE_GROUP(" << int(F.flip) << ", " << W[0] << ", " << W[1] << ", " << W[2] << ", " << W[3]
+            << ", " << (kept == 1 ? "1 + (threadIdx.x >> 7), 128" : "3 + (threadIdx.x >> 6), 64") << ")\n";
         else o << "    FDEV_PHASE_STORE" << (warp_local ? "_WARP(" : "(") << int(F.flip) << ", " << W[0] << ", " << W[1] << ", "
                << W[2] << ", " << W[3] << ")\n";
       }

@@ -1048,6 +1048,20 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
     // changes qualify once predicates must stay off the lanes, and the run measured 0.43 s vs 0.41 s
     static const bool warp_local = getenv("SVB200_WARP_LOCAL") && std::string(getenv("SVB200_WARP_LOCAL")) == "1";
     std::vector<int> W;   // warp-bit positions of the current epoch
+    // Group-local phase changes: tile positions no phase of the pass needs as a register stay on the
+    // top thread bits for the whole pass (at most two, highest first), so each 128-thread half (one
+    // fixed bit) or 64-thread quarter (two) of the CTA holds the same amplitudes in every phase and
+    // its round trips synchronise only that group (named barrier, fused_jit.cpp) -- the groups
+    // drift apart and one group's round trip overlaps the others' arithmetic.
+    std::vector<int> fixed;
+    static const bool group_on = !(getenv("SVB200_GROUP_BAR") && std::string(getenv("SVB200_GROUP_BAR")) == "0");
+    if (group_on && b == kMaxB && !warp_local) {
+      u64 used = 0;
+      for (u64 d : dense_tile) used |= d;
+      for (int p = b - 1; p >= 3 && fixed.size() < 2; --p)
+        if (!((used >> p) & 1)) fixed.push_back(p);
+      std::reverse(fixed.begin(), fixed.end());   // make_phase_thr puts them last, in this order
+    }
     for (size_t k = 0; k < sched.size(); ++k) {
       const auto& ph = sched[k];
       std::vector<int> R;
@@ -1080,6 +1094,32 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
         for (int p : W)
           if (std::find(R.begin(), R.end(), p) != R.end()) W.clear();
         if (!W.empty() && !lanes_ok(R, W, b)) W.clear();
+      } else if (!fixed.empty()) {
+        std::vector<int> Rf = R;
+        fill_regs(Rf, b, fixed);
+        bool ok = lanes_ok(Rf, fixed, b);
+        for (int p : fixed) ok = ok && std::find(Rf.begin(), Rf.end(), p) == Rf.end();
+        if (ok) {
+          // keep the group bits only if no predicate position is pushed onto a lane by them
+          FPhase A0, A1;
+          std::vector<int> R0 = R;
+          fill_regs(R0, b);
+          make_phase_thr(A0, R0, b, use);
+          make_phase_thr(A1, Rf, b, use, fixed);
+          int u0 = 0, u1 = 0;
+          for (int j = 0; j < 5; ++j) {
+            u0 += use[A0.thr[j]] ? 1 : 0;
+            u1 += use[A1.thr[j]] ? 1 : 0;
+          }
+          ok = u1 <= u0;
+        }
+        if (ok) {
+          R = Rf;
+          W = fixed;
+        } else {
+          fill_regs(R, b);
+          W.clear();
+        }
       } else {
         fill_regs(R, b);
       }
