@@ -81,6 +81,15 @@ void ensure_results(sv_handle* h, size_t doubles) {
 // (default 600) -- or as soon as NCCL reports an asynchronous error -- the communicator is
 // aborted (ncclCommAbort, which also tears down the waiting kernels) and the call fails with a
 // device error instead of hanging every rank.
+void host_prof_mark(const char* what) {
+  static const bool on = getenv("SVB200_HOST_PROF") && std::string(getenv("SVB200_HOST_PROF")) == "1";
+  if (!on) return;
+  static auto last = std::chrono::steady_clock::now();
+  const auto now = std::chrono::steady_clock::now();
+  std::fprintf(stderr, "[host_prof] %-28s +%.3f ms\n", what, std::chrono::duration<double, std::milli>(now - last).count());
+  last = now;
+}
+
 void stream_sync(sv_handle* h) {
   if (!h->comm) {
     CUDA_CHECK(cudaStreamSynchronize(h->stream));
@@ -610,6 +619,7 @@ static void free_aux(sv_handle* h) {
 static double adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const sv_obs& obs, int ncols, double2* lam,
                                 double* jac_row) {
   apply_observable(h, obs, h->state, lam, {h->state, lam});                      // lambda = O psi
+  host_prof_mark("row: lambda enqueued");
   // reverse sweep on LOGICAL bit offsets; generators become bra-kets whose psi/lambda selector
   // (xmask) is set per batch to the top bit of the two-array state
   std::vector<Prim> prims;
@@ -654,7 +664,9 @@ static double adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const
   }
   // im[0..ncols) = Im<lambda_k|G_k|psi_k> (this rank's part), im[ncols] = Re<psi|lambda> = <O>
   std::vector<double> im(ncols + 1, 0.0);
+  host_prof_mark("row: prims built");
   im[ncols] = reduce_dot_re(h, h->state, lam);
+  host_prof_mark("row: <psi|lambda> (synced)");
   const std::vector<double2*> both = {h->state, lam};
   schedule_sharded(h, both, prims, [&](std::vector<Prim>& batch) {
     const int top = h->nl;
@@ -681,7 +693,9 @@ static double adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const
     for (auto& g : gens) im[g.first] += g.second.imag();
     batch.clear();
   });
+  host_prof_mark("row: sweep returned");
   stream_sync(h);
+  host_prof_mark("row: synced");
   dist_allreduce_sum(h, im.data(), im.size());
   for (int c = 0; c < ncols; ++c) jac_row[c] = -2.0 * prefactor[c] * im[c];
   return im[ncols];
@@ -710,7 +724,9 @@ static bool adjoint_fused(sv_handle* h, const sv_op* ops, int n_ops, const sv_ob
   if (!h->adj_lam) CUDA_CHECK(cudaMalloc(&h->adj_lam, half));
   if (need > 1 && !h->adj_saved) CUDA_CHECK(cudaMalloc(&h->adj_saved, half));
 
+  host_prof_mark("adjoint: start");
   run_ops(h, {h->state}, ops, n_ops, 1);                       // forward pass (once)
+  host_prof_mark("adjoint: forward enqueued");
   std::vector<double> ev(n_obs);
   double2* buf = h->adj_lam;   // lambda
   double2* saved = h->adj_saved;

@@ -637,7 +637,9 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
   // would then leave the ranks with different layouts and the next swap would exchange
   // mismatched halves.  Every rank must keep the same layout: no relabeling when world > 1.
   const bool remap = remap_env && h->world == 1 && allow_remap;
+  host_prof_mark("fused: enter");
   const std::shared_ptr<Program> prog_ptr = cached_program(h, prims, remap, state_hi != nullptr);
+  host_prof_mark("fused: program ready");
   Program& prog = *prog_ptr;
   if (state_hi)
     for (auto& A : prog.passes) A.hi_mask = 1ull << (h->nl - 1);
@@ -698,7 +700,9 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
   }
   std::memcpy(host.data() + align(b_ph) + align(b_op), prog.coef.data(), b_cf);
   if (b_jt) std::memcpy(host.data() + align(b_ph) + align(b_op) + align(b_cf), prog.jit_tabs.data(), b_jt);
+  host_prof_mark("fused: records built");
   stream_sync(h);   // previous program may still be in use
+  host_prof_mark("fused: prev program synced");
   char* dbuf = (char*)program_buffer(h, total);
   CUDA_CHECK(cudaMemcpyAsync(dbuf, host.data(), total, cudaMemcpyHostToDevice, h->stream));
   const DPhase* d_ph = (const DPhase*)dbuf;
@@ -759,6 +763,7 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
       CUDA_CHECK(cudaGetLastError());
     }
   }
+  host_prof_mark("fused: launched");
   if (n_gen) {
     // fixed-order reduction over the persistent CTAs -> one complex per program slot
     ensure_results(h, size_t(2) * n_gen);

@@ -12,6 +12,10 @@
 
 #include "../../include/svb200.h"
 
+// SVB200_HOST_PROF=1: host-side timeline of the adjoint / fused-program paths on stderr
+// (diagnostics: wall time since the previous mark, and whether the stream was idle)
+void host_prof_mark(const char* what);
+
 typedef unsigned long long u64;
 using cplx = std::complex<double>;
 
