@@ -13,6 +13,7 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstring>
+#include <iterator>
 #include <map>
 #include <mutex>
 #include <string>
@@ -1030,7 +1031,20 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
     A.n_tiles = 1ull << (nl - b);
     A.phase_begin = int(prog.phases.size());
     A.gen_base = int(prog.gen_slot_of.size());
-    const auto sched = schedule_phases(P, take, prog.n_prims_merged);
+    auto sched = schedule_phases(P, take, prog.n_prims_merged);
+    // Tail deferral: a last phase holding only a few ops costs a whole shared-memory round trip
+    // (and often the op-free store phase after it); when more passes follow anyway, its ops move to
+    // the next pass, whose first phases usually hold their bits.  Nothing left in this pass depends
+    // on them (they were scheduled last), and ops merged into them stay merged.
+    static const int defer_k = getenv("SVB200_DEFER_TAIL") ? atoi(getenv("SVB200_DEFER_TAIL")) : 3;
+    if (defer_k > 0 && sched.size() >= 2 && !rest.empty() && int(sched.back().second.size()) <= defer_k) {
+      std::vector<int> back = sched.back().second;
+      sched.pop_back();
+      std::sort(back.begin(), back.end());
+      std::vector<int> merged;
+      std::merge(rest.begin(), rest.end(), back.begin(), back.end(), std::back_inserter(merged));
+      rest.swap(merged);
+    }
     std::vector<u64> dense_tile(sched.size(), 0);   // register (dense) tile positions per phase
     std::vector<u64> pred_tile(sched.size(), 0);    // tile positions its ops test per thread
     for (size_t k = 0; k < sched.size(); ++k) {
