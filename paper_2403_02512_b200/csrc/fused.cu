@@ -552,7 +552,7 @@ std::shared_ptr<Program> cached_program(sv_handle* h, const std::vector<Prim>& p
   }
   auto prog = std::make_shared<Program>(build_program(h->nl, prims, remap, pin));
   lst->insert(lst->begin(), {PlanKey{h->nl, remap, pin, prims}, prog});
-  if (lst->size() > 4) lst->pop_back();
+  if (lst->size() > 16) lst->pop_back();   // a sharded circuit runs one program per exchange-free batch
   return prog;
 }
 

@@ -945,16 +945,13 @@ std::vector<std::pair<u64, std::vector<int>>> schedule_phases(std::vector<Prim>&
 
 }  // namespace
 
-Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, bool pin_top) {
+// One planning run with tail-deferral threshold defer_k (0: off) and the scaled-rotation form hints.
+Program build_program_k(int nl, const std::vector<Prim>& prims_in, bool remap, bool pin_top, int defer_k,
+                        const std::vector<uint8_t>& hint) {
   Program prog;
   std::vector<Prim> P = prims_in;
   prog.n_prims_in = int64_t(P.size());
-  const u64 skey = structure_key(nl, prims_in, remap, pin_top);
-  {
-    std::lock_guard<std::mutex> lk(g_tan_mu);
-    auto it = g_tan_forms.find(skey);
-    if (it != g_tan_forms.end()) prog.tan_hint = it->second;
-  }
+  prog.tan_hint = hint;
   const int b = std::min(tile_bits(), nl);
   const int LB = std::min(low_bits(), nl);   // physical bits the direct store's 8-lane groups cover
   const int LBT = std::max(LB, std::min(tile_low_bits(), b - 3));   // physical bits every tile contains
@@ -1036,14 +1033,15 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
     // (and often the op-free store phase after it); when more passes follow anyway, its ops move to
     // the next pass, whose first phases usually hold their bits.  Nothing left in this pass depends
     // on them (they were scheduled last), and ops merged into them stay merged.
-    static const int defer_k = getenv("SVB200_DEFER_TAIL") ? atoi(getenv("SVB200_DEFER_TAIL")) : 3;
-    if (defer_k > 0 && sched.size() >= 2 && !rest.empty() && int(sched.back().second.size()) <= defer_k) {
+    static const bool defer_loop = getenv("SVB200_DEFER_LOOP") && std::string(getenv("SVB200_DEFER_LOOP")) == "1";
+    while (defer_k > 0 && sched.size() >= 2 && !rest.empty() && int(sched.back().second.size()) <= defer_k) {
       std::vector<int> back = sched.back().second;
       sched.pop_back();
       std::sort(back.begin(), back.end());
       std::vector<int> merged;
       std::merge(rest.begin(), rest.end(), back.begin(), back.end(), std::back_inserter(merged));
       rest.swap(merged);
+      if (!defer_loop) break;
     }
     std::vector<u64> dense_tile(sched.size(), 0);   // register (dense) tile positions per phase
     std::vector<u64> pred_tile(sched.size(), 0);    // tile positions its ops test per thread
@@ -1291,13 +1289,54 @@ Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, boo
   for (auto& A : prog.passes) A.n_gen_total = int(prog.gen_slot_of.size());
   prog.gen_scale.resize(prog.gen_slot_of.size(), 1.0);
   absorb_rotation_signs(prog, jit_enabled());
-  if (!prog.tan_forms.empty()) {
-    std::lock_guard<std::mutex> lk(g_tan_mu);
-    if (g_tan_forms.size() > 4096) g_tan_forms.clear();
-    g_tan_forms[skey] = prog.tan_forms;
-  }
   return prog;
 }
+
+// Tail-deferral threshold chosen per circuit structure (see build_program; guarded by g_tan_mu).
+static std::map<u64, int> g_defer_choice;
+
+// Plan a program.  Pass construction is greedy and sensitive to where passes end, so the first plan
+// of a circuit structure is built with several tail-deferral thresholds and the cheapest is kept,
+// by a cost model fitted to the bench circuit's measured pass times: a pass costs ~1.8 phases (its
+// HBM stream + tile load/store), a phase one shared-memory round trip plus its arithmetic.  The
+// choice is remembered per structure (like the rotation forms), so re-plans with new parameter
+// values plan once.  SVB200_DEFER_TAIL=k pins the threshold.
+Program build_program(int nl, const std::vector<Prim>& prims_in, bool remap, bool pin_top) {
+  const u64 skey = structure_key(nl, prims_in, remap, pin_top);
+  std::vector<uint8_t> hint;
+  int chosen = -1;
+  {
+    std::lock_guard<std::mutex> lk(g_tan_mu);
+    auto it = g_tan_forms.find(skey);
+    if (it != g_tan_forms.end()) hint = it->second;
+    auto jt = g_defer_choice.find(skey);
+    if (jt != g_defer_choice.end()) chosen = jt->second;
+  }
+  static const int forced = getenv("SVB200_DEFER_TAIL") ? std::max(0, atoi(getenv("SVB200_DEFER_TAIL"))) : -1;
+  if (forced >= 0) chosen = forced;
+  Program prog;
+  if (chosen >= 0) {
+    prog = build_program_k(nl, prims_in, remap, pin_top, chosen, hint);
+  } else {
+    double best = 1e300;
+    for (int k : {3, 2, 1, 0}) {
+      Program cand = build_program_k(nl, prims_in, remap, pin_top, k, hint);
+      const double cost = 1.8 * double(cand.passes.size()) + double(cand.phases.size()) + double(cand.singles.size());
+      if (cost < best) {
+        best = cost;
+        chosen = k;
+        prog = std::move(cand);
+      }
+    }
+  }
+  std::lock_guard<std::mutex> lk(g_tan_mu);
+  if (g_tan_forms.size() > 4096) g_tan_forms.clear();
+  if (g_defer_choice.size() > 4096) g_defer_choice.clear();
+  if (!prog.tan_forms.empty()) g_tan_forms[skey] = prog.tan_forms;
+  g_defer_choice[skey] = chosen;
+  return prog;
+}
+
 
 void serialize_program(const Program& prog, int nl, std::vector<int64_t>& I, std::vector<double>& Dv) {
   I.clear();
