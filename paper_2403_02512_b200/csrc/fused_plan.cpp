@@ -1178,6 +1178,39 @@ Program build_program_k(int nl, const std::vector<Prim>& prims_in, bool remap, b
         return x < y;
       });
       static const bool sort_all = !(getenv("SVB200_REMAP_SORT") && std::string(getenv("SVB200_REMAP_SORT")) == "0");
+      // The positions sent to physical bits 0..2 become the last phase's lanes (direct store).  A
+      // quarter-warp's 16-byte loads are conflict-free only when its three lane positions cover all
+      // residues mod 3 (the swizzle folds tile position p into chunk bit p mod 3), so among the
+      // soonest-needed candidates take three with distinct residues that the last phase neither
+      // holds in registers nor tests as predicates.
+      static const bool lane_res = !(getenv("SVB200_LANE_RESIDUE") && std::string(getenv("SVB200_LANE_RESIDUE")) == "0");
+      if (lane_res && sort_all && A.n_phases > 0 && cand.size() >= 3 && LB == 3) {
+        const FPhase& Lp = prog.phases[A.phase_begin + A.n_phases - 1];
+        u64 predp = 0;   // physical positions the last phase tests per thread
+        for (int oi = Lp.op_begin; oi < Lp.op_end; ++oi) {
+          const FOp& o = prog.ops[oi];
+          predp |= o.pm | o.fpm | o.xm;
+          for (int j = 0; j < o.nt; ++j)
+            if (o.treg[j] == 0xFF) predp |= 1ull << o.tphys[j];
+        }
+        std::vector<int> pick;
+        int used = 0;
+        for (int x : cand) {
+          const int t = tile_pos_of[x];
+          bool reg = false;
+          for (int k = 0; k < kRB; ++k) reg |= Lp.reg[k] == t;
+          if (reg || ((predp >> x) & 1) || ((used >> (t % 3)) & 1)) continue;
+          used |= 1 << (t % 3);
+          pick.push_back(x);
+          if (pick.size() == 3) break;
+        }
+        if (pick.size() == 3) {
+          std::vector<int> reordered(pick.begin(), pick.end());
+          for (int x : cand)
+            if (std::find(pick.begin(), pick.end(), x) == pick.end()) reordered.push_back(x);
+          cand.swap(reordered);
+        }
+      }
       if (sort_all) {
         // every tile position, not only 0..LBT-1: the qubits needed soonest take the lowest
         // physical positions of the tile, the ones needed last the highest.  Low positions are
@@ -1414,7 +1447,8 @@ void serialize_program(const Program& prog, int nl, std::vector<int64_t>& I, std
 
 void plan_program_serialized(int n_qubits, const std::vector<Prim>& prims, std::vector<int64_t>& ints,
                              std::vector<double>& dbls) {
-  const fused::Program prog = fused::build_program(n_qubits, prims, true);
+  static const bool remap = !(getenv("SVB200_REMAP") && std::string(getenv("SVB200_REMAP")) == "0");
+  const fused::Program prog = fused::build_program(n_qubits, prims, remap);
   fused::serialize_program(prog, n_qubits, ints, dbls);
 }
 
