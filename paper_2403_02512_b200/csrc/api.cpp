@@ -212,6 +212,17 @@ static void exec_prims(sv_handle* h, const std::vector<double2*>& states, std::v
 // Controls and diagonal bits on global qubits never need a swap (resolve_global).
 // `exec` receives each batch already relabeled to physical positions and resolved against
 // this rank's global bits (the forward pass and the fused adjoint sweep share this schedule).
+// this rank's view of a batch: global controls / diagonal bits resolved, skipped prims dropped
+static void resolve_batch(sv_handle* h, std::vector<Prim>& batch) {
+  std::vector<Prim> out;
+  out.reserve(batch.size());
+  for (Prim& p : batch) {
+    resolve_global(p, h->nl, h->rank);
+    if (!p.skip) out.push_back(p);
+  }
+  batch.swap(out);
+}
+
 static void schedule_sharded(sv_handle* h, const std::vector<double2*>& states, const std::vector<Prim>& L,
                              const std::function<void(std::vector<Prim>&)>& exec) {
   std::vector<PrimReq> req(L.size());
@@ -233,11 +244,13 @@ static void schedule_sharded(sv_handle* h, const std::vector<double2*>& states, 
       }
     }
     if (!batch.empty()) {
+      // physical positions; controls / diagonal bits on global positions are NOT resolved here:
+      // the batch is identical on every rank, and exec resolves it (resolve_global) or runs it
+      // rank-uniformly (fused programs evaluate global bits in the kernel)
       std::vector<Prim> phys_prims;
       for (int i : batch) {
         Prim p = L[i];
         relabel_prim(p, h->phys.data());
-        resolve_global(p, h->nl, h->rank);
         if (!p.skip) phys_prims.push_back(p);
       }
       exec(phys_prims);
@@ -264,7 +277,20 @@ static void run_ops_sharded(sv_handle* h, const std::vector<double2*>& states, c
     for (auto& pc : lower_op(ops[i], h->n, col, false, nullptr))
       if (!pc.fwd.skip) L.push_back(pc.fwd);
   }
-  schedule_sharded(h, states, L, [&](std::vector<Prim>& batch) { exec_prims(h, states, batch, fuse); });
+  static const bool uniform_on = !(getenv("SVB200_RANK_UNIFORM") && std::string(getenv("SVB200_RANK_UNIFORM")) == "0");
+  schedule_sharded(h, states, L, [&](std::vector<Prim>& batch) {
+    if (uniform_on && fuse && !h->recording && h->prec == 64 && h->nl >= 5) {
+      // one program for every rank (global bits evaluated in the kernel): in-tile relabeling allowed
+      fold_diag_phases(batch);
+      const std::vector<int> perm = apply_prims_fused(h, states, batch, nullptr, nullptr, true, true);
+      for (int o = 0; o < h->n; ++o)
+        if (h->phys[o] < h->nl) h->phys[o] = perm[h->phys[o]];
+      batch.clear();
+      return;
+    }
+    resolve_batch(h, batch);
+    exec_prims(h, states, batch, fuse);
+  });
 }
 
 // Single GPU: undo the qubit relabeling that fused passes leave behind (qubit at logical offset o
@@ -669,6 +695,7 @@ static double adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const
   host_prof_mark("row: <psi|lambda> (synced)");
   const std::vector<double2*> both = {h->state, lam};
   schedule_sharded(h, both, prims, [&](std::vector<Prim>& batch) {
+    resolve_batch(h, batch);
     const int top = h->nl;
     for (Prim& p : batch)
       if (p.type == PRIM_GEN || p.type == PRIM_GEND) p.xmask = 1ull << top;

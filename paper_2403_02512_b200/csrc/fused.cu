@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(256, DB ? 1 : 2) k_fused(double2* __restrict__
     for (int ph = 0; ph < P.n_phases; ++ph) {
       const DPhase& F = s_ph[ph];
       const int s0 = F.s_lo[tid & 15] ^ F.s_hi[tid >> 4];
-      const u64 phys_base = base | F.g_lo[tid & 15] | F.g_hi[tid >> 4];
+      const u64 phys_base = base | F.g_lo[tid & 15] | F.g_hi[tid >> 4] | P.gbits;
       const int W0 = F.W[0], W1 = F.W[1], W2 = F.W[2], W3 = F.W[3];
       double2 a[kRegs];
 #pragma unroll
@@ -609,12 +609,18 @@ void release_fused(sv_handle* h) {
 }
 
 std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& states, const std::vector<Prim>& prims,
-                                   std::vector<std::pair<int, cplx>>* gen_out, double2* state_hi, bool allow_remap) {
+                                   std::vector<std::pair<int, cplx>>* gen_out, double2* state_hi, bool allow_remap,
+                                   bool rank_uniform) {
   using namespace fused;
   std::vector<int> identity(h->nl);
   for (int p = 0; p < h->nl; ++p) identity[p] = p;
   // two-array state (state_hi): the top bit selects the array; singles run on each half
-  auto run_single = [&](double2* st, const Prim& p) {
+  auto run_single = [&](double2* st, const Prim& p0) {
+    Prim p = p0;
+    if (rank_uniform) {   // the per-primitive kernels see only local bits: resolve for this rank
+      resolve_global(p, h->nl, h->rank);
+      if (p.skip) return;
+    }
     if (!state_hi) {
       launch_prim(h, st, p);
       return;
@@ -636,7 +642,9 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
   // unconditional on another), so each rank plans a different program; an in-tile relabeling
   // would then leave the ranks with different layouts and the next swap would exchange
   // mismatched halves.  Every rank must keep the same layout: no relabeling when world > 1.
-  const bool remap = remap_env && h->world == 1 && allow_remap;
+  // (rank_uniform programs are identical on every rank, so they may relabel)
+  const bool remap = remap_env && (h->world == 1 || rank_uniform) && allow_remap;
+  const u64 gbits = rank_uniform ? (u64(h->rank) << h->nl) : 0ull;
   host_prof_mark("fused: enter");
   const std::shared_ptr<Program> prog_ptr = cached_program(h, prims, remap, state_hi != nullptr);
   host_prof_mark("fused: program ready");
@@ -725,7 +733,8 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
         continue;
       }
       const FPassArgs& A = prog.passes[s.index];
-      const DPass D = make_dpass(A, h->nl, grid);
+      DPass D = make_dpass(A, h->nl, grid);
+      D.gbits = gbits;
       const bool full = prog.full[s.index];
       const int threads = 1 << (A.b - kRB);
       const size_t smem = (db ? 2 : 1) * (size_t(1) << b) * sizeof(double2) + size_t(D.n_phases) * sizeof(DPhase) +
@@ -741,6 +750,7 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
       if (jp && jp->pp) {
         // ping-pong loop: one 512-thread CTA per SM, three tile buffers (fused_dev.cuh run_pass_pp)
         DPass Dp = make_dpass(A, h->nl, pp_grid);
+        Dp.gbits = gbits;
         const size_t psmem = fdev::pp_smem_bytes(A.b, A.n_gen > 0);
         jit_launch(*jp, h->device, unsigned(pp_grid), fdev::kPPThreads, psmem, st, state, state_hi, &Dp, ph, d_jt, d_gen);
       } else if (jp) {

@@ -351,6 +351,8 @@ struct DPass {
   int st_tsm[kTB];     // swizzled shared offset of thread-index bit j at store
   unsigned ld_hsel, st_hsel;   // slots whose index carries the hi bit
   int b, nthr, n_phases, n_ops, n_gen, gen_base, n_gen_total, pad;
+  u64 gbits;           // sharded rank-uniform programs: this rank's global bits (positions >= nl),
+                       // ORed into every predicate base (never into addresses)
 };
 
 // The tile loop of one pass for the generated (per-pass specialised) kernels: persistent CTAs;
@@ -768,7 +770,7 @@ __device__ __forceinline__ void run_pass_pp(double2* __restrict__ state, double2
 #endif
 #define FDEV_PHASE_LOAD(F, W0, W1, W2, W3)                                                                       \
   const int s0 = (F).s_lo[threadIdx.x & 15] ^ (F).s_hi[threadIdx.x >> 4];                                      \
-  const u64 pb = base | (F).g_lo[threadIdx.x & 15] | (F).g_hi[threadIdx.x >> 4];                                \
+  const u64 pb = base | (F).g_lo[threadIdx.x & 15] | (F).g_hi[threadIdx.x >> 4] | P.gbits;                                \
   double2 a[fdev::kRegs];                                                                                       \
   _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r) a[r] =                                                \
       FDEV_TILE(s0 ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)); \
@@ -784,7 +786,7 @@ __device__ __forceinline__ void run_pass_pp(double2* __restrict__ state, double2
 #endif
 #define FDEV_PHASE_LOAD_X(S0, PB, W0, W1, W2, W3)                                                                \
   const int s0 = (S0) ^ FDEV_TILE_OFF;                                                                         \
-  const u64 pb = base | (PB);                                                                                   \
+  const u64 pb = base | (PB) | P.gbits;                                                                                   \
   double2 a[fdev::kRegs];                                                                                       \
   _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r) a[r] =                                                \
       FDEV_TILE(s0 ^ ((r & 1) ? (W0) : 0) ^ ((r & 2) ? (W1) : 0) ^ ((r & 4) ? (W2) : 0) ^ ((r & 8) ? (W3) : 0)); \
@@ -850,7 +852,7 @@ __device__ __forceinline__ void run_pass_pp(double2* __restrict__ state, double2
 // prefetch), a[r] = state[pb | OFF(r)]; s0 is still the thread's shared-memory slot for the store
 #define FDEV_PHASE_LOAD_G(S0, PB, O0, O1, O2, O3)                                                                \
   const int s0 = (S0);                                                                                         \
-  const u64 pb = base | (PB);                                                                                   \
+  const u64 pb = base | (PB) | P.gbits;                                                                                   \
   double2 a[fdev::kRegs];                                                                                       \
   _Pragma("unroll") for (int r = 0; r < fdev::kRegs; ++r) {                                                     \
     const u64 g_ = pb | (((r & 1) ? (O0) : 0ull) | ((r & 2) ? (O1) : 0ull) | ((r & 4) ? (O2) : 0ull) |         \

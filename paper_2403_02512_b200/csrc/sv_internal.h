@@ -231,9 +231,12 @@ void ensure_results(sv_handle* h, size_t doubles);
 // gen_out (adjoint sweep, PRIM_GEN prims present): receives (Prim::slot, <lambda|G|psi>) pairs
 // state_hi: two-array state (indices with the top local bit live in state_hi; that bit is pinned)
 // allow_remap = false: no in-tile relabeling (the program leaves every qubit where it found it)
+// rank_uniform (sharded): prims still carry their controls / diagonal bits on global positions
+// (>= nl), identical on every rank; the kernels evaluate them against this rank's global bits
+// (DPass::gbits), so every rank runs the same program and in-tile relabeling is allowed
 std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& states, const std::vector<Prim>& prims,
                                    std::vector<std::pair<int, cplx>>* gen_out = nullptr, double2* state_hi = nullptr,
-                                   bool allow_remap = true);
+                                   bool allow_remap = true, bool rank_uniform = false);
 // flat serialisation of the fused program for an op list (host only; tests re-execute it on CPU)
 void plan_program_serialized(int n_qubits, const std::vector<Prim>& prims, std::vector<int64_t>& ints,
                              std::vector<double>& dbls);
