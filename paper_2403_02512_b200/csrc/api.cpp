@@ -694,8 +694,23 @@ static double adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const
   im[ncols] = reduce_dot_re(h, h->state, lam);
   host_prof_mark("row: <psi|lambda> (synced)");
   const std::vector<double2*> both = {h->state, lam};
+  static const bool uniform_on = !(getenv("SVB200_RANK_UNIFORM") && std::string(getenv("SVB200_RANK_UNIFORM")) == "0");
+  const bool uniform = uniform_on && h->world > 1;
   schedule_sharded(h, both, prims, [&](std::vector<Prim>& batch) {
-    resolve_batch(h, batch);
+    if (uniform) {
+      // rank-uniform program on the nl+1-bit two-array state: the psi/lambda selector takes
+      // position nl, so global positions move up by one (gbits = rank << (nl + 1) in the kernels)
+      const int nl0 = h->nl;
+      auto up = [&](u64 m) { return (m & ((1ull << nl0) - 1)) | ((m >> nl0) << (nl0 + 1)); };
+      for (Prim& p : batch) {
+        p.fmask = up(p.fmask);
+        p.fval = up(p.fval);
+        for (int j = 0; j < p.nb; ++j)
+          if (p.pos[j] >= nl0) ++p.pos[j];
+      }
+    } else {
+      resolve_batch(h, batch);
+    }
     const int top = h->nl;
     for (Prim& p : batch)
       if (p.type == PRIM_GEN || p.type == PRIM_GEND) p.xmask = 1ull << top;
@@ -706,7 +721,7 @@ static double adjoint_fused_row(sv_handle* h, const sv_op* ops, int n_ops, const
     std::vector<int> perm;
     try {
       // psi = h->state, lambda = lam: one logical 2^(nl+1) state whose top bit (pinned) picks the array
-      perm = apply_prims_fused(h, {h->state}, batch, &gens, lam);
+      perm = apply_prims_fused(h, {h->state}, batch, &gens, lam, true, uniform);
     } catch (...) {
       h->nl -= 1;
       h->n_local /= 2;
