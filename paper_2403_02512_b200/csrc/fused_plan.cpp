@@ -982,6 +982,12 @@ Program build_program_k(int nl, const std::vector<Prim>& prims_in, bool remap, b
       for (size_t k = 1; k < remaining.size() && int(starts.size()) < n_starts; ++k)
         if (req[remaining[k]].dense & ~low) starts.push_back(k);
       size_t best_taken = 0;
+      static const int pass_score = getenv("SVB200_PASS_SCORE") ? atoi(getenv("SVB200_PASS_SCORE")) : 0;
+      struct Cand {
+        u64 Bc;
+        std::vector<int> tk, rs;
+      };
+      std::vector<Cand> cands;
       for (size_t s0 : starts) {
         u64 Bc = low;
         Deferred defc;
@@ -1003,12 +1009,36 @@ Program build_program_k(int nl, const std::vector<Prim>& prims_in, bool remap, b
             rs.push_back(i);
           }
         }
+        if (pass_score > 0) {
+          cands.push_back({Bc, std::move(tk), std::move(rs)});
+          continue;
+        }
         if (tk.size() > best_taken) {
           best_taken = tk.size();
           B = Bc;
           take.swap(tk);
           rest.swap(rs);
         }
+      }
+      if (pass_score > 0) {
+        // SVB200_PASS_SCORE=k: schedule the k largest candidates (on a copy: scheduling merges
+        // prims) and keep the one with the most prims per cost (phases + 1.8 for the pass itself)
+        std::stable_sort(cands.begin(), cands.end(), [](const Cand& x, const Cand& y) { return x.tk.size() > y.tk.size(); });
+        double best_score = -1.0;
+        size_t best_i = 0;
+        for (size_t ci = 0; ci < cands.size() && int(ci) < pass_score; ++ci) {
+          std::vector<Prim> Pc = P;
+          int64_t mg = 0;
+          const auto sc = schedule_phases(Pc, cands[ci].tk, mg);
+          const double score = double(cands[ci].tk.size()) / (double(sc.size()) + 1.8);
+          if (score > best_score) {
+            best_score = score;
+            best_i = ci;
+          }
+        }
+        B = cands[best_i].Bc;
+        take.swap(cands[best_i].tk);
+        rest.swap(cands[best_i].rs);
       }
     }
     for (int p = 0; p < nl && popcount64(B) < b; ++p) B |= 1ull << p;   // fill: longest contiguous runs
