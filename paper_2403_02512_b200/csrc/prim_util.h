@@ -8,6 +8,8 @@
 #pragma once
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "sv_internal.h"
@@ -20,6 +22,12 @@ struct PrimReq {
 };
 
 inline bool prim_is_xlike(const std::vector<cplx>& m) { return m.size() == 4 && m[0] == m[3] && m[1] == m[2]; }
+
+// SVB200_GEN_SEL_GENERAL=1: the round-1 rule (the psi/lambda bit as a general action), for A/B
+inline bool gen_sel_general() {
+  static const bool on = getenv("SVB200_GEN_SEL_GENERAL") && std::string(getenv("SVB200_GEN_SEL_GENERAL")) == "1";
+  return on;
+}
 
 inline PrimReq prim_requirements(const Prim& p) {
   PrimReq r;
@@ -34,17 +42,23 @@ inline PrimReq prim_requirements(const Prim& p) {
     for (int j = 0; j < p.nb; ++j) r.support |= 1ull << p.pos[j];
     r.zb = r.support;
   } else if (p.type == PRIM_GEND) {
-    // diagonal generator: Z-like everywhere except the psi/lambda bit it reads across
+    // diagonal generator: Z-like everywhere; the psi/lambda bit must be a register bit (dense)
     r.support = p.fmask | p.xmask;
     for (int j = 0; j < p.nb; ++j) r.support |= 1ull << p.pos[j];
     r.dense = p.xmask;
-    r.zb = r.support & ~p.xmask;
+    r.zb = r.support & ~(gen_sel_general() ? p.xmask : 0ull);
   } else if (p.type == PRIM_GEN) {
     // reads psi and lambda on its targets (general) across the psi/lambda bit; controls Z-like
     for (int j = 0; j < p.nb; ++j) r.dense |= 1ull << p.pos[j];
     r.dense |= p.xmask;
     r.support = p.fmask | r.dense;
     r.zb = p.fmask & ~r.dense;
+    // A bra-ket only reads the state and no gate acts on the psi/lambda bit, so for commutation
+    // that bit is Z-like: bra-kets commute with each other and with gates on other qubits (a
+    // unitary V on both arrays that commutes with G leaves <lambda|G|psi> unchanged).  Treating
+    // it as a general action chained every bra-ket to the previous one: one deferred bra-ket
+    // blocked all later ones and ended the pass (reverse sweeps took ~3x the forward's passes).
+    if (!gen_sel_general()) r.zb |= p.xmask;
   } else {
     for (int j = 0; j < p.nb; ++j) r.dense |= 1ull << p.pos[j];
     r.support = p.fmask | r.dense;
