@@ -764,8 +764,8 @@ struct XchgParams {
   int nc;
 };
 
+template <int IT>   // IT local + IT remote 16-byte loads in flight per thread and partner
 __global__ void __launch_bounds__(kThreads) k_exchange_multi(double2* __restrict__ a, const XchgParams P) {
-  constexpr int IT = 4;   // 4 local + 4 remote 16-byte loads in flight per thread and partner
   const u64 stride = u64(gridDim.x) * kThreads * IT;
   for (u64 t0 = u64(blockIdx.x) * kThreads * IT + threadIdx.x; t0 < P.count; t0 += stride) {
 #pragma unroll
@@ -1031,8 +1031,12 @@ void launch_exchange_multi(sv_handle* h, double2* a, double2* const* peer_by_c, 
   P.count = count;
   P.nc = nc;
   P.ins = make_ins(split_fmask);
-  const unsigned g = unsigned(std::min<u64>(grid_for(count, kThreads * 4), 148ull * 8));
-  k_exchange_multi<<<g, kThreads, 0, h->stream>>>(a, P);
+  // SVB200_XCHG_IT: loads in flight per thread and partner (4 default; 8 measured for A/B)
+  static const int it = getenv("SVB200_XCHG_IT") ? atoi(getenv("SVB200_XCHG_IT")) : 4;
+  const unsigned g = unsigned(std::min<u64>(grid_for(count, kThreads * it), 148ull * 8));
+  if (it == 8) k_exchange_multi<8><<<g, kThreads, 0, h->stream>>>(a, P);
+  else if (it == 2) k_exchange_multi<2><<<g, kThreads, 0, h->stream>>>(a, P);
+  else k_exchange_multi<4><<<g, kThreads, 0, h->stream>>>(a, P);
   h->launches++;
   CUDA_CHECK(cudaGetLastError());
 }
