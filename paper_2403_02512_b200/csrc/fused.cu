@@ -29,6 +29,7 @@
 #include "fused_dev.cuh"
 
 namespace fused {
+static_assert(fdev::kGenSub == 4, "fused_jit.cpp fdev_gen_sub must match fdev::kGenSub");
 namespace {
 
 using fdev::cacc_conj;
@@ -756,7 +757,7 @@ std::vector<int> apply_prims_fused(sv_handle* h, const std::vector<double2*>& st
       } else if (jp) {
         // generated kernel of this pass: [tile] [phase records] [generator accumulators]
         const size_t jsmem = (jdb ? 4 : (jp->split ? 3 : 2)) * (size_t(1) << (b - 1)) * sizeof(double2) + size_t(D.n_phases) * sizeof(DPhase) +
-                             (A.n_gen ? size_t(threads / 32) * kMaxGens * sizeof(double2) : 0);
+                             (A.n_gen ? size_t(threads / 32) * kMaxGens * fdev::kGenSub * sizeof(double2) : 0);
         jit_launch(*jp, h->device, g, threads, jsmem, st, state, state_hi, &D, ph, d_jt, d_gen);
       } else if (two) {
         if (db && full) launch_fused<true, true, true>(g, threads, smem, st, state, D, ph, op, d_cf, d_gen, state_hi);

@@ -16,6 +16,7 @@ constexpr int kRB = 4;           // register bits per thread
 constexpr int kRegs = 1 << kRB;  // amplitudes per thread
 constexpr int kTB = kMaxB - kRB; // max thread-index bits
 constexpr int kMaxGens = 64;     // generator slots per pass (per-warp shared accumulators)
+constexpr int kGenSub = 4;       // accumulators per warp and slot in run_pass: one per 8-lane group
 constexpr int kMtGeneral = 0, kMtReal = 1, kMtRxLike = 2;
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
@@ -309,15 +310,20 @@ __device__ __forceinline__ void gen_parity(const double2 (&a)[kRegs], const doub
   im += ei + (d.x * oi + d.y * orr);
 }
 
-// warp-reduce one bra-ket and add it to this warp's shared accumulator (every lane calls)
+// reduce one bra-ket over groups of 32 / SUB lanes and add each group's sum to its own accumulator
+// of this warp's slot (every lane calls).  SUB = 4: 3 shuffle rounds instead of 5 per bra-ket, the
+// four 8-lane sums land in adjacent accumulators (conflict-free); the end of the kernel adds them in
+// fixed order with the warps' (deterministic).
+template <int SUB>
 __device__ __forceinline__ void gen_commit(double re, double im, double2* __restrict__ acc_warp, int slot) {
-  for (int s = 16; s > 0; s >>= 1) {
+  for (int s = 16 / SUB; s > 0; s >>= 1) {
     re += __shfl_xor_sync(0xffffffffu, re, s);
     im += __shfl_xor_sync(0xffffffffu, im, s);
   }
-  if ((threadIdx.x & 31) == 0) {
-    acc_warp[slot].x += re;
-    acc_warp[slot].y += im;
+  if ((threadIdx.x & (32 / SUB - 1)) == 0) {
+    double2& c = acc_warp[slot * SUB + (threadIdx.x & 31) / (32 / SUB)];
+    c.x += re;
+    c.y += im;
   }
 }
 
@@ -389,7 +395,7 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     const int n16p = P.n_phases * int(sizeof(DPhase) / 16);
     for (int i = tid; i < n16p; i += nthreads) dst[i] = src[i];
     if (P.n_gen)
-      for (int i = tid; i < (nthreads >> 5) * kMaxGens; i += nthreads) s_gen[i] = make_double2(0.0, 0.0);
+      for (int i = tid; i < (nthreads >> 5) * kMaxGens * kGenSub; i += nthreads) s_gen[i] = make_double2(0.0, 0.0);
   }
   u64 ld_tid = 0, st_tid = 0;
   int st_sw = 0;
@@ -416,7 +422,7 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     for (u64 v = blockIdx.x; m && v; m &= m - 1, v >>= 1)
       if (v & 1) base |= m & (~m + 1);
   }
-  double2* acc_warp = s_gen + (tid >> 5) * kMaxGens;
+  double2* acc_warp = s_gen + (tid >> 5) * kMaxGens * kGenSub;
   auto issue_load = [&](u64 b0, double2* buf) {
     double2 *p_lo, *p_hi;
     slot_ptrs(b0 | ld_tid, p_lo, p_hi);
@@ -548,10 +554,11 @@ __device__ __forceinline__ void run_pass(double2* __restrict__ state, double2* _
     const int nw = nthreads >> 5;
     for (int g = tid; g < P.n_gen; g += nthreads) {
       double2 s = make_double2(0.0, 0.0);
-      for (int w = 0; w < nw; ++w) {
-        s.x += s_gen[w * kMaxGens + g].x;
-        s.y += s_gen[w * kMaxGens + g].y;
-      }
+      for (int w = 0; w < nw; ++w)
+        for (int q = 0; q < kGenSub; ++q) {
+          s.x += s_gen[(w * kMaxGens + g) * kGenSub + q].x;
+          s.y += s_gen[(w * kMaxGens + g) * kGenSub + q].y;
+        }
       gen_partials[size_t(blockIdx.x) * P.n_gen_total + P.gen_base + g] = s;
     }
   }

@@ -62,7 +62,10 @@ const int kPairK1[6] = {1, 2, 3, 2, 3, 3};
 
 // Source generator for one pass.  Records, in emission order, which op coefficients go into the
 // parameter block (cf_refs) and which coefficient tables go into the device table (tab_refs).
+constexpr int fdev_gen_sub = 4;   // == fdev::kGenSub (fused.cu checks): accumulators per warp and slot
+
 struct Gen {
+  bool pp = false;   // ping-pong loop: one accumulator per warp and slot (its smem is full)
   std::ostringstream o;
   std::vector<std::pair<int, int>> cf_refs;   // (pass-local op, c[] index)
   std::vector<std::pair<int, int>> tab_refs;  // (pass-local op, table length)
@@ -211,7 +214,7 @@ bool emit_op(Gen& g, int i, const FOp& op, bool parity_tab, int& dyn, VCtx* vc =
       return false;
     }
     o << "      }\n";
-    o << "      fdev::gen_commit(re, im, acc_warp, " << op.slot << ");\n";
+    o << "      fdev::gen_commit<" << (g.pp ? 1 : fdev_gen_sub) << ">(re, im, acc_warp, " << op.slot << ");\n";
     o << "    }\n";
     return true;
   }
@@ -499,6 +502,7 @@ std::string jit_pass_source(const Program& prog, int pass, bool two, bool db, st
   const bool split = split_on && direct && jit_ctas_per_sm() <= 2 && !jit_pp();
   // ping-pong tile loop (fused_dev.cuh run_pass_pp): direct passes on full 12-bit tiles
   const bool pp = jit_pp() && direct && A.b == kMaxB && A.nthr == kMaxB - kRB;
+  g.pp = pp;
   // first phase straight from global memory after an L2 prefetch (fused_dev.cuh run_pass DFL)
   static const bool dfl_on = getenv("SVB200_JIT_DFL") && std::string(getenv("SVB200_JIT_DFL")) == "1";
   const bool dfl = dfl_on && direct && !pp && !split;
