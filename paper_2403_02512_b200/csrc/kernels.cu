@@ -402,7 +402,7 @@ struct PauliGroupsArgs {
   int ng;
 };
 
-template <class C>
+template <class C, int PF>
 __global__ void __launch_bounds__(kThreads) k_pauli_apply_multi(const C* __restrict__ psi, C* __restrict__ lam,
                                                                 u64 n, const PauliGroupsArgs G,
                                                                 const PauliApplyTermDev* __restrict__ terms, int nterms,
@@ -412,19 +412,71 @@ __global__ void __launch_bounds__(kThreads) k_pauli_apply_multi(const C* __restr
   __syncthreads();
   for (u64 i = u64(blockIdx.x) * kThreads + threadIdx.x; i < n; i += u64(gridDim.x) * kThreads) {
     double2 o = accumulate ? wide(lam[i]) : make_double2(0.0, 0.0);
+    if (PF) {
+      // every group's gather issued before any arithmetic: kMaxXG loads in flight per thread
+      // (the gathers are L2 hits in x-mask order; one at a time they were latency-bound)
+      double2 b[kMaxXG];
+#pragma unroll
+      for (int g = 0; g < kMaxXG; ++g)
+        if (g < G.ng) b[g] = wide(psi[i ^ G.x[g]]);
+#pragma unroll
+      for (int g = 0; g < kMaxXG; ++g) {
+        if (g >= G.ng) break;
+        const u64 j = i ^ G.x[g];
+        double2 s = make_double2(0.0, 0.0);
+        for (int t = G.t_begin[g]; t < G.t_begin[g + 1]; ++t) {
+          const double sg = (__popcll(j & sat2[t].z) & 1) ? -1.0 : 1.0;
+          s.x = fma(sg, sat2[t].cc.x, s.x);
+          s.y = fma(sg, sat2[t].cc.y, s.y);
+        }
+        o = cfma(s, b[g], o);
+      }
+    } else {
+      for (int g = 0; g < G.ng; ++g) {
+        const u64 j = i ^ G.x[g];
+        const double2 b = wide(psi[j]);
+        double2 s = make_double2(0.0, 0.0);
+        for (int t = G.t_begin[g]; t < G.t_begin[g + 1]; ++t) {
+          const double sg = (__popcll(j & sat2[t].z) & 1) ? -1.0 : 1.0;
+          s.x = fma(sg, sat2[t].cc.x, s.x);
+          s.y = fma(sg, sat2[t].cc.y, s.y);
+        }
+        o = cfma(s, b, o);
+      }
+    }
+    lam[i] = narrow<C>(o);
+  }
+}
+
+// Batched expectation of up to kMaxXG non-diagonal x-groups: sum_i Re(conj(psi_i) (H_batch psi)_i)
+// with (H_batch psi)_i formed in registers exactly as k_pauli_apply_multi forms lambda_i (in x-mask
+// order the gathers are L2 hits), so DRAM reads psi about once per batch instead of once per
+// x-group; nothing is written.
+template <class C>
+__global__ void __launch_bounds__(kThreads) k_pauli_expval_multi(const C* __restrict__ psi, u64 n, const PauliGroupsArgs G,
+                                                                 const PauliApplyTermDev* __restrict__ terms, int nterms,
+                                                                 double* __restrict__ partials) {
+  extern __shared__ PauliApplyTermDev sat3[];
+  for (int t = threadIdx.x; t < nterms; t += kThreads) sat3[t] = terms[t];
+  __syncthreads();
+  double v[1] = {0.0};
+  for (u64 i = u64(blockIdx.x) * kThreads + threadIdx.x; i < n; i += u64(gridDim.x) * kThreads) {
+    const double2 a = wide(psi[i]);
+    double2 o = make_double2(0.0, 0.0);
     for (int g = 0; g < G.ng; ++g) {
       const u64 j = i ^ G.x[g];
       const double2 b = wide(psi[j]);
       double2 s = make_double2(0.0, 0.0);
       for (int t = G.t_begin[g]; t < G.t_begin[g + 1]; ++t) {
-        const double sg = (__popcll(j & sat2[t].z) & 1) ? -1.0 : 1.0;
-        s.x = fma(sg, sat2[t].cc.x, s.x);
-        s.y = fma(sg, sat2[t].cc.y, s.y);
+        const double sg = (__popcll(j & sat3[t].z) & 1) ? -1.0 : 1.0;
+        s.x = fma(sg, sat3[t].cc.x, s.x);
+        s.y = fma(sg, sat3[t].cc.y, s.y);
       }
       o = cfma(s, b, o);
     }
-    lam[i] = narrow<C>(o);
+    v[0] = fma(a.x, o.x, fma(a.y, o.y, v[0]));   // Re(conj(a) o)
   }
+  block_reduce_store<1>(v, partials);
 }
 
 // ---------------------------------------------------------------------------
@@ -1186,6 +1238,47 @@ void pauli_group_apply(sv_handle* h, const double2* psi, double2* lam, u64 xmask
   CUDA_CHECK(cudaGetLastError());
 }
 
+// <psi|H|psi> of non-diagonal x-groups in batches of kMaxXG (x-mask order); one partial sum per
+// batch into d_out[0..nbatches).  Returns the number of batches.
+int pauli_groups_expval_batched(sv_handle* h, const double2* psi,
+                                std::vector<std::pair<u64, std::vector<PauliTerm>>> groups, double* d_out) {
+  std::stable_sort(groups.begin(), groups.end(),
+                   [](const std::pair<u64, std::vector<PauliTerm>>& a, const std::pair<u64, std::vector<PauliTerm>>& b) {
+                     return a.first < b.first;
+                   });
+  const unsigned g = red_grid(h->n_local);
+  int nb = 0;
+  for (size_t g0 = 0; g0 < groups.size(); g0 += kMaxXG, ++nb) {
+    PauliGroupsArgs G;
+    std::vector<PauliApplyTermDev> dt;
+    G.ng = int(std::min<size_t>(kMaxXG, groups.size() - g0));
+    for (int k = 0; k < G.ng; ++k) {
+      G.x[k] = groups[g0 + k].first;
+      G.t_begin[k] = int(dt.size());
+      for (const auto& t : groups[g0 + k].second) dt.push_back({t.zmask, d2(t.cc)});
+    }
+    G.t_begin[G.ng] = int(dt.size());
+    ensure_partials(h, g);
+    auto* d_terms = (const PauliApplyTermDev*)scratch_upload(h, dt.data(), dt.size() * sizeof(PauliApplyTermDev));
+    const size_t smem = dt.size() * sizeof(PauliApplyTermDev);
+    if (smem > 48 * 1024)
+      for (const void* f : {(const void*)k_pauli_expval_multi<double2>, (const void*)k_pauli_expval_multi<float2>})
+        CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    const double bytes = (G.ng + 1.0) * double(amp_bytes(h)) * double(h->n_local);
+    cudaEvent_t ev[2];
+    stat_begin(h, KC_REDUCE, bytes, ev);
+    if (h->prec == 32)
+      k_pauli_expval_multi<float2><<<g, kThreads, smem, h->stream>>>(SV_F32(psi), h->n_local, G, d_terms, int(dt.size()), h->d_partials);
+    else
+      k_pauli_expval_multi<double2><<<g, kThreads, smem, h->stream>>>(psi, h->n_local, G, d_terms, int(dt.size()), h->d_partials);
+    stat_end(h, KC_REDUCE, bytes, ev);
+    h->launches++;
+    CUDA_CHECK(cudaGetLastError());
+    sum_partials(h, h->d_partials, g, 1, d_out + nb);
+  }
+  return nb;
+}
+
 void pauli_groups_apply(sv_handle* h, const double2* psi, double2* lam,
                         const std::vector<std::pair<u64, std::vector<PauliTerm>>>& all_groups) {
   const unsigned g = unsigned(std::min<u64>(grid_for(h->n_local, kThreads * 4), 148ull * 64));
@@ -1224,14 +1317,22 @@ void pauli_groups_apply(sv_handle* h, const double2* psi, double2* lam,
     auto* d_terms = (const PauliApplyTermDev*)scratch_upload(h, dt.data(), dt.size() * sizeof(PauliApplyTermDev));
     const size_t smem = dt.size() * sizeof(PauliApplyTermDev);
     if (smem > 48 * 1024)
-      for (const void* f : {(const void*)k_pauli_apply_multi<double2>, (const void*)k_pauli_apply_multi<float2>})
+      for (const void* f : {(const void*)k_pauli_apply_multi<double2, 0>, (const void*)k_pauli_apply_multi<float2, 0>,
+                            (const void*)k_pauli_apply_multi<double2, 1>, (const void*)k_pauli_apply_multi<float2, 1>})
         CUDA_CHECK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     const int acc = written || g0 > 0;
     const double bytes = (G.ng + 1.0 + (acc ? 1.0 : 0.0)) * double(amp_bytes(h)) * double(h->n_local);
     cudaEvent_t ev[2];
     stat_begin(h, KC_APPLY_OBS, bytes, ev);
-    SV_LAUNCH2(h, k_pauli_apply_multi, SV_CFG(g, kThreads, smem, h->stream), psi, lam, h->n_local, G, d_terms,
-               int(dt.size()), acc);
+    // SVB200_PAULI_PF=1: issue every group's gather first -- measured slower (config 5: 0.94 vs 0.72 s)
+    static const bool pf = getenv("SVB200_PAULI_PF") && std::string(getenv("SVB200_PAULI_PF")) == "1";
+    if (h->prec == 32) {
+      if (pf) k_pauli_apply_multi<float2, 1><<<g, kThreads, smem, h->stream>>>(SV_F32(psi), SV_F32(lam), h->n_local, G, d_terms, int(dt.size()), acc);
+      else k_pauli_apply_multi<float2, 0><<<g, kThreads, smem, h->stream>>>(SV_F32(psi), SV_F32(lam), h->n_local, G, d_terms, int(dt.size()), acc);
+    } else {
+      if (pf) k_pauli_apply_multi<double2, 1><<<g, kThreads, smem, h->stream>>>(psi, lam, h->n_local, G, d_terms, int(dt.size()), acc);
+      else k_pauli_apply_multi<double2, 0><<<g, kThreads, smem, h->stream>>>(psi, lam, h->n_local, G, d_terms, int(dt.size()), acc);
+    }
     stat_end(h, KC_APPLY_OBS, bytes, ev);
     CUDA_CHECK(cudaGetLastError());
   }

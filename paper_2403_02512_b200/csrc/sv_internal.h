@@ -205,6 +205,8 @@ struct PauliTerm {
 };
 // K14: state = scale * exp(i f), f(i) = sum_t Re(cc_t) (-1)^{pc(i & zmask_t)} (one write-only pass)
 void init_uniform_phase(sv_handle* h, double2* state, const std::vector<PauliTerm>& terms, double scale);
+int pauli_groups_expval_batched(sv_handle* h, const double2* psi,
+                                std::vector<std::pair<u64, std::vector<PauliTerm>>> groups, double* d_out);
 void pauli_group_expval_async(sv_handle* h, const double2* state, u64 xmask, const std::vector<PauliTerm>& terms,
                               double* d_out);
 void pauli_group_apply(sv_handle* h, const double2* psi, double2* lam, u64 xmask,
